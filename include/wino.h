@@ -1,0 +1,182 @@
+/*
+ * wino.h -- C ABI of the B200-native complex-Winograd int8 convolution.
+ *
+ * Method: Meng & Brothers, "Efficient Winograd Convolution via Integer
+ * Arithmetic" (arXiv 1901.01965).  "P:n" cites line n of the paper text
+ * (reference PAPER.md); "A<n>" cites a reading recorded in DESIGN.md.
+ *
+ * What the library computes (all integer, bit-exact, no CPU fallback):
+ *   y = 3x3 stride-1 dilation-1 correlation of x with w, zero padding `pad`,
+ *   evaluated as the complex Winograd F(4x4,3x3) over the Gaussian integers
+ *   with interpolation points {0, +-1, +-i}:
+ *       Y = A^T [ (G g G^T) (.) (B^T d B) ] A
+ *   with the conjugate-pair / real-split savings (16 real + 10 Karatsuba
+ *   complex products = 46 general multiplications per tile),
+ *   the imaginary output skipped, and, when filter_scaling != 0, the
+ *   paper's integer filter-precision scaling of the Winograd-domain filters
+ *   (n / 2^p downscale with 6-bit codes, 8-bit m / 2^q reverse scale before
+ *   the output transform), composed with the complex
+ *   F(4x4) as an extension (A17).  G is used scaled by 4 (A2) so one final
+ *   out32 = rha(Re Y / 16) recovers the convolution (A11).
+ *
+ * Conventions
+ *   - Every function returns a wino_status; nothing aborts or throws.
+ *   - All tensor pointers passed to wino_transform_filter / wino_conv2d_int8
+ *     are DEVICE pointers on the plan's device, 16-byte aligned, owned by
+ *     the caller (the library never allocates or frees device memory).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Work is enqueued asynchronously; launch errors are returned
+ *     at once, device faults surface at the caller's next synchronisation.
+ *   - Calls on different streams are safe when each uses its own workspace.
+ *   - int8 tensors are two's-complement; there are no zero points (A12).
+ */
+#ifndef WINO_H
+#define WINO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    WINO_OK = 0,
+    WINO_ERR_INVALID_ARG = -1,   /* NULL / misaligned pointer, bad enum, wrong device  */
+    WINO_ERR_UNSUPPORTED = -2,   /* shape or flag outside the supported set            */
+    WINO_ERR_SHAPE = -3,         /* inconsistent sizes                                  */
+    WINO_ERR_RANGE = -4,         /* requant shift out of [0, 62], multiplier < 1        */
+    WINO_ERR_CUDA = -5,          /* a CUDA runtime call failed (launch or attribute)    */
+    WINO_ERR_NOMEM = -6          /* host allocation of the plan failed                  */
+} wino_status;
+
+/* Tensor layouts; x and y share the layout of the plan.
+ *   WINO_NCHW: x [N][Cin][H][W],  w [Cout][Cin][3][3] (OIHW), y [N][Cout][Ho][Wo]
+ *   WINO_NHWC: x [N][H][W][Cin],  w [Cout][3][3][Cin] (OHWI), y [N][Ho][Wo][Cout]
+ * with Ho = H + 2 pad - 2, Wo = W + 2 pad - 2.                                   */
+enum { WINO_NCHW = 0, WINO_NHWC = 1 };
+
+/* Output element type.
+ *   WINO_OUT_INT32: y = out32 = rha(Re Y / 16)  (the convolution itself when
+ *                   unscaled; int32, wraps never: |y| < 2^31 for Cin <= 896).
+ *   WINO_OUT_INT8:  y = clamp(rha(out32 * requant_mult / 2^requant_shift),
+ *                   -128, 127) with a 64-bit product (A14).                     */
+enum { WINO_OUT_INT8 = 0, WINO_OUT_INT32 = 1 };
+
+typedef struct {
+    int n, h, w;          /* batch and input spatial size, each >= 1                  */
+    int c_in, c_out;      /* 1 <= c_in <= 896 (int32 exactness, A23), c_out >= 1       */
+    int pad;              /* 0 or 1; h + 2 pad >= 3 and w + 2 pad >= 3                 */
+    int layout;           /* WINO_NCHW or WINO_NHWC                                    */
+    int filter_scaling;   /* 0: exact (codes all 0); 1: the paper's scheme */
+    int filter_target_max;/* 255 (the paper's int9 target, A6); only value supported   */
+    int out_mode;         /* WINO_OUT_INT8 or WINO_OUT_INT32                           */
+} wino_conv_desc;
+
+typedef struct wino_plan_s *wino_plan_t;
+
+/* Geometry and workspace layout of a plan (read-only, for tests and tools). */
+typedef struct {
+    int ho, wo;                 /* output spatial size                                */
+    int tiles_h, tiles_w;       /* ceil(ho/4), ceil(wo/4)                             */
+    long long tiles;            /* T = n * tiles_h * tiles_w                          */
+    int cin_pad;                /* c_in rounded up to 32 (one int8 MMA K step)        */
+    int cout_pad;               /* c_out rounded up to n_block                        */
+    int n_block;                /* GEMM N tile (couts per CTA)                         */
+    int m_block;                /* GEMM M tile (tiles per CTA) = 128                   */
+    int planes;                 /* 46 = 16 real + 10 x {re, im, re+im}        */
+    int pieces;                 /* 2 int8 pieces per operand value (hi s8, lo u8)      */
+    int chunk_images;           /* images per workspace chunk                          */
+    int n_chunks;
+    long long chunk_tiles_pad;  /* tiles per chunk rounded up to m_block               */
+    size_t v_offset, v_bytes;   /* V  = B^T d B operand planes inside the workspace    */
+    size_t m_offset, m_bytes;   /* M  = per-plane int32 GEMM results                   */
+    size_t workspace_bytes;
+    size_t filter_bytes;        /* transformed-filter buffer (w_wino)                  */
+    size_t codes_bytes;         /* c_out * 36 bytes                                    */
+    size_t x_bytes, y_bytes;    /* input / output tensor sizes in bytes                */
+} wino_plan_info;
+
+/* Human-readable text for a status code (static storage, never NULL). */
+const char *wino_status_string(wino_status s);
+
+/* Validate `desc` and build an immutable plan for CUDA device `device`.
+ * The plan holds host metadata only.  Returns WINO_ERR_UNSUPPORTED for
+ * pad not in {0,1}, n/h/w/c < 1, h + 2 pad < 3 or w + 2 pad < 3,
+ * c_in > 896, filter_target_max != 255, and WINO_ERR_INVALID_ARG for bad
+ * enums or NULL pointers.  The device must be sm_100 (B200).            */
+wino_status wino_plan(const wino_conv_desc *desc, int device, wino_plan_t *out);
+wino_status wino_plan_destroy(wino_plan_t plan);
+wino_status wino_plan_query(wino_plan_t plan, wino_plan_info *info);
+
+/* Sizes of the caller-allocated device buffers (0 on a NULL plan). */
+size_t wino_filter_bytes(wino_plan_t plan);     /* w_wino                      */
+size_t wino_codes_bytes(wino_plan_t plan);      /* scale_codes = c_out * 36    */
+size_t wino_workspace_bytes(wino_plan_t plan);  /* V and M of one batch chunk  */
+size_t wino_output_bytes(wino_plan_t plan);     /* y                            */
+
+/* Offline filter transform: for every output channel,
+ *   W = G_int g G_int^T (G_int = 4G) for all input channels;
+ *   per position (X-Y location) the max over input channels of
+ *   max(|Re W|, |Im W|) (A5) selects the code (n, p) of P:317-330 read as A3
+ *   (code = (n << 2) | (p - 4), 0 = unscaled, A4; mirrors share their
+ *   primary's code); W' = rha(W n / 2^p) (A7);
+ *   then the 46 GEMM operand planes (16 real, and re, im, re+im per complex
+ *   primary for the Karatsuba product) split into int8 pieces.
+ *   w           device, int8, layout per desc (OIHW or OHWI)
+ *   w_wino      device, wino_filter_bytes(plan) bytes, written (opaque layout,
+ *               documented in DESIGN.md "HBM layout")
+ *   scale_codes device, [c_out][36] uint8, written (all 0 when
+ *               filter_scaling == 0)                                        */
+wino_status wino_transform_filter(wino_plan_t plan, const int8_t *w, void *w_wino,
+                                  uint8_t *scale_codes, void *stream);
+
+/* The convolution hot path:
+ * input transform D = B^T d B per tile and channel, 46 Winograd-domain
+ * int8 GEMMs [tiles x Cin] x [Cin x Cout] on the tcgen05 tensor cores with
+ * int32 accumulation, Karatsuba recombination, reverse scaling
+ * M'' = rha(M m / 2^q) with (m, q) derived from `scale_codes` on the device
+ * (A8), real-only output transform, rha(./16), crop, optional
+ * requantisation, store.
+ *   x            device, int8 input, layout per desc
+ *   w_wino       device, produced by wino_transform_filter for this plan
+ *   scale_codes  device, [c_out][36] 6-bit codes -- THE explicit filter-scale
+ *                parameter: the codes W' was scaled with (from
+ *                wino_transform_filter, or any codes applied consistently);
+ *                every entry must be 0 or decode to n in [8,15] (else the
+ *                result is unspecified; validate with wino_check_codes)
+ *   requant_mult, requant_shift  used for WINO_OUT_INT8 only: mult >= 1,
+ *                shift in [0, 62], else WINO_ERR_RANGE
+ *   y            device, wino_output_bytes(plan) bytes, written
+ *   workspace    device, wino_workspace_bytes(plan) bytes, scratch (holds
+ *                V and M of the last chunk afterwards, see wino_plan_info) */
+wino_status wino_conv2d_int8(wino_plan_t plan, const int8_t *x, const void *w_wino,
+                             const uint8_t *scale_codes, int32_t requant_mult, int requant_shift,
+                             void *y, void *workspace, void *stream);
+
+/* End-to-end variant with HOST tensors: enqueues the host-to-device copy of
+ * x (x_host -> x_dev), wino_conv2d_int8, and the device-to-host copy of y
+ * (y_dev -> y_host) on `stream`.  x_host / y_host should be pinned
+ * (cudaHostAlloc) for asynchronous copies; x_dev / y_dev are caller-owned
+ * device staging buffers of wino_plan_info.x_bytes / y_bytes.  The caller
+ * synchronises the stream before reading y_host.                          */
+wino_status wino_conv2d_int8_host(wino_plan_t plan, const int8_t *x_host, const void *w_wino,
+                                  const uint8_t *scale_codes, int32_t requant_mult,
+                                  int requant_shift, void *y_host, int8_t *x_dev, void *y_dev,
+                                  void *workspace, void *stream);
+
+/* Device-side validation of a code table: writes 1 to *bad_flag (device
+ * int32, caller-zeroed) if any of the c_out*36 codes is neither 0 nor a
+ * valid code (n in [8,15]).                                               */
+wino_status wino_check_codes(wino_plan_t plan, const uint8_t *scale_codes, int32_t *bad_flag,
+                             void *stream);
+
+/* Harness op for the VGG stack (A22): 2x2 stride-2 max pool on int8,
+ * layout per `layout`, y [N][C][H/2][W/2] or [N][H/2][W/2][C].           */
+wino_status wino_maxpool2_int8(const int8_t *x, int n, int h, int w, int c, int layout,
+                               int8_t *y, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WINO_H */

@@ -1,0 +1,167 @@
+// k_output.cu -- K4: Karatsuba recombination, reverse
+// scaling M'' = rha(M m / 2^q), the real-only output
+// transform Y = A^T M'' A that never forms the imaginary coefficients
+// (P:163-170), out32 = rha(Y / 16) (G used as 4G, A2/A11),
+// crop, optional requantisation (A14) and the store.
+//
+// One thread per (tile, output channel); consecutive threads take
+// consecutive channels, so the 46 plane reads of M are coalesced.
+//
+// Real-only transform.  A^T rows are a_0 = (1,1,1,1,1,0), a_1 = (0,1,-1,i,-i,0),
+// a_2 = (0,1,1,-1,-1,0), a_3 = (0,1,-1,-i,i,1); a_j4 = conj(a_j3).  For a row
+// r in {0,1,2,5} with real entries M0,M1,M2,M5 and primary z = x + iy at
+// column 3 (column 4 holds conj z):
+//   Z[r][0] = M0+M1+M2+2x   Z[r][1] = M1-M2-2y   Z[r][2] = M1+M2-2x   Z[r][3] = M1-M2+M5+2y
+// Row 3 is complex (w_c at c in {0,1,2,5}, w3 = M[3][3], w4 = M[3][4]) and
+// row 4 is its conjugate, so
+//   Y[0][j] = Z0+Z1+Z2+2Re Z3   Y[1][j] = Z1-Z2-2Im Z3
+//   Y[2][j] = Z1+Z2-2Re Z3      Y[3][j] = Z1-Z2+Z5+2Im Z3.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "layout.cuh"
+
+namespace wino {
+
+__device__ __forceinline__ uint32_t rscale(uint32_t v, int code) {
+  if (!code) return v;
+  int n, p, m, q;
+  decode_code(code, n, p);
+  inverse_factor(n, p, m, q);
+  return (uint32_t)(int32_t)rha_shift64((long long)(int32_t)v * m, q);
+}
+
+__global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t* __restrict__ M,
+                                                          const uint8_t* __restrict__ codes, int n0, int imgs,
+                                                          int32_t rq_mult, int rq_shift, void* __restrict__ y) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)imgs * g.tpi * g.cout;
+  if (idx >= total) return;
+  const int co = (int)(idx % g.cout);
+  const long long t = idx / g.cout;
+  const long long ps = g.chunk_tiles_pad * (long long)g.cout_pad;
+  const int32_t* mp = M + t * g.cout_pad + co;
+
+  uint32_t mr[16], cr[10], cim[10];
+#pragma unroll
+  for (int s = 0; s < 16; s++) mr[s] = (uint32_t)__ldg(mp + s * ps);
+#pragma unroll
+  for (int k = 0; k < 10; k++) {   // Karatsuba: Re = P0 - P1, Im = P2 - P0 - P1
+    uint32_t p0 = (uint32_t)__ldg(mp + (16 + 3 * k) * ps), p1 = (uint32_t)__ldg(mp + (17 + 3 * k) * ps),
+             p2 = (uint32_t)__ldg(mp + (18 + 3 * k) * ps);
+    cr[k] = p0 - p1;
+    cim[k] = p2 - p0 - p1;
+  }
+  if (g.scaling) {   // reverse scaling before the final transforms
+    const uint8_t* cc = codes + (long long)co * 36;
+#pragma unroll
+    for (int s = 0; s < 16; s++) mr[s] = rscale(mr[s], __ldg(cc + real_pos(s)));
+#pragma unroll
+    for (int k = 0; k < 10; k++) {
+      int code = __ldg(cc + cpx_pos(k));
+      cr[k] = rscale(cr[k], code);
+      cim[k] = rscale(cim[k], code);
+    }
+  }
+  // Z = M'' A  (rows 0,1,2,5 real; row 3 complex)
+  uint32_t Z[4][4], zr[4], zi[4];
+#pragma unroll
+  for (int ri = 0; ri < 4; ri++) {
+    uint32_t M0 = mr[ri * 4], M1 = mr[ri * 4 + 1], M2 = mr[ri * 4 + 2], M5 = mr[ri * 4 + 3];
+    uint32_t x2 = 2 * cr[ri], y2 = 2 * cim[ri];
+    Z[ri][0] = M0 + M1 + M2 + x2;
+    Z[ri][1] = M1 - M2 - y2;
+    Z[ri][2] = M1 + M2 - x2;
+    Z[ri][3] = M1 - M2 + M5 + y2;
+  }
+  {
+    uint32_t w0r = cr[4], w1r = cr[5], w2r = cr[6], w5r = cr[7], w3r = cr[8], w4r = cr[9];
+    uint32_t w0i = cim[4], w1i = cim[5], w2i = cim[6], w5i = cim[7], w3i = cim[8], w4i = cim[9];
+    zr[0] = w0r + w1r + w2r + w3r + w4r;        zi[0] = w0i + w1i + w2i + w3i + w4i;
+    zr[1] = w1r - w2r - w3i + w4i;              zi[1] = w1i - w2i + w3r - w4r;
+    zr[2] = w1r + w2r - w3r - w4r;              zi[2] = w1i + w2i - w3i - w4i;
+    zr[3] = w1r - w2r + w3i - w4i + w5r;        zi[3] = w1i - w2i - w3r + w4r + w5i;
+  }
+  const int rem = (int)(t % g.tpi);
+  const int img = n0 + (int)(t / g.tpi);
+  const int ty = rem / g.tw, tx = rem % g.tw;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    uint32_t Yc[4];
+    Yc[0] = Z[0][j] + Z[1][j] + Z[2][j] + 2 * zr[j];
+    Yc[1] = Z[1][j] - Z[2][j] - 2 * zi[j];
+    Yc[2] = Z[1][j] + Z[2][j] - 2 * zr[j];
+    Yc[3] = Z[1][j] - Z[2][j] + Z[3][j] + 2 * zi[j];
+    const int ox = 4 * tx + j;
+    if (ox >= g.wo) continue;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int oy = 4 * ty + i;
+      if (oy >= g.ho) continue;
+      const int32_t o32 = (int32_t)rha_shift64((long long)(int32_t)Yc[i], 4);   // rha(Y / 16)
+      const long long yi = g.layout == 1 ? (((long long)img * g.ho + oy) * g.wo + ox) * g.cout + co
+                                         : (((long long)img * g.cout + co) * g.ho + oy) * g.wo + ox;
+      if (g.out_mode == 1) {
+        static_cast<int32_t*>(y)[yi] = o32;
+      } else {
+        long long r = rq_shift > 0 ? rha_shift64((long long)o32 * rq_mult, rq_shift) : (long long)o32 * rq_mult;
+        r = r > 127 ? 127 : (r < -128 ? -128 : r);
+        static_cast<int8_t*>(y)[yi] = (int8_t)r;
+      }
+    }
+  }
+}
+
+cudaError_t launch_output_transform(const Geom& g, const int32_t* m, const uint8_t* codes, int n0, int imgs,
+                                    int32_t rq_mult, int rq_shift, void* y, cudaStream_t st) {
+  long long total = (long long)imgs * g.tpi * g.cout;
+  unsigned blocks = (unsigned)((total + 255) / 256);
+  k_output_transform<<<blocks, 256, 0, st>>>(g, m, codes, n0, imgs, rq_mult, rq_shift, y);
+  return cudaGetLastError();
+}
+
+cudaError_t setup_output_transform() { return cudaSuccess; }
+
+// ------------------------------------------------------------------ misc
+__global__ void k_check_codes(const uint8_t* __restrict__ codes, int count, int32_t* bad) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) {
+    int c = codes[i];
+    if (c != 0 && (c >= 64 || (c >> 2) < 8)) atomicOr(bad, 1);
+  }
+}
+cudaError_t launch_check_codes(const uint8_t* codes, int count, int32_t* bad, cudaStream_t st) {
+  k_check_codes<<<(count + 255) / 256, 256, 0, st>>>(codes, count, bad);
+  return cudaGetLastError();
+}
+
+__global__ void k_maxpool2(const int8_t* __restrict__ x, int n, int h, int w, int c, int layout, int8_t* __restrict__ y) {
+  const int ho = h / 2, wo = w / 2;
+  const long long total = (long long)n * ho * wo * c;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  int ci, ox, oy, img;
+  if (layout == 1) {
+    ci = (int)(i % c); long long r = i / c; ox = (int)(r % wo); r /= wo; oy = (int)(r % ho); img = (int)(r / ho);
+  } else {
+    ox = (int)(i % wo); long long r = i / wo; oy = (int)(r % ho); r /= ho; ci = (int)(r % c); img = (int)(r / c);
+  }
+  int m = -128;
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++) {
+      int yy = 2 * oy + a, xx = 2 * ox + b;
+      int v = layout == 1 ? x[(((long long)img * h + yy) * w + xx) * c + ci] : x[(((long long)img * c + ci) * h + yy) * w + xx];
+      m = v > m ? v : m;
+    }
+  y[i] = (int8_t)m;
+}
+cudaError_t launch_maxpool2(const int8_t* x, int n, int h, int w, int c, int layout, int8_t* y, cudaStream_t st) {
+  long long total = (long long)n * (h / 2) * (w / 2) * c;
+  k_maxpool2<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(x, n, h, w, c, layout, y);
+  return cudaGetLastError();
+}
+
+}  // namespace wino

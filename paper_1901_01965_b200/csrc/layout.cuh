@@ -1,0 +1,107 @@
+// layout.cuh -- geometry, plane numbering and HBM operand layouts of the
+// CUDA path.  (The CPU oracle has its own, independent definitions.)
+//
+// Winograd-domain positions: the 6x6 grid has 16 always-real
+// positions R x R, R = {0,1,2,5}, and 10 conjugate pairs whose primaries are
+//   (0,3) (1,3) (2,3) (5,3) (3,0) (3,1) (3,2) (3,5) (3,3) (3,4)
+// mirrored (swap 3<->4 in each index in {3,4}) to
+//   (0,4) (1,4) (2,4) (5,4) (4,0) (4,1) (4,2) (4,5) (4,4) (4,3).
+// GEMM planes (46 = 16 + 10 x 3):
+//   plane s       (s < 16)  real position (R[s/4], R[s%4])
+//   plane 16+3k+0           Re of primary k   (Karatsuba P0 = Re V * Re W)
+//   plane 16+3k+1           Im of primary k   (P1 = Im V * Im W)
+//   plane 16+3k+2           Re + Im           (P2 = (Re V + Im V)(Re W + Im W))
+// Every operand value v (|v| <= 2048) is split into two int8 pieces
+//   piece 0: hi = v >> 8 (s8, in [-8, 7]);  piece 1: lo = v & 255 (u8)
+// so v = 256 hi + lo, and a plane product is
+//   V W = 65536 hh + 256 (hl + lh) + ll     (exact mod 2^32).
+//
+// Operand images are stored pre-tiled in the UMMA canonical K-major
+// no-swizzle layout so one 1-D bulk copy moves a whole stage:
+//   block of R rows (R = 128 tiles for V, n_block couts for W) and K = cin_pad
+//   bytes; byte (row r, k) of a block lives at
+//     (k / 32) * R * 32  +  (r / 8) * 256  +  ((k % 32) / 16) * 128  +  (r % 8) * 16  +  k % 16
+//   (core matrix = 8 rows x 16 B; LBO = 128, SBO = 256; a 32-byte K step of
+//   the block is R*32 contiguous bytes, and all K steps are contiguous).
+//   V image: [plane][piece][tile_block][kstep][R=128 x 32 B]
+//   W image: [plane][piece][cout_block][kstep][R=n_block x 32 B]
+//   M      : [plane][tile (chunk_tiles_pad)][cout_pad] int32
+#pragma once
+#include <cstdint>
+
+namespace wino {
+
+constexpr int kPlanes = 46;
+constexpr int kRealPlanes = 16;
+constexpr int kPrimaries = 10;
+constexpr int kPieces = 2;
+constexpr int kMBlock = 128;   // GEMM M (tiles per CTA) = TMEM lanes
+constexpr int kKStep = 32;     // int8 MMA K
+
+struct Geom {
+  int n, h, w, cin, cout, pad, layout;
+  int ho, wo, th, tw, tpi;     // output size, tiles per row/col, tiles per image
+  int cin_pad, cout_pad, nblk, ksteps;
+  int scaling, target, out_mode;
+  int chunk_imgs;
+  long long chunk_tiles_pad;   // multiple of kMBlock
+};
+
+__host__ __device__ __forceinline__ long long tiled_offset(int r, int k, int R) {
+  return (long long)(k >> 5) * R * 32 + (r >> 3) * 256 + ((k >> 4) & 1) * 128 + (r & 7) * 16 + (k & 15);
+}
+
+// Byte offset of V piece `pp` (= plane*2 + piece), chunk tile t, channel k.
+__host__ __device__ __forceinline__ long long v_offset(const Geom& g, int pp, long long t, int k) {
+  long long blk = t / kMBlock;
+  int r = (int)(t % kMBlock);
+  return (long long)pp * g.chunk_tiles_pad * g.cin_pad + blk * (long long)g.ksteps * kMBlock * 32 +
+         tiled_offset(r, k, kMBlock);
+}
+// Byte offset of W piece `pp`, output channel co, input channel k.
+__host__ __device__ __forceinline__ long long w_offset(const Geom& g, int pp, int co, int k) {
+  int blk = co / g.nblk, r = co % g.nblk;
+  return (long long)pp * g.cout_pad * g.cin_pad + (long long)blk * g.ksteps * g.nblk * 32 +
+         tiled_offset(r, k, g.nblk);
+}
+
+// Position index (r*6+c) of real plane s and of complex primary k / its mirror.
+__host__ __device__ __forceinline__ int real_pos(int s) {
+  const int R[4] = {0, 1, 2, 5};
+  return R[s >> 2] * 6 + R[s & 3];
+}
+__host__ __device__ __forceinline__ int cpx_pos(int k) {
+  const int P[10] = {0 * 6 + 3, 1 * 6 + 3, 2 * 6 + 3, 5 * 6 + 3, 3 * 6 + 0,
+                     3 * 6 + 1, 3 * 6 + 2, 3 * 6 + 5, 3 * 6 + 3, 3 * 6 + 4};
+  return P[k];
+}
+__host__ __device__ __forceinline__ int cpx_mirror_pos(int k) {
+  const int P[10] = {0 * 6 + 4, 1 * 6 + 4, 2 * 6 + 4, 5 * 6 + 4, 4 * 6 + 0,
+                     4 * 6 + 1, 4 * 6 + 2, 4 * 6 + 5, 4 * 6 + 4, 4 * 6 + 3};
+  return P[k];
+}
+
+// round-half-away-from-zero of v / 2^k (k >= 1), 64-bit.
+__device__ __forceinline__ long long rha_shift64(long long v, int k) {
+  long long a = v < 0 ? -v : v;
+  long long r = (a + (1ll << (k - 1))) >> k;
+  return v < 0 ? -r : r;
+}
+
+// Decode a 6-bit code (n << 2 | (p - 4)); 0 = unscaled.
+__device__ __forceinline__ void decode_code(int code, int& n, int& p) {
+  n = code >> 2;
+  p = (code & 3) + 4;
+}
+// Inverse factor: the largest q in {7..4} with m = rha(2^(q+p)/n) <= 255.
+__device__ __forceinline__ void inverse_factor(int n, int p, int& m, int& q) {
+  for (q = 7; q >= 4; --q) {
+    long long num = 1ll << (q + p);
+    m = (int)((2 * num + n) / (2 * n));
+    if (m <= 255) return;
+  }
+  q = 4;
+  m = 255;   // unreachable for valid codes (n >= 8)
+}
+
+}  // namespace wino

@@ -1,0 +1,228 @@
+// wino_abi.cu -- the C ABI declared in include/wino.h: plan validation,
+// workspace sizing (batch chunks sized to stay L2-resident), and sequencing of
+// the K2 -> K3 -> K4 launches per chunk on the caller's stream.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <cuda_runtime.h>
+
+#include "../../include/wino.h"
+#include "kernels.cuh"
+#include "layout.cuh"
+
+struct wino_plan_s {
+  wino_conv_desc d;
+  int device;
+  wino::Geom g;
+  int n_chunks;
+  size_t v_bytes, m_bytes, ws_bytes, f_bytes, x_bytes, y_bytes;
+};
+
+namespace {
+
+std::mutex g_setup_mu;
+bool g_setup_done[64] = {};
+
+wino_status setup_device(int device) {
+  std::lock_guard<std::mutex> lk(g_setup_mu);
+  if (device < 0 || device >= 64) return WINO_ERR_INVALID_ARG;
+  if (g_setup_done[device]) return WINO_OK;
+  int old = -1;
+  if (cudaGetDevice(&old) != cudaSuccess) return WINO_ERR_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return WINO_ERR_CUDA;
+  cudaError_t e = wino::setup_filter_transform();
+  if (e == cudaSuccess) e = wino::setup_input_transform();
+  if (e == cudaSuccess) e = wino::setup_gemm();
+  if (e == cudaSuccess) e = wino::setup_output_transform();
+  cudaSetDevice(old);
+  if (e != cudaSuccess) return WINO_ERR_CUDA;
+  g_setup_done[device] = true;
+  return WINO_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+wino_status check_device(const wino_plan_s* p) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess) return WINO_ERR_CUDA;
+  return cur == p->device ? WINO_OK : WINO_ERR_INVALID_ARG;
+}
+
+long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
+
+size_t chunk_budget_bytes() {
+  const char* env = std::getenv("WINO_CHUNK_MB");
+  long mb = env ? std::atol(env) : 64;
+  if (mb < 1) mb = 1;
+  return (size_t)mb << 20;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wino_status_string(wino_status s) {
+  switch (s) {
+    case WINO_OK: return "ok";
+    case WINO_ERR_INVALID_ARG: return "invalid argument (null/misaligned pointer, bad enum or wrong device)";
+    case WINO_ERR_UNSUPPORTED: return "unsupported shape or flag";
+    case WINO_ERR_SHAPE: return "inconsistent sizes";
+    case WINO_ERR_RANGE: return "value out of range (requant multiplier/shift)";
+    case WINO_ERR_CUDA: return "CUDA runtime error";
+    case WINO_ERR_NOMEM: return "out of host memory";
+  }
+  return "unknown status";
+}
+
+wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) {
+  if (!desc || !out) return WINO_ERR_INVALID_ARG;
+  *out = nullptr;
+  const wino_conv_desc& d = *desc;
+  if (d.layout != WINO_NCHW && d.layout != WINO_NHWC) return WINO_ERR_INVALID_ARG;
+  if (d.out_mode != WINO_OUT_INT8 && d.out_mode != WINO_OUT_INT32) return WINO_ERR_INVALID_ARG;
+  if (d.filter_scaling != 0 && d.filter_scaling != 1) return WINO_ERR_INVALID_ARG;
+  if (d.n < 1 || d.h < 1 || d.w < 1 || d.c_in < 1 || d.c_out < 1) return WINO_ERR_UNSUPPORTED;
+  if (d.pad != 0 && d.pad != 1) return WINO_ERR_UNSUPPORTED;
+  if (d.h + 2 * d.pad < 3 || d.w + 2 * d.pad < 3) return WINO_ERR_UNSUPPORTED;
+  // int32 exactness of M'' and Y (A23): 896 unscaled, 768 scaled
+  if (d.c_in > (d.filter_scaling ? 768 : 896)) return WINO_ERR_UNSUPPORTED;
+  if (d.filter_target_max != 255) return WINO_ERR_UNSUPPORTED;
+  if (d.c_out > (1 << 20) || (long long)d.n * d.h * d.w > (1ll << 40)) return WINO_ERR_UNSUPPORTED;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) return WINO_ERR_CUDA;
+  if (device < 0 || device >= ndev) return WINO_ERR_INVALID_ARG;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return WINO_ERR_CUDA;
+  if (prop.major != 10 || prop.minor != 0) return WINO_ERR_UNSUPPORTED;   // sm_100a cubin only
+  wino_status st = setup_device(device);
+  if (st != WINO_OK) return st;
+
+  wino_plan_s* p = new (std::nothrow) wino_plan_s;
+  if (!p) return WINO_ERR_NOMEM;
+  std::memset(p, 0, sizeof(*p));
+  p->d = d;
+  p->device = device;
+  wino::Geom& g = p->g;
+  g.n = d.n; g.h = d.h; g.w = d.w; g.cin = d.c_in; g.cout = d.c_out; g.pad = d.pad; g.layout = d.layout;
+  g.ho = d.h + 2 * d.pad - 2;
+  g.wo = d.w + 2 * d.pad - 2;
+  g.th = (g.ho + 3) / 4;
+  g.tw = (g.wo + 3) / 4;
+  g.tpi = g.th * g.tw;
+  g.cin_pad = (int)round_up(d.c_in, wino::kKStep);
+  const int cout16 = (int)round_up(d.c_out, 16);
+  g.nblk = cout16 >= 64 ? 64 : cout16;
+  g.cout_pad = (int)round_up(d.c_out, g.nblk);
+  g.ksteps = g.cin_pad / wino::kKStep;
+  g.scaling = d.filter_scaling;
+  g.target = d.filter_target_max;
+  g.out_mode = d.out_mode;
+  // batch chunk: V + M of one chunk within the L2-sized budget
+  const size_t per_img = (size_t)g.tpi * (2 * wino::kPlanes * (size_t)g.cin_pad + wino::kPlanes * 4 * (size_t)g.cout_pad);
+  long long imgs = (long long)(chunk_budget_bytes() / (per_img ? per_img : 1));
+  if (imgs < 1) imgs = 1;
+  if (imgs > d.n) imgs = d.n;
+  g.chunk_imgs = (int)imgs;
+  g.chunk_tiles_pad = round_up((long long)imgs * g.tpi, wino::kMBlock);
+  p->n_chunks = (int)((d.n + imgs - 1) / imgs);
+  p->v_bytes = (size_t)2 * wino::kPlanes * g.chunk_tiles_pad * g.cin_pad;
+  p->m_bytes = (size_t)wino::kPlanes * g.chunk_tiles_pad * g.cout_pad * 4;
+  p->ws_bytes = p->v_bytes + p->m_bytes;
+  p->f_bytes = (size_t)2 * wino::kPlanes * g.cout_pad * g.cin_pad;
+  p->x_bytes = (size_t)d.n * d.h * d.w * d.c_in;
+  p->y_bytes = (size_t)d.n * g.ho * g.wo * d.c_out * (d.out_mode == WINO_OUT_INT32 ? 4 : 1);
+  *out = p;
+  return WINO_OK;
+}
+
+wino_status wino_plan_destroy(wino_plan_t plan) {
+  if (!plan) return WINO_ERR_INVALID_ARG;
+  delete plan;
+  return WINO_OK;
+}
+
+wino_status wino_plan_query(wino_plan_t p, wino_plan_info* info) {
+  if (!p || !info) return WINO_ERR_INVALID_ARG;
+  std::memset(info, 0, sizeof(*info));
+  info->ho = p->g.ho; info->wo = p->g.wo;
+  info->tiles_h = p->g.th; info->tiles_w = p->g.tw;
+  info->tiles = (long long)p->d.n * p->g.tpi;
+  info->cin_pad = p->g.cin_pad; info->cout_pad = p->g.cout_pad;
+  info->n_block = p->g.nblk; info->m_block = wino::kMBlock;
+  info->planes = wino::kPlanes; info->pieces = wino::kPieces;
+  info->chunk_images = p->g.chunk_imgs; info->n_chunks = p->n_chunks;
+  info->chunk_tiles_pad = p->g.chunk_tiles_pad;
+  info->v_offset = 0; info->v_bytes = p->v_bytes;
+  info->m_offset = p->v_bytes; info->m_bytes = p->m_bytes;
+  info->workspace_bytes = p->ws_bytes;
+  info->filter_bytes = p->f_bytes;
+  info->codes_bytes = (size_t)p->d.c_out * 36;
+  info->x_bytes = p->x_bytes; info->y_bytes = p->y_bytes;
+  return WINO_OK;
+}
+
+size_t wino_filter_bytes(wino_plan_t p) { return p ? p->f_bytes : 0; }
+size_t wino_codes_bytes(wino_plan_t p) { return p ? (size_t)p->d.c_out * 36 : 0; }
+size_t wino_workspace_bytes(wino_plan_t p) { return p ? p->ws_bytes : 0; }
+size_t wino_output_bytes(wino_plan_t p) { return p ? p->y_bytes : 0; }
+
+wino_status wino_transform_filter(wino_plan_t p, const int8_t* w, void* w_wino, uint8_t* codes, void* stream) {
+  if (!p || !w || !w_wino || !codes) return WINO_ERR_INVALID_ARG;
+  if (!aligned16(w_wino)) return WINO_ERR_INVALID_ARG;
+  wino_status st = check_device(p);
+  if (st != WINO_OK) return st;
+  cudaError_t e = wino::launch_filter_transform(p->g, w, static_cast<int8_t*>(w_wino), codes,
+                                                static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? WINO_OK : WINO_ERR_CUDA;
+}
+
+wino_status wino_conv2d_int8(wino_plan_t p, const int8_t* x, const void* w_wino, const uint8_t* codes,
+                             int32_t rq_mult, int rq_shift, void* y, void* workspace, void* stream) {
+  if (!p || !x || !w_wino || !codes || !y || !workspace) return WINO_ERR_INVALID_ARG;
+  if (!aligned16(x) || !aligned16(w_wino) || !aligned16(y) || !aligned16(workspace)) return WINO_ERR_INVALID_ARG;
+  if (p->d.out_mode == WINO_OUT_INT8 && (rq_mult < 1 || rq_shift < 0 || rq_shift > 62)) return WINO_ERR_RANGE;
+  wino_status st = check_device(p);
+  if (st != WINO_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int8_t* vimg = static_cast<int8_t*>(workspace);
+  int32_t* m = reinterpret_cast<int32_t*>(static_cast<int8_t*>(workspace) + p->v_bytes);
+  const wino::Geom& g = p->g;
+  for (int n0 = 0; n0 < p->d.n; n0 += g.chunk_imgs) {
+    const int imgs = p->d.n - n0 < g.chunk_imgs ? p->d.n - n0 : g.chunk_imgs;
+    const long long tiles_pad = round_up((long long)imgs * g.tpi, wino::kMBlock);
+    cudaError_t e = wino::launch_input_transform(g, x, n0, imgs, vimg, s);
+    if (e == cudaSuccess) e = wino::launch_gemm(g, tiles_pad, vimg, static_cast<const int8_t*>(w_wino), m, s);
+    if (e == cudaSuccess) e = wino::launch_output_transform(g, m, codes, n0, imgs, rq_mult, rq_shift, y, s);
+    if (e != cudaSuccess) return WINO_ERR_CUDA;
+  }
+  return WINO_OK;
+}
+
+wino_status wino_conv2d_int8_host(wino_plan_t p, const int8_t* x_host, const void* w_wino, const uint8_t* codes,
+                                  int32_t rq_mult, int rq_shift, void* y_host, int8_t* x_dev, void* y_dev,
+                                  void* workspace, void* stream) {
+  if (!p || !x_host || !y_host || !x_dev || !y_dev) return WINO_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(x_dev, x_host, p->x_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return WINO_ERR_CUDA;
+  wino_status st = wino_conv2d_int8(p, x_dev, w_wino, codes, rq_mult, rq_shift, y_dev, workspace, stream);
+  if (st != WINO_OK) return st;
+  if (cudaMemcpyAsync(y_host, y_dev, p->y_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return WINO_ERR_CUDA;
+  return WINO_OK;
+}
+
+wino_status wino_check_codes(wino_plan_t p, const uint8_t* codes, int32_t* bad_flag, void* stream) {
+  if (!p || !codes || !bad_flag) return WINO_ERR_INVALID_ARG;
+  cudaError_t e = wino::launch_check_codes(codes, p->d.c_out * 36, bad_flag, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? WINO_OK : WINO_ERR_CUDA;
+}
+
+wino_status wino_maxpool2_int8(const int8_t* x, int n, int h, int w, int c, int layout, int8_t* y, void* stream) {
+  if (!x || !y || n < 1 || h < 2 || w < 2 || c < 1) return WINO_ERR_INVALID_ARG;
+  if (layout != WINO_NCHW && layout != WINO_NHWC) return WINO_ERR_INVALID_ARG;
+  cudaError_t e = wino::launch_maxpool2(x, n, h, w, c, layout, y, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? WINO_OK : WINO_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+"""Test-side decoding of the documented HBM layouts (DESIGN.md "HBM layout",
+csrc/layout.cuh comment) and of the oracle's complex values into the 46
+plane order.  Pure indexing -- no method arithmetic beyond the trivial
+Karatsuba sum re+im that defines the third plane of each pair."""
+import numpy as np
+
+R = [0, 1, 2, 5]
+REAL_POS = [r * 6 + c for r in R for c in R]
+CPX_POS = [0 * 6 + 3, 1 * 6 + 3, 2 * 6 + 3, 5 * 6 + 3, 3 * 6 + 0, 3 * 6 + 1, 3 * 6 + 2, 3 * 6 + 5, 3 * 6 + 3,
+           3 * 6 + 4]
+
+
+def tiled_offset(r, k, R_rows):
+    r = np.asarray(r, np.int64); k = np.asarray(k, np.int64)
+    return (k >> 5) * R_rows * 32 + (r >> 3) * 256 + ((k >> 4) & 1) * 128 + (r & 7) * 16 + (k & 15)
+
+
+def decode_pieces(buf: np.ndarray, rows: int, R_rows: int, ksteps: int, cin: int, pp_stride: int):
+    """buf: int8 image.  Returns int array [46][rows][cin] of hi*256 + lo."""
+    r = np.arange(rows)[:, None]; k = np.arange(cin)[None, :]
+    off = (r // R_rows) * ksteps * R_rows * 32 + tiled_offset(r % R_rows, k, R_rows)
+    out = np.zeros((46, rows, cin), np.int64)
+    for pl in range(46):
+        hi = buf[2 * pl * pp_stride + off].astype(np.int64)
+        lo = buf[(2 * pl + 1) * pp_stride + off].astype(np.int64) & 255
+        out[pl] = hi * 256 + lo
+    return out
+
+
+def complex_to_planes(Z: np.ndarray) -> np.ndarray:
+    """Z [..., 36, 2] (re, im per position) -> [46, ...] plane values."""
+    planes = [Z[..., p, 0] for p in REAL_POS]
+    for p in CPX_POS:
+        re, im = Z[..., p, 0], Z[..., p, 1]
+        planes += [re, im, re + im]
+    return np.stack(planes, 0)
+
+
+def karatsuba_planes_to_complex(Mp: np.ndarray):
+    """GPU per-plane int32 results [46, ...] -> (real [16, ...], re [10, ...], im [10, ...]) as int32 wrap."""
+    Mp = Mp.astype(np.int64)
+    real = Mp[:16]
+    p0, p1, p2 = Mp[16::3], Mp[17::3], Mp[18::3]
+    wrap = lambda v: ((v + 2 ** 31) % 2 ** 32) - 2 ** 31
+    return wrap(real), wrap(p0 - p1), wrap(p2 - p0 - p1)

@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle,
+element by element on the same seeded inputs.  Integer work => bit-exact."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import oracle as O
+import layout_decode as LD
+
+pytestmark = pytest.mark.gpu
+
+
+def _wino():
+    import paper_1901_01965_b200 as W
+    return W
+
+
+def _run(x, w, layout, pad=1, scaling=True, out_mode=1, M0=1, S=0, chunk_mb=None):
+    W = _wino()
+    if chunk_mb is not None:
+        os.environ["WINO_CHUNK_MB"] = str(chunk_mb)
+    try:
+        if layout == O.NCHW:
+            n, ci, h, wd = x.shape
+        else:
+            n, h, wd, ci = x.shape
+        co = w.shape[0]
+        conv = W.WinoConv2d(n, h, wd, ci, co, pad, layout, scaling, out_mode)
+    finally:
+        os.environ.pop("WINO_CHUNK_MB", None)
+    xd = torch.from_numpy(x).cuda(); wdv = torch.from_numpy(w).cuda()
+    conv.transform_filter(wdv)
+    y = conv(xd, M0, S)
+    torch.cuda.synchronize()
+    return conv, y.cpu().numpy()
+
+
+def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates=True):
+    conv, y32 = _run(x, w, layout, pad, scaling, 1, chunk_mb=chunk_mb)
+    ref = O.wino_conv(x, w, pad, layout, scaling=scaling, want_M=intermediates)
+    np.testing.assert_array_equal(y32, ref.out32)
+    if not scaling:
+        np.testing.assert_array_equal(y32.astype(np.int64), O.direct_conv(x, w, pad, layout))
+    if intermediates:
+        info = conv.info
+        co, ci = w.shape[0], (w.shape[1] if layout == O.NCHW else w.shape[3])
+        # K1: codes and W' operand planes, byte exact
+        _, Wp, codes = O.filter_transform(w, layout, scaling=scaling)
+        np.testing.assert_array_equal(conv.codes.cpu().numpy(), codes)
+        wbuf = conv.w_wino.cpu().numpy()
+        wpl = LD.decode_pieces(wbuf, info.cout_pad, info.n_block, info.cin_pad // 32, info.cin_pad,
+                               info.cout_pad * info.cin_pad)
+        np.testing.assert_array_equal(wpl[:, :co, :ci], LD.complex_to_planes(Wp))
+        assert not wpl[:, co:, :].any() and not wpl[:, :, ci:].any()
+        if info.n_chunks == 1:
+            # K2: V planes of every tile, byte exact
+            T = int(info.tiles)
+            vbuf = conv.v_image().cpu().numpy()
+            vpl = LD.decode_pieces(vbuf, T, 128, info.cin_pad // 32, info.cin_pad,
+                                   info.chunk_tiles_pad * info.cin_pad)
+            D = O.input_transform(x, pad, layout)
+            np.testing.assert_array_equal(vpl[:, :, :ci], LD.complex_to_planes(D))
+            # K3: per-plane GEMM results recombined (Karatsuba) == oracle M (pre reverse scaling)
+            mp = conv.m_planes().cpu().numpy()[:, :T, :co]
+            real, re, im = LD.karatsuba_planes_to_complex(mp)
+            Mo = ref.M.transpose(2, 0, 1, 3)        # [36][T][co][2]
+            np.testing.assert_array_equal(real, Mo[LD.REAL_POS, :, :, 0])
+            np.testing.assert_array_equal(re, Mo[LD.CPX_POS, :, :, 0])
+            np.testing.assert_array_equal(im, Mo[LD.CPX_POS, :, :, 1])
+    return conv
+
+
+@pytest.mark.parametrize("layout", [O.NHWC, O.NCHW])
+@pytest.mark.parametrize("scaling", [False, True])
+def test_c1_all_stages(layout, scaling):
+    """BASELINE configs[0]: batch 1, 8x8, 4->4, scaling off then on; every
+    kernel's output (codes, W', V, M, y) against the oracle."""
+    x, w = synth.config_inputs("C1", layout)
+    _check_layer(x, w, layout, 1, scaling)
+
+
+@pytest.mark.parametrize("case", [
+    # n, h, w, cin, cout, pad, layout    -- ragged maps, several tile / cout blocks, K tails
+    (2, 40, 37, 17, 70, 1, O.NHWC),
+    (1, 23, 30, 64, 16, 0, O.NHWC),
+    (3, 13, 9, 3, 5, 1, O.NCHW),
+    (1, 3, 3, 1, 1, 0, O.NHWC),
+    (2, 1, 1, 2, 3, 1, O.NCHW),
+    (1, 57, 11, 40, 33, 1, O.NCHW),
+    (4, 18, 18, 96, 128, 1, O.NHWC),
+])
+@pytest.mark.parametrize("scaling", [False, True])
+def test_random_shapes_all_stages(case, scaling):
+    n, h, wd, ci, co, pad, layout = case
+    rng = np.random.default_rng(hash((case, scaling)) % 2 ** 32)
+    x, w = synth.random_layer(rng, n, h, wd, ci, co, layout)
+    _check_layer(x, w, layout, pad, scaling)
+
+
+@pytest.mark.parametrize("xv,wv", [(-128, -128), (127, 127), (-128, 127)])
+@pytest.mark.parametrize("scaling", [False, True])
+def test_extremes(xv, wv, scaling):
+    x = np.full((2, 12, 13, 40), xv, np.int8); w = np.full((24, 3, 3, 40), wv, np.int8)
+    _check_layer(x, w, O.NHWC, 1, scaling)
+
+
+def test_multi_chunk_matches_single_chunk():
+    rng = np.random.default_rng(77)
+    x, w = synth.random_layer(rng, 7, 20, 20, 32, 48, O.NHWC)
+    conv, y = _run(x, w, O.NHWC, scaling=True, chunk_mb=1)
+    assert conv.info.n_chunks > 1
+    np.testing.assert_array_equal(y, O.wino_conv(x, w, 1, O.NHWC, scaling=True).out32)
+
+
+@pytest.mark.parametrize("layout", [O.NHWC, O.NCHW])
+def test_int8_requant_output(layout):
+    rng = np.random.default_rng(5)
+    x, w = synth.random_layer(rng, 2, 15, 14, 24, 20, layout)
+    for M0, S in [(1, 0), (1, 9), (3, 11), (7, 1)]:
+        _, y8 = _run(x, w, layout, scaling=True, out_mode=0, M0=M0, S=S)
+        ref = O.wino_conv(x, w, 1, layout, scaling=True, M0=M0, S=S)
+        np.testing.assert_array_equal(y8, ref.y8)
+
+
+def test_max_cin_unscaled_896_and_scaled_768():
+    rng = np.random.default_rng(9)
+    for ci, scaling in [(896, False), (768, True)]:
+        x = rng.integers(-128, 128, (1, 6, 7, ci)).astype(np.int8)
+        w = np.where(rng.integers(0, 2, (3, 3, 3, ci)) == 1, 127, -128).astype(np.int8)
+        _check_layer(x, w, O.NHWC, 1, scaling, intermediates=False)
+
+
+def test_plan_rejects():
+    W = _wino()
+    L = W._lib
+    bad = [dict(pad=2), dict(c_in=897, filter_scaling=0), dict(c_in=769, filter_scaling=1), dict(h=0),
+           dict(h=1, pad=0), dict(filter_target_max=127)]
+    for kw in bad:
+        d = dict(n=1, h=8, w=8, c_in=4, c_out=4, pad=1, layout=1, filter_scaling=1, filter_target_max=255,
+                 out_mode=0)
+        d.update(kw)
+        with pytest.raises(W.WinoError) as e:
+            L.wino_plan(L.wino_conv_desc(**d), 0)
+        assert e.value.status == L.WINO_ERR_UNSUPPORTED
+    d = L.wino_conv_desc(1, 8, 8, 4, 4, 1, 7, 1, 255, 0)
+    with pytest.raises(W.WinoError) as e:
+        L.wino_plan(d, 0)
+    assert e.value.status == L.WINO_ERR_INVALID_ARG
+
+
+def test_conv_rejects_bad_requant_and_null():
+    W = _wino()
+    conv = W.WinoConv2d(1, 8, 8, 4, 4, 1, W.WINO_NHWC, True, W.WINO_OUT_INT8)
+    x = torch.zeros(conv.x_shape, dtype=torch.int8, device="cuda")
+    with pytest.raises(W.WinoError) as e:
+        conv(x, requant_mult=0, requant_shift=3)
+    assert e.value.status == W._lib.WINO_ERR_RANGE
+    with pytest.raises(W.WinoError):
+        W._lib.wino_conv2d_int8(conv.plan, 0, conv.w_wino.data_ptr(), conv.codes.data_ptr(), 1, 0, 0,
+                                conv.workspace.data_ptr(), 0)
+
+
+def test_host_entry_point_matches_device_path():
+    W = _wino()
+    x, w = synth.config_inputs("C2", n=3)
+    conv = W.WinoConv2d(3, 56, 56, 64, 64, 1, W.WINO_NHWC, True, W.WINO_OUT_INT8)
+    conv.transform_filter(torch.from_numpy(w).cuda())
+    S = synth.requant_shift(synth.CONFIGS["C2"].layers[0])
+    y_dev = conv(torch.from_numpy(x).cuda(), 1, S)
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.empty(conv.y_shape, dtype=torch.int8).pin_memory()
+    xd = torch.empty(conv.x_shape, dtype=torch.int8, device="cuda")
+    yd = torch.empty(conv.y_shape, dtype=torch.int8, device="cuda")
+    conv.call_host(xh, yh, xd, yd, 1, S)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(yh.numpy(), y_dev.cpu().numpy())
+    np.testing.assert_array_equal(yh.numpy(), O.wino_conv(x, w, 1, O.NHWC, True, M0=1, S=S).y8)
+
+
+def test_check_codes_and_maxpool():
+    W = _wino()
+    conv = W.WinoConv2d(1, 8, 8, 4, 4, 1, W.WINO_NHWC, True, W.WINO_OUT_INT8)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    codes = torch.zeros((4, 36), dtype=torch.uint8, device="cuda"); codes[1, 3] = 8 << 2 | 1
+    W._lib.wino_check_codes(conv.plan, codes.data_ptr(), bad.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert bad.item() == 0
+    codes[2, 5] = 5 << 2
+    W._lib.wino_check_codes(conv.plan, codes.data_ptr(), bad.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert bad.item() == 1
+    rng = np.random.default_rng(1)
+    for layout in (O.NHWC, O.NCHW):
+        x = rng.integers(-128, 128, (2, 10, 12, 7)).astype(np.int8)
+        if layout == O.NCHW:
+            x = np.ascontiguousarray(x.transpose(0, 3, 1, 2))
+        y = W.maxpool2(torch.from_numpy(x).cuda(), layout).cpu().numpy()
+        np.testing.assert_array_equal(y, O.maxpool2(x, layout))
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_full_size_configs_sampled(name):
+    """Full BASELINE sizes in the bench launch configuration (NHWC, int8 out,
+    default chunking); whole images sampled (first, middle, last) and compared
+    bit-exactly with the oracle run on those images alone."""
+    W = _wino()
+    layer = synth.CONFIGS[name].layers[0]
+    x, w = synth.config_inputs(name)
+    S = synth.requant_shift(layer)
+    conv = W.WinoConv2d(layer.n, layer.h, layer.w, layer.c_in, layer.c_out, 1, W.WINO_NHWC, True,
+                        W.WINO_OUT_INT8)
+    conv.transform_filter(torch.from_numpy(w).cuda())
+    y = conv(torch.from_numpy(x).cuda(), 1, S).cpu().numpy()
+    for i in sorted({0, layer.n // 2, layer.n - 1}):
+        ref = O.wino_conv(x[i:i + 1], w, 1, O.NHWC, True, M0=1, S=S)
+        np.testing.assert_array_equal(y[i:i + 1], ref.y8)
+    # codes computed on the device equal the oracle's
+    np.testing.assert_array_equal(conv.codes.cpu().numpy(), O.filter_transform(w, O.NHWC, True)[2])
