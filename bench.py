@@ -1,0 +1,444 @@
+"""Benchmark of the complex-Winograd int8 3x3 conv hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One step = the whole hot path over one batch of
+synthetic input: filter transform + scaling (K1) and the convolution
+(K2 input transform -> K3 tcgen05 GEMMs -> K4 output transform, per chunk).
+Weak scaling: every rank runs its own batch of the configuration (data
+parallel by batch, no collective on the data path).  Inputs and weights are
+rotated over enough distinct sets that they never stay resident in the 126 MB
+L2 between steps.  Rank 0 prints one JSON line.
+
+`--impl reference` times the CPU oracle (oracle/, plain C) on the host cores,
+one bounded sample of the same workload per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "int8 3x3 conv effective TOPS (direct-conv ops/s)"
+L2_BYTES = 126 * 2 ** 20
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def _peaks():
+    p = {}
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    return {
+        "hbm_gbs": float(p.get("hbm_gbs", 6650.0)),
+        "bf16_tflops": float(p.get("bf16_tflops", 1590.0)),
+        "bf16_tflops_sustained": float(p.get("bf16_tflops_sustained", 1400.0)),
+        "source": "MEASURED_PEAKS.json (measured)" if p else "B200_PROFILING.md fallback",
+    }
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML while running."""
+
+    def __init__(self, dev_index: int, period_s: float = 0.01):
+        self.dev_index, self.period = dev_index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            self.err = str(e)
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+            "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_01965_b200 as W
+    from paper_1901_01965_b200 import _lib as L
+
+    rank, local_rank, world = _env_rank()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = synth.CONFIGS[args.config]
+    layer = cfg.layers[0]
+    S = synth.requant_shift(layer)
+    conv = W.WinoConv2d(layer.n, layer.h, layer.w, layer.c_in, layer.c_out, layer.pad, W.WINO_NHWC, layer.scaling,
+                        W.WINO_OUT_INT8, device=local_rank)
+    info = conv.info
+    x_bytes, y_bytes = info.x_bytes, info.y_bytes
+    w_bytes = layer.c_out * 9 * layer.c_in
+    per_set = x_bytes + w_bytes + y_bytes
+    n_sets = max(2, math.ceil(1.2 * L2_BYTES / per_set))
+    xs, ws, ys = [], [], []
+    for i in range(n_sets):
+        # first set: the seeded config tensors; later sets: re-seeded batches of the same recipe
+        x, w = synth.config_inputs(args.config, rank=rank * 1000 + i)
+        xs.append(torch.from_numpy(x).to(dev)); ws.append(torch.from_numpy(w).to(dev))
+        ys.append(torch.empty(conv.y_shape, dtype=torch.int8, device=dev))
+    stream = torch.cuda.Stream(device=dev)
+    sp = stream.cuda_stream
+    w_wino, codes, wsp = conv.w_wino.data_ptr(), conv.codes.data_ptr(), conv.workspace.data_ptr()
+
+    def step(i):
+        j = i % n_sets
+        L.wino_transform_filter(conv.plan, ws[j].data_ptr(), w_wino, codes, sp)
+        L.wino_conv2d_int8(conv.plan, xs[j].data_ptr(), w_wino, codes, 1, S, ys[j].data_ptr(), wsp, sp)
+
+    launches_per_step = 1 + 3 * info.n_chunks
+    # CUDA graphs: one per rotation slot (launch-bound otherwise)
+    graphs = []
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+        stream.synchronize()
+        if not args.no_graph:
+            for j in range(n_sets):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    step(j)
+                graphs.append(g)
+            for j in range(max(args.warmup, 3)):
+                graphs[j % n_sets].replay()
+            stream.synchronize()
+
+    def run_steps(k, offset=0):
+        with torch.cuda.stream(stream):
+            for i in range(k):
+                if graphs:
+                    graphs[(i + offset) % n_sets].replay()
+                else:
+                    step(i + offset)
+
+    # ---------------- timed region
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        run_steps(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_local = ev0.elapsed_time(ev1) / 1e3
+    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    ops_step = synth.direct_ops(layer)
+    value = world * ops_step * args.steps / t_max / 1e12
+
+    # ---------------- per-kernel durations (roofline), same stream, outside the timed region
+    kern = profile_kernels(conv, xs, ws, ys, S, stream, n_sets, max(10, min(args.steps, 200)))
+    # ---------------- e2e through the C ABI with host buffers (pinned), copies inside the region
+    e2e = run_e2e(conv, xs, ws, S, stream, n_sets, max(3, min(args.steps, 100)), world, dist if world > 1 else None,
+                  dev)
+
+    if rank == 0:
+        peaks = _peaks()
+        roof = roofline(kern, info, layer, peaks)
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_max * 1e3 / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "config": {
+                "workload": f"{cfg.name}: {cfg.description}", "batch_per_gpu": layer.n, "h": layer.h, "w": layer.w,
+                "c_in": layer.c_in, "c_out": layer.c_out, "pad": layer.pad, "layout": "NHWC",
+                "filter_scaling": layer.scaling, "output": f"int8 requantised (M0=1, S={S})",
+                "step": "filter transform + scaling (K1) + conv (K2,K3,K4 per chunk)",
+                "l2": f"inputs/weights/outputs rotated over {n_sets} sets "
+                      f"({n_sets * per_set / 2 ** 20:.0f} MiB > 126 MiB L2)",
+                "parallelism": f"dp{world} (batch-sharded, weak scaling, no data-path collective)",
+                "chunks": info.n_chunks, "cuda_graph": bool(graphs),
+            },
+            "roofline": roof["dominant"],
+            "kernels": roof["all"],
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+        }
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps):
+    """Average device duration of each kernel type (events on the launching stream)."""
+    import torch
+    from paper_1901_01965_b200 import _lib as L
+    info = conv.info
+    sp = stream.cuda_stream
+    names = {1: "k1_filter", 2: "k2_input", 3: "k3_gemm", 4: "k4_output"}
+    acc = {k: [] for k in names}
+    w_wino, codes, wsp = conv.w_wino.data_ptr(), conv.codes.data_ptr(), conv.workspace.data_ptr()
+    with torch.cuda.stream(stream):
+        for r in range(reps):
+            j = r % n_sets
+            evs = []
+            e = torch.cuda.Event(enable_timing=True); e.record(stream); evs.append((1, e))
+            L.wino_transform_filter(conv.plan, ws[j].data_ptr(), w_wino, codes, sp)
+            e2 = torch.cuda.Event(enable_timing=True); e2.record(stream)
+            marks = [(1, e, e2)]
+            for c in range(info.n_chunks):
+                for st in (2, 3, 4):
+                    a = torch.cuda.Event(enable_timing=True); a.record(stream)
+                    L.wino_conv2d_int8_stage(conv.plan, st, c, xs[j].data_ptr(), w_wino, codes, 1, S,
+                                             ys[j].data_ptr(), wsp, sp)
+                    b = torch.cuda.Event(enable_timing=True); b.record(stream)
+                    marks.append((st, a, b))
+            stream.synchronize()
+            for st, a, b in marks:
+                acc[st].append(a.elapsed_time(b) / 1e3)
+    out = {}
+    for st, v in acc.items():
+        per_launch = float(np.median(v))
+        count = 1 if st == 1 else info.n_chunks
+        out[names[st]] = {"s_per_launch": per_launch, "launches_per_step": count, "s_per_step": per_launch * count}
+    return out
+
+
+def roofline(kern, info, layer, peaks):
+    """Algorithmic work per launch against the measured peaks."""
+    T = info.tiles
+    chunk_tiles = min(info.chunk_images, layer.n) * info.tiles_h * info.tiles_w
+    nch = info.n_chunks
+    hbm = peaks["hbm_gbs"]
+    i8_sus = 2.0 * peaks["bf16_tflops_sustained"]   # int8 dense = 2 x bf16 (nominal ratio 4.5/2.25)
+    x_chunk = chunk_tiles * 16 * layer.c_in        # ~ bytes of x per chunk (16 px per tile)
+    res = {}
+    # K1: reads w (9 Cin Cout B), writes W' image (92 Cin_pad Cout_pad B) + codes
+    k1_bytes = 9 * layer.c_in * layer.c_out + info.filter_bytes + 36 * layer.c_out
+    # K2: reads x of the chunk, writes V (92 B per tile and channel)
+    k2_bytes = x_chunk + 92 * chunk_tiles * info.cin_pad
+    # K3: 46 general multiplies per (tile, cin, cout) = the paper's count, 2 ops each
+    k3_ops = 2 * 46 * chunk_tiles * layer.c_in * layer.c_out
+    k3_bytes = 92 * chunk_tiles * info.cin_pad + 46 * 4 * chunk_tiles * info.cout_pad + info.filter_bytes
+    # K4: reads 46 int32 per (tile, cout), writes y int8
+    k4_bytes = 46 * 4 * chunk_tiles * layer.c_out + chunk_tiles * 16 * layer.c_out
+    spec = {
+        "k1_filter": ("hbm", k1_bytes, hbm, "GB/s"),
+        "k2_input": ("hbm", k2_bytes, hbm, "GB/s"),
+        "k3_gemm": ("tensor", k3_ops, i8_sus, "TOPS"),
+        "k4_output": ("hbm", k4_bytes, hbm, "GB/s"),
+    }
+    all_k = {}
+    for name, (bound, work, peak, unit) in spec.items():
+        t = kern[name]["s_per_launch"]
+        achieved = work / t / (1e9 if unit == "GB/s" else 1e12)
+        d = {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": unit,
+             "frac": round(achieved / peak, 4), "traffic": None, "us_per_launch": round(t * 1e6, 3),
+             "launches_per_step": kern[name]["launches_per_step"],
+             "share_of_step": None, "algorithmic_per_launch": work}
+        if name == "k3_gemm":
+            d["hbm_view"] = {"bytes_per_launch": k3_bytes, "achieved_gbs": round(k3_bytes / t / 1e9, 1),
+                             "frac_of_hbm": round(k3_bytes / t / 1e9 / hbm, 4)}
+        all_k[name] = d
+    tot = sum(kern[k]["s_per_step"] for k in kern)
+    for k in all_k:
+        all_k[k]["share_of_step"] = round(kern[k]["s_per_step"] / tot, 4)
+    dom = max(all_k, key=lambda k: kern[k]["s_per_step"])
+    dominant = dict(all_k[dom]); dominant["kernel"] = dom
+    dominant["peak_source"] = peaks["source"] + (
+        "; int8 = 2 x bf16 sustained" if dom == "k3_gemm" else "; hbm_gbs")
+    return {"dominant": dominant, "all": all_k}
+
+
+def run_e2e(conv, xs, ws, S, stream, n_sets, reps, world, dist, dev):
+    """Same metric through the C ABI with HOST buffers: every step copies x and w
+    from pinned host memory, runs K1..K4, and reads y back to pinned host memory."""
+    import torch
+    from paper_1901_01965_b200 import _lib as L
+    info = conv.info
+    sp = stream.cuda_stream
+    k = min(n_sets, 8)
+    xh = [xs[i].cpu().pin_memory() for i in range(k)]
+    wh = [ws[i].cpu().pin_memory() for i in range(k)]
+    yh = [torch.empty(conv.y_shape, dtype=torch.int8).pin_memory() for _ in range(k)]
+    xd = torch.empty(conv.x_shape, dtype=torch.int8, device=dev)
+    yd = torch.empty(conv.y_shape, dtype=torch.int8, device=dev)
+    wd = torch.empty(conv.w_shape, dtype=torch.int8, device=dev)
+    w_wino, codes, wsp = conv.w_wino.data_ptr(), conv.codes.data_ptr(), conv.workspace.data_ptr()
+
+    def step(i):
+        j = i % k
+        wd.copy_(wh[j], non_blocking=True)
+        L.wino_transform_filter(conv.plan, wd.data_ptr(), w_wino, codes, sp)
+        L.wino_conv2d_int8_host(conv.plan, xh[j].data_ptr(), w_wino, codes, 1, S, yh[j].data_ptr(),
+                                xd.data_ptr(), yd.data_ptr(), wsp, sp)
+
+    with torch.cuda.stream(stream):
+        for i in range(3):
+            step(i)
+        stream.synchronize()
+        if dist is not None:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(reps):
+            step(i)
+        e1.record(stream)
+        stream.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    layer_ops = synth.direct_ops(synth.LayerCfg(conv.desc.n, conv.desc.h, conv.desc.w, conv.desc.c_in,
+                                                conv.desc.c_out, conv.desc.pad))
+    v = world * layer_ops * reps / float(t.item()) / 1e12
+    return {"value": round(v, 3), "unit": "TOPS", "h2d_bytes_per_step": int(info.x_bytes + np.prod(conv.w_shape)),
+            "d2h_bytes_per_step": int(info.y_bytes), "steps": reps,
+            "ms_per_step": round(float(t.item()) * 1e3 / reps, 4)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle arm
+def _oracle_sample(config, budget_s):
+    """A bounded sample of the workload for the CPU oracle: the first `rows`
+    output rows of one image (pad 1), sized to ~budget_s seconds."""
+    from oracle import oracle as O
+    layer = synth.CONFIGS[config].layers[0]
+    x, w = synth.config_inputs(config, n=1)
+    S = synth.requant_shift(layer)
+
+    def run(rows):
+        xs = np.ascontiguousarray(x[:, :rows])
+        t0 = time.perf_counter()
+        O.wino_conv(xs, w, layer.pad, O.NHWC, scaling=layer.scaling, M0=1, S=S)
+        return time.perf_counter() - t0
+
+    rows = min(layer.h, 4)
+    dt = run(rows)
+    while rows < layer.h and dt < budget_s / 3:
+        rows = min(layer.h, rows * 2)
+        dt = run(rows)
+    ops = synth.direct_ops(synth.LayerCfg(1, rows, layer.w, layer.c_in, layer.c_out, layer.pad))
+    return run, rows, ops, dt
+
+
+def cpu_baseline(config, budget_s=10.0):
+    import oracle.oracle as O
+    O.build()
+    run, rows, ops, _ = _oracle_sample(config, budget_s / 2)
+    reps, t = 0, 0.0
+    while t < budget_s / 2 or reps < 1:
+        t += run(rows); reps += 1
+    cores = len(os.sched_getaffinity(0))
+    return {"value": round(ops * reps / t / 1e12, 6), "unit": "TOPS", "cores": cores, "kind": "oracle",
+            "sample": f"oracle.wino_conv (plain C, OpenMP {cores} threads) on image 0 rows 0..{rows - 1} "
+                      f"of {config} ({ops:.3e} direct ops) x {reps}; {t:.2f} s"}
+
+
+def run_reference(args):
+    rank, _, world = _env_rank()
+    if rank != 0:
+        return
+    import oracle.oracle as O
+    O.build()
+    per_step_budget = max(0.05, min(2.0, 120.0 / max(1, args.steps + args.warmup)))
+    run, rows, ops, _ = _oracle_sample(args.config, per_step_budget)
+    for _ in range(args.warmup):
+        run(rows)
+    t = 0.0
+    for _ in range(args.steps):
+        t += run(rows)
+    v = ops * args.steps / t / 1e12
+    cores = len(os.sched_getaffinity(0))
+    layer = synth.CONFIGS[args.config].layers[0]
+    cfg = synth.CONFIGS[args.config]
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "TOPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3 / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.description}", "batch_per_gpu": layer.n, "h": layer.h,
+                       "w": layer.w, "c_in": layer.c_in, "c_out": layer.c_out, "layout": "NHWC",
+                       "filter_scaling": layer.scaling},
+            "cpu_baseline": {"value": round(v, 6), "unit": "TOPS", "cores": cores, "kind": "oracle",
+                             "sample": f"per step: oracle.wino_conv on image 0 rows 0..{rows - 1} "
+                                       f"({ops:.3e} direct ops)"},
+            "e2e": {"value": round(v, 6), "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -65,7 +65,8 @@ enum { WINO_OUT_INT8 = 0, WINO_OUT_INT32 = 1 };
 
 typedef struct {
     int n, h, w;          /* batch and input spatial size, each >= 1                  */
-    int c_in, c_out;      /* 1 <= c_in <= 896 (int32 exactness, A23), c_out >= 1       */
+    int c_in, c_out;      /* 1 <= c_in <= 896 (768 scaled; int32 exactness, A23),
+                             1 <= c_out <= 2048                                       */
     int pad;              /* 0 or 1; h + 2 pad >= 3 and w + 2 pad >= 3                 */
     int layout;           /* WINO_NCHW or WINO_NHWC                                    */
     int filter_scaling;   /* 0: exact (codes all 0); 1: the paper's scheme */
@@ -90,7 +91,8 @@ typedef struct {
     int n_chunks;
     long long chunk_tiles_pad;  /* tiles per chunk rounded up to m_block               */
     size_t v_offset, v_bytes;   /* V  = B^T d B operand planes inside the workspace    */
-    size_t m_offset, m_bytes;   /* M  = per-plane int32 GEMM results                   */
+    size_t m_offset, m_bytes;   /* M'' = 36 int32 per (tile, cout) after Karatsuba and
+                                   reverse scaling: [36][chunk_tiles_pad][cout_pad]    */
     size_t workspace_bytes;
     size_t filter_bytes;        /* transformed-filter buffer (w_wino)                  */
     size_t codes_bytes;         /* c_out * 36 bytes                                    */
@@ -103,7 +105,7 @@ const char *wino_status_string(wino_status s);
 /* Validate `desc` and build an immutable plan for CUDA device `device`.
  * The plan holds host metadata only.  Returns WINO_ERR_UNSUPPORTED for
  * pad not in {0,1}, n/h/w/c < 1, h + 2 pad < 3 or w + 2 pad < 3,
- * c_in > 896, filter_target_max != 255, and WINO_ERR_INVALID_ARG for bad
+ * c_in > 896 (> 768 with filter_scaling), c_out > 2048, filter_target_max != 255, and WINO_ERR_INVALID_ARG for bad
  * enums or NULL pointers.  The device must be sm_100 (B200).            */
 wino_status wino_plan(const wino_conv_desc *desc, int device, wino_plan_t *out);
 wino_status wino_plan_destroy(wino_plan_t plan);
@@ -164,6 +166,19 @@ wino_status wino_conv2d_int8_host(wino_plan_t plan, const int8_t *x_host, const 
                                   const uint8_t *scale_codes, int32_t requant_mult,
                                   int requant_shift, void *y_host, int8_t *x_dev, void *y_dev,
                                   void *workspace, void *stream);
+
+/* Profiling / testing entry point: enqueue ONE kernel of the hot path for
+ * batch chunk `chunk` (0 <= chunk < wino_plan_info.n_chunks):
+ *   stage 2 = input transform (x -> V in the workspace),
+ *   stage 3 = Winograd-domain GEMMs (V, w_wino -> M in the workspace),
+ *   stage 4 = output transform (M, scale_codes -> y).
+ * Running stages 2, 3, 4 for every chunk in order is exactly
+ * wino_conv2d_int8.  Arguments as for wino_conv2d_int8; WINO_ERR_INVALID_ARG
+ * for a bad stage or chunk.                                               */
+wino_status wino_conv2d_int8_stage(wino_plan_t plan, int stage, int chunk, const int8_t *x,
+                                   const void *w_wino, const uint8_t *scale_codes,
+                                   int32_t requant_mult, int requant_shift, void *y,
+                                   void *workspace, void *stream);
 
 /* Device-side validation of a code table: writes 1 to *bad_flag (device
  * int32, caller-zeroed) if any of the c_out*36 codes is neither 0 nor a

@@ -18,7 +18,7 @@ WINO_OUT_INT8, WINO_OUT_INT32 = 0, 1
 # every symbol include/wino.h declares
 EXPORTS = ("wino_status_string", "wino_plan", "wino_plan_destroy", "wino_plan_query", "wino_filter_bytes",
            "wino_codes_bytes", "wino_workspace_bytes", "wino_output_bytes", "wino_transform_filter",
-           "wino_conv2d_int8", "wino_conv2d_int8_host", "wino_check_codes", "wino_maxpool2_int8")
+           "wino_conv2d_int8", "wino_conv2d_int8_host", "wino_conv2d_int8_stage", "wino_check_codes", "wino_maxpool2_int8")
 
 
 class wino_conv_desc(ctypes.Structure):
@@ -64,6 +64,8 @@ def lib():
         L.wino_transform_filter.argtypes = [P, P, P, P, P]; L.wino_transform_filter.restype = I
         L.wino_conv2d_int8.argtypes = [P, P, P, P, I32, I, P, P, P]; L.wino_conv2d_int8.restype = I
         L.wino_conv2d_int8_host.argtypes = [P, P, P, P, I32, I, P, P, P, P, P]; L.wino_conv2d_int8_host.restype = I
+        L.wino_conv2d_int8_stage.argtypes = [P, I, I, P, P, P, I32, I, P, P, P]
+        L.wino_conv2d_int8_stage.restype = I
         L.wino_check_codes.argtypes = [P, P, P, P]; L.wino_check_codes.restype = I
         L.wino_maxpool2_int8.argtypes = [P, I, I, I, I, I, P, P]; L.wino_maxpool2_int8.restype = I
         _lib = L
@@ -118,6 +120,13 @@ def wino_conv2d_int8_host(plan, x_host_ptr: int, w_wino_ptr: int, codes_ptr: int
     _check(lib().wino_conv2d_int8_host(plan, x_host_ptr, w_wino_ptr, codes_ptr, int(requant_mult),
                                        int(requant_shift), y_host_ptr, x_dev_ptr, y_dev_ptr, ws_ptr, stream),
            "wino_conv2d_int8_host")
+
+
+def wino_conv2d_int8_stage(plan, stage: int, chunk: int, x_ptr: int, w_wino_ptr: int, codes_ptr: int,
+                           requant_mult: int, requant_shift: int, y_ptr: int, ws_ptr: int, stream: int) -> None:
+    _check(lib().wino_conv2d_int8_stage(plan, int(stage), int(chunk), x_ptr, w_wino_ptr, codes_ptr,
+                                        int(requant_mult), int(requant_shift), y_ptr, ws_ptr, stream),
+           "wino_conv2d_int8_stage")
 
 
 def wino_check_codes(plan, codes_ptr: int, bad_ptr: int, stream: int) -> None:

@@ -72,10 +72,12 @@ class WinoConv2d:
     def v_image(self):
         return self.workspace[self.info.v_offset:self.info.v_offset + self.info.v_bytes]
 
-    def m_planes(self):
+    def m_slots(self):
+        """M'' of the last chunk: [36][chunk_tiles_pad][cout_pad] int32 (after
+        Karatsuba recombination and reverse scaling)."""
         i = self.info
         return self.workspace[i.m_offset:i.m_offset + i.m_bytes].view(torch.int32).view(
-            i.planes, i.chunk_tiles_pad, i.cout_pad)
+            36, i.chunk_tiles_pad, i.cout_pad)
 
 
 def maxpool2(x: torch.Tensor, layout=L.WINO_NHWC, stream=None):

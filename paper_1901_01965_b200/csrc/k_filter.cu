@@ -2,13 +2,8 @@
 // paper's per-(OFM, position) integer scale factors, downscale, Karatsuba
 // operand planes and int8 piece split.
 //
-// One CTA per output channel (the unit the paper scales, P:312: "applied to
-// the filters used to generate one output feature map").  Each thread
-// transforms a strided subset of the input channels into shared memory
-// (36 int16 per channel: 16 real values + 10 complex primaries as re,im),
-// the CTA reduces the per-position max magnitude across channels, threads
-// 0..25 derive the 6-bit codes, and every thread then writes its channels'
-// scaled, split operand bytes into the pre-tiled W image.
+// One warp per output channel (see k_filter_transform); the transform is
+// recomputed in the second pass instead of being stored.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -64,117 +59,134 @@ __device__ __forceinline__ int rha_mul_shift(int v, int n, int p) {  // rha(v n 
   return prod < 0 ? -r : r;
 }
 
-__global__ void __launch_bounds__(256) k_filter_transform(Geom g, const int8_t* __restrict__ w,
-                                                          int8_t* __restrict__ wimg, uint8_t* __restrict__ codes) {
-  extern __shared__ int16_t s_w[];      // [cin][36]
-  __shared__ int s_max[8][26];
+constexpr int kFilterWarps = 4;   // warps per CTA; one CTA per output channel
+
+// Scaled operand planes of one (cout, cin) filter: 46 values.
+__device__ __forceinline__ void scaled_planes(const int t[36], const int* sn, const int* sp, int vals[46]) {
+#pragma unroll
+  for (int s = 0; s < 16; s++) vals[s] = sn[s] ? rha_mul_shift(t[s], sn[s], sp[s]) : t[s];   // W' = rha(W n / 2^p)
+#pragma unroll
+  for (int k = 0; k < 10; k++) {
+    const int n = sn[16 + k], p = sp[16 + k];
+    const int re = n ? rha_mul_shift(t[16 + 2 * k], n, p) : t[16 + 2 * k];
+    const int im = n ? rha_mul_shift(t[17 + 2 * k], n, p) : t[17 + 2 * k];
+    vals[16 + 3 * k + 0] = re;
+    vals[16 + 3 * k + 1] = im;
+    vals[16 + 3 * k + 2] = re + im;
+  }
+}
+
+__device__ __forceinline__ void load_filter(const Geom& g, const int8_t* __restrict__ w, int co, int ci, int gg[3][3]) {
+#pragma unroll
+  for (int u = 0; u < 3; u++)
+#pragma unroll
+    for (int v = 0; v < 3; v++)
+      gg[u][v] = g.layout == 0 ? w[((long long)co * g.cin + ci) * 9 + u * 3 + v]
+                               : w[((long long)co * 9 + u * 3 + v) * g.cin + ci];
+}
+
+// One CTA per output channel (the unit the paper scales, P:312: "applied to
+// the filters used to generate one output feature map"), channels split over
+// its warps.
+//   pass 1: transform every input channel (thread-strided), max magnitude per
+//           position across channels, codes (P:322-330 read as A3);
+//   pass 2: per 32-channel group (one per warp), recompute, scale, split and
+//           stage the 92 operand bytes per channel in shared memory, then write
+//           whole 16-byte rows of the pre-tiled W image.
+__global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, const int8_t* __restrict__ w,
+                                                                         int8_t* __restrict__ wimg,
+                                                                         uint8_t* __restrict__ codes) {
+  __shared__ __align__(16) int8_t s_stage[kFilterWarps][2 * kPlanes][32];
+  __shared__ int s_max[kFilterWarps][26];
   __shared__ int s_n[26], s_p[26];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int co = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool live = co < g.cout;
 
   int mx[26];
 #pragma unroll
   for (int i = 0; i < 26; i++) mx[i] = 0;
   if (live) {
-    for (int ci = tid; ci < g.cin; ci += blockDim.x) {
-      int gg[3][3];
-#pragma unroll
-      for (int u = 0; u < 3; u++)
-#pragma unroll
-        for (int v = 0; v < 3; v++)
-          gg[u][v] = g.layout == 0 ? w[((long long)co * g.cin + ci) * 9 + u * 3 + v]
-                                   : w[((long long)co * 9 + u * 3 + v) * g.cin + ci];
-      int t[36];
+    for (int ci = threadIdx.x; ci < g.cin; ci += blockDim.x) {
+      int gg[3][3], t[36];
+      load_filter(g, w, co, ci, gg);
       filter_tile_transform(gg, t);
-#pragma unroll
-      for (int i = 0; i < 36; i++) s_w[ci * 36 + i] = (int16_t)t[i];
 #pragma unroll
       for (int s = 0; s < 16; s++) mx[s] = max(mx[s], abs(t[s]));
 #pragma unroll
       for (int k = 0; k < 10; k++) mx[16 + k] = max(mx[16 + k], max(abs(t[16 + 2 * k]), abs(t[17 + 2 * k])));
     }
   }
-  // max over input channels per position
 #pragma unroll
   for (int i = 0; i < 26; i++) {
-    int v = mx[i];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) s_max[warp][i] = v;
+    for (int o = 16; o > 0; o >>= 1) mx[i] = max(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
+    if (lane == 0) s_max[warp][i] = mx[i];
   }
   __syncthreads();
-  if (tid < 26) {
+  if (threadIdx.x < 26) {
     int m = 0;
-    for (int wv = 0; wv < (int)(blockDim.x >> 5); wv++) m = max(m, s_max[wv][tid]);
+#pragma unroll
+    for (int wv = 0; wv < kFilterWarps; wv++) m = max(m, s_max[wv][threadIdx.x]);
     int n = 0, p = 0;
     if (g.scaling && m > g.target) {
       // P:322-329 read per DESIGN.md A3: x = floor(255*128/max), y = floor(log2 x),
       // n = x >> (y - 3) (4-bit, in [8, 15]), p = 10 - y (in [4, 7]).
-      int x = (g.target * 128) / m;
-      int y = 31 - __clz(x);
+      const int x = (g.target * 128) / m;
+      const int y = 31 - __clz(x);
       n = y >= 3 ? (x >> (y - 3)) : (x << (3 - y));
       p = 10 - y;
     }
-    s_n[tid] = n;
-    s_p[tid] = p;
+    s_n[threadIdx.x] = n;
+    s_p[threadIdx.x] = p;
     if (live) {
-      int code = n ? ((n << 2) | (p - 4)) : 0;   // 6-bit code, 0 = unscaled
-      if (tid < 16) {
-        codes[co * 36 + real_pos(tid)] = (uint8_t)code;
+      const int i = threadIdx.x;
+      const uint8_t code = (uint8_t)(n ? ((n << 2) | (p - 4)) : 0);   // 6-bit code, 0 = unscaled
+      if (i < 16) {
+        codes[co * 36 + real_pos(i)] = code;
       } else {
-        codes[co * 36 + cpx_pos(tid - 16)] = (uint8_t)code;
-        codes[co * 36 + cpx_mirror_pos(tid - 16)] = (uint8_t)code;   // mirrors share the factor
+        codes[co * 36 + cpx_pos(i - 16)] = code;
+        codes[co * 36 + cpx_mirror_pos(i - 16)] = code;   // mirrors share the factor
       }
     }
   }
   __syncthreads();
+  int sn[26], sp[26];
+#pragma unroll
+  for (int i = 0; i < 26; i++) { sn[i] = s_n[i]; sp[i] = s_p[i]; }
 
-  // Scaled operand planes, split into int8 pieces, into the pre-tiled image.
-  const long long pp_stride = (long long)g.cout_pad * g.cin_pad;
-  const long long base0 = w_offset(g, 0, co, 0);   // pp = 0 offset of (co, k = 0)
-  for (int ci = tid; ci < g.cin_pad; ci += blockDim.x) {
-    const long long off = base0 + tiled_offset(co % g.nblk, ci, g.nblk) - tiled_offset(co % g.nblk, 0, g.nblk);
+  for (int c0 = warp * 32; c0 < g.cin_pad; c0 += kFilterWarps * 32) {
+    const int ci = c0 + lane;
     int vals[46];
     if (live && ci < g.cin) {
-      int sv[36];
-#pragma unroll
-      for (int i = 0; i < 36; i++) sv[i] = s_w[ci * 36 + i];
-#pragma unroll
-      for (int s = 0; s < 16; s++) {
-        int n = s_n[s];
-        vals[s] = n ? rha_mul_shift(sv[s], n, s_p[s]) : sv[s];        // W' = rha(W n / 2^p)
-      }
-#pragma unroll
-      for (int k = 0; k < 10; k++) {
-        int n = s_n[16 + k], p = s_p[16 + k];
-        int re = n ? rha_mul_shift(sv[16 + 2 * k], n, p) : sv[16 + 2 * k];
-        int im = n ? rha_mul_shift(sv[17 + 2 * k], n, p) : sv[17 + 2 * k];
-        vals[16 + 3 * k + 0] = re;          // Karatsuba operands
-        vals[16 + 3 * k + 1] = im;
-        vals[16 + 3 * k + 2] = re + im;
-      }
+      int gg[3][3], t[36];
+      load_filter(g, w, co, ci, gg);
+      filter_tile_transform(gg, t);
+      scaled_planes(t, sn, sp, vals);
     } else {
 #pragma unroll
       for (int i = 0; i < 46; i++) vals[i] = 0;
     }
 #pragma unroll
     for (int pl = 0; pl < 46; pl++) {
-      int v = vals[pl];
-      wimg[off + (2 * pl + 0) * pp_stride] = (int8_t)(v >> 8);            // hi, s8
-      wimg[off + (2 * pl + 1) * pp_stride] = (int8_t)(uint8_t)(v & 255);  // lo, u8
+      s_stage[warp][2 * pl + 0][lane] = (int8_t)(vals[pl] >> 8);             // hi, s8
+      s_stage[warp][2 * pl + 1][lane] = (int8_t)(uint8_t)(vals[pl] & 255);   // lo, u8
     }
+    __syncwarp();
+    for (int idx = lane; idx < 2 * kPlanes * 2; idx += 32) {   // (piece-plane, 16-channel half)
+      const int pp = idx >> 1, hf = idx & 1;
+      const int4 v = *reinterpret_cast<const int4*>(&s_stage[warp][pp][hf * 16]);
+      *reinterpret_cast<int4*>(wimg + w_offset(g, pp, co, c0 + hf * 16)) = v;
+    }
+    __syncwarp();
   }
 }
 
 cudaError_t launch_filter_transform(const Geom& g, const int8_t* w, int8_t* wimg, uint8_t* codes, cudaStream_t st) {
-  size_t smem = (size_t)g.cin * 36 * sizeof(int16_t);
-  k_filter_transform<<<g.cout_pad, 256, smem, st>>>(g, w, wimg, codes);
+  k_filter_transform<<<g.cout_pad, kFilterWarps * 32, 0, st>>>(g, w, wimg, codes);
   return cudaGetLastError();
 }
 
-cudaError_t setup_filter_transform() {
-  return cudaFuncSetAttribute(k_filter_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, 896 * 36 * 2);
-}
+cudaError_t setup_filter_transform() { return cudaSuccess; }
 
 }  // namespace wino

@@ -1,21 +1,30 @@
-// k_gemm.cu -- K3: the Winograd-domain channel contraction: for
-// each of the 46 operand planes p, M_p[tiles x Cout] = V_p[tiles x Cin] .
-// W'_p[Cin x Cout], on the tcgen05 tensor cores (kind::i8, int32 accumulation
-// in TMEM).  Every operand is split into an s8 high and a u8 low piece
-// (layout.cuh), so one plane is four UMMAs per 32-channel K step into three
-// TMEM accumulators:
-//     acc_hh += Vhi . Whi          (weight 2^16)
-//     acc_x  += Vhi . Wlo + Vlo . Whi   (weight 2^8)
-//     acc_ll += Vlo . Wlo          (weight 1)
-// and the epilogue forms M = 2^16 acc_hh + 2^8 acc_x + acc_ll (exact mod
-// 2^32; the true |M| < 2^31 for Cin <= 896, A23).
+// k_gemm.cu -- K3: the Winograd-domain channel contraction on the
+// tcgen05 tensor cores, with the Karatsuba recombination and
+// the reverse scaling fused into the epilogue.
 //
-// CTA = 128 threads, one (plane, 128-tile block, n_block-cout block):
-//   warp 0 lane 0  producer: 1-D bulk copies (TMA engine) of whole pre-tiled
-//                  K stages into shared memory, mbarrier complete_tx
-//   warp 1 lane 0  MMA issuer: tcgen05.mma per K step, tcgen05.commit frees
-//                  the stage
-//   warps 0..3     epilogue: tcgen05.ld (warp w owns TMEM lanes 32w..32w+31)
+// For each of the 46 operand planes p:  M_p[tiles x Cout] = V_p . W'_p
+// (kind::i8, int32 accumulation in TMEM).  Every operand is split into an s8
+// high and a u8 low piece (layout.cuh), so one plane is four UMMAs per
+// 32-channel K step into three TMEM accumulators
+//     acc_hh += Vhi.Whi   acc_x += Vhi.Wlo + Vlo.Whi   acc_ll += Vlo.Wlo
+// and M_p = 2^16 acc_hh + 2^8 acc_x + acc_ll (exact mod 2^32; the true value
+// fits int32 for the plan's Cin limits, A23).
+//
+// Work unit = (Winograd position, 128-tile block, n_block-cout block).  A real
+// position is one plane; a complex primary is its three Karatsuba planes
+// P0 = Re.Re, P1 = Im.Im, P2 = (Re+Im)(Re+Im), processed back to back; the
+// epilogue keeps Re = P0 - P1 and S = P0 + P1 in registers and finishes
+// Im = P2 - S, then applies M'' = rha(M m / 2^q) per (cout, position) code
+// and stores the 36 values per (tile, cout) of M'' -- the only hand-off to K4.
+//
+// Persistent CTA per SM, warp-specialised (10 warps):
+//   warp 0 (1 lane)  producer: 1-D bulk copies (TMA engine) of pre-tiled K
+//                    stages, mbarrier complete_tx, kStages-deep ring
+//   warp 1 (1 lane)  MMA issuer: tcgen05.mma, tcgen05.commit -> stage free /
+//                    accumulator full; TMEM accumulators double-buffered so the
+//                    epilogue of plane i overlaps the MMAs of plane i+1
+//   warps 2..9       epilogue: warp w reads TMEM lanes 32(w%4).., column half
+//                    (w-2)/4
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -25,37 +34,85 @@
 
 namespace wino {
 
-constexpr int kStages = 4;
+constexpr int kStages = 6;
 constexpr int kKStepsPerStage = 2;
+constexpr int kEpiWarps = 8;
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kABytesPerKStep = kMBlock * kKStep;   // 4096
+constexpr int kPositions = 26;                           // 10 complex primaries, 16 real
 
 __host__ __device__ inline uint32_t gemm_stage_bytes(int nblk) {
   return 2u * kKStepsPerStage * kABytesPerKStep + 2u * kKStepsPerStage * (uint32_t)nblk * kKStep;
 }
-__host__ __device__ inline uint32_t gemm_tmem_cols(int nblk) {
-  uint32_t need = 3u * (uint32_t)nblk, c = 32;
-  while (c < need) c <<= 1;
-  return c;
+// stages + barriers/LUT (1 KB) + per-CTA code table [26 positions][cout_pad] bytes
+inline size_t gemm_smem_bytes(int nblk, int cout_pad) {
+  return (size_t)kStages * gemm_stage_bytes(nblk) + 1024 + (size_t)kPositions * cout_pad;
 }
-inline size_t gemm_smem_bytes(int nblk) { return (size_t)kStages * gemm_stage_bytes(nblk) + 1024; }
+constexpr int kMaxCoutPadSmem = 2048;   // code table bound used for the smem attribute
 
-__global__ void __launch_bounds__(128, 1)
-    k_gemm(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ M, int ksteps,
-           long long tiles_pad, int cout_pad, int cin_pad, int nblk) {
+// One TMEM load of C columns (C = 16 or 8) for the calling warp's 32 lanes.
+template <int C>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&r)[C]);
+template <>
+__device__ __forceinline__ void tmem_ld<16>(uint32_t taddr, uint32_t (&r)[16]) {
+  tmem_ld16(taddr, r);
+}
+template <>
+__device__ __forceinline__ void tmem_ld<8>(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+
+__device__ __forceinline__ int32_t rscale_lut(uint32_t v, int code, const uint32_t* lut) {
+  if (!code) return (int32_t)v;
+  const uint32_t e = lut[code];
+  return (int32_t)rha_shift64((long long)(int32_t)v * (int)(e & 0xffffu), (int)(e >> 16));
+}
+
+// unit u -> (position index pidx, tile block, cout block); complex units first
+// (they carry three planes) so the static round robin ends on the light ones.
+__device__ __forceinline__ void decode_unit(int u, int tblocks, int nblocks, int& pidx, int& tb, int& nb) {
+  const int per = tblocks * nblocks;
+  pidx = u / per;
+  const int rest = u - pidx * per;
+  nb = rest / tblocks;
+  tb = rest - nb * tblocks;
+}
+__device__ __forceinline__ int unit_planes(int pidx) { return pidx < kPrimaries ? 3 : 1; }
+__device__ __forceinline__ int unit_plane0(int pidx) {
+  return pidx < kPrimaries ? kRealPlanes + 3 * pidx : pidx - kPrimaries;
+}
+
+template <int NBLK>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ Mpp,
+           const uint8_t* __restrict__ codes, int cout, int ksteps, long long tiles_pad, int tblocks, int cout_pad,
+           int cin_pad, int scaling) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int tb = blockIdx.x, nb = blockIdx.y, plane = blockIdx.z;
+  constexpr int kHalf = NBLK / 2;                 // columns per epilogue warp
+  constexpr int kChunk = kHalf >= 16 ? 16 : 8;    // columns per tcgen05.ld
+  constexpr uint32_t kAccCols = 3 * NBLK;         // hh, x, ll
+  constexpr uint32_t kTmemCols = 512;
+  static_assert(2 * kAccCols <= kTmemCols, "double-buffered accumulators must fit TMEM");
+
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t a_bytes = kKStepsPerStage * kABytesPerKStep;
-  const uint32_t b_bytes = kKStepsPerStage * (uint32_t)nblk * kKStep;
+  const uint32_t b_bytes = kKStepsPerStage * (uint32_t)NBLK * kKStep;
   const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint32_t* lut = tmem_slot + 4;                  // 64 entries: code -> m | q << 16
+  uint8_t* s_codes = smem + kStages * stage_bytes + 1024;   // [pidx][cout_pad] codes
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages), done = smem_u32(bars + 2 * kStages);
-  const uint32_t tmem_cols = gemm_tmem_cols(nblk);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
+  const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
+  const int nblocks = cout_pad / NBLK;
+  const int n_units = tblocks * nblocks * kPositions;
+  const int n_it = (ksteps + kKStepsPerStage - 1) / kKStepsPerStage;
 
   if (warp == 0) {
-    tmem_alloc(smem_u32(tmem_slot), tmem_cols);
+    tmem_alloc(smem_u32(tmem_slot), kTmemCols);
     tmem_relinquish();
   }
   if (threadIdx.x == 32) {
@@ -63,99 +120,202 @@ __global__ void __launch_bounds__(128, 1)
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; b++) {
+      mbar_init(tfull0 + 8 * b, 1);
+      mbar_init(tempty0 + 8 * b, kEpiWarps);
+    }
     fence_mbar_init();
+  }
+  if (threadIdx.x >= 64 && threadIdx.x < 128) {   // inverse factors of all 64 codes (A8)
+    const int code = threadIdx.x - 64;
+    int n, p, m, q;
+    decode_code(code, n, p);
+    uint32_t e = 0;
+    if (n >= 8) {
+      inverse_factor(n, p, m, q);
+      e = (uint32_t)m | ((uint32_t)q << 16);
+    }
+    lut[code] = e;
+  }
+  // scale codes of every (position, cout), position-major (0 = unscaled)
+  for (int i = threadIdx.x; i < kPositions * cout_pad; i += blockDim.x) {
+    const int pidx = i / cout_pad, co = i - pidx * cout_pad;
+    const int pos = pidx < kPrimaries ? cpx_pos(pidx) : real_pos(pidx - kPrimaries);
+    s_codes[i] = (scaling && co < cout) ? codes[(long long)co * 36 + pos] : 0;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int n_it = (ksteps + kKStepsPerStage - 1) / kKStepsPerStage;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- producer
-    const int8_t* vh = V + (long long)(2 * plane) * tiles_pad * cin_pad + (long long)tb * ksteps * kABytesPerKStep;
-    const int8_t* vl = vh + tiles_pad * cin_pad;
-    const int8_t* wh = W + (long long)(2 * plane) * cout_pad * cin_pad + (long long)nb * ksteps * nblk * kKStep;
-    const int8_t* wl = wh + (long long)cout_pad * cin_pad;
-    for (int it = 0; it < n_it; ++it) {
-      const int s = it % kStages;
-      const uint32_t ph = (it / kStages) & 1;
-      mbar_wait(empty0 + 8 * s, ph ^ 1);
-      const int k0 = it * kKStepsPerStage;
-      const int kn = min(kKStepsPerStage, ksteps - k0);
-      const uint32_t ab = kn * kABytesPerKStep, bb = kn * (uint32_t)nblk * kKStep;
-      const uint32_t st = sbase + s * stage_bytes;
-      mbar_arrive_expect_tx(full0 + 8 * s, 2 * ab + 2 * bb);
-      bulk_g2s(st, vh + (long long)k0 * kABytesPerKStep, ab, full0 + 8 * s);
-      bulk_g2s(st + a_bytes, vl + (long long)k0 * kABytesPerKStep, ab, full0 + 8 * s);
-      bulk_g2s(st + 2 * a_bytes, wh + (long long)k0 * nblk * kKStep, bb, full0 + 8 * s);
-      bulk_g2s(st + 2 * a_bytes + b_bytes, wl + (long long)k0 * nblk * kKStep, bb, full0 + 8 * s);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
-    const uint32_t id_ss = idesc_i8(kMBlock, nblk, 1, 1), id_su = idesc_i8(kMBlock, nblk, 1, 0);
-    const uint32_t id_us = idesc_i8(kMBlock, nblk, 0, 1), id_uu = idesc_i8(kMBlock, nblk, 0, 0);
-    const uint32_t acc_hh = tmem, acc_x = tmem + nblk, acc_ll = tmem + 2 * nblk;
-    for (int it = 0; it < n_it; ++it) {
-      const int s = it % kStages;
-      const uint32_t ph = (it / kStages) & 1;
-      mbar_wait(full0 + 8 * s, ph);
-      tc_fence_after();
-      const int k0 = it * kKStepsPerStage;
-      const int kn = min(kKStepsPerStage, ksteps - k0);
-      const uint32_t st = sbase + s * stage_bytes;
-      for (int kk = 0; kk < kn; ++kk) {
-        const uint32_t acc = (k0 + kk) > 0;
-        const uint64_t a_hi = umma_desc(st + kk * kABytesPerKStep, 128, 256);
-        const uint64_t a_lo = umma_desc(st + a_bytes + kk * kABytesPerKStep, 128, 256);
-        const uint64_t b_hi = umma_desc(st + 2 * a_bytes + kk * nblk * kKStep, 128, 256);
-        const uint64_t b_lo = umma_desc(st + 2 * a_bytes + b_bytes + kk * nblk * kKStep, 128, 256);
-        umma_i8(acc_hh, a_hi, b_hi, id_ss, acc);
-        umma_i8(acc_x, a_hi, b_lo, id_su, acc);
-        umma_i8(acc_x, a_lo, b_hi, id_us, 1);
-        umma_i8(acc_ll, a_lo, b_lo, id_uu, acc);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ producer
+      int it = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int pidx, tb, nb;
+        decode_unit(u, tblocks, nblocks, pidx, tb, nb);
+        for (int pl = 0; pl < unit_planes(pidx); pl++) {
+          const int plane = unit_plane0(pidx) + pl;
+          const int8_t* vh = V + (long long)(2 * plane) * tiles_pad * cin_pad + (long long)tb * ksteps * kABytesPerKStep;
+          const int8_t* vl = vh + tiles_pad * cin_pad;
+          const int8_t* wh = W + (long long)(2 * plane) * cout_pad * cin_pad + (long long)nb * ksteps * NBLK * kKStep;
+          const int8_t* wl = wh + (long long)cout_pad * cin_pad;
+          for (int ks = 0; ks < n_it; ks++, it++) {
+            const int s = it % kStages;
+            mbar_wait(empty0 + 8 * s, ((it / kStages) & 1) ^ 1);
+            const int k0 = ks * kKStepsPerStage;
+            const int kn = min(kKStepsPerStage, ksteps - k0);
+            const uint32_t ab = kn * kABytesPerKStep, bb = kn * (uint32_t)NBLK * kKStep;
+            const uint32_t st = sbase + s * stage_bytes;
+            mbar_arrive_expect_tx(full0 + 8 * s, 2 * ab + 2 * bb);
+            bulk_g2s(st, vh + (long long)k0 * kABytesPerKStep, ab, full0 + 8 * s);
+            bulk_g2s(st + a_bytes, vl + (long long)k0 * kABytesPerKStep, ab, full0 + 8 * s);
+            bulk_g2s(st + 2 * a_bytes, wh + (long long)k0 * NBLK * kKStep, bb, full0 + 8 * s);
+            bulk_g2s(st + 2 * a_bytes + b_bytes, wl + (long long)k0 * NBLK * kKStep, bb, full0 + 8 * s);
+          }
+        }
       }
-      umma_commit(empty0 + 8 * s);   // stage reusable once these MMAs have read it
     }
-    umma_commit(done);
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: M = 2^16 hh + 2^8 x + ll, int32 row-major [tile][cout]
-  mbar_wait(done, 0);
-  tc_fence_after();
-  const long long row = (long long)tb * kMBlock + warp * 32 + lane;
-  int32_t* mrow = M + ((long long)plane * tiles_pad + row) * cout_pad + (long long)nb * nblk;
-  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-  for (int c0 = 0; c0 < nblk; c0 += 16) {
-    uint32_t h[16], x[16], l[16];
-    tmem_ld16(lane_base + c0, h);
-    tmem_ld16(lane_base + nblk + c0, x);
-    tmem_ld16(lane_base + 2 * nblk + c0, l);
-    tmem_ld_wait();
-    uint32_t v[16];
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      const uint32_t id_ss = idesc_i8(kMBlock, NBLK, 1, 1), id_su = idesc_i8(kMBlock, NBLK, 1, 0);
+      const uint32_t id_us = idesc_i8(kMBlock, NBLK, 0, 1), id_uu = idesc_i8(kMBlock, NBLK, 0, 0);
+      int it = 0, pc = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int pidx, tb, nb;
+        decode_unit(u, tblocks, nblocks, pidx, tb, nb);
+        for (int pl = 0; pl < unit_planes(pidx); pl++, pc++) {
+          const int b = pc & 1;
+          mbar_wait(tempty0 + 8 * b, ((pc >> 1) & 1) ^ 1);   // epilogue drained this buffer
+          tc_fence_after();
+          const uint32_t acc_hh = tmem + b * kAccCols, acc_x = acc_hh + NBLK, acc_ll = acc_hh + 2 * NBLK;
+          for (int ks = 0; ks < n_it; ks++, it++) {
+            const int s = it % kStages;
+            mbar_wait(full0 + 8 * s, (it / kStages) & 1);
+            tc_fence_after();
+            const int k0 = ks * kKStepsPerStage;
+            const int kn = min(kKStepsPerStage, ksteps - k0);
+            const uint32_t st = sbase + s * stage_bytes;
+            for (int kk = 0; kk < kn; ++kk) {
+              const uint32_t acc = (k0 + kk) > 0;
+              const uint64_t a_hi = umma_desc(st + kk * kABytesPerKStep, 128, 256);
+              const uint64_t a_lo = umma_desc(st + a_bytes + kk * kABytesPerKStep, 128, 256);
+              const uint64_t b_hi = umma_desc(st + 2 * a_bytes + kk * NBLK * kKStep, 128, 256);
+              const uint64_t b_lo = umma_desc(st + 2 * a_bytes + b_bytes + kk * NBLK * kKStep, 128, 256);
+              umma_i8(acc_hh, a_hi, b_hi, id_ss, acc);
+              umma_i8(acc_x, a_hi, b_lo, id_su, acc);
+              umma_i8(acc_x, a_lo, b_hi, id_us, 1);
+              umma_i8(acc_ll, a_lo, b_lo, id_uu, acc);
+            }
+            umma_commit(empty0 + 8 * s);   // stage reusable once these MMAs have read it
+          }
+          umma_commit(tfull0 + 8 * b);     // accumulator set b complete
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue
+    const int ew = warp - 2;
+    const int quad = warp & 3;            // TMEM lane quadrant this warp may access
+    const int col0 = (ew >> 2) * kHalf;   // column half
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    const long long ps = tiles_pad * (long long)cout_pad;   // M'' slot stride
+    int pc = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int pidx, tb, nb;
+      decode_unit(u, tblocks, nblocks, pidx, tb, nb);
+      const long long row = (long long)tb * kMBlock + quad * 32 + lane;
+      const int cbase = nb * NBLK + col0;
+      const bool cpx = pidx < kPrimaries;
+      uint32_t re[kHalf], sm[kHalf];
+      for (int pl = 0; pl < unit_planes(pidx); pl++, pc++) {
+        const int b = pc & 1;
+        mbar_wait(tfull0 + 8 * b, (pc >> 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = lane_base + b * kAccCols + col0;
 #pragma unroll
-    for (int j = 0; j < 16; j++) v[j] = (h[j] << 16) + (x[j] << 8) + l[j];
+        for (int c = 0; c < kHalf; c += kChunk) {
+          uint32_t h[kChunk], x[kChunk], l[kChunk];
+          tmem_ld<kChunk>(acc + c, h);
+          tmem_ld<kChunk>(acc + NBLK + c, x);
+          tmem_ld<kChunk>(acc + 2 * NBLK + c, l);
+          tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 16; j += 4)
-      *reinterpret_cast<int4*>(mrow + c0 + j) = make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]);
+          for (int j = 0; j < kChunk; j++) {
+            const uint32_t v = (h[j] << 16) + (x[j] << 8) + l[j];
+            if (!cpx) {
+              re[c + j] = v;
+            } else if (pl == 0) {          // P0
+              re[c + j] = v;
+              sm[c + j] = v;
+            } else if (pl == 1) {          // P1: Re = P0 - P1, S = P0 + P1
+              re[c + j] -= v;
+              sm[c + j] += v;
+            } else {                       // P2: Im = P2 - P0 - P1
+              sm[c + j] = v - sm[c + j];
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty0 + 8 * b);
+      }
+      // reverse scaling and store of M'' (slots: real s, Re 16+k, Im 26+k)
+      const int slot_re = cpx ? kRealPlanes + pidx : pidx - kPrimaries;
+      int32_t* out_re = Mpp + (long long)slot_re * ps + row * cout_pad + cbase;
+      int32_t* out_im = Mpp + (long long)(kRealPlanes + kPrimaries + pidx) * ps + row * cout_pad + cbase;
+      const uint32_t* crow = reinterpret_cast<const uint32_t*>(s_codes + pidx * cout_pad + cbase);
+#pragma unroll
+      for (int c = 0; c < kHalf; c += 4) {
+        int32_t r4[4], i4[4];
+        const uint32_t c4 = crow[c >> 2];   // four consecutive couts' codes
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const int code = (int)((c4 >> (8 * j)) & 0xffu);
+          r4[j] = rscale_lut(re[c + j], code, lut);
+          if (cpx) i4[j] = rscale_lut(sm[c + j], code, lut);
+        }
+        *reinterpret_cast<int4*>(out_re + c) = make_int4(r4[0], r4[1], r4[2], r4[3]);
+        if (cpx) *reinterpret_cast<int4*>(out_im + c) = make_int4(i4[0], i4[1], i4[2], i4[3]);
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, tmem_cols);
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
-cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t* vimg, const int8_t* wimg, int32_t* m,
-                        cudaStream_t st) {
-  dim3 grid((unsigned)(tiles_pad_launch / kMBlock), g.cout_pad / g.nblk, kPlanes);
-  k_gemm<<<grid, 128, gemm_smem_bytes(g.nblk), st>>>(vimg, wimg, m, g.ksteps, g.chunk_tiles_pad, g.cout_pad, g.cin_pad,
-                                                    g.nblk);
+static int g_num_sms = 0;
+
+cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t* vimg, const int8_t* wimg,
+                        const uint8_t* codes, int32_t* mpp, cudaStream_t st) {
+  const int tblocks = (int)(tiles_pad_launch / kMBlock);
+  const int n_units = tblocks * (g.cout_pad / g.nblk) * kPositions;
+  const int grid = n_units < g_num_sms ? n_units : g_num_sms;
+  const size_t smem = gemm_smem_bytes(g.nblk, g.cout_pad);
+#define WINO_LAUNCH_GEMM(N)                                                                              \
+  k_gemm<N><<<grid, kGemmThreads, smem, st>>>(vimg, wimg, mpp, codes, g.cout, g.ksteps, g.chunk_tiles_pad, \
+                                              tblocks, g.cout_pad, g.cin_pad, g.scaling)
+  switch (g.nblk) {
+    case 16: WINO_LAUNCH_GEMM(16); break;
+    case 32: WINO_LAUNCH_GEMM(32); break;
+    case 64: WINO_LAUNCH_GEMM(64); break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef WINO_LAUNCH_GEMM
   return cudaGetLastError();
 }
 
 cudaError_t setup_gemm() {
-  return cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(128));
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(16, kMaxCoutPadSmem));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(32, kMaxCoutPadSmem));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(64, kMaxCoutPadSmem));
+  return e;
 }
 
 }  // namespace wino

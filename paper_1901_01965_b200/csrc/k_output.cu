@@ -1,11 +1,13 @@
-// k_output.cu -- K4: Karatsuba recombination, reverse
-// scaling M'' = rha(M m / 2^q), the real-only output
-// transform Y = A^T M'' A that never forms the imaginary coefficients
-// (P:163-170), out32 = rha(Y / 16) (G used as 4G, A2/A11),
-// crop, optional requantisation (A14) and the store.
+// k_output.cu -- K4: the real-only output transform Y = A^T M'' A that never
+// forms the imaginary coefficients, out32 = rha(Y / 16)
+// (G used as 4G, A2/A11), crop, optional requantisation (A14) and
+// the store.  M'' (after Karatsuba recombination and reverse scaling, both done
+// in K3's epilogue) arrives as 36 int32 slots per (tile, cout):
+//   slot s < 16: real position (R[s/4], R[s%4]);  16+k / 26+k: Re / Im of
+//   complex primary k (layout.cuh order).
 //
 // One thread per (tile, output channel); consecutive threads take
-// consecutive channels, so the 46 plane reads of M are coalesced.
+// consecutive channels, so the 36 slot reads are coalesced.
 //
 // Real-only transform.  A^T rows are a_0 = (1,1,1,1,1,0), a_1 = (0,1,-1,i,-i,0),
 // a_2 = (0,1,1,-1,-1,0), a_3 = (0,1,-1,-i,i,1); a_j4 = conj(a_j3).  For a row
@@ -16,6 +18,7 @@
 // row 4 is its conjugate, so
 //   Y[0][j] = Z0+Z1+Z2+2Re Z3   Y[1][j] = Z1-Z2-2Im Z3
 //   Y[2][j] = Z1+Z2-2Re Z3      Y[3][j] = Z1-Z2+Z5+2Im Z3.
+// All sums are int32 with wrap-around: exact because the true Y fits (A23).
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -24,16 +27,7 @@
 
 namespace wino {
 
-__device__ __forceinline__ uint32_t rscale(uint32_t v, int code) {
-  if (!code) return v;
-  int n, p, m, q;
-  decode_code(code, n, p);
-  inverse_factor(n, p, m, q);
-  return (uint32_t)(int32_t)rha_shift64((long long)(int32_t)v * m, q);
-}
-
-__global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t* __restrict__ M,
-                                                          const uint8_t* __restrict__ codes, int n0, int imgs,
+__global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t* __restrict__ M, int n0, int imgs,
                                                           int32_t rq_mult, int rq_shift, void* __restrict__ y) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)imgs * g.tpi * g.cout;
@@ -47,22 +41,9 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
 #pragma unroll
   for (int s = 0; s < 16; s++) mr[s] = (uint32_t)__ldg(mp + s * ps);
 #pragma unroll
-  for (int k = 0; k < 10; k++) {   // Karatsuba: Re = P0 - P1, Im = P2 - P0 - P1
-    uint32_t p0 = (uint32_t)__ldg(mp + (16 + 3 * k) * ps), p1 = (uint32_t)__ldg(mp + (17 + 3 * k) * ps),
-             p2 = (uint32_t)__ldg(mp + (18 + 3 * k) * ps);
-    cr[k] = p0 - p1;
-    cim[k] = p2 - p0 - p1;
-  }
-  if (g.scaling) {   // reverse scaling before the final transforms
-    const uint8_t* cc = codes + (long long)co * 36;
-#pragma unroll
-    for (int s = 0; s < 16; s++) mr[s] = rscale(mr[s], __ldg(cc + real_pos(s)));
-#pragma unroll
-    for (int k = 0; k < 10; k++) {
-      int code = __ldg(cc + cpx_pos(k));
-      cr[k] = rscale(cr[k], code);
-      cim[k] = rscale(cim[k], code);
-    }
+  for (int k = 0; k < 10; k++) {
+    cr[k] = (uint32_t)__ldg(mp + (16 + k) * ps);
+    cim[k] = (uint32_t)__ldg(mp + (26 + k) * ps);
   }
   // Z = M'' A  (rows 0,1,2,5 real; row 3 complex)
   uint32_t Z[4][4], zr[4], zi[4];
@@ -113,11 +94,11 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
   }
 }
 
-cudaError_t launch_output_transform(const Geom& g, const int32_t* m, const uint8_t* codes, int n0, int imgs,
-                                    int32_t rq_mult, int rq_shift, void* y, cudaStream_t st) {
+cudaError_t launch_output_transform(const Geom& g, const int32_t* m, int n0, int imgs, int32_t rq_mult,
+                                    int rq_shift, void* y, cudaStream_t st) {
   long long total = (long long)imgs * g.tpi * g.cout;
   unsigned blocks = (unsigned)((total + 255) / 256);
-  k_output_transform<<<blocks, 256, 0, st>>>(g, m, codes, n0, imgs, rq_mult, rq_shift, y);
+  k_output_transform<<<blocks, 256, 0, st>>>(g, m, n0, imgs, rq_mult, rq_shift, y);
   return cudaGetLastError();
 }
 

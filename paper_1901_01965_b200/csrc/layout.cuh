@@ -25,7 +25,9 @@
 //   the block is R*32 contiguous bytes, and all K steps are contiguous).
 //   V image: [plane][piece][tile_block][kstep][R=128 x 32 B]
 //   W image: [plane][piece][cout_block][kstep][R=n_block x 32 B]
-//   M      : [plane][tile (chunk_tiles_pad)][cout_pad] int32
+//   M''    : [slot 36][tile (chunk_tiles_pad)][cout_pad] int32, after Karatsuba
+//            recombination and reverse scaling; slot s < 16 real position s,
+//            16+k = Re and 26+k = Im of complex primary k
 #pragma once
 #include <cstdint>
 
@@ -35,6 +37,7 @@ constexpr int kPlanes = 46;
 constexpr int kRealPlanes = 16;
 constexpr int kPrimaries = 10;
 constexpr int kPieces = 2;
+constexpr int kSlots = 36;    // M'' values per (tile, cout)
 constexpr int kMBlock = 128;   // GEMM M (tiles per CTA) = TMEM lanes
 constexpr int kKStep = 32;     // int8 MMA K
 
@@ -65,20 +68,15 @@ __host__ __device__ __forceinline__ long long w_offset(const Geom& g, int pp, in
          tiled_offset(r, k, g.nblk);
 }
 
-// Position index (r*6+c) of real plane s and of complex primary k / its mirror.
-__host__ __device__ __forceinline__ int real_pos(int s) {
-  const int R[4] = {0, 1, 2, 5};
-  return R[s >> 2] * 6 + R[s & 3];
+// Position index (r*6+c) of real plane s and of complex primary k / its mirror
+// (arithmetic, so no local-memory tables; R = {0,1,2,5} -> R[i] = i + 2 (i == 3)).
+__host__ __device__ __forceinline__ int rsel(int i) { return i + (i == 3 ? 2 : 0); }
+__host__ __device__ __forceinline__ int real_pos(int s) { return rsel(s >> 2) * 6 + rsel(s & 3); }
+__host__ __device__ __forceinline__ int cpx_pos(int k) {      // (R[k],3) | (3,R[k-4]) | (3,3) | (3,4)
+  return k < 4 ? rsel(k) * 6 + 3 : (k < 8 ? 18 + rsel(k - 4) : 21 + (k - 8));
 }
-__host__ __device__ __forceinline__ int cpx_pos(int k) {
-  const int P[10] = {0 * 6 + 3, 1 * 6 + 3, 2 * 6 + 3, 5 * 6 + 3, 3 * 6 + 0,
-                     3 * 6 + 1, 3 * 6 + 2, 3 * 6 + 5, 3 * 6 + 3, 3 * 6 + 4};
-  return P[k];
-}
-__host__ __device__ __forceinline__ int cpx_mirror_pos(int k) {
-  const int P[10] = {0 * 6 + 4, 1 * 6 + 4, 2 * 6 + 4, 5 * 6 + 4, 4 * 6 + 0,
-                     4 * 6 + 1, 4 * 6 + 2, 4 * 6 + 5, 4 * 6 + 4, 4 * 6 + 3};
-  return P[k];
+__host__ __device__ __forceinline__ int cpx_mirror_pos(int k) {   // (R[k],4) | (4,R[k-4]) | (4,4) | (4,3)
+  return k < 4 ? rsel(k) * 6 + 4 : (k < 8 ? 24 + rsel(k - 4) : 28 - (k - 8));
 }
 
 // round-half-away-from-zero of v / 2^k (k >= 1), 64-bit.

@@ -89,7 +89,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   // int32 exactness of M'' and Y (A23): 896 unscaled, 768 scaled
   if (d.c_in > (d.filter_scaling ? 768 : 896)) return WINO_ERR_UNSUPPORTED;
   if (d.filter_target_max != 255) return WINO_ERR_UNSUPPORTED;
-  if (d.c_out > (1 << 20) || (long long)d.n * d.h * d.w > (1ll << 40)) return WINO_ERR_UNSUPPORTED;
+  if (d.c_out > 2048 || (long long)d.n * d.h * d.w > (1ll << 40)) return WINO_ERR_UNSUPPORTED;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess) return WINO_ERR_CUDA;
   if (device < 0 || device >= ndev) return WINO_ERR_INVALID_ARG;
@@ -113,14 +113,14 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.tpi = g.th * g.tw;
   g.cin_pad = (int)round_up(d.c_in, wino::kKStep);
   const int cout16 = (int)round_up(d.c_out, 16);
-  g.nblk = cout16 >= 64 ? 64 : cout16;
+  g.nblk = cout16 <= 16 ? 16 : (cout16 <= 32 ? 32 : 64);
   g.cout_pad = (int)round_up(d.c_out, g.nblk);
   g.ksteps = g.cin_pad / wino::kKStep;
   g.scaling = d.filter_scaling;
   g.target = d.filter_target_max;
   g.out_mode = d.out_mode;
   // batch chunk: V + M of one chunk within the L2-sized budget
-  const size_t per_img = (size_t)g.tpi * (2 * wino::kPlanes * (size_t)g.cin_pad + wino::kPlanes * 4 * (size_t)g.cout_pad);
+  const size_t per_img = (size_t)g.tpi * (2 * wino::kPlanes * (size_t)g.cin_pad + wino::kSlots * 4 * (size_t)g.cout_pad);
   long long imgs = (long long)(chunk_budget_bytes() / (per_img ? per_img : 1));
   if (imgs < 1) imgs = 1;
   if (imgs > d.n) imgs = d.n;
@@ -128,7 +128,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.chunk_tiles_pad = round_up((long long)imgs * g.tpi, wino::kMBlock);
   p->n_chunks = (int)((d.n + imgs - 1) / imgs);
   p->v_bytes = (size_t)2 * wino::kPlanes * g.chunk_tiles_pad * g.cin_pad;
-  p->m_bytes = (size_t)wino::kPlanes * g.chunk_tiles_pad * g.cout_pad * 4;
+  p->m_bytes = (size_t)wino::kSlots * g.chunk_tiles_pad * g.cout_pad * 4;
   p->ws_bytes = p->v_bytes + p->m_bytes;
   p->f_bytes = (size_t)2 * wino::kPlanes * g.cout_pad * g.cin_pad;
   p->x_bytes = (size_t)d.n * d.h * d.w * d.c_in;
@@ -178,26 +178,51 @@ wino_status wino_transform_filter(wino_plan_t p, const int8_t* w, void* w_wino, 
   return e == cudaSuccess ? WINO_OK : WINO_ERR_CUDA;
 }
 
-wino_status wino_conv2d_int8(wino_plan_t p, const int8_t* x, const void* w_wino, const uint8_t* codes,
-                             int32_t rq_mult, int rq_shift, void* y, void* workspace, void* stream) {
+static wino_status run_stage(const wino_plan_s* p, int stage, int chunk, const int8_t* x, const void* w_wino,
+                             const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y, void* workspace,
+                             cudaStream_t s) {
+  const wino::Geom& g = p->g;
+  const int n0 = chunk * g.chunk_imgs;
+  const int imgs = p->d.n - n0 < g.chunk_imgs ? p->d.n - n0 : g.chunk_imgs;
+  const long long tiles_pad = round_up((long long)imgs * g.tpi, wino::kMBlock);
+  int8_t* vimg = static_cast<int8_t*>(workspace);
+  int32_t* m = reinterpret_cast<int32_t*>(static_cast<int8_t*>(workspace) + p->v_bytes);
+  cudaError_t e = cudaErrorInvalidValue;
+  if (stage == 2) e = wino::launch_input_transform(g, x, n0, imgs, vimg, s);
+  if (stage == 3) e = wino::launch_gemm(g, tiles_pad, vimg, static_cast<const int8_t*>(w_wino), codes, m, s);
+  if (stage == 4) e = wino::launch_output_transform(g, m, n0, imgs, rq_mult, rq_shift, y, s);
+  return e == cudaSuccess ? WINO_OK : WINO_ERR_CUDA;
+}
+
+static wino_status check_conv_args(const wino_plan_s* p, const int8_t* x, const void* w_wino, const uint8_t* codes,
+                                   int32_t rq_mult, int rq_shift, void* y, void* workspace) {
   if (!p || !x || !w_wino || !codes || !y || !workspace) return WINO_ERR_INVALID_ARG;
   if (!aligned16(x) || !aligned16(w_wino) || !aligned16(y) || !aligned16(workspace)) return WINO_ERR_INVALID_ARG;
   if (p->d.out_mode == WINO_OUT_INT8 && (rq_mult < 1 || rq_shift < 0 || rq_shift > 62)) return WINO_ERR_RANGE;
-  wino_status st = check_device(p);
+  return check_device(p);
+}
+
+wino_status wino_conv2d_int8(wino_plan_t p, const int8_t* x, const void* w_wino, const uint8_t* codes,
+                             int32_t rq_mult, int rq_shift, void* y, void* workspace, void* stream) {
+  wino_status st = check_conv_args(p, x, w_wino, codes, rq_mult, rq_shift, y, workspace);
   if (st != WINO_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int8_t* vimg = static_cast<int8_t*>(workspace);
-  int32_t* m = reinterpret_cast<int32_t*>(static_cast<int8_t*>(workspace) + p->v_bytes);
-  const wino::Geom& g = p->g;
-  for (int n0 = 0; n0 < p->d.n; n0 += g.chunk_imgs) {
-    const int imgs = p->d.n - n0 < g.chunk_imgs ? p->d.n - n0 : g.chunk_imgs;
-    const long long tiles_pad = round_up((long long)imgs * g.tpi, wino::kMBlock);
-    cudaError_t e = wino::launch_input_transform(g, x, n0, imgs, vimg, s);
-    if (e == cudaSuccess) e = wino::launch_gemm(g, tiles_pad, vimg, static_cast<const int8_t*>(w_wino), m, s);
-    if (e == cudaSuccess) e = wino::launch_output_transform(g, m, codes, n0, imgs, rq_mult, rq_shift, y, s);
-    if (e != cudaSuccess) return WINO_ERR_CUDA;
-  }
+  for (int c = 0; c < p->n_chunks; c++)
+    for (int stage = 2; stage <= 4; stage++) {
+      st = run_stage(p, stage, c, x, w_wino, codes, rq_mult, rq_shift, y, workspace, s);
+      if (st != WINO_OK) return st;
+    }
   return WINO_OK;
+}
+
+wino_status wino_conv2d_int8_stage(wino_plan_t p, int stage, int chunk, const int8_t* x, const void* w_wino,
+                                   const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y, void* workspace,
+                                   void* stream) {
+  wino_status st = check_conv_args(p, x, w_wino, codes, rq_mult, rq_shift, y, workspace);
+  if (st != WINO_OK) return st;
+  if (stage < 2 || stage > 4 || chunk < 0 || chunk >= p->n_chunks) return WINO_ERR_INVALID_ARG;
+  return run_stage(p, stage, chunk, x, w_wino, codes, rq_mult, rq_shift, y, workspace,
+                   static_cast<cudaStream_t>(stream));
 }
 
 wino_status wino_conv2d_int8_host(wino_plan_t p, const int8_t* x_host, const void* w_wino, const uint8_t* codes,
