@@ -228,35 +228,45 @@ def run_ours(args):
 
 
 def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps):
-    """Average device duration of each kernel type (events on the launching stream)."""
+    """Average device duration of each kernel type, measured inside the real
+    graphed pipeline: every rotation slot's step is captured with timing
+    event-record nodes (external events) between consecutive kernels."""
     import torch
     from paper_1901_01965_b200 import _lib as L
     info = conv.info
     sp = stream.cuda_stream
     names = {1: "k1_filter", 2: "k2_input", 3: "k3_gemm", 4: "k4_output"}
-    acc = {k: [] for k in names}
     w_wino, codes, wsp = conv.w_wino.data_ptr(), conv.codes.data_ptr(), conv.workspace.data_ptr()
-    with torch.cuda.stream(stream):
-        for r in range(reps):
-            j = r % n_sets
-            evs = []
-            e = torch.cuda.Event(enable_timing=True); e.record(stream); evs.append((1, e))
+    graphs = []
+    for j in range(n_sets):
+        evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2 + 3 * info.n_chunks)]
+        order = [1] + [st for _ in range(info.n_chunks) for st in (2, 3, 4)]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            evs[0].record(stream)
             L.wino_transform_filter(conv.plan, ws[j].data_ptr(), w_wino, codes, sp)
-            e2 = torch.cuda.Event(enable_timing=True); e2.record(stream)
-            marks = [(1, e, e2)]
+            evs[1].record(stream)
+            e = 2
             for c in range(info.n_chunks):
                 for st in (2, 3, 4):
-                    a = torch.cuda.Event(enable_timing=True); a.record(stream)
                     L.wino_conv2d_int8_stage(conv.plan, st, c, xs[j].data_ptr(), w_wino, codes, 1, S,
                                              ys[j].data_ptr(), wsp, sp)
-                    b = torch.cuda.Event(enable_timing=True); b.record(stream)
-                    marks.append((st, a, b))
+                    evs[e].record(stream)
+                    e += 1
+        graphs.append((g, evs, order))
+    acc = {k: [] for k in names}
+    with torch.cuda.stream(stream):
+        for r in range(reps + 2):
+            g, evs, order = graphs[r % n_sets]
+            g.replay()
             stream.synchronize()
-            for st, a, b in marks:
-                acc[st].append(a.elapsed_time(b) / 1e3)
+            if r < 2:
+                continue   # warm-up replays
+            for i, st in enumerate(order):
+                acc[st].append(evs[i].elapsed_time(evs[i + 1]) / 1e3)
     out = {}
     for st, v in acc.items():
-        per_launch = float(np.median(v))
+        per_launch = float(np.mean(v))
         count = 1 if st == 1 else info.n_chunks
         out[names[st]] = {"s_per_launch": per_launch, "launches_per_step": count, "s_per_step": per_launch * count}
     return out

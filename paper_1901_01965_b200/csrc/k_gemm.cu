@@ -17,14 +17,14 @@
 // Im = P2 - S, then applies M'' = rha(M m / 2^q) per (cout, position) code
 // and stores the 36 values per (tile, cout) of M'' -- the only hand-off to K4.
 //
-// Persistent CTA per SM, warp-specialised (10 warps):
+// Persistent CTA per SM, warp-specialised (18 warps):
 //   warp 0 (1 lane)  producer: 1-D bulk copies (TMA engine) of pre-tiled K
 //                    stages, mbarrier complete_tx, kStages-deep ring
 //   warp 1 (1 lane)  MMA issuer: tcgen05.mma, tcgen05.commit -> stage free /
 //                    accumulator full; TMEM accumulators double-buffered so the
 //                    epilogue of plane i overlaps the MMAs of plane i+1
-//   warps 2..9       epilogue: warp w reads TMEM lanes 32(w%4).., column half
-//                    (w-2)/4
+//   warps 2..17      epilogue: warp w reads TMEM lanes 32(w%4).., column
+//                    quarter (w-2)/4
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -34,9 +34,9 @@
 
 namespace wino {
 
-constexpr int kStages = 6;
+constexpr int kStages = 4;
 constexpr int kKStepsPerStage = 2;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;                           // 4 per TMEM lane quadrant
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kABytesPerKStep = kMBlock * kKStep;   // 4096
 constexpr int kPositions = 26;                           // 10 complex primaries, 16 real
@@ -45,12 +45,14 @@ __host__ __device__ inline uint32_t gemm_stage_bytes(int nblk) {
   return 2u * kKStepsPerStage * kABytesPerKStep + 2u * kKStepsPerStage * (uint32_t)nblk * kKStep;
 }
 // stages + barriers/LUT (1 KB) + per-CTA code table [26 positions][cout_pad] bytes
+// + per-epilogue-warp store staging (32 rows x nblk/4 int32)
 inline size_t gemm_smem_bytes(int nblk, int cout_pad) {
-  return (size_t)kStages * gemm_stage_bytes(nblk) + 1024 + (size_t)kPositions * cout_pad;
+  return (size_t)kStages * gemm_stage_bytes(nblk) + 1024 + (size_t)kPositions * cout_pad +
+         (size_t)kEpiWarps * 32 * (nblk / 4) * 4;
 }
 constexpr int kMaxCoutPadSmem = 2048;   // code table bound used for the smem attribute
 
-// One TMEM load of C columns (C = 16 or 8) for the calling warp's 32 lanes.
+// One TMEM load of C columns (C = 16, 8 or 4) for the calling warp's 32 lanes.
 template <int C>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&r)[C]);
 template <>
@@ -64,10 +66,23 @@ __device__ __forceinline__ void tmem_ld<8>(uint32_t taddr, uint32_t (&r)[8]) {
                : "r"(taddr));
 }
 
-__device__ __forceinline__ int32_t rscale_lut(uint32_t v, int code, const uint32_t* lut) {
-  if (!code) return (int32_t)v;
-  const uint32_t e = lut[code];
-  return (int32_t)rha_shift64((long long)(int32_t)v * (int)(e & 0xffffu), (int)(e >> 16));
+template <>
+__device__ __forceinline__ void tmem_ld<4>(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+
+// M'' = rha(M m / 2^q) (A9) = sign(M) ((|M| m + 2^(q-1)) >> q) with an
+// unsigned 32x32->64 product; e = m | q << 16 | 2^(q-1) << 20 ... packed as
+// (m, q, half); the unscaled code maps to m = 1, q = 0, half = 0 (identity),
+// so the path is branch-free.
+__device__ __forceinline__ int32_t rscale_e(uint32_t v, uint32_t e) {
+  const int32_t vi = (int32_t)v;
+  const uint32_t m = e & 0xffu, q = (e >> 8) & 0xffu, half = e >> 16;
+  const uint64_t prod = (uint64_t)(uint32_t)abs(vi) * m + half;
+  const int32_t r = (int32_t)(uint32_t)(prod >> q);
+  return vi < 0 ? -r : r;
 }
 
 // unit u -> (position index pidx, tile block, cout block); complex units first
@@ -90,8 +105,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
            const uint8_t* __restrict__ codes, int cout, int ksteps, long long tiles_pad, int tblocks, int cout_pad,
            int cin_pad, int scaling) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int kHalf = NBLK / 2;                 // columns per epilogue warp
-  constexpr int kChunk = kHalf >= 16 ? 16 : 8;    // columns per tcgen05.ld
+  constexpr int kHalf = NBLK / 4;                 // columns per epilogue warp (quarter of N)
+  constexpr int kChunk = kHalf >= 8 ? 8 : kHalf;     // columns per tcgen05.ld (bounded live registers)
   constexpr uint32_t kAccCols = 3 * NBLK;         // hh, x, ll
   constexpr uint32_t kTmemCols = 512;
   static_assert(2 * kAccCols <= kTmemCols, "double-buffered accumulators must fit TMEM");
@@ -104,6 +119,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   uint32_t* lut = tmem_slot + 4;                  // 64 entries: code -> m | q << 16
   uint8_t* s_codes = smem + kStages * stage_bytes + 1024;   // [pidx][cout_pad] codes
+  int4* s_stage = reinterpret_cast<int4*>(s_codes + kPositions * cout_pad);   // [warp][32 rows][kHalf/4] int4
   const uint32_t sbase = smem_u32(smem);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
@@ -128,14 +144,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   if (threadIdx.x >= 64 && threadIdx.x < 128) {   // inverse factors of all 64 codes (A8)
     const int code = threadIdx.x - 64;
-    int n, p, m, q;
+    int n, p, m = 1, q = 0;                        // code 0 (and invalid codes): identity
     decode_code(code, n, p);
-    uint32_t e = 0;
-    if (n >= 8) {
-      inverse_factor(n, p, m, q);
-      e = (uint32_t)m | ((uint32_t)q << 16);
-    }
-    lut[code] = e;
+    if (n >= 8) inverse_factor(n, p, m, q);
+    lut[code] = (uint32_t)m | ((uint32_t)q << 8) | ((q ? (1u << (q - 1)) : 0u) << 16);
   }
   // scale codes of every (position, cout), position-major (0 = unscaled)
   for (int i = threadIdx.x; i < kPositions * cout_pad; i += blockDim.x) {
@@ -157,8 +169,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         decode_unit(u, tblocks, nblocks, pidx, tb, nb);
         for (int pl = 0; pl < unit_planes(pidx); pl++) {
           const int plane = unit_plane0(pidx) + pl;
-          const int8_t* vh = V + (long long)(2 * plane) * tiles_pad * cin_pad + (long long)tb * ksteps * kABytesPerKStep;
-          const int8_t* vl = vh + tiles_pad * cin_pad;
+          // V: one 4 KB block per (tile block, K step, plane-piece); W: contiguous K steps
+          const int8_t* vblk = V + ((long long)tb * ksteps * (2 * kPlanes) + 2 * plane) * kVBlockBytes;
           const int8_t* wh = W + (long long)(2 * plane) * cout_pad * cin_pad + (long long)nb * ksteps * NBLK * kKStep;
           const int8_t* wl = wh + (long long)cout_pad * cin_pad;
           for (int ks = 0; ks < n_it; ks++, it++) {
@@ -169,8 +181,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint32_t ab = kn * kABytesPerKStep, bb = kn * (uint32_t)NBLK * kKStep;
             const uint32_t st = sbase + s * stage_bytes;
             mbar_arrive_expect_tx(full0 + 8 * s, 2 * ab + 2 * bb);
-            bulk_g2s(st, vh + (long long)k0 * kABytesPerKStep, ab, full0 + 8 * s);
-            bulk_g2s(st + a_bytes, vl + (long long)k0 * kABytesPerKStep, ab, full0 + 8 * s);
+            for (int kk = 0; kk < kn; kk++) {
+              const int8_t* src = vblk + (long long)(k0 + kk) * (2 * kPlanes) * kVBlockBytes;
+              bulk_g2s(st + kk * kABytesPerKStep, src, kABytesPerKStep, full0 + 8 * s);                      // hi
+              bulk_g2s(st + a_bytes + kk * kABytesPerKStep, src + kVBlockBytes, kABytesPerKStep, full0 + 8 * s);  // lo
+            }
             bulk_g2s(st + 2 * a_bytes, wh + (long long)k0 * NBLK * kKStep, bb, full0 + 8 * s);
             bulk_g2s(st + 2 * a_bytes + b_bytes, wl + (long long)k0 * NBLK * kKStep, bb, full0 + 8 * s);
           }
@@ -219,66 +234,77 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------ epilogue
     const int ew = warp - 2;
     const int quad = warp & 3;            // TMEM lane quadrant this warp may access
-    const int col0 = (ew >> 2) * kHalf;   // column half
-    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    const int col0 = (ew >> 2) * kHalf;   // column quarter
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + col0;
     const long long ps = tiles_pad * (long long)cout_pad;   // M'' slot stride
+    constexpr int kCpr = kHalf / 4;                          // int4 chunks per staged row
+    int4* stg = s_stage + ew * 32 * kCpr;
     int pc = 0;
+    // one accumulator set -> M_p = 2^16 hh + 2^8 x + ll for this warp's kHalf columns
+    auto take_plane = [&](uint32_t (&v)[kHalf]) {
+      const int b = pc & 1;
+      mbar_wait(tfull0 + 8 * b, (pc >> 1) & 1);
+      tc_fence_after();
+      const uint32_t acc = lane_base + b * kAccCols;
+#pragma unroll
+      for (int c = 0; c < kHalf; c += kChunk) {
+        uint32_t h[kChunk], x[kChunk], l[kChunk];
+        tmem_ld<kChunk>(acc + c, h);
+        tmem_ld<kChunk>(acc + NBLK + c, x);
+        tmem_ld<kChunk>(acc + 2 * NBLK + c, l);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < kChunk; j++) v[c + j] = (h[j] << 16) + (x[j] << 8) + l[j];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8 * b);
+      pc++;
+    };
+    // reverse-scale kHalf values with this unit's codes, transpose through shared
+    // memory (16-byte chunks XOR-swizzled by row) and store whole row segments.
+    auto store_slot = [&](const uint32_t (&v)[kHalf], const uint32_t* crow, int32_t* gslot) {
+#pragma unroll
+      for (int c = 0; c < kHalf; c += 4) {
+        const uint32_t c4 = crow[c >> 2];   // four consecutive couts' codes
+        int32_t v4[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) v4[j] = rscale_e(v[c + j], lut[(c4 >> (8 * j)) & 0x3fu]);
+        stg[lane * kCpr + ((c >> 2) ^ (lane & (kCpr - 1)))] = make_int4(v4[0], v4[1], v4[2], v4[3]);
+      }
+      __syncwarp();
+      constexpr int kRowsPerIt = 32 / kCpr;
+#pragma unroll
+      for (int it = 0; it < kCpr; it++) {
+        const int r = it * kRowsPerIt + lane / kCpr, cc = lane % kCpr;
+        const int4 val = stg[r * kCpr + (cc ^ (r & (kCpr - 1)))];
+        *reinterpret_cast<int4*>(gslot + (long long)r * cout_pad + cc * 4) = val;
+      }
+      __syncwarp();
+    };
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       int pidx, tb, nb;
       decode_unit(u, tblocks, nblocks, pidx, tb, nb);
-      const long long row = (long long)tb * kMBlock + quad * 32 + lane;
       const int cbase = nb * NBLK + col0;
-      const bool cpx = pidx < kPrimaries;
-      uint32_t re[kHalf], sm[kHalf];
-      for (int pl = 0; pl < unit_planes(pidx); pl++, pc++) {
-        const int b = pc & 1;
-        mbar_wait(tfull0 + 8 * b, (pc >> 1) & 1);
-        tc_fence_after();
-        const uint32_t acc = lane_base + b * kAccCols + col0;
-#pragma unroll
-        for (int c = 0; c < kHalf; c += kChunk) {
-          uint32_t h[kChunk], x[kChunk], l[kChunk];
-          tmem_ld<kChunk>(acc + c, h);
-          tmem_ld<kChunk>(acc + NBLK + c, x);
-          tmem_ld<kChunk>(acc + 2 * NBLK + c, l);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < kChunk; j++) {
-            const uint32_t v = (h[j] << 16) + (x[j] << 8) + l[j];
-            if (!cpx) {
-              re[c + j] = v;
-            } else if (pl == 0) {          // P0
-              re[c + j] = v;
-              sm[c + j] = v;
-            } else if (pl == 1) {          // P1: Re = P0 - P1, S = P0 + P1
-              re[c + j] -= v;
-              sm[c + j] += v;
-            } else {                       // P2: Im = P2 - P0 - P1
-              sm[c + j] = v - sm[c + j];
-            }
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty0 + 8 * b);
-      }
-      // reverse scaling and store of M'' (slots: real s, Re 16+k, Im 26+k)
-      const int slot_re = cpx ? kRealPlanes + pidx : pidx - kPrimaries;
-      int32_t* out_re = Mpp + (long long)slot_re * ps + row * cout_pad + cbase;
-      int32_t* out_im = Mpp + (long long)(kRealPlanes + kPrimaries + pidx) * ps + row * cout_pad + cbase;
+      const long long row0 = (long long)tb * kMBlock + quad * 32;
       const uint32_t* crow = reinterpret_cast<const uint32_t*>(s_codes + pidx * cout_pad + cbase);
+      if (pidx >= kPrimaries) {                    // real position: one plane
+        uint32_t v[kHalf];
+        take_plane(v);
+        store_slot(v, crow, Mpp + (long long)(pidx - kPrimaries) * ps + row0 * cout_pad + cbase);
+      } else {                                     // complex primary: Karatsuba P0, P1, P2
+        uint32_t re[kHalf], sm[kHalf], v[kHalf];
+        take_plane(re);                            // P0
 #pragma unroll
-      for (int c = 0; c < kHalf; c += 4) {
-        int32_t r4[4], i4[4];
-        const uint32_t c4 = crow[c >> 2];   // four consecutive couts' codes
+        for (int j = 0; j < kHalf; j++) sm[j] = re[j];
+        take_plane(v);                             // P1: Re = P0 - P1, S = P0 + P1
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const int code = (int)((c4 >> (8 * j)) & 0xffu);
-          r4[j] = rscale_lut(re[c + j], code, lut);
-          if (cpx) i4[j] = rscale_lut(sm[c + j], code, lut);
-        }
-        *reinterpret_cast<int4*>(out_re + c) = make_int4(r4[0], r4[1], r4[2], r4[3]);
-        if (cpx) *reinterpret_cast<int4*>(out_im + c) = make_int4(i4[0], i4[1], i4[2], i4[3]);
+        for (int j = 0; j < kHalf; j++) { re[j] -= v[j]; sm[j] += v[j]; }
+        take_plane(v);                             // P2: Im = P2 - P0 - P1
+#pragma unroll
+        for (int j = 0; j < kHalf; j++) sm[j] = v[j] - sm[j];
+        store_slot(re, crow, Mpp + (long long)(kRealPlanes + pidx) * ps + row0 * cout_pad + cbase);
+        store_slot(sm, crow, Mpp + (long long)(kRealPlanes + kPrimaries + pidx) * ps + row0 * cout_pad + cbase);
       }
     }
   }

@@ -2,12 +2,17 @@
 // Gaussian arithmetic, Karatsuba operand planes and
 // int8 piece split, written in the pre-tiled UMMA layout (layout.cuh).
 //
-// CTA = 256 threads = 16 tiles x 16 input channels (one 16-byte K half of a
-// core-matrix row).  Phase 1 stages the 16 overlapping 6x6 patches in shared
-// memory (one 16-byte vector per pixel for NHWC with Cin % 16 == 0),
-// phase 2 transforms one (tile, channel) per thread -- only the 16 real
-// values and the 10 conjugate primaries are formed -- and stages
-// the 92 output bytes, phase 3 writes whole 16-byte core-matrix rows.
+// Thread = (tile, pair of adjacent input channels).  A warp covers 4
+// consecutive tiles (4 consecutive rows of one core matrix) x 16 channels
+// (one 16-byte K half), so every 2-byte store of the warp lands in one
+// contiguous 64-byte run.  Per channel only the 16 real values and the 10
+// conjugate primaries are formed: d' = B^T d column by column,
+// then the same combinations along each row of d'.  The two channels'
+// values v0, v1 of a plane are packed with one PRMT into
+// [lo0, lo1, hi0, hi1] (lo = v & 255, hi = v >> 8 as int8 -- the low two
+// bytes of the two's complement int32) and stored as two 16-bit halves.
+// All 92 plane-pieces of a (tile block, K step) are 4 KB apart, so every
+// store is an immediate offset from one base pointer.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -16,128 +21,180 @@
 
 namespace wino {
 
-constexpr int kTilesPerCta = 16;
-constexpr int kChPerCta = 16;
+constexpr int kInWarps = 8;
+constexpr int kInTilesPerWarp = 4;
+constexpr int kInTilesPerCta = kInWarps * kInTilesPerWarp;   // 32
+constexpr int kInChPerCta = 16;
 
-__global__ void __launch_bounds__(256) k_input_transform(Geom g, const int8_t* __restrict__ x, int n0, int imgs,
-                                                         int8_t* __restrict__ vimg) {
-  __shared__ __align__(16) int8_t s_patch[kTilesPerCta][36][kChPerCta];
-  __shared__ __align__(16) int8_t s_out[2 * kPlanes][kTilesPerCta][kChPerCta];
-  const int tid = threadIdx.x;
-  const long long t0 = (long long)blockIdx.x * kTilesPerCta;
-  const int ci0 = blockIdx.y * kChPerCta;
-  const long long tiles = (long long)imgs * g.tpi;
+// Sign-extend byte `b` of w: PTX prmt default mode replicates the byte's msb
+// for selector nibbles with bit 3 set (CUDA's __byte_perm masks that bit off).
+__device__ __forceinline__ int sbyte(uint32_t w, int b) {
+  const uint32_t sel = b == 0 ? 0x8880u : (b == 1 ? 0x9991u : (b == 2 ? 0xAAA2u : 0xBBB3u));
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "r"(sel));
+  return (int)r;
+}
 
-  // ---- phase 1: gather the zero-padded 6x6 patches (origin (4ty - pad, 4tx - pad))
-  const bool vec = (g.layout == 1) && (g.cin % 16 == 0);
-  if (vec) {
-    for (int idx = tid; idx < kTilesPerCta * 36; idx += blockDim.x) {
-      int tl = idx / 36, pix = idx % 36;
-      long long t = t0 + tl;
-      int4 v = make_int4(0, 0, 0, 0);
-      if (t < tiles) {
-        int img = n0 + (int)(t / g.tpi), rem = (int)(t % g.tpi);
-        int iy = 4 * (rem / g.tw) - g.pad + pix / 6, ix = 4 * (rem % g.tw) - g.pad + pix % 6;
-        if (iy >= 0 && iy < g.h && ix >= 0 && ix < g.w)
-          v = __ldg(reinterpret_cast<const int4*>(x + (((long long)img * g.h + iy) * g.w + ix) * g.cin + ci0));
-      }
-      *reinterpret_cast<int4*>(&s_patch[tl][pix][0]) = v;
-    }
-  } else {
-    for (int idx = tid; idx < kTilesPerCta * 36 * kChPerCta; idx += blockDim.x) {
-      int tl = idx / (36 * kChPerCta), rest = idx % (36 * kChPerCta);
-      int ch, pix;
-      if (g.layout == 0) { ch = rest / 36; pix = rest % 36; }   // NCHW: spatial fastest
-      else { pix = rest / kChPerCta; ch = rest % kChPerCta; }
-      long long t = t0 + tl;
-      int c = ci0 + ch;
-      int8_t v = 0;
-      if (t < tiles && c < g.cin) {
-        int img = n0 + (int)(t / g.tpi), rem = (int)(t % g.tpi);
-        int iy = 4 * (rem / g.tw) - g.pad + pix / 6, ix = 4 * (rem % g.tw) - g.pad + pix % 6;
-        if (iy >= 0 && iy < g.h && ix >= 0 && ix < g.w)
-          v = g.layout == 0 ? x[(((long long)img * g.cin + c) * g.h + iy) * g.w + ix]
-                            : x[(((long long)img * g.h + iy) * g.w + ix) * g.cin + c];
-      }
-      s_patch[tl][pix][ch] = v;
-    }
-  }
-  __syncthreads();
+// The 46 operand-plane values of one channel from d' rows (e0, e1, e2, e5 real;
+// row 3 = ra + i rb), in plane order (layout.cuh).
+struct Rows {
+  int e0[6], e1[6], e2[6], e5[6], ra[6], rb[6];
+};
 
-  // ---- phase 2: one (tile, channel) per thread
+template <int RI>
+__device__ __forceinline__ void real_row_planes(const int (&e)[6], int (&v)[7]) {
+  const int s24 = e[2] + e[4], s13 = e[1] + e[3];
+  v[0] = e[0] - e[4];          // (R[RI], 0)
+  v[1] = s13 + s24;            // (R[RI], 1)
+  v[2] = s24 - s13;            // (R[RI], 2)
+  v[3] = e[5] - e[1];          // (R[RI], 5)
+  v[4] = e[4] - e[2];          // Re (R[RI], 3)
+  v[5] = e[3] - e[1];          // Im (R[RI], 3)
+  v[6] = v[4] + v[5];          // Re + Im
+}
+
+__device__ __forceinline__ void st16(int8_t* p, uint32_t v) { *reinterpret_cast<uint16_t*>(p) = (uint16_t)v; }
+
+// Store plane `pl` for both channels: piece 0 (hi) and piece 1 (lo), 4 KB apart per piece.
+template <int PL>
+__device__ __forceinline__ void store_plane(int8_t* base, int v0, int v1) {
+  const uint32_t pk = __byte_perm((uint32_t)v0, (uint32_t)v1, 0x5140);   // [lo0, lo1, hi0, hi1]
+  st16(base + (2 * PL + 0) * 4096, pk >> 16);                            // hi pair (s8)
+  st16(base + (2 * PL + 1) * 4096, pk);                                  // lo pair (u8)
+}
+
+__global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const int8_t* __restrict__ x, int n0,
+                                                                   int imgs, int8_t* __restrict__ vimg) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tl = lane >> 3, cp = lane & 7;                      // tile within warp, channel pair
+  const int t = blockIdx.x * kInTilesPerCta + warp * kInTilesPerWarp + tl;   // chunk tile
+  const int c = blockIdx.y * kInChPerCta + 2 * cp;              // first channel of the pair
+  const int tiles = imgs * g.tpi;
+
+  // ---- gather the zero-padded 6x6 patch at origin (4ty - pad, 4tx - pad): 2 channels per pixel
+  uint32_t w[36];
   {
-    const int tl = tid >> 4, ch = tid & 15;
-    int d[6][6];
-#pragma unroll
-    for (int a = 0; a < 6; a++)
-#pragma unroll
-      for (int b = 0; b < 6; b++) d[a][b] = s_patch[tl][a * 6 + b][ch];
-    // d' = B^T d, row formulas of P:184-189 (row 4 = conj(row 3) is not formed)
-    int e0[6], e1[6], e2[6], e5[6], ra[6], rb[6];
-#pragma unroll
-    for (int j = 0; j < 6; j++) {
-      int s24 = d[2][j] + d[4][j], s13 = d[1][j] + d[3][j];
-      e0[j] = d[0][j] - d[4][j];
-      e1[j] = s13 + s24;
-      e2[j] = s24 - s13;
-      ra[j] = d[4][j] - d[2][j];     // Re d'[3][j]
-      rb[j] = d[3][j] - d[1][j];     // Im d'[3][j]
-      e5[j] = d[5][j] - d[1][j];
+    int img = 0, iy0 = -1000000, ix0 = -1000000;   // padding tiles read nothing
+    if (t < tiles) {
+      const int rem = t % g.tpi, ty = rem / g.tw;
+      img = n0 + t / g.tpi;
+      iy0 = 4 * ty - g.pad;
+      ix0 = 4 * (rem - ty * g.tw) - g.pad;
     }
-    int v[46];
-    // D = d' B: the same combinations along each row; real rows first
-    const int* rows[4] = {e0, e1, e2, e5};
+    const bool cok = c < g.cin;
+    bool vx[6];
 #pragma unroll
-    for (int ri = 0; ri < 4; ri++) {
-      const int* e = rows[ri];
-      int s24 = e[2] + e[4], s13 = e[1] + e[3];
-      v[ri * 4 + 0] = e[0] - e[4];
-      v[ri * 4 + 1] = s13 + s24;
-      v[ri * 4 + 2] = s24 - s13;
-      v[ri * 4 + 3] = e[5] - e[1];
-      int re = e[4] - e[2], im = e[3] - e[1];        // primary k = ri : (R[ri], 3)
-      v[16 + 3 * ri + 0] = re;
-      v[16 + 3 * ri + 1] = im;
-      v[16 + 3 * ri + 2] = re + im;
-    }
-    // complex row 3 (a + i b): columns 0, 1, 2, 5 -> primaries k = 4..7
-    {
-      int as24 = ra[2] + ra[4], as13 = ra[1] + ra[3], bs24 = rb[2] + rb[4], bs13 = rb[1] + rb[3];
-      int re[4] = {ra[0] - ra[4], as13 + as24, as24 - as13, ra[5] - ra[1]};
-      int im[4] = {rb[0] - rb[4], bs13 + bs24, bs24 - bs13, rb[5] - rb[1]};
+    for (int b = 0; b < 6; b++) vx[b] = cok && ix0 + b >= 0 && ix0 + b < g.w;
+    if (g.layout == 1 && (g.cin & 1) == 0) {
+      // NHWC, even Cin: one 16-bit load per pixel; row pointer hoisted, column offsets b*Cin
+      const int8_t* p0 = x + ((long long)img * g.h * g.w + (long long)iy0 * g.w + ix0) * g.cin + c;
+      const long long rstride = (long long)g.w * g.cin;
 #pragma unroll
-      for (int c = 0; c < 4; c++) {
-        v[16 + 3 * (4 + c) + 0] = re[c];
-        v[16 + 3 * (4 + c) + 1] = im[c];
-        v[16 + 3 * (4 + c) + 2] = re[c] + im[c];
+      for (int a = 0; a < 6; a++) {
+        const bool vy = iy0 + a >= 0 && iy0 + a < g.h;
+        const uint16_t* rp = reinterpret_cast<const uint16_t*>(p0 + a * rstride);
+#pragma unroll
+        for (int b = 0; b < 6; b++) w[a * 6 + b] = (vy && vx[b]) ? (uint32_t)__ldg(rp + (b * g.cin >> 1)) : 0u;
       }
-      // (3,3) = (e4 - e2) + i (e3 - e1),  (3,4) = (e4 - e2) - i (e3 - e1), e = a + i b
-      int r33 = ra[4] - ra[2] - rb[3] + rb[1], i33 = rb[4] - rb[2] + ra[3] - ra[1];
-      int r34 = ra[4] - ra[2] + rb[3] - rb[1], i34 = rb[4] - rb[2] - ra[3] + ra[1];
-      v[16 + 3 * 8 + 0] = r33; v[16 + 3 * 8 + 1] = i33; v[16 + 3 * 8 + 2] = r33 + i33;
-      v[16 + 3 * 9 + 0] = r34; v[16 + 3 * 9 + 1] = i34; v[16 + 3 * 9 + 2] = r34 + i34;
-    }
+    } else {
+      // generic path (NCHW or odd Cin): byte loads
+      const long long cstep = g.layout == 1 ? 1 : (long long)g.h * g.w;
 #pragma unroll
-    for (int pl = 0; pl < kPlanes; pl++) {
-      s_out[2 * pl + 0][tl][ch] = (int8_t)(v[pl] >> 8);             // hi, s8
-      s_out[2 * pl + 1][tl][ch] = (int8_t)(uint8_t)(v[pl] & 255);   // lo, u8
+      for (int a = 0; a < 6; a++)
+#pragma unroll
+        for (int b = 0; b < 6; b++) {
+          const int iy = iy0 + a, ix = ix0 + b;
+          uint32_t v = 0;
+          if (vx[b] && iy >= 0 && iy < g.h) {
+            const long long i0 = g.layout == 1 ? (((long long)img * g.h + iy) * g.w + ix) * g.cin + c
+                                               : (((long long)img * g.cin + c) * g.h + iy) * g.w + ix;
+            v = (uint8_t)__ldg(x + i0);
+            if (c + 1 < g.cin) v |= (uint32_t)(uint8_t)__ldg(x + i0 + cstep) << 8;
+          }
+          w[a * 6 + b] = v;
+        }
     }
   }
-  __syncthreads();
 
-  // ---- phase 3: 16-byte rows of the pre-tiled V image
-  for (int idx = tid; idx < 2 * kPlanes * kTilesPerCta; idx += blockDim.x) {
-    int pp = idx / kTilesPerCta, tl = idx % kTilesPerCta;
-    int4 val = *reinterpret_cast<const int4*>(&s_out[pp][tl][0]);
-    *reinterpret_cast<int4*>(vimg + v_offset(g, pp, t0 + tl, ci0)) = val;
+  // ---- d' = B^T d per column, for both channels
+  Rows r[2];
+#pragma unroll
+  for (int j = 0; j < 6; j++) {
+#pragma unroll
+    for (int ch = 0; ch < 2; ch++) {
+      const int d0 = sbyte(w[0 * 6 + j], ch), d1 = sbyte(w[1 * 6 + j], ch), d2 = sbyte(w[2 * 6 + j], ch);
+      const int d3 = sbyte(w[3 * 6 + j], ch), d4 = sbyte(w[4 * 6 + j], ch), d5 = sbyte(w[5 * 6 + j], ch);
+      const int s24 = d2 + d4, s13 = d1 + d3;
+      r[ch].e0[j] = d0 - d4;
+      r[ch].e1[j] = s13 + s24;
+      r[ch].e2[j] = s24 - s13;
+      r[ch].ra[j] = d4 - d2;     // Re d'[3][j]
+      r[ch].rb[j] = d3 - d1;     // Im d'[3][j]
+      r[ch].e5[j] = d5 - d1;
+    }
+  }
+
+  // ---- D = d' B along rows; store every plane as soon as it is formed
+  const long long tb = t / kMBlock;
+  const int row = t % kMBlock;
+  const int k = c;   // channel index inside cin_pad
+  int8_t* base = vimg + (tb * g.ksteps + (k >> 5)) * (long long)(2 * kPlanes * 4096) + (row >> 3) * 256 +
+                 ((k >> 4) & 1) * 128 + (row & 7) * 16 + (k & 15);
+  {
+    int v0[7], v1[7];
+    real_row_planes<0>(r[0].e0, v0); real_row_planes<0>(r[1].e0, v1);
+    store_plane<0>(base, v0[0], v1[0]); store_plane<1>(base, v0[1], v1[1]);
+    store_plane<2>(base, v0[2], v1[2]); store_plane<3>(base, v0[3], v1[3]);
+    store_plane<16>(base, v0[4], v1[4]); store_plane<17>(base, v0[5], v1[5]); store_plane<18>(base, v0[6], v1[6]);
+    real_row_planes<1>(r[0].e1, v0); real_row_planes<1>(r[1].e1, v1);
+    store_plane<4>(base, v0[0], v1[0]); store_plane<5>(base, v0[1], v1[1]);
+    store_plane<6>(base, v0[2], v1[2]); store_plane<7>(base, v0[3], v1[3]);
+    store_plane<19>(base, v0[4], v1[4]); store_plane<20>(base, v0[5], v1[5]); store_plane<21>(base, v0[6], v1[6]);
+    real_row_planes<2>(r[0].e2, v0); real_row_planes<2>(r[1].e2, v1);
+    store_plane<8>(base, v0[0], v1[0]); store_plane<9>(base, v0[1], v1[1]);
+    store_plane<10>(base, v0[2], v1[2]); store_plane<11>(base, v0[3], v1[3]);
+    store_plane<22>(base, v0[4], v1[4]); store_plane<23>(base, v0[5], v1[5]); store_plane<24>(base, v0[6], v1[6]);
+    real_row_planes<3>(r[0].e5, v0); real_row_planes<3>(r[1].e5, v1);
+    store_plane<12>(base, v0[0], v1[0]); store_plane<13>(base, v0[1], v1[1]);
+    store_plane<14>(base, v0[2], v1[2]); store_plane<15>(base, v0[3], v1[3]);
+    store_plane<25>(base, v0[4], v1[4]); store_plane<26>(base, v0[5], v1[5]); store_plane<27>(base, v0[6], v1[6]);
+  }
+  // complex row 3 = a + i b: columns 0, 1, 2, 5 -> primaries 4..7; (3,3) -> 8; (3,4) -> 9
+  {
+    int re[2][4], im[2][4], q[2][4];
+#pragma unroll
+    for (int ch = 0; ch < 2; ch++) {
+      const int* a = r[ch].ra;
+      const int* b = r[ch].rb;
+      const int as24 = a[2] + a[4], as13 = a[1] + a[3], bs24 = b[2] + b[4], bs13 = b[1] + b[3];
+      re[ch][0] = a[0] - a[4]; re[ch][1] = as13 + as24; re[ch][2] = as24 - as13; re[ch][3] = a[5] - a[1];
+      im[ch][0] = b[0] - b[4]; im[ch][1] = bs13 + bs24; im[ch][2] = bs24 - bs13; im[ch][3] = b[5] - b[1];
+      // (3,3) = (e4 - e2) + i (e3 - e1),  (3,4) = (e4 - e2) - i (e3 - e1), e = a + i b
+      q[ch][0] = a[4] - a[2] - b[3] + b[1];
+      q[ch][1] = b[4] - b[2] + a[3] - a[1];
+      q[ch][2] = a[4] - a[2] + b[3] - b[1];
+      q[ch][3] = b[4] - b[2] - a[3] + a[1];
+    }
+    store_plane<28>(base, re[0][0], re[1][0]); store_plane<29>(base, im[0][0], im[1][0]);
+    store_plane<30>(base, re[0][0] + im[0][0], re[1][0] + im[1][0]);
+    store_plane<31>(base, re[0][1], re[1][1]); store_plane<32>(base, im[0][1], im[1][1]);
+    store_plane<33>(base, re[0][1] + im[0][1], re[1][1] + im[1][1]);
+    store_plane<34>(base, re[0][2], re[1][2]); store_plane<35>(base, im[0][2], im[1][2]);
+    store_plane<36>(base, re[0][2] + im[0][2], re[1][2] + im[1][2]);
+    store_plane<37>(base, re[0][3], re[1][3]); store_plane<38>(base, im[0][3], im[1][3]);
+    store_plane<39>(base, re[0][3] + im[0][3], re[1][3] + im[1][3]);
+    store_plane<40>(base, q[0][0], q[1][0]); store_plane<41>(base, q[0][1], q[1][1]);
+    store_plane<42>(base, q[0][0] + q[0][1], q[1][0] + q[1][1]);
+    store_plane<43>(base, q[0][2], q[1][2]); store_plane<44>(base, q[0][3], q[1][3]);
+    store_plane<45>(base, q[0][2] + q[0][3], q[1][2] + q[1][3]);
   }
 }
 
 cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st) {
-  long long tiles = (long long)imgs * g.tpi;
-  long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
-  dim3 grid((unsigned)(tiles_pad / kTilesPerCta), g.cin_pad / kChPerCta);
-  k_input_transform<<<grid, 256, 0, st>>>(g, x, n0, imgs, vimg);
+  const long long tiles = (long long)imgs * g.tpi;
+  const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
+  dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
+  k_input_transform<<<grid, kInWarps * 32, 0, st>>>(g, x, n0, imgs, vimg);
   return cudaGetLastError();
 }
 

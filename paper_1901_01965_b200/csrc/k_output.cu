@@ -27,15 +27,25 @@
 
 namespace wino {
 
+constexpr int kOutCoBlock = 64;                       // couts per CTA
+constexpr int kOutTiles = 256 / kOutCoBlock;            // tiles per CTA
+
+// |Y| < 2^31 - 8 for every supported plan (16 * 128^2 * 9 * 896 < 2^31 - 8),
+// so rha(Y / 16) is exact in 32-bit arithmetic.
+__device__ __forceinline__ int32_t rha16_32(uint32_t yv) {
+  const int32_t y = (int32_t)yv;
+  const int32_t r = (abs(y) + 8) >> 4;
+  return y < 0 ? -r : r;
+}
+
 __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t* __restrict__ M, int n0, int imgs,
                                                           int32_t rq_mult, int rq_shift, void* __restrict__ y) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long total = (long long)imgs * g.tpi * g.cout;
-  if (idx >= total) return;
-  const int co = (int)(idx % g.cout);
-  const long long t = idx / g.cout;
+  const int tl = threadIdx.x / kOutCoBlock, cl = threadIdx.x % kOutCoBlock;
+  const int t = blockIdx.x * kOutTiles + tl;              // chunk tile
+  const int co = blockIdx.y * kOutCoBlock + cl;
+  if (t >= imgs * g.tpi || co >= g.cout) return;
   const long long ps = g.chunk_tiles_pad * (long long)g.cout_pad;
-  const int32_t* mp = M + t * g.cout_pad + co;
+  const int32_t* mp = M + (long long)t * g.cout_pad + co;
 
   uint32_t mr[16], cr[10], cim[10];
 #pragma unroll
@@ -64,9 +74,17 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
     zr[2] = w1r + w2r - w3r - w4r;              zi[2] = w1i + w2i - w3i - w4i;
     zr[3] = w1r - w2r + w3i - w4i + w5r;        zi[3] = w1i - w2i - w3r + w4r + w5i;
   }
-  const int rem = (int)(t % g.tpi);
-  const int img = n0 + (int)(t / g.tpi);
-  const int ty = rem / g.tw, tx = rem % g.tw;
+  const int img = n0 + t / g.tpi, rem = t % g.tpi;
+  const int ty = rem / g.tw, tx = rem - ty * g.tw;
+  // output element (oy, ox) = base + oy * ystride + ox * xstride
+  const bool nhwc = g.layout == 1;
+  const long long ebase = nhwc ? (long long)img * g.ho * g.wo * g.cout + co : ((long long)img * g.cout + co) * g.ho * g.wo;
+  const int xstride = nhwc ? g.cout : 1, ystride = nhwc ? g.wo * g.cout : g.wo;
+  const int oy0 = 4 * ty, ox0 = 4 * tx;
+  const int ni = min(4, g.ho - oy0), nj = min(4, g.wo - ox0);
+  // requantisation fast path: multiplier 1 and shift <= 30 fit 32-bit arithmetic
+  const bool rq_fast = rq_mult == 1 && rq_shift <= 30;
+  const uint32_t rq_half = rq_shift > 0 ? (1u << (rq_shift - 1)) : 0u;
 #pragma unroll
   for (int j = 0; j < 4; j++) {
     uint32_t Yc[4];
@@ -74,21 +92,25 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
     Yc[1] = Z[1][j] - Z[2][j] - 2 * zi[j];
     Yc[2] = Z[1][j] + Z[2][j] - 2 * zr[j];
     Yc[3] = Z[1][j] - Z[2][j] + Z[3][j] + 2 * zi[j];
-    const int ox = 4 * tx + j;
-    if (ox >= g.wo) continue;
+    if (j >= nj) continue;
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-      const int oy = 4 * ty + i;
-      if (oy >= g.ho) continue;
-      const int32_t o32 = (int32_t)rha_shift64((long long)(int32_t)Yc[i], 4);   // rha(Y / 16)
-      const long long yi = g.layout == 1 ? (((long long)img * g.ho + oy) * g.wo + ox) * g.cout + co
-                                         : (((long long)img * g.cout + co) * g.ho + oy) * g.wo + ox;
+      if (i >= ni) continue;
+      const int32_t o32 = rha16_32(Yc[i]);   // rha(Y / 16)
+      const long long yi = ebase + (long long)(oy0 + i) * ystride + (ox0 + j) * xstride;
       if (g.out_mode == 1) {
         static_cast<int32_t*>(y)[yi] = o32;
       } else {
-        long long r = rq_shift > 0 ? rha_shift64((long long)o32 * rq_mult, rq_shift) : (long long)o32 * rq_mult;
-        r = r > 127 ? 127 : (r < -128 ? -128 : r);
-        static_cast<int8_t*>(y)[yi] = (int8_t)r;
+        int32_t r8;
+        if (rq_fast) {
+          const uint32_t a = (uint32_t)abs(o32);
+          const int32_t r = (int32_t)((a + rq_half) >> rq_shift);   // |o32| <= 2^31 - 1 + 2^29 < 2^32
+          r8 = o32 < 0 ? max(-r, -128) : min(r, 127);
+        } else {
+          long long r = rq_shift > 0 ? rha_shift64((long long)o32 * rq_mult, rq_shift) : (long long)o32 * rq_mult;
+          r8 = (int32_t)(r > 127 ? 127 : (r < -128 ? -128 : r));
+        }
+        static_cast<int8_t*>(y)[yi] = (int8_t)r8;
       }
     }
   }
@@ -96,9 +118,9 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
 
 cudaError_t launch_output_transform(const Geom& g, const int32_t* m, int n0, int imgs, int32_t rq_mult,
                                     int rq_shift, void* y, cudaStream_t st) {
-  long long total = (long long)imgs * g.tpi * g.cout;
-  unsigned blocks = (unsigned)((total + 255) / 256);
-  k_output_transform<<<blocks, 256, 0, st>>>(g, m, n0, imgs, rq_mult, rq_shift, y);
+  const int tiles = imgs * g.tpi;
+  dim3 grid((unsigned)((tiles + kOutTiles - 1) / kOutTiles), (unsigned)((g.cout + kOutCoBlock - 1) / kOutCoBlock));
+  k_output_transform<<<grid, 256, 0, st>>>(g, m, n0, imgs, rq_mult, rq_shift, y);
   return cudaGetLastError();
 }
 

@@ -23,7 +23,9 @@
 //     (k / 32) * R * 32  +  (r / 8) * 256  +  ((k % 32) / 16) * 128  +  (r % 8) * 16  +  k % 16
 //   (core matrix = 8 rows x 16 B; LBO = 128, SBO = 256; a 32-byte K step of
 //   the block is R*32 contiguous bytes, and all K steps are contiguous).
-//   V image: [plane][piece][tile_block][kstep][R=128 x 32 B]
+//   V image: [tile_block][kstep][plane*2 + piece][R=128 x 32 B]  (the 92
+//            plane-pieces of one (tile block, K step) 4 KB apart, so K2 stores
+//            with immediate offsets; K3 copies one 4 KB block per piece/K step)
 //   W image: [plane][piece][cout_block][kstep][R=n_block x 32 B]
 //   M''    : [slot 36][tile (chunk_tiles_pad)][cout_pad] int32, after Karatsuba
 //            recombination and reverse scaling; slot s < 16 real position s,
@@ -54,12 +56,12 @@ __host__ __device__ __forceinline__ long long tiled_offset(int r, int k, int R) 
   return (long long)(k >> 5) * R * 32 + (r >> 3) * 256 + ((k >> 4) & 1) * 128 + (r & 7) * 16 + (k & 15);
 }
 
+constexpr int kVBlockBytes = kMBlock * kKStep;   // one (plane-piece, tile block, K step) block = 4 KB
 // Byte offset of V piece `pp` (= plane*2 + piece), chunk tile t, channel k.
 __host__ __device__ __forceinline__ long long v_offset(const Geom& g, int pp, long long t, int k) {
-  long long blk = t / kMBlock;
-  int r = (int)(t % kMBlock);
-  return (long long)pp * g.chunk_tiles_pad * g.cin_pad + blk * (long long)g.ksteps * kMBlock * 32 +
-         tiled_offset(r, k, kMBlock);
+  const long long blk = t / kMBlock;
+  const int r = (int)(t % kMBlock);
+  return ((blk * g.ksteps + (k >> 5)) * (2 * kPlanes) + pp) * kVBlockBytes + tiled_offset(r, k & 31, kMBlock);
 }
 // Byte offset of W piece `pp`, output channel co, input channel k.
 __host__ __device__ __forceinline__ long long w_offset(const Geom& g, int pp, int co, int k) {

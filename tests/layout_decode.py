@@ -27,6 +27,19 @@ def decode_pieces(buf: np.ndarray, rows: int, R_rows: int, ksteps: int, cin: int
     return out
 
 
+def decode_v(buf: np.ndarray, tiles: int, ksteps: int, cin: int):
+    """V image [tile_block][kstep][92 plane-pieces][4 KB] -> int [46][tiles][cin] (hi*256 + lo)."""
+    t = np.arange(tiles)[:, None]; k = np.arange(cin)[None, :]
+    blk = ((t // 128) * ksteps + (k >> 5)) * 92
+    within = tiled_offset(t % 128, k & 31, 128)
+    out = np.zeros((46, tiles, cin), np.int64)
+    for pl in range(46):
+        hi = buf[(blk + 2 * pl) * 4096 + within].astype(np.int64)
+        lo = buf[(blk + 2 * pl + 1) * 4096 + within].astype(np.int64) & 255
+        out[pl] = hi * 256 + lo
+    return out
+
+
 def complex_to_planes(Z: np.ndarray) -> np.ndarray:
     """Z [..., 36, 2] (re, im per position) -> [46, ...] plane values."""
     planes = [Z[..., p, 0] for p in REAL_POS]

@@ -59,8 +59,7 @@ def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates
             # K2: V planes of every tile, byte exact
             T = int(info.tiles)
             vbuf = conv.v_image().cpu().numpy()
-            vpl = LD.decode_pieces(vbuf, T, 128, info.cin_pad // 32, info.cin_pad,
-                                   info.chunk_tiles_pad * info.cin_pad)
+            vpl = LD.decode_v(vbuf, T, info.cin_pad // 32, info.cin_pad)
             D = O.input_transform(x, pad, layout)
             np.testing.assert_array_equal(vpl[:, :, :ci], LD.complex_to_planes(D))
             # K3: M'' (GEMMs + Karatsuba recombination + reverse scaling) == oracle M''
