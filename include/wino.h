@@ -186,6 +186,13 @@ wino_status wino_conv2d_int8_stage(wino_plan_t plan, int stage, int chunk, const
 wino_status wino_check_codes(wino_plan_t plan, const uint8_t *scale_codes, int32_t *bad_flag,
                              void *stream);
 
+/* Debug only: when `device_buffer` is non-NULL, subsequent GEMM (K3) launches
+ * write a per-CTA timeline of globaltimer stamps into it (uint64
+ * [grid][16 planes][6 events]: producer issued, MMA saw data, MMA got TMEM
+ * buffer, MMA committed, epilogue saw accumulators, epilogue finished unit).
+ * The buffer must hold num_SMs * 96 uint64.  NULL turns tracing off.      */
+wino_status wino_debug_set_trace(void *device_buffer);
+
 /* Harness op for the VGG stack (A22): 2x2 stride-2 max pool on int8,
  * layout per `layout`, y [N][C][H/2][W/2] or [N][H/2][W/2][C].           */
 wino_status wino_maxpool2_int8(const int8_t *x, int n, int h, int w, int c, int layout,

@@ -18,7 +18,8 @@ WINO_OUT_INT8, WINO_OUT_INT32 = 0, 1
 # every symbol include/wino.h declares
 EXPORTS = ("wino_status_string", "wino_plan", "wino_plan_destroy", "wino_plan_query", "wino_filter_bytes",
            "wino_codes_bytes", "wino_workspace_bytes", "wino_output_bytes", "wino_transform_filter",
-           "wino_conv2d_int8", "wino_conv2d_int8_host", "wino_conv2d_int8_stage", "wino_check_codes", "wino_maxpool2_int8")
+           "wino_conv2d_int8", "wino_conv2d_int8_host", "wino_conv2d_int8_stage", "wino_check_codes", "wino_maxpool2_int8",
+           "wino_debug_set_trace")
 
 
 class wino_conv_desc(ctypes.Structure):
@@ -68,6 +69,7 @@ def lib():
         L.wino_conv2d_int8_stage.restype = I
         L.wino_check_codes.argtypes = [P, P, P, P]; L.wino_check_codes.restype = I
         L.wino_maxpool2_int8.argtypes = [P, I, I, I, I, I, P, P]; L.wino_maxpool2_int8.restype = I
+        L.wino_debug_set_trace.argtypes = [P]; L.wino_debug_set_trace.restype = I
         _lib = L
     return _lib
 

@@ -34,6 +34,16 @@
 
 namespace wino {
 
+// Debug timeline (wino_debug_set_trace): per CTA, per plane (first kTracePlanes),
+// globaltimer stamps: 0 producer issued loads, 1 MMA saw data, 2 MMA got TMEM
+// buffer, 3 MMA committed, 4 epilogue saw accumulators, 5 epilogue finished unit.
+constexpr int kTracePlanes = 16, kTraceEvents = 6;
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 constexpr int kStages = 4;
 constexpr int kKStepsPerStage = 2;
 constexpr int kEpiWarps = 16;                           // 4 per TMEM lane quadrant
@@ -103,7 +113,10 @@ template <int NBLK>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ Mpp,
            const uint8_t* __restrict__ codes, int cout, int ksteps, long long tiles_pad, int tblocks, int cout_pad,
-           int cin_pad, int scaling) {
+           int cin_pad, int scaling, uint64_t* __restrict__ trace) {
+  uint64_t* tr = trace ? trace + (size_t)blockIdx.x * kTracePlanes * kTraceEvents : nullptr;
+#define WINO_TRACE(plane_i, ev) \
+  do { if (tr && (plane_i) < kTracePlanes) tr[(plane_i) * kTraceEvents + (ev)] = gtimer(); } while (0)
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int kHalf = NBLK / 4;                 // columns per epilogue warp (quarter of N)
   constexpr int kChunk = kHalf >= 8 ? 8 : kHalf;     // columns per tcgen05.ld (bounded live registers)
@@ -163,11 +176,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ producer
-      int it = 0;
+      int it = 0, ppc = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         int pidx, tb, nb;
         decode_unit(u, tblocks, nblocks, pidx, tb, nb);
-        for (int pl = 0; pl < unit_planes(pidx); pl++) {
+        for (int pl = 0; pl < unit_planes(pidx); pl++, ppc++) {
           const int plane = unit_plane0(pidx) + pl;
           // V: one 4 KB block per (tile block, K step, plane-piece); W: contiguous K steps
           const int8_t* vblk = V + ((long long)tb * ksteps * (2 * kPlanes) + 2 * plane) * kVBlockBytes;
@@ -188,6 +201,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
             bulk_g2s(st + 2 * a_bytes, wh + (long long)k0 * NBLK * kKStep, bb, full0 + 8 * s);
             bulk_g2s(st + 2 * a_bytes + b_bytes, wl + (long long)k0 * NBLK * kKStep, bb, full0 + 8 * s);
+            if (ks == 0) WINO_TRACE(ppc, 0);
           }
         }
       }
@@ -205,11 +219,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int b = pc & 1;
           mbar_wait(tempty0 + 8 * b, ((pc >> 1) & 1) ^ 1);   // epilogue drained this buffer
           tc_fence_after();
+          WINO_TRACE(pc, 2);
           const uint32_t acc_hh = tmem + b * kAccCols, acc_x = acc_hh + NBLK, acc_ll = acc_hh + 2 * NBLK;
           for (int ks = 0; ks < n_it; ks++, it++) {
             const int s = it % kStages;
             mbar_wait(full0 + 8 * s, (it / kStages) & 1);
             tc_fence_after();
+            if (ks == 0) WINO_TRACE(pc, 1);
             const int k0 = ks * kKStepsPerStage;
             const int kn = min(kKStepsPerStage, ksteps - k0);
             const uint32_t st = sbase + s * stage_bytes;
@@ -227,6 +243,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             umma_commit(empty0 + 8 * s);   // stage reusable once these MMAs have read it
           }
           umma_commit(tfull0 + 8 * b);     // accumulator set b complete
+          WINO_TRACE(pc, 3);
         }
       }
     }
@@ -245,6 +262,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int b = pc & 1;
       mbar_wait(tfull0 + 8 * b, (pc >> 1) & 1);
       tc_fence_after();
+      if (warp == 2 && lane == 0) WINO_TRACE(pc, 4);
       const uint32_t acc = lane_base + b * kAccCols;
 #pragma unroll
       for (int c = 0; c < kHalf; c += kChunk) {
@@ -306,6 +324,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         store_slot(re, crow, Mpp + (long long)(kRealPlanes + pidx) * ps + row0 * cout_pad + cbase);
         store_slot(sm, crow, Mpp + (long long)(kRealPlanes + kPrimaries + pidx) * ps + row0 * cout_pad + cbase);
       }
+      if (warp == 2 && lane == 0) WINO_TRACE(pc - 1, 5);
     }
   }
   tc_fence_before();
@@ -314,6 +333,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 static int g_num_sms = 0;
+static uint64_t* g_trace = nullptr;
+void set_gemm_trace(void* buf) { g_trace = static_cast<uint64_t*>(buf); }
 
 cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t* vimg, const int8_t* wimg,
                         const uint8_t* codes, int32_t* mpp, cudaStream_t st) {
@@ -323,7 +344,7 @@ cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t*
   const size_t smem = gemm_smem_bytes(g.nblk, g.cout_pad);
 #define WINO_LAUNCH_GEMM(N)                                                                              \
   k_gemm<N><<<grid, kGemmThreads, smem, st>>>(vimg, wimg, mpp, codes, g.cout, g.ksteps, g.chunk_tiles_pad, \
-                                              tblocks, g.cout_pad, g.cin_pad, g.scaling)
+                                              tblocks, g.cout_pad, g.cin_pad, g.scaling, g_trace)
   switch (g.nblk) {
     case 16: WINO_LAUNCH_GEMM(16); break;
     case 32: WINO_LAUNCH_GEMM(32); break;
@@ -331,6 +352,7 @@ cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t*
     default: return cudaErrorInvalidValue;
   }
 #undef WINO_LAUNCH_GEMM
+#undef WINO_TRACE
   return cudaGetLastError();
 }
 

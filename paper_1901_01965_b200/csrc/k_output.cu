@@ -38,6 +38,9 @@ __device__ __forceinline__ int32_t rha16_32(uint32_t yv) {
   return y < 0 ? -r : r;
 }
 
+// NHWC: layout 1 / 0; OUT8: int8 (requantised) / int32 output; RQFAST: multiplier 1
+// and shift <= 30, so requantisation fits 32-bit arithmetic.
+template <bool NHWC, bool OUT8, bool RQFAST>
 __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t* __restrict__ M, int n0, int imgs,
                                                           int32_t rq_mult, int rq_shift, void* __restrict__ y) {
   const int tl = threadIdx.x / kOutCoBlock, cl = threadIdx.x % kOutCoBlock;
@@ -76,14 +79,14 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
   }
   const int img = n0 + t / g.tpi, rem = t % g.tpi;
   const int ty = rem / g.tw, tx = rem - ty * g.tw;
-  // output element (oy, ox) = base + oy * ystride + ox * xstride
-  const bool nhwc = g.layout == 1;
-  const long long ebase = nhwc ? (long long)img * g.ho * g.wo * g.cout + co : ((long long)img * g.cout + co) * g.ho * g.wo;
-  const int xstride = nhwc ? g.cout : 1, ystride = nhwc ? g.wo * g.cout : g.wo;
   const int oy0 = 4 * ty, ox0 = 4 * tx;
   const int ni = min(4, g.ho - oy0), nj = min(4, g.wo - ox0);
-  // requantisation fast path: multiplier 1 and shift <= 30 fit 32-bit arithmetic
-  const bool rq_fast = rq_mult == 1 && rq_shift <= 30;
+  // output element (oy0 + i, ox0 + j) = ybase + i * ystride + j * xstride (element units)
+  const int xstride = NHWC ? g.cout : 1, ystride = NHWC ? g.wo * g.cout : g.wo;
+  const long long ybase = NHWC ? (((long long)img * g.ho + oy0) * g.wo + ox0) * g.cout + co
+                               : (((long long)img * g.cout + co) * g.ho + oy0) * g.wo + ox0;
+  int8_t* y8 = static_cast<int8_t*>(y) + (OUT8 ? ybase : 0);
+  int32_t* y32 = static_cast<int32_t*>(y) + (OUT8 ? 0 : ybase);
   const uint32_t rq_half = rq_shift > 0 ? (1u << (rq_shift - 1)) : 0u;
 #pragma unroll
   for (int j = 0; j < 4; j++) {
@@ -92,25 +95,21 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
     Yc[1] = Z[1][j] - Z[2][j] - 2 * zi[j];
     Yc[2] = Z[1][j] + Z[2][j] - 2 * zr[j];
     Yc[3] = Z[1][j] - Z[2][j] + Z[3][j] + 2 * zi[j];
-    if (j >= nj) continue;
+    if (j >= nj) break;
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-      if (i >= ni) continue;
+      if (i >= ni) break;
       const int32_t o32 = rha16_32(Yc[i]);   // rha(Y / 16)
-      const long long yi = ebase + (long long)(oy0 + i) * ystride + (ox0 + j) * xstride;
-      if (g.out_mode == 1) {
-        static_cast<int32_t*>(y)[yi] = o32;
+      const int off = i * ystride + j * xstride;
+      if (!OUT8) {
+        y32[off] = o32;
+      } else if (RQFAST) {
+        const uint32_t a = (uint32_t)abs(o32);
+        const int32_t r = (int32_t)((a + rq_half) >> rq_shift);   // |o32| + 2^29 < 2^32
+        y8[off] = (int8_t)(o32 < 0 ? max(-r, -128) : min(r, 127));
       } else {
-        int32_t r8;
-        if (rq_fast) {
-          const uint32_t a = (uint32_t)abs(o32);
-          const int32_t r = (int32_t)((a + rq_half) >> rq_shift);   // |o32| <= 2^31 - 1 + 2^29 < 2^32
-          r8 = o32 < 0 ? max(-r, -128) : min(r, 127);
-        } else {
-          long long r = rq_shift > 0 ? rha_shift64((long long)o32 * rq_mult, rq_shift) : (long long)o32 * rq_mult;
-          r8 = (int32_t)(r > 127 ? 127 : (r < -128 ? -128 : r));
-        }
-        static_cast<int8_t*>(y)[yi] = (int8_t)r8;
+        long long r = rq_shift > 0 ? rha_shift64((long long)o32 * rq_mult, rq_shift) : (long long)o32 * rq_mult;
+        y8[off] = (int8_t)(r > 127 ? 127 : (r < -128 ? -128 : r));
       }
     }
   }
@@ -120,7 +119,18 @@ cudaError_t launch_output_transform(const Geom& g, const int32_t* m, int n0, int
                                     int rq_shift, void* y, cudaStream_t st) {
   const int tiles = imgs * g.tpi;
   dim3 grid((unsigned)((tiles + kOutTiles - 1) / kOutTiles), (unsigned)((g.cout + kOutCoBlock - 1) / kOutCoBlock));
-  k_output_transform<<<grid, 256, 0, st>>>(g, m, n0, imgs, rq_mult, rq_shift, y);
+  const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 30;
+#define WINO_K4(A, B, C) k_output_transform<A, B, C><<<grid, 256, 0, st>>>(g, m, n0, imgs, rq_mult, rq_shift, y)
+  if (nhwc) {
+    if (!out8) WINO_K4(true, false, false);
+    else if (fast) WINO_K4(true, true, true);
+    else WINO_K4(true, true, false);
+  } else {
+    if (!out8) WINO_K4(false, false, false);
+    else if (fast) WINO_K4(false, true, true);
+    else WINO_K4(false, true, false);
+  }
+#undef WINO_K4
   return cudaGetLastError();
 }
 

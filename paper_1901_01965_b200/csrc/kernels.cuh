@@ -21,6 +21,8 @@ cudaError_t setup_gemm();
 cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t* vimg, const int8_t* wimg,
                         const uint8_t* codes, int32_t* mpp, cudaStream_t st);
 
+void set_gemm_trace(void* buf);   // debug timeline buffer (nullptr = off)
+
 // K4: A^T M'' A + /16 + requant + store (k_output.cu)
 cudaError_t setup_output_transform();
 cudaError_t launch_output_transform(const Geom& g, const int32_t* mpp, int n0, int imgs, int32_t rq_mult,

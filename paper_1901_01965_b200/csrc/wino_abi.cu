@@ -54,7 +54,7 @@ long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 
 size_t chunk_budget_bytes() {
   const char* env = std::getenv("WINO_CHUNK_MB");
-  long mb = env ? std::atol(env) : 64;
+  long mb = env ? std::atol(env) : 128;
   if (mb < 1) mb = 1;
   return (size_t)mb << 20;
 }
@@ -241,6 +241,11 @@ wino_status wino_check_codes(wino_plan_t p, const uint8_t* codes, int32_t* bad_f
   if (!p || !codes || !bad_flag) return WINO_ERR_INVALID_ARG;
   cudaError_t e = wino::launch_check_codes(codes, p->d.c_out * 36, bad_flag, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? WINO_OK : WINO_ERR_CUDA;
+}
+
+wino_status wino_debug_set_trace(void* device_buffer) {
+  wino::set_gemm_trace(device_buffer);
+  return WINO_OK;
 }
 
 wino_status wino_maxpool2_int8(const int8_t* x, int n, int h, int w, int c, int layout, int8_t* y, void* stream) {
