@@ -121,21 +121,31 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    from paper_1901_01965_b200 import shard as SH
     cfg = synth.CONFIGS[args.config]
     layer = cfg.layers[0]
     S = synth.requant_shift(layer)
-    conv = W.WinoConv2d(layer.n, layer.h, layer.w, layer.c_in, layer.c_out, layer.pad, W.WINO_NHWC, layer.scaling,
+    # weak: every rank runs the whole configuration on its own batch; strong: the
+    # configuration's batch (or Cout for batch < world) is split over the ranks
+    sh = SH.shard(layer.n, layer.c_out, world, rank) if args.scaling == "strong" else \
+        {"mode": "replica", "n0": 0, "n": layer.n, "co0": 0, "co": layer.c_out}
+    conv = W.WinoConv2d(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad, W.WINO_NHWC, layer.scaling,
                         W.WINO_OUT_INT8, device=local_rank)
     info = conv.info
     x_bytes, y_bytes = info.x_bytes, info.y_bytes
-    w_bytes = layer.c_out * 9 * layer.c_in
+    w_bytes = sh["co"] * 9 * layer.c_in
     per_set = x_bytes + w_bytes + y_bytes
     n_sets = max(2, math.ceil(1.2 * L2_BYTES / per_set))
     xs, ws, ys = [], [], []
     for i in range(n_sets):
         # first set: the seeded config tensors; later sets: re-seeded batches of the same recipe
-        x, w = synth.config_inputs(args.config, rank=rank * 1000 + i)
-        xs.append(torch.from_numpy(x).to(dev)); ws.append(torch.from_numpy(w).to(dev))
+        if args.scaling == "strong":   # global tensors, this rank's slice
+            x, w = synth.config_inputs(args.config, rank=i)
+            x = x[sh["n0"]: sh["n0"] + sh["n"]]
+            w = np.ascontiguousarray(w[sh["co0"]: sh["co0"] + sh["co"]])
+        else:
+            x, w = synth.config_inputs(args.config, rank=rank * 1000 + i)
+        xs.append(torch.from_numpy(np.ascontiguousarray(x)).to(dev)); ws.append(torch.from_numpy(w).to(dev))
         ys.append(torch.empty(conv.y_shape, dtype=torch.int8, device=dev))
     stream = torch.cuda.Stream(device=dev)
     sp = stream.cuda_stream
@@ -188,22 +198,27 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
-    ops_step = synth.direct_ops(layer)
-    value = world * ops_step * args.steps / t_max / 1e12
+    ops_step = synth.direct_ops(layer)                     # one rank's configuration
+    job_ops = ops_step * (world if args.scaling == "weak" else 1)
+    value = job_ops * args.steps / t_max / 1e12
 
     # ---------------- per-kernel durations (roofline), same stream, outside the timed region
     kern = profile_kernels(conv, xs, ws, ys, S, stream, n_sets, 60)
     # ---------------- e2e through the C ABI with host buffers (pinned), copies inside the region
     e2e = run_e2e(conv, xs, ws, S, stream, n_sets, max(3, min(args.steps, 100)), world, dist if world > 1 else None,
-                  dev)
+                  dev, job_ops)
 
     if rank == 0:
         peaks = _peaks()
-        roof = roofline(kern, info, layer, peaks)
+        roof = roofline(kern, info, synth.LayerCfg(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad),
+                        peaks)
+        path = path_roofline(synth.LayerCfg(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad), info,
+                             peaks, t_max / args.steps)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "TOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max * 1e3 / args.steps, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "scaling": "weak" if args.scaling == "weak" else "strong", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic",
             "config": {
                 "workload": f"{cfg.name}: {cfg.description}", "batch_per_gpu": layer.n, "h": layer.h, "w": layer.w,
                 "c_in": layer.c_in, "c_out": layer.c_out, "pad": layer.pad, "layout": "NHWC",
@@ -211,10 +226,11 @@ def run_ours(args):
                 "step": "filter transform + scaling (K1) + conv (K2,K3,K4 per chunk)",
                 "l2": f"inputs/weights/outputs rotated over {n_sets} sets "
                       f"({n_sets * per_set / 2 ** 20:.0f} MiB > 126 MiB L2)",
-                "parallelism": f"dp{world} (batch-sharded, weak scaling, no data-path collective)",
+                "parallelism": f"dp{world} ({'replicated per-rank batches, weak scaling' if args.scaling == 'weak' else sh['mode'] + '-sharded, strong scaling'}; no data-path collective)",
                 "chunks": info.n_chunks, "cuda_graph": bool(graphs),
             },
             "roofline": roof["dominant"],
+            "path_roofline": path,
             "kernels": roof["all"],
             "kernel_sum_vs_step": round(sum(k["s_per_step"] for k in kern.values()) / (t_max / args.steps), 3),
             "gpu_launches": launches_per_step * args.steps,
@@ -312,7 +328,20 @@ def roofline(kern, info, layer, peaks):
     return {"dominant": dominant, "all": all_k}
 
 
-def run_e2e(conv, xs, ws, S, stream, n_sets, reps, world, dist, dev):
+def path_roofline(layer, info, peaks, t_step):
+    """t_roof = max(2*46*T*Cin*Cout / P_int8, (x + y + W') / HBM) for one
+    rank's step, and the achieved fraction of it."""
+    T = info.tiles
+    ops46 = 2 * 46 * T * layer.c_in * layer.c_out
+    byts = info.x_bytes + info.y_bytes + 92 * layer.c_in * layer.c_out + 9 * layer.c_in * layer.c_out
+    i8 = 2.0 * peaks["bf16_tflops_sustained"] * 1e12
+    t_roof = max(ops46 / i8, byts / (peaks["hbm_gbs"] * 1e9))
+    return {"t_roof_us": round(t_roof * 1e6, 3), "t_step_us": round(t_step * 1e6, 3),
+            "frac": round(t_roof / t_step, 4), "bound": "tensor" if ops46 / i8 > byts / (peaks["hbm_gbs"] * 1e9)
+            else "hbm", "roofline_effective_tops": round(synth.direct_ops(layer) / t_roof / 1e12, 1)}
+
+
+def run_e2e(conv, xs, ws, S, stream, n_sets, reps, world, dist, dev, job_ops):
     """Same metric through the C ABI with HOST buffers: every step copies x and w
     from pinned host memory, runs K1..K4, and reads y back to pinned host memory."""
     import torch
@@ -350,9 +379,7 @@ def run_e2e(conv, xs, ws, S, stream, n_sets, reps, world, dist, dev):
     t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    layer_ops = synth.direct_ops(synth.LayerCfg(conv.desc.n, conv.desc.h, conv.desc.w, conv.desc.c_in,
-                                                conv.desc.c_out, conv.desc.pad))
-    v = world * layer_ops * reps / float(t.item()) / 1e12
+    v = job_ops * reps / float(t.item()) / 1e12
     return {"value": round(v, 3), "unit": "TOPS", "h2d_bytes_per_step": int(info.x_bytes + np.prod(conv.w_shape)),
             "d2h_bytes_per_step": int(info.y_bytes), "steps": reps,
             "ms_per_step": round(float(t.item()) * 1e3 / reps, 4)}
@@ -433,6 +460,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()

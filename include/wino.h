@@ -186,7 +186,9 @@ wino_status wino_conv2d_int8_stage(wino_plan_t plan, int stage, int chunk, const
 wino_status wino_check_codes(wino_plan_t plan, const uint8_t *scale_codes, int32_t *bad_flag,
                              void *stream);
 
-/* Debug only: when `device_buffer` is non-NULL, subsequent GEMM (K3) launches
+/* Debug only (effective when libwino is built with -DWINO_K3_TRACE, e.g.
+ * WINO_NVCC_FLAGS=-DWINO_K3_TRACE python paper_1901_01965_b200/build.py --force):
+ * when `device_buffer` is non-NULL, subsequent GEMM (K3) launches
  * write a per-CTA timeline of globaltimer stamps into it (uint64
  * [grid][16 planes][6 events]: producer issued, MMA saw data, MMA got TMEM
  * buffer, MMA committed, epilogue saw accumulators, epilogue finished unit).

@@ -34,7 +34,7 @@
 
 namespace wino {
 
-// Debug timeline (wino_debug_set_trace): per CTA, per plane (first kTracePlanes),
+// Debug timeline (wino_debug_set_trace; compiled in with -DWINO_K3_TRACE): per CTA, per plane (first kTracePlanes),
 // globaltimer stamps: 0 producer issued loads, 1 MMA saw data, 2 MMA got TMEM
 // buffer, 3 MMA committed, 4 epilogue saw accumulators, 5 epilogue finished unit.
 constexpr int kTracePlanes = 16, kTraceEvents = 6;
@@ -114,9 +114,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ Mpp,
            const uint8_t* __restrict__ codes, int cout, int ksteps, long long tiles_pad, int tblocks, int cout_pad,
            int cin_pad, int scaling, uint64_t* __restrict__ trace) {
+#ifdef WINO_K3_TRACE
   uint64_t* tr = trace ? trace + (size_t)blockIdx.x * kTracePlanes * kTraceEvents : nullptr;
 #define WINO_TRACE(plane_i, ev) \
   do { if (tr && (plane_i) < kTracePlanes) tr[(plane_i) * kTraceEvents + (ev)] = gtimer(); } while (0)
+#else
+  (void)trace;
+#define WINO_TRACE(plane_i, ev) do { } while (0)
+#endif
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int kHalf = NBLK / 4;                 // columns per epilogue warp (quarter of N)
   constexpr int kChunk = kHalf >= 8 ? 8 : kHalf;     // columns per tcgen05.ld (bounded live registers)

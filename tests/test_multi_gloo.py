@@ -1,0 +1,71 @@
+"""N > 1 host logic on CPU: world_size-2 gloo process groups.  Each rank
+computes its shard with the CPU oracle (standing in for its GPU), the shards
+are gathered, and the result must equal the single-process computation;
+max-over-ranks timing is the max of the per-rank values."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import synth
+from oracle import oracle as O
+from paper_1901_01965_b200 import shard as SH
+
+
+def _free_port():
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); p = s.getsockname()[1]; s.close(); return p
+
+
+def _worker(rank, world, port, n, c_out, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(123)
+        x, w = synth.random_layer(rng, n, 9, 10, 5, c_out, O.NHWC)
+        sh = SH.shard(n, c_out, world, rank)
+        xs = x[sh["n0"]: sh["n0"] + sh["n"]]
+        ws = w[sh["co0"]: sh["co0"] + sh["co"]]
+        if xs.shape[0] and ws.shape[0]:
+            local = O.wino_conv(xs, ws, 1, O.NHWC, scaling=True).out32
+        else:
+            local = np.zeros((xs.shape[0], 9, 10, ws.shape[0]), np.int32)
+        full = SH.gather_nhwc(torch.from_numpy(local), (n, 9, 10, c_out), sh, world)
+        t = SH.max_over_ranks(float(rank + 1) * 0.5)
+        if rank == 0:
+            q.put((full.numpy(), t, sh["mode"]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,c_out", [(5, 6), (2, 7), (1, 5), (1, 1)])
+def test_sharded_equals_single(n, c_out):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, c_out, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    full, t, mode = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(123)
+    x, w = synth.random_layer(rng, n, 9, 10, 5, c_out, O.NHWC)
+    np.testing.assert_array_equal(full, O.wino_conv(x, w, 1, O.NHWC, scaling=True).out32)
+    assert t == 1.0                        # max over ranks of (0.5, 1.0)
+    assert mode == ("batch" if n >= world else "cout")
+
+
+def test_split_is_a_partition():
+    for total in range(0, 20):
+        for world in range(1, 9):
+            parts = [SH.split(total, world, r) for r in range(world)]
+            assert sum(c for _, c in parts) == total
+            pos = 0
+            for s, c in parts:
+                assert s == pos; pos += c
