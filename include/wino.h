@@ -102,6 +102,10 @@ typedef struct {
 /* Human-readable text for a status code (static storage, never NULL). */
 const char *wino_status_string(wino_status s);
 
+/* Text of the CUDA runtime error behind the calling thread's most recent
+ * WINO_ERR_CUDA ("no error" if none); static storage, never NULL.        */
+const char *wino_last_cuda_error(void);
+
 /* Validate `desc` and build an immutable plan for CUDA device `device`.
  * The plan holds host metadata only.  Returns WINO_ERR_UNSUPPORTED for
  * pad not in {0,1}, n/h/w/c < 1, h + 2 pad < 3 or w + 2 pad < 3,

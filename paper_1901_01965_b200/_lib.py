@@ -16,7 +16,7 @@ WINO_NCHW, WINO_NHWC = 0, 1
 WINO_OUT_INT8, WINO_OUT_INT32 = 0, 1
 
 # every symbol include/wino.h declares
-EXPORTS = ("wino_status_string", "wino_plan", "wino_plan_destroy", "wino_plan_query", "wino_filter_bytes",
+EXPORTS = ("wino_status_string", "wino_last_cuda_error", "wino_plan", "wino_plan_destroy", "wino_plan_query", "wino_filter_bytes",
            "wino_codes_bytes", "wino_workspace_bytes", "wino_output_bytes", "wino_transform_filter",
            "wino_conv2d_int8", "wino_conv2d_int8_host", "wino_conv2d_int8_stage", "wino_check_codes", "wino_maxpool2_int8",
            "wino_debug_set_trace")
@@ -41,7 +41,8 @@ class wino_plan_info(ctypes.Structure):
 
 class WinoError(RuntimeError):
     def __init__(self, status: int, where: str):
-        super().__init__(f"{where}: {status_string(status)} (status {status})")
+        extra = f": {lib().wino_last_cuda_error().decode()}" if status == WINO_ERR_CUDA else ""
+        super().__init__(f"{where}: {status_string(status)} (status {status}){extra}")
         self.status = status
 
 
@@ -57,6 +58,7 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         P, I, I32, SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int32, ctypes.c_size_t
         L.wino_status_string.argtypes = [I]; L.wino_status_string.restype = ctypes.c_char_p
+        L.wino_last_cuda_error.argtypes = []; L.wino_last_cuda_error.restype = ctypes.c_char_p
         L.wino_plan.argtypes = [ctypes.POINTER(wino_conv_desc), I, ctypes.POINTER(P)]; L.wino_plan.restype = I
         L.wino_plan_destroy.argtypes = [P]; L.wino_plan_destroy.restype = I
         L.wino_plan_query.argtypes = [P, ctypes.POINTER(wino_plan_info)]; L.wino_plan_query.restype = I

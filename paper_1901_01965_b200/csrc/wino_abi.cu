@@ -22,6 +22,13 @@ struct wino_plan_s {
 
 namespace {
 
+thread_local cudaError_t g_last_cuda_error = cudaSuccess;
+wino_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return WINO_OK;
+  g_last_cuda_error = e;
+  return WINO_ERR_CUDA;
+}
+
 std::mutex g_setup_mu;
 bool g_setup_done[64] = {};
 
@@ -37,7 +44,7 @@ wino_status setup_device(int device) {
   if (e == cudaSuccess) e = wino::setup_gemm();
   if (e == cudaSuccess) e = wino::setup_output_transform();
   cudaSetDevice(old);
-  if (e != cudaSuccess) return WINO_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_status(e);
   g_setup_done[device] = true;
   return WINO_OK;
 }
@@ -62,6 +69,8 @@ size_t chunk_budget_bytes() {
 }  // namespace
 
 extern "C" {
+
+const char* wino_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda_error); }
 
 const char* wino_status_string(wino_status s) {
   switch (s) {
@@ -175,7 +184,7 @@ wino_status wino_transform_filter(wino_plan_t p, const int8_t* w, void* w_wino, 
   if (st != WINO_OK) return st;
   cudaError_t e = wino::launch_filter_transform(p->g, w, static_cast<int8_t*>(w_wino), codes,
                                                 static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? WINO_OK : WINO_ERR_CUDA;
+  return cuda_status(e);
 }
 
 static wino_status run_stage(const wino_plan_s* p, int stage, int chunk, const int8_t* x, const void* w_wino,
@@ -191,7 +200,7 @@ static wino_status run_stage(const wino_plan_s* p, int stage, int chunk, const i
   if (stage == 2) e = wino::launch_input_transform(g, x, n0, imgs, vimg, s);
   if (stage == 3) e = wino::launch_gemm(g, tiles_pad, vimg, static_cast<const int8_t*>(w_wino), codes, m, s);
   if (stage == 4) e = wino::launch_output_transform(g, m, n0, imgs, rq_mult, rq_shift, y, s);
-  return e == cudaSuccess ? WINO_OK : WINO_ERR_CUDA;
+  return cuda_status(e);
 }
 
 static wino_status check_conv_args(const wino_plan_s* p, const int8_t* x, const void* w_wino, const uint8_t* codes,
@@ -230,17 +239,18 @@ wino_status wino_conv2d_int8_host(wino_plan_t p, const int8_t* x_host, const voi
                                   void* workspace, void* stream) {
   if (!p || !x_host || !y_host || !x_dev || !y_dev) return WINO_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (cudaMemcpyAsync(x_dev, x_host, p->x_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return WINO_ERR_CUDA;
+  cudaError_t ce = cudaMemcpyAsync(x_dev, x_host, p->x_bytes, cudaMemcpyHostToDevice, s);
+  if (ce != cudaSuccess) return cuda_status(ce);
   wino_status st = wino_conv2d_int8(p, x_dev, w_wino, codes, rq_mult, rq_shift, y_dev, workspace, stream);
   if (st != WINO_OK) return st;
-  if (cudaMemcpyAsync(y_host, y_dev, p->y_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return WINO_ERR_CUDA;
+  ce = cudaMemcpyAsync(y_host, y_dev, p->y_bytes, cudaMemcpyDeviceToHost, s);
+  if (ce != cudaSuccess) return cuda_status(ce);
   return WINO_OK;
 }
 
 wino_status wino_check_codes(wino_plan_t p, const uint8_t* codes, int32_t* bad_flag, void* stream) {
   if (!p || !codes || !bad_flag) return WINO_ERR_INVALID_ARG;
-  cudaError_t e = wino::launch_check_codes(codes, p->d.c_out * 36, bad_flag, static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? WINO_OK : WINO_ERR_CUDA;
+  return cuda_status(wino::launch_check_codes(codes, p->d.c_out * 36, bad_flag, static_cast<cudaStream_t>(stream)));
 }
 
 wino_status wino_debug_set_trace(void* device_buffer) {
@@ -251,8 +261,7 @@ wino_status wino_debug_set_trace(void* device_buffer) {
 wino_status wino_maxpool2_int8(const int8_t* x, int n, int h, int w, int c, int layout, int8_t* y, void* stream) {
   if (!x || !y || n < 1 || h < 2 || w < 2 || c < 1) return WINO_ERR_INVALID_ARG;
   if (layout != WINO_NCHW && layout != WINO_NHWC) return WINO_ERR_INVALID_ARG;
-  cudaError_t e = wino::launch_maxpool2(x, n, h, w, c, layout, y, static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? WINO_OK : WINO_ERR_CUDA;
+  return cuda_status(wino::launch_maxpool2(x, n, h, w, c, layout, y, static_cast<cudaStream_t>(stream)));
 }
 
 }  // extern "C"
