@@ -91,8 +91,8 @@ typedef struct {
     int n_chunks;
     long long chunk_tiles_pad;  /* tiles per chunk rounded up to m_block               */
     size_t v_offset, v_bytes;   /* V  = B^T d B operand planes inside the workspace    */
-    size_t m_offset, m_bytes;   /* M'' = 36 int32 per (tile, cout) after Karatsuba and
-                                   reverse scaling: [36][chunk_tiles_pad][cout_pad]    */
+    size_t m_offset, m_bytes;   /* M  = 36 int32 per (tile, cout) after Karatsuba,
+                                   before reverse scaling; swizzled tiles  */
     size_t workspace_bytes;
     size_t filter_bytes;        /* transformed-filter buffer (w_wino)                  */
     size_t codes_bytes;         /* c_out * 36 bytes                                    */

@@ -72,12 +72,10 @@ class WinoConv2d:
     def v_image(self):
         return self.workspace[self.info.v_offset:self.info.v_offset + self.info.v_bytes]
 
-    def m_slots(self):
-        """M'' of the last chunk: [36][chunk_tiles_pad][cout_pad] int32 (after
-        Karatsuba recombination and reverse scaling)."""
+    def m_raw(self):
+        """Raw per-plane M of the last chunk (int32, layout in DESIGN.md / layout.cuh)."""
         i = self.info
-        return self.workspace[i.m_offset:i.m_offset + i.m_bytes].view(torch.int32).view(
-            36, i.chunk_tiles_pad, i.cout_pad)
+        return self.workspace[i.m_offset:i.m_offset + i.m_bytes].view(torch.int32)
 
 
 def maxpool2(x: torch.Tensor, layout=L.WINO_NHWC, stream=None):

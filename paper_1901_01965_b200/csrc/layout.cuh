@@ -27,9 +27,14 @@
 //            plane-pieces of one (tile block, K step) 4 KB apart, so K2 stores
 //            with immediate offsets; K3 copies one 4 KB block per piece/K step)
 //   W image: [plane][piece][cout_block][kstep][R=n_block x 32 B]
-//   M''    : [slot 36][tile (chunk_tiles_pad)][cout_pad] int32, after Karatsuba
-//            recombination and reverse scaling; slot s < 16 real position s,
-//            16+k = Re and 26+k = Im of complex primary k
+//   M      : [slot 36][tile_block][cout_block][128 rows][n_block] int32 -- GEMM
+//            results after the Karatsuba recombination, before reverse scaling
+//            (K4): slot s < 16 real position s, 16+k = Re and 26+k = Im of
+//            complex primary k; within a 128 x n_block tile, element
+//            (r, c) sits at r * n_block + ((c / 4) ^ (r & swz)) * 4 + c % 4 with
+//            swz = min(n_block / 4, 8) - 1 (16-byte chunks XOR-swizzled by row,
+//            so K3's shared-memory staging is bank-conflict free and the tile
+//            leaves with one bulk copy)
 #pragma once
 #include <cstdint>
 
@@ -62,6 +67,13 @@ __host__ __device__ __forceinline__ long long v_offset(const Geom& g, int pp, lo
   const long long blk = t / kMBlock;
   const int r = (int)(t % kMBlock);
   return ((blk * g.ksteps + (k >> 5)) * (2 * kPlanes) + pp) * kVBlockBytes + tiled_offset(r, k & 31, kMBlock);
+}
+// Element offset of (chunk tile t, cout co) inside one plane of M.
+__host__ __device__ __forceinline__ long long m_offset(const Geom& g, long long t, int co) {
+  const int r = (int)(t & (kMBlock - 1)), c = co % g.nblk, nb = co / g.nblk;
+  const int cpr = g.nblk >> 2, swz = (cpr < 8 ? cpr : 8) - 1;
+  return ((t >> 7) * (long long)(g.cout_pad / g.nblk) + nb) * (kMBlock * g.nblk) + r * g.nblk +
+         (((c >> 2) ^ (r & swz)) << 2) + (c & 3);
 }
 // Byte offset of W piece `pp`, output channel co, input channel k.
 __host__ __device__ __forceinline__ long long w_offset(const Geom& g, int pp, int co, int k) {

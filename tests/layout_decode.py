@@ -56,3 +56,14 @@ def karatsuba_planes_to_complex(Mp: np.ndarray):
     p0, p1, p2 = Mp[16::3], Mp[17::3], Mp[18::3]
     wrap = lambda v: ((v + 2 ** 31) % 2 ** 32) - 2 ** 31
     return wrap(real), wrap(p0 - p1), wrap(p2 - p0 - p1)
+
+
+def decode_m(buf: np.ndarray, tiles: int, cout: int, cout_pad: int, nblk: int, tiles_pad: int, slots=36):
+    """M (int32 [slots][tile_block][cout_block][128][nblk], 16-byte chunks
+    XOR-swizzled by row) -> [slots][tiles][cout]."""
+    t = np.arange(tiles)[:, None]; c = np.arange(cout)[None, :]
+    r = t % 128; cc = c % nblk; nb = c // nblk
+    cpr = nblk // 4; swz = min(cpr, 8) - 1
+    off = ((t // 128) * (cout_pad // nblk) + nb) * (128 * nblk) + r * nblk + (((cc >> 2) ^ (r & swz)) << 2) + (cc & 3)
+    buf = buf.reshape(slots, tiles_pad * cout_pad)
+    return np.stack([buf[p][off] for p in range(slots)], 0)
