@@ -9,6 +9,7 @@
 
 #include "kernels.cuh"
 #include "layout.cuh"
+#include "ptx.cuh"
 
 namespace wino {
 
@@ -102,6 +103,8 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int co = blockIdx.x;
   const bool live = co < g.cout;
+  pdl_trigger();
+  pdl_wait();   // w_wino / codes are read by the previous step's GEMM
 
   int mx[26];
 #pragma unroll
@@ -183,8 +186,7 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
 }
 
 cudaError_t launch_filter_transform(const Geom& g, const int8_t* w, int8_t* wimg, uint8_t* codes, cudaStream_t st) {
-  k_filter_transform<<<g.cout_pad, kFilterWarps * 32, 0, st>>>(g, w, wimg, codes);
-  return cudaGetLastError();
+  return launch_pdl(k_filter_transform, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
 }
 
 cudaError_t setup_filter_transform() { return cudaSuccess; }

@@ -14,15 +14,18 @@
 // P0 = Re.Re, P1 = Im.Im, P2 = (Re+Im)(Re+Im), kept in Karatsuba form over the
 // whole channel sum and recombined once here:
 //     Re = P0 - P1,  Im = P2 - P0 - P1.
-// The output is M = 36 int32 per (tile, cout) (16 real values, 10 Re, 10 Im);
-// the reverse scaling is applied by K4, one thread per (tile, cout).
+// Then the reverse scaling M'' = rha(M m / 2^q) with (m, q)
+// derived on the device from the per-(cout, position) 6-bit codes.  The output
+// is M'' = 36 int32 per (tile, cout) (16 real values, 10 Re, 10 Im).
 // Persistent CTA per SM, warp-specialised (10 warps):
 //   warps 0..7   epilogue: warp w reads TMEM lanes 32(w%4).. (its quadrant),
 //                column half w/4; combines the pieces (and the Karatsuba planes),
 //                writes each 128 x n_block int32 output tile into a shared-memory
 //                staging buffer laid out exactly like M (16-byte chunks
-//                XOR-swizzled by row), and one thread stores the whole tile with a
-//                single bulk copy (TMA engine)
+//                XOR-swizzled by row); then every epilogue thread reverse-scales a
+//                fixed 4-column strip of the staged tile in place (4 scale entries
+//                per tile instead of one per value), and one thread stores the
+//                whole tile with a single bulk copy (TMA engine)
 //   warp 8       producer (1 lane): 1-D bulk copies of pre-tiled K stages into a
 //                kStages-deep ring, mbarrier complete_tx
 //   warp 9       MMA issuer (1 lane): tcgen05.mma, tcgen05.commit -> stage free /
@@ -56,6 +59,11 @@ __device__ __forceinline__ void decode_unit(int u, int tblocks, int nblocks, int
   nb = rest / tblocks;
   tb = rest - nb * tblocks;
 }
+// k-th unit of this CTA: boustrophedon rounds over the grid, so CTAs that draw
+// an extra three-plane unit early draw one fewer one-plane unit later.
+__device__ __forceinline__ int cta_unit(int k) {
+  return k * (int)gridDim.x + ((k & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
+}
 __device__ __forceinline__ int unit_planes(int pidx) { return pidx < kPrimaries ? 3 : 1; }
 __device__ __forceinline__ int unit_plane0(int pidx) {
   return pidx < kPrimaries ? kRealPlanes + 3 * pidx : pidx - kPrimaries;
@@ -75,10 +83,12 @@ __device__ __forceinline__ uint64_t gtimer() {
 __host__ __device__ inline uint32_t gemm_stage_bytes(int nblk) {
   return 2u * kKStepsPerStage * kABytesPerKStep + 2u * kKStepsPerStage * (uint32_t)nblk * kKStep;
 }
-// stages + 2 staging tiles (128 x nblk int32) + barriers
-inline size_t gemm_smem_bytes(int nblk) {
-  return (size_t)kStages * gemm_stage_bytes(nblk) + 2 * (size_t)kMBlock * nblk * 4 + 1024;
+// stages + 2 staging tiles (128 x nblk int32) + barriers/LUT (1 KB) + codes [26][cout_pad]
+inline size_t gemm_smem_bytes(int nblk, int cout_pad) {
+  return (size_t)kStages * gemm_stage_bytes(nblk) + 2 * (size_t)kMBlock * nblk * 4 + 1024 +
+         (size_t)(kPrimaries + kRealPlanes) * cout_pad;
 }
+constexpr int kMaxCoutPad = 2048;
 
 template <int C>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&r)[C]);
@@ -89,14 +99,25 @@ __device__ __forceinline__ void tmem_ld<8>(uint32_t taddr, uint32_t (&r)[8]) {
                : "r"(taddr));
 }
 
+// M'' = rha(M m / 2^q) = sign(M) ((|M| m + 2^(q-1)) >> q) (A9) with
+// e = m | q << 8 | 2^(q-1) << 16; the unscaled code maps to m = 1, q = 0.
+__device__ __forceinline__ int32_t rscale_e(uint32_t v, uint32_t e) {
+  const int32_t vi = (int32_t)v;
+  const uint32_t m = e & 0xffu, q = (e >> 8) & 0xffu, half = e >> 16;
+  const uint64_t prod = (uint64_t)(uint32_t)abs(vi) * m + half;
+  const int32_t r = (int32_t)(uint32_t)(prod >> q);
+  return vi < 0 ? -r : r;
+}
+
 __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync %0, %1;" ::"n"(kEpiBarrier), "n"(kEpiWarps * 32) : "memory");
 }
 
 template <int NBLK>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_gemm(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ Mraw, int ksteps,
-           long long tiles_pad, int tblocks, int cout_pad, int cin_pad, uint64_t* __restrict__ trace) {
+    k_gemm(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ Mraw,
+           const uint8_t* __restrict__ codes, int cout, int scaling, int ksteps, long long tiles_pad, int tblocks,
+           int cout_pad, int cin_pad, uint64_t* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int kHalf = NBLK / 2;                 // columns per epilogue warp (8, 16 or 32)
   constexpr int kCpr = NBLK / 4;                  // 16-byte chunks per tile row
@@ -123,6 +144,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* staging = smem + kStages * stage_bytes;                       // 2 x kTileBytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(staging + 2 * kTileBytes);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint32_t* lut = tmem_slot + 4;                                         // 64: code -> (m, q, half)
+  uint8_t* s_codes = reinterpret_cast<uint8_t*>(lut + 64);               // [26 positions][cout_pad]
   const uint32_t sbase = smem_u32(smem);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
@@ -145,6 +168,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     fence_mbar_init();
   }
+  pdl_trigger();
+  if (threadIdx.x < 64) {   // inverse factor of every 6-bit code (A8); code 0 -> identity
+    int n, p, m = 1, q = 0;
+    decode_code(threadIdx.x, n, p);
+    if (n >= 8) inverse_factor(n, p, m, q);
+    lut[threadIdx.x] = (uint32_t)m | ((uint32_t)q << 8) | ((q ? (1u << (q - 1)) : 0u) << 16);
+  }
+  pdl_wait();   // V, W' and the codes come from the kernels just before
+  for (int i = threadIdx.x; i < kPositions * cout_pad; i += blockDim.x) {   // codes, position-major
+    const int pidx = i / cout_pad, co = i - pidx * cout_pad;
+    const int pos = pidx < kPrimaries ? cpx_pos(pidx) : real_pos(pidx - kPrimaries);
+    s_codes[i] = (scaling && co < cout) ? codes[(long long)co * 36 + pos] : 0;
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -154,7 +190,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------ producer
       int it = 0, ui = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      for (int ku = 0, u = cta_unit(0); u < n_units; u = cta_unit(++ku)) {
        int pidx, tb, nb;
        decode_unit(u, tblocks, nblocks, pidx, tb, nb);
        for (int pl = 0; pl < unit_planes(pidx); pl++, ui++) {
@@ -189,7 +225,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t id_ss = idesc_i8(kMBlock, NBLK, 1, 1), id_su = idesc_i8(kMBlock, NBLK, 1, 0);
       const uint32_t id_us = idesc_i8(kMBlock, NBLK, 0, 1), id_uu = idesc_i8(kMBlock, NBLK, 0, 0);
       int it = 0, pc = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      for (int ku = 0, u = cta_unit(0); u < n_units; u = cta_unit(++ku)) {
        int pidx, tbu, nbu;
        decode_unit(u, tblocks, nblocks, pidx, tbu, nbu);
        for (int pl = 0; pl < unit_planes(pidx); pl++, pc++) {
@@ -254,14 +290,33 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) mbar_arrive(tempty0 + 8 * b);   // TMEM buffer free for the MMAs of plane pc+2
       pc++;
     };
-    // one 128 x n_block output tile -> staging buffer (to & 1) -> one bulk store
-    auto store_tile = [&](const uint32_t (&v)[kHalf], int32_t* dst) {
+    // this thread's strip in the reverse-scale pass: chunk column sc, rows sr0 + k*kStripStep
+    constexpr int kEpiThreads = kEpiWarps * 32;
+    constexpr int kStripStep = kEpiThreads / kCpr;            // rows between a thread's chunks
+    constexpr int kStripRows = kMBlock / kStripStep;          // chunks per thread per tile
+    const int sc = threadIdx.x % kCpr, sr0 = threadIdx.x / kCpr;
+    // one 128 x n_block output tile -> staging buffer (to & 1) -> reverse scale -> one bulk store
+    auto store_tile = [&](const uint32_t (&v)[kHalf], int32_t* dst, const uint8_t* crow) {
       epi_barrier();   // staging buffer (to & 1) no longer read by the store of tile to-2
       int4* tile = reinterpret_cast<int4*>(staging + (to & 1) * kTileBytes);
 #pragma unroll
       for (int c = 0; c < kHalf; c += 4) {
         const int ch = (col0 + c) >> 2;
         tile[row * kCpr + (ch ^ (row & kSwz))] = make_int4((int)v[c], (int)v[c + 1], (int)v[c + 2], (int)v[c + 3]);
+      }
+      epi_barrier();
+      if (scaling) {   // M'' = rha(M m / 2^q) on this thread's 4 columns (sc*4 .. sc*4+3)
+        const uint32_t c4 = reinterpret_cast<const uint32_t*>(crow)[sc];
+        const uint32_t e0 = lut[c4 & 0x3fu], e1 = lut[(c4 >> 8) & 0x3fu], e2 = lut[(c4 >> 16) & 0x3fu],
+                       e3 = lut[(c4 >> 24) & 0x3fu];
+#pragma unroll
+        for (int k = 0; k < kStripRows; k++) {
+          const int r = sr0 + k * kStripStep;
+          int4* pch = tile + r * kCpr + (sc ^ (r & kSwz));
+          const int4 raw = *pch;
+          *pch = make_int4(rscale_e((uint32_t)raw.x, e0), rscale_e((uint32_t)raw.y, e1),
+                           rscale_e((uint32_t)raw.z, e2), rscale_e((uint32_t)raw.w, e3));
+        }
       }
       fence_proxy_async_smem();   // generic-proxy writes -> visible to the bulk copy
       epi_barrier();
@@ -273,14 +328,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       to++;
     };
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    for (int ku = 0, u = cta_unit(0); u < n_units; u = cta_unit(++ku)) {
       int pidx, tb, nb;
       decode_unit(u, tblocks, nblocks, pidx, tb, nb);
       const long long tile_off = ((long long)tb * nblocks + nb) * (kMBlock * NBLK);
+      const uint8_t* crow = s_codes + pidx * cout_pad + nb * NBLK;
       if (pidx >= kPrimaries) {                    // real position: one plane
         uint32_t v[kHalf];
         take_plane(v);
-        store_tile(v, Mraw + (long long)(pidx - kPrimaries) * ps + tile_off);
+        store_tile(v, Mraw + (long long)(pidx - kPrimaries) * ps + tile_off, crow);
       } else {                                     // complex primary: Karatsuba P0, P1, P2
         uint32_t re[kHalf], sm[kHalf], v[kHalf];
         take_plane(re);                            // P0
@@ -292,8 +348,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         take_plane(v);                             // P2: Im = P2 - S
 #pragma unroll
         for (int j = 0; j < kHalf; j++) v[j] -= sm[j];
-        store_tile(re, Mraw + (long long)(kRealPlanes + pidx) * ps + tile_off);
-        store_tile(v, Mraw + (long long)(kRealPlanes + kPrimaries + pidx) * ps + tile_off);
+        store_tile(re, Mraw + (long long)(kRealPlanes + pidx) * ps + tile_off, crow);
+        store_tile(v, Mraw + (long long)(kRealPlanes + kPrimaries + pidx) * ps + tile_off, crow);
       }
     }
     if (warp == 0 && lane == 0) bulk_wait0();   // all tile stores complete before exit
@@ -309,15 +365,16 @@ static uint64_t* g_trace = nullptr;
 void set_gemm_trace(void* buf) { g_trace = static_cast<uint64_t*>(buf); }
 
 cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t* vimg, const int8_t* wimg,
-                        int32_t* mraw, cudaStream_t st) {
+                        const uint8_t* codes, int32_t* mraw, cudaStream_t st) {
   // tile blocks of this launch; M strides use the full chunk geometry (K4 reads with it)
   const int tblocks = (int)(tiles_pad_launch / kMBlock);
   const int n_units = tblocks * (g.cout_pad / g.nblk) * kPositions;
   const int grid = n_units < g_num_sms ? n_units : g_num_sms;
-  const size_t smem = gemm_smem_bytes(g.nblk);
+  const size_t smem = gemm_smem_bytes(g.nblk, g.cout_pad);
+  cudaError_t e;
 #define WINO_LAUNCH_GEMM(N)                                                                                  \
-  k_gemm<N><<<grid, kGemmThreads, smem, st>>>(vimg, wimg, mraw, g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, \
-                                              g.cin_pad, g_trace)
+  e = launch_pdl(k_gemm<N>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw, codes, g.cout, g.scaling, \
+                 g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad, g_trace)
   switch (g.nblk) {
     case 16: WINO_LAUNCH_GEMM(16); break;
     case 32: WINO_LAUNCH_GEMM(32); break;
@@ -325,16 +382,16 @@ cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t*
     default: return cudaErrorInvalidValue;
   }
 #undef WINO_LAUNCH_GEMM
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t setup_gemm() {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(16));
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(32));
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(64));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(16, kMaxCoutPad));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(32, kMaxCoutPad));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(64, kMaxCoutPad));
   return e;
 }
 

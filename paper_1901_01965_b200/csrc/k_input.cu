@@ -18,6 +18,7 @@
 
 #include "kernels.cuh"
 #include "layout.cuh"
+#include "ptx.cuh"
 
 namespace wino {
 
@@ -70,6 +71,8 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
   const int t = blockIdx.x * kInTilesPerCta + warp * kInTilesPerWarp + tl;   // chunk tile
   const int c = blockIdx.y * kInChPerCta + 2 * cp;              // first channel of the pair
   const int tiles = imgs * g.tpi;
+  pdl_trigger();
+  pdl_wait();   // x may come from the previous kernel (layer stacks); V may still be read by the previous GEMM
 
   // ---- gather the zero-padded 6x6 patch at origin (4ty - pad, 4tx - pad): 2 channels per pixel
   uint32_t w[36];
@@ -194,8 +197,7 @@ cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int i
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
   dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
-  k_input_transform<<<grid, kInWarps * 32, 0, st>>>(g, x, n0, imgs, vimg);
-  return cudaGetLastError();
+  return launch_pdl(k_input_transform, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
 }
 
 cudaError_t setup_input_transform() { return cudaSuccess; }

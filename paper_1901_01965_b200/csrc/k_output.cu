@@ -1,7 +1,5 @@
-// k_output.cu -- K4: reverse scaling M'' = rha(M m / 2^q) of the 36 values per
-// (tile, cout) that K3 leaves (16 real, 10 Re, 10 Im after the Karatsuba
-// recombination) with (m, q) derived on the device from the 6-bit codes
-// (A8/A9), the
+// k_output.cu -- K4: on the 36 values per (tile, cout) that K3 leaves (M'':
+// 16 real, 10 Re, 10 Im after Karatsuba recombination and reverse scaling), the
 // real-only output transform Y = A^T M'' A that never forms the imaginary
 // coefficients, out32 = rha(Y / 16) (G used as 4G,
 // DESIGN.md A2/A11), crop, optional requantisation (A14) and the store.
@@ -24,6 +22,7 @@
 
 #include "kernels.cuh"
 #include "layout.cuh"
+#include "ptx.cuh"
 
 namespace wino {
 
@@ -40,31 +39,14 @@ __device__ __forceinline__ int32_t rha16_32(uint32_t yv) {
 
 // NHWC: layout 1 / 0; OUT8: int8 (requantised) / int32 output; RQFAST: multiplier 1
 // and shift <= 30, so requantisation fits 32-bit arithmetic.
-// M'' = rha(M m / 2^q) = sign(M) ((|M| m + 2^(q-1)) >> q) with e = m | q << 8 |
-// 2^(q-1) << 16 (the unscaled code maps to the identity m = 1, q = 0).
-__device__ __forceinline__ uint32_t rscale_e(uint32_t v, uint32_t e) {
-  const int32_t vi = (int32_t)v;
-  const uint32_t m = e & 0xffu, q = (e >> 8) & 0xffu, half = e >> 16;
-  const uint64_t prod = (uint64_t)(uint32_t)abs(vi) * m + half;
-  const int32_t r = (int32_t)(uint32_t)(prod >> q);
-  return (uint32_t)(vi < 0 ? -r : r);
-}
-
 template <bool NHWC, bool OUT8, bool RQFAST>
-__global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t* __restrict__ M,
-                                                          const uint8_t* __restrict__ codes, int n0, int imgs,
+__global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t* __restrict__ M, int n0, int imgs,
                                                           int32_t rq_mult, int rq_shift, void* __restrict__ y) {
-  __shared__ uint32_t lut[64];   // inverse factor of every 6-bit code (A8)
-  if (threadIdx.x < 64) {
-    int n, p, m = 1, q = 0;       // code 0 (and invalid codes): identity
-    decode_code(threadIdx.x, n, p);
-    if (n >= 8) inverse_factor(n, p, m, q);
-    lut[threadIdx.x] = (uint32_t)m | ((uint32_t)q << 8) | ((q ? (1u << (q - 1)) : 0u) << 16);
-  }
-  __syncthreads();
   const int tl = threadIdx.x / kOutCoBlock, cl = threadIdx.x % kOutCoBlock;
   const int t = blockIdx.x * kOutTiles + tl;              // chunk tile
   const int co = blockIdx.y * kOutCoBlock + cl;
+  pdl_trigger();
+  pdl_wait();   // M'' comes from the GEMM just before
   if (t >= imgs * g.tpi || co >= g.cout) return;
   const long long ps = g.chunk_tiles_pad * (long long)g.cout_pad;
   const int32_t* mp = M + m_offset(g, t, co);
@@ -76,22 +58,6 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
   for (int k = 0; k < 10; k++) {
     cr[k] = (uint32_t)__ldg(mp + (16 + k) * ps);
     cim[k] = (uint32_t)__ldg(mp + (26 + k) * ps);
-  }
-  if (g.scaling) {   // reverse scaling before the final transforms
-    uint32_t cw[9];  // this output channel's 36 codes (mirrors equal their primaries)
-    const uint32_t* c32 = reinterpret_cast<const uint32_t*>(codes + (long long)co * 36);
-#pragma unroll
-    for (int i = 0; i < 9; i++) cw[i] = __ldg(c32 + i);
-#define WINO_CODE(pos) ((cw[(pos) >> 2] >> (8 * ((pos) & 3))) & 0x3fu)
-#pragma unroll
-    for (int s = 0; s < 16; s++) mr[s] = rscale_e(mr[s], lut[WINO_CODE(real_pos(s))]);
-#pragma unroll
-    for (int k = 0; k < 10; k++) {
-      const uint32_t e = lut[WINO_CODE(cpx_pos(k))];
-      cr[k] = rscale_e(cr[k], e);
-      cim[k] = rscale_e(cim[k], e);
-    }
-#undef WINO_CODE
   }
   // Z = M'' A  (rows 0,1,2,5 real; row 3 complex)
   uint32_t Z[4][4], zr[4], zi[4];
@@ -150,12 +116,13 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
   }
 }
 
-cudaError_t launch_output_transform(const Geom& g, const int32_t* m, const uint8_t* codes, int n0, int imgs,
-                                    int32_t rq_mult, int rq_shift, void* y, cudaStream_t st) {
+cudaError_t launch_output_transform(const Geom& g, const int32_t* m, int n0, int imgs, int32_t rq_mult,
+                                    int rq_shift, void* y, cudaStream_t st) {
   const int tiles = imgs * g.tpi;
   dim3 grid((unsigned)((tiles + kOutTiles - 1) / kOutTiles), (unsigned)((g.cout + kOutCoBlock - 1) / kOutCoBlock));
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 30;
-#define WINO_K4(A, B, C) k_output_transform<A, B, C><<<grid, 256, 0, st>>>(g, m, codes, n0, imgs, rq_mult, rq_shift, y)
+  cudaError_t e;
+#define WINO_K4(A, B, C) e = launch_pdl(k_output_transform<A, B, C>, grid, dim3(256), 0, st, g, m, n0, imgs, rq_mult, rq_shift, y)
   if (nhwc) {
     if (!out8) WINO_K4(true, false, false);
     else if (fast) WINO_K4(true, true, true);
@@ -166,7 +133,7 @@ cudaError_t launch_output_transform(const Geom& g, const int32_t* m, const uint8
     else WINO_K4(false, true, false);
   }
 #undef WINO_K4
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t setup_output_transform() { return cudaSuccess; }

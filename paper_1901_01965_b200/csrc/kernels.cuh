@@ -7,6 +7,25 @@
 
 namespace wino {
 
+// Launch with programmatic stream serialization (PDL): the kernel may start while
+// the previous kernel in the stream finishes; it calls pdl_wait() before touching
+// global memory the previous kernels produce or consume.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // K1: filter transform + scaling + operand planes (k_filter.cu)
 cudaError_t setup_filter_transform();
 cudaError_t launch_filter_transform(const Geom& g, const int8_t* w, int8_t* wimg, uint8_t* codes, cudaStream_t st);
@@ -16,17 +35,17 @@ cudaError_t launch_filter_transform(const Geom& g, const int8_t* w, int8_t* wimg
 cudaError_t setup_input_transform();
 cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st);
 
-// K3: 46 Winograd-domain int8 GEMMs on tcgen05 -> raw per-plane M (k_gemm.cu)
+// K3: 46 Winograd-domain int8 GEMMs on tcgen05 + Karatsuba + reverse scaling -> M'' (k_gemm.cu)
 cudaError_t setup_gemm();
 cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t* vimg, const int8_t* wimg,
-                        int32_t* mraw, cudaStream_t st);
+                        const uint8_t* codes, int32_t* mpp, cudaStream_t st);
 
 void set_gemm_trace(void* buf);   // debug timeline buffer (nullptr = off)
 
-// K4: Karatsuba + reverse scaling + A^T M'' A + /16 + requant + store (k_output.cu)
+// K4: A^T M'' A + /16 + requant + store (k_output.cu)
 cudaError_t setup_output_transform();
-cudaError_t launch_output_transform(const Geom& g, const int32_t* mraw, const uint8_t* codes, int n0, int imgs,
-                                    int32_t rq_mult, int rq_shift, void* y, cudaStream_t st);
+cudaError_t launch_output_transform(const Geom& g, const int32_t* mpp, int n0, int imgs, int32_t rq_mult,
+                                    int rq_shift, void* y, cudaStream_t st);
 
 // misc (k_misc.cu)
 cudaError_t launch_check_codes(const uint8_t* codes, int count, int32_t* bad, cudaStream_t st);

@@ -198,8 +198,8 @@ static wino_status run_stage(const wino_plan_s* p, int stage, int chunk, const i
   int32_t* m = reinterpret_cast<int32_t*>(static_cast<int8_t*>(workspace) + p->v_bytes);
   cudaError_t e = cudaErrorInvalidValue;
   if (stage == 2) e = wino::launch_input_transform(g, x, n0, imgs, vimg, s);
-  if (stage == 3) e = wino::launch_gemm(g, tiles_pad, vimg, static_cast<const int8_t*>(w_wino), m, s);
-  if (stage == 4) e = wino::launch_output_transform(g, m, codes, n0, imgs, rq_mult, rq_shift, y, s);
+  if (stage == 3) e = wino::launch_gemm(g, tiles_pad, vimg, static_cast<const int8_t*>(w_wino), codes, m, s);
+  if (stage == 4) e = wino::launch_output_transform(g, m, n0, imgs, rq_mult, rq_shift, y, s);
   return cuda_status(e);
 }
 

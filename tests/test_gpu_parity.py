@@ -62,11 +62,11 @@ def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates
             vpl = LD.decode_v(vbuf, T, info.cin_pad // 32, info.cin_pad)
             D = O.input_transform(x, pad, layout)
             np.testing.assert_array_equal(vpl[:, :, :ci], LD.complex_to_planes(D))
-            # K3: GEMMs + Karatsuba recombination == oracle M (before reverse scaling)
+            # K3: GEMMs + Karatsuba recombination + reverse scaling == oracle M''
             mraw = conv.m_raw().cpu().numpy()
             ms = LD.decode_m(mraw, T, co, info.cout_pad, info.n_block, info.chunk_tiles_pad)
             real, re, im = ms[:16], ms[16:26], ms[26:36]
-            Mo = ref.M.transpose(2, 0, 1, 3)        # [36][T][co][2]
+            Mo = ref.Mpp.transpose(2, 0, 1, 3)      # [36][T][co][2]
             np.testing.assert_array_equal(real, Mo[LD.REAL_POS, :, :, 0])
             np.testing.assert_array_equal(re, Mo[LD.CPX_POS, :, :, 0])
             np.testing.assert_array_equal(im, Mo[LD.CPX_POS, :, :, 1])
