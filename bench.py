@@ -244,6 +244,139 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_ours_stack(args):
+    """--config C5: the VGG-16 13-layer stack (BASELINE configs[4]) per step:
+    13 filter transforms + 13 convs (requantised) + 4 max pools, batch 256 per rank."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1901_01965_b200 import _lib as L
+    from paper_1901_01965_b200.stack import ConvStack
+
+    rank, local_rank, world = _env_rank()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = synth.CONFIGS["C5"]
+    shifts = synth.stack_shifts("C5")
+    n = cfg.layers[0].n
+    st = ConvStack(n, cfg.layers, cfg.pools_after, shifts, device=local_rank)
+    n_sets = 2
+    xs, wss = [], []
+    for i in range(n_sets):
+        x, ws = synth.stack_inputs("C5", rank=rank * 1000 + i)
+        xs.append(torch.from_numpy(x).to(dev))
+        wss.append([torch.from_numpy(w).to(dev) for w in ws])
+    stream = torch.cuda.Stream(device=dev)
+
+    def step(j):
+        st.transform_filters(wss[j], stream)
+        st(xs[j], stream)
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i % n_sets)
+        stream.synchronize()
+        graphs = []
+        for j in range(n_sets):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step(j)
+            graphs.append(g)
+        for j in range(3):
+            graphs[j % n_sets].replay()
+        stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for i in range(args.steps):
+                graphs[i % n_sets].replay()
+            ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    ops_step = sum(synth.direct_ops(l) for l in cfg.layers)
+    value = world * ops_step * args.steps / t_max / 1e12
+    # per-layer path roofline (SURVEY 8(d)) summed over the stack
+    peaks = _peaks()
+    i8 = 2.0 * peaks["bf16_tflops_sustained"] * 1e12
+    t_roof = 0.0
+    for l, c in zip(cfg.layers, st.convs):
+        ops46 = 2 * 46 * c.info.tiles * l.c_in * l.c_out
+        byts = c.info.x_bytes + c.info.y_bytes + 92 * l.c_in * l.c_out
+        t_roof += max(ops46 / i8, byts / (peaks["hbm_gbs"] * 1e9))
+    # e2e: host x in, host final activation out, through the C ABI calls
+    xh = xs[0].cpu().pin_memory()
+    out = st(xs[0], stream)
+    torch.cuda.synchronize()
+    yh = torch.empty(out.shape, dtype=torch.int8).pin_memory()
+    xd = torch.empty_like(xs[0])
+    reps = 3
+    with torch.cuda.stream(stream):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(reps):
+            xd.copy_(xh, non_blocking=True)
+            step_out = None
+            st.transform_filters(wss[0], stream)
+            step_out = st(xd, stream)
+            yh.copy_(step_out, non_blocking=True)
+        e1.record(stream)
+        stream.synchronize()
+    te = e0.elapsed_time(e1) / 1e3
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_max * 1e3 / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "config": {"workload": f"C5: {cfg.description}", "batch_per_gpu": n, "layers": len(cfg.layers),
+                       "layout": "NHWC", "filter_scaling": True, "requant_shifts": shifts,
+                       "step": "13 filter transforms + 13 convs (K2,K3,K4 per chunk) + 4 max pools",
+                       "l2": "activations 0.8 GB per layer >> 126 MiB L2; 2 input sets rotated",
+                       "parallelism": f"dp{world} (replicated per-rank batches, weak scaling)"},
+            "path_roofline": {"t_roof_us": round(t_roof * 1e6, 2), "t_step_us": round(t_max / args.steps * 1e6, 2),
+                              "frac": round(t_roof / (t_max / args.steps), 4),
+                              "roofline_effective_tops": round(ops_step / t_roof / 1e12, 1)},
+            "gpu_launches": st.launches() * args.steps + len(cfg.layers) * args.steps,
+            "clocks": clk.summary(),
+            "e2e": {"value": round(world * ops_step * reps / te / 1e12, 3), "unit": "TOPS",
+                    "h2d_bytes_per_step": int(xh.numel()), "d2h_bytes_per_step": int(yh.numel()),
+                    "steps": reps},
+        }
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline_stack(shifts)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline_stack(shifts):
+    import oracle.oracle as O
+    O.build()
+    cfg = synth.CONFIGS["C5"]
+    x, ws = synth.stack_inputs("C5", n=1)
+    t0 = time.perf_counter()
+    cur = x
+    for i, w in enumerate(ws):
+        cur = O.wino_conv(cur, w, 1, O.NHWC, scaling=True, M0=1, S=shifts[i]).y8
+        if i in cfg.pools_after:
+            cur = O.maxpool2(cur, O.NHWC)
+    t = time.perf_counter() - t0
+    ops = sum(synth.direct_ops(l, n=1) for l in cfg.layers)
+    cores = len(os.sched_getaffinity(0))
+    return {"value": round(ops / t / 1e12, 6), "unit": "TOPS", "cores": cores, "kind": "oracle",
+            "sample": f"oracle stack (13 layers + pools) on image 0 of C5 ({ops:.3e} direct ops); {t:.2f} s"}
+
+
 def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps):
     """Average device duration of each kernel type: for each kernel, a CUDA
     graph of `reps` back-to-back launches of that kernel alone (input/output
@@ -341,47 +474,65 @@ def path_roofline(layer, info, peaks, t_step):
             else "hbm", "roofline_effective_tops": round(synth.direct_ops(layer) / t_roof / 1e12, 1)}
 
 
-def run_e2e(conv, xs, ws, S, stream, n_sets, reps, world, dist, dev, job_ops):
+def run_e2e(conv, xs, ws, S, stream, n_sets, reps, world, dist, dev, job_ops, n_streams=3):
     """Same metric through the C ABI with HOST buffers: every step copies x and w
-    from pinned host memory, runs K1..K4, and reads y back to pinned host memory."""
+    from pinned host memory, runs K1..K4 (wino_transform_filter +
+    wino_conv2d_int8_host, whose H2D / D2H copies are inside the call) and reads
+    y back to pinned host memory.  Steps rotate over `n_streams` streams, each
+    with its own device buffers, so one step's copies overlap another's compute
+    (how a user pipelines the API)."""
     import torch
     from paper_1901_01965_b200 import _lib as L
     info = conv.info
-    sp = stream.cuda_stream
     k = min(n_sets, 8)
     xh = [xs[i].cpu().pin_memory() for i in range(k)]
     wh = [ws[i].cpu().pin_memory() for i in range(k)]
     yh = [torch.empty(conv.y_shape, dtype=torch.int8).pin_memory() for _ in range(k)]
-    xd = torch.empty(conv.x_shape, dtype=torch.int8, device=dev)
-    yd = torch.empty(conv.y_shape, dtype=torch.int8, device=dev)
-    wd = torch.empty(conv.w_shape, dtype=torch.int8, device=dev)
-    w_wino, codes, wsp = conv.w_wino.data_ptr(), conv.codes.data_ptr(), conv.workspace.data_ptr()
+    lanes = []
+    for si in range(n_streams):
+        st = stream if si == 0 else torch.cuda.Stream(device=dev)
+        lanes.append({
+            "st": st, "sp": st.cuda_stream,
+            "xd": torch.empty(conv.x_shape, dtype=torch.int8, device=dev),
+            "yd": torch.empty(conv.y_shape, dtype=torch.int8, device=dev),
+            "wd": torch.empty(conv.w_shape, dtype=torch.int8, device=dev),
+            "ww": conv.w_wino if si == 0 else torch.empty_like(conv.w_wino),
+            "cd": conv.codes if si == 0 else torch.empty_like(conv.codes),
+            "ws": conv.workspace if si == 0 else torch.empty_like(conv.workspace),
+        })
 
     def step(i):
-        j = i % k
-        wd.copy_(wh[j], non_blocking=True)
-        L.wino_transform_filter(conv.plan, wd.data_ptr(), w_wino, codes, sp)
-        L.wino_conv2d_int8_host(conv.plan, xh[j].data_ptr(), w_wino, codes, 1, S, yh[j].data_ptr(),
-                                xd.data_ptr(), yd.data_ptr(), wsp, sp)
+        j, ln = i % k, lanes[i % n_streams]
+        with torch.cuda.stream(ln["st"]):
+            ln["wd"].copy_(wh[j], non_blocking=True)
+        L.wino_transform_filter(conv.plan, ln["wd"].data_ptr(), ln["ww"].data_ptr(), ln["cd"].data_ptr(), ln["sp"])
+        L.wino_conv2d_int8_host(conv.plan, xh[j].data_ptr(), ln["ww"].data_ptr(), ln["cd"].data_ptr(), 1, S,
+                                yh[j].data_ptr(), ln["xd"].data_ptr(), ln["yd"].data_ptr(), ln["ws"].data_ptr(),
+                                ln["sp"])
 
-    with torch.cuda.stream(stream):
-        for i in range(3):
-            step(i)
-        stream.synchronize()
-        if dist is not None:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(reps):
-            step(i)
-        e1.record(stream)
-        stream.synchronize()
+    for i in range(3 * n_streams):
+        step(i)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for ln in lanes[1:]:
+        ln["st"].wait_event(e0)
+    for i in range(reps):
+        step(i)
+    for ln in lanes[1:]:
+        ev = torch.cuda.Event()
+        ev.record(ln["st"])
+        stream.wait_event(ev)
+    e1.record(stream)
+    torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     v = job_ops * reps / float(t.item()) / 1e12
     return {"value": round(v, 3), "unit": "TOPS", "h2d_bytes_per_step": int(info.x_bytes + np.prod(conv.w_shape)),
-            "d2h_bytes_per_step": int(info.y_bytes), "steps": reps,
+            "d2h_bytes_per_step": int(info.y_bytes), "steps": reps, "streams": n_streams,
             "ms_per_step": round(float(t.item()) * 1e3 / reps, 4)}
 
 
@@ -457,7 +608,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
@@ -468,6 +619,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "C5":
+        run_ours_stack(args)
     else:
         run_ours(args)
 

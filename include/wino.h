@@ -72,6 +72,8 @@ typedef struct {
     int filter_scaling;   /* 0: exact (codes all 0); 1: the paper's scheme */
     int filter_target_max;/* 255 (the paper's int9 target, A6); only value supported   */
     int out_mode;         /* WINO_OUT_INT8 or WINO_OUT_INT32                           */
+    int workspace_mb;     /* batch-chunk budget for V + M in MiB; 0 = default (128, or
+                             env WINO_CHUNK_MB).  Larger = fewer, longer launches.     */
 } wino_conv_desc;
 
 typedef struct wino_plan_s *wino_plan_t;

@@ -25,7 +25,8 @@ EXPORTS = ("wino_status_string", "wino_last_cuda_error", "wino_plan", "wino_plan
 class wino_conv_desc(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("h", ctypes.c_int), ("w", ctypes.c_int), ("c_in", ctypes.c_int),
                 ("c_out", ctypes.c_int), ("pad", ctypes.c_int), ("layout", ctypes.c_int),
-                ("filter_scaling", ctypes.c_int), ("filter_target_max", ctypes.c_int), ("out_mode", ctypes.c_int)]
+                ("filter_scaling", ctypes.c_int), ("filter_target_max", ctypes.c_int), ("out_mode", ctypes.c_int),
+                ("workspace_mb", ctypes.c_int)]
 
 
 class wino_plan_info(ctypes.Structure):

@@ -15,11 +15,12 @@ class WinoConv2d:
     """
 
     def __init__(self, n, h, w, c_in, c_out, pad=1, layout=L.WINO_NHWC, filter_scaling=True,
-                 out_mode=L.WINO_OUT_INT8, device=None):
+                 out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device)
-        self.desc = L.wino_conv_desc(n, h, w, c_in, c_out, pad, layout, int(bool(filter_scaling)), 255, out_mode)
+        self.desc = L.wino_conv_desc(n, h, w, c_in, c_out, pad, layout, int(bool(filter_scaling)), 255, out_mode,
+                                     workspace_mb)
         self.plan = L.wino_plan(self.desc, device)
         self.info = L.wino_plan_query(self.plan)
         self.layout, self.out_mode = layout, out_mode
@@ -30,7 +31,11 @@ class WinoConv2d:
         self.y_dtype = torch.int8 if out_mode == L.WINO_OUT_INT8 else torch.int32
         self.w_wino = torch.empty(self.info.filter_bytes, dtype=torch.int8, device=self.device)
         self.codes = torch.empty((c_out, 36), dtype=torch.uint8, device=self.device)
-        self.workspace = torch.empty(self.info.workspace_bytes, dtype=torch.int8, device=self.device)
+        if workspace is not None:   # caller-shared scratch (e.g. one buffer for a layer stack)
+            assert workspace.numel() >= self.info.workspace_bytes and workspace.dtype == torch.int8
+            self.workspace = workspace
+        else:
+            self.workspace = torch.empty(self.info.workspace_bytes, dtype=torch.int8, device=self.device)
 
     def __del__(self):
         plan = getattr(self, "plan", None)

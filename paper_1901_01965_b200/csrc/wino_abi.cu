@@ -59,9 +59,9 @@ wino_status check_device(const wino_plan_s* p) {
 
 long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 
-size_t chunk_budget_bytes() {
+size_t chunk_budget_bytes(int desc_mb) {
   const char* env = std::getenv("WINO_CHUNK_MB");
-  long mb = env ? std::atol(env) : 128;
+  long mb = desc_mb > 0 ? desc_mb : (env ? std::atol(env) : 128);
   if (mb < 1) mb = 1;
   return (size_t)mb << 20;
 }
@@ -92,6 +92,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   if (d.layout != WINO_NCHW && d.layout != WINO_NHWC) return WINO_ERR_INVALID_ARG;
   if (d.out_mode != WINO_OUT_INT8 && d.out_mode != WINO_OUT_INT32) return WINO_ERR_INVALID_ARG;
   if (d.filter_scaling != 0 && d.filter_scaling != 1) return WINO_ERR_INVALID_ARG;
+  if (d.workspace_mb < 0) return WINO_ERR_INVALID_ARG;
   if (d.n < 1 || d.h < 1 || d.w < 1 || d.c_in < 1 || d.c_out < 1) return WINO_ERR_UNSUPPORTED;
   if (d.pad != 0 && d.pad != 1) return WINO_ERR_UNSUPPORTED;
   if (d.h + 2 * d.pad < 3 || d.w + 2 * d.pad < 3) return WINO_ERR_UNSUPPORTED;
@@ -130,7 +131,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.out_mode = d.out_mode;
   // batch chunk: V + M of one chunk within the L2-sized budget
   const size_t per_img = (size_t)g.tpi * (2 * wino::kPlanes * (size_t)g.cin_pad + wino::kSlots * 4 * (size_t)g.cout_pad);
-  long long imgs = (long long)(chunk_budget_bytes() / (per_img ? per_img : 1));
+  long long imgs = (long long)(chunk_budget_bytes(d.workspace_mb) / (per_img ? per_img : 1));
   if (imgs < 1) imgs = 1;
   if (imgs > d.n) imgs = d.n;
   g.chunk_imgs = (int)imgs;

@@ -141,3 +141,18 @@ def direct_ops(layer: LayerCfg, n: int | None = None) -> int:
     nn = layer.n if n is None else n
     ho, wo = layer.h + 2 * layer.pad - 2, layer.w + 2 * layer.pad - 2
     return 2 * nn * ho * wo * layer.c_in * layer.c_out * 9
+
+
+def stack_shifts(name: str = "C5"):
+    """Requantisation shift per layer of a stack config (A14): sigma_in
+    = 73.9 (uniform int8) into layer 1, 32 into every later layer."""
+    cfg = CONFIGS[name]
+    return [requant_shift(l, 73.9 if i == 0 else 32.0) for i, l in enumerate(cfg.layers)]
+
+
+def stack_inputs(name: str = "C5", n: int | None = None, layout: int = NHWC, rank: int = 0):
+    """(x, [w_l]) for a layer stack: x from layer 0's seed, each layer's w from its own seed."""
+    cfg = CONFIGS[name]
+    x, _ = config_inputs(name, layout, rank=rank, layer=0, n=n)
+    ws = [config_inputs(name, layout, rank=rank, layer=i, n=1)[1] for i in range(len(cfg.layers))]
+    return x, ws

@@ -145,7 +145,7 @@ def test_plan_rejects():
         with pytest.raises(W.WinoError) as e:
             L.wino_plan(L.wino_conv_desc(**d), 0)
         assert e.value.status == L.WINO_ERR_UNSUPPORTED
-    d = L.wino_conv_desc(1, 8, 8, 4, 4, 1, 7, 1, 255, 0)
+    d = L.wino_conv_desc(1, 8, 8, 4, 4, 1, 7, 1, 255, 0, 0)
     with pytest.raises(W.WinoError) as e:
         L.wino_plan(d, 0)
     assert e.value.status == L.WINO_ERR_INVALID_ARG
@@ -217,3 +217,34 @@ def test_full_size_configs_sampled(name):
         np.testing.assert_array_equal(y[i:i + 1], ref.y8)
     # codes computed on the device equal the oracle's
     np.testing.assert_array_equal(conv.codes.cpu().numpy(), O.filter_transform(w, O.NHWC, True)[2])
+
+
+def _oracle_stack(x, ws, shifts, pools):
+    outs, cur = [], x
+    for i, w in enumerate(ws):
+        cur = O.wino_conv(cur, w, 1, O.NHWC, scaling=True, M0=1, S=shifts[i]).y8
+        if i in pools:
+            cur = O.maxpool2(cur, O.NHWC)
+        outs.append(cur)
+    return outs
+
+
+def test_vgg16_stack_full_size_sampled():
+    """BASELINE configs[4] at full size (13 layers, 224x224, batch 256, requantised,
+    max-pooled): images 0 and 255 compared layer by layer with the oracle."""
+    from paper_1901_01965_b200.stack import ConvStack
+    cfg = synth.CONFIGS["C5"]
+    shifts = synth.stack_shifts("C5")
+    x, ws = synth.stack_inputs("C5")
+    st = ConvStack(x.shape[0], cfg.layers, cfg.pools_after, shifts)
+    st.transform_filters([torch.from_numpy(w).cuda() for w in ws])
+    st(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    for img in (0, x.shape[0] - 1):
+        ref = _oracle_stack(x[img:img + 1], ws, shifts, set(cfg.pools_after))
+        for i in range(len(ws)):
+            got = (st.pooled[i] if i in st.pooled else st.outs[i])[img:img + 1].cpu().numpy()
+            np.testing.assert_array_equal(got, ref[i], err_msg=f"layer {i} image {img}")
+    # the activations stay informative (requant shifts neither saturate nor vanish)
+    last = (st.pooled.get(len(ws) - 1, st.outs[-1])).cpu().numpy()
+    assert 4 < np.abs(last.astype(np.int32)).mean() < 100
