@@ -23,9 +23,9 @@
 //                writes each 128 x n_block int32 output tile into a shared-memory
 //                staging buffer laid out exactly like M (16-byte chunks
 //                XOR-swizzled by row); then every epilogue thread reverse-scales a
-//                fixed 4-column strip of the staged tile in place (4 scale entries
-//                per tile instead of one per value), and one thread stores the
-//                whole tile with a single bulk copy (TMA engine)
+//                fixed 4-column strip of the staged tile (4 scale entries per tile
+//                instead of one per value) and writes it with coalesced 16-byte
+//                stores (each warp covers two whole 256-byte rows)
 //   warp 8       producer (1 lane): 1-D bulk copies of pre-tiled K stages into a
 //                kStages-deep ring, mbarrier complete_tx
 //   warp 9       MMA issuer (1 lane): tcgen05.mma, tcgen05.commit -> stage free /
@@ -295,9 +295,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr int kStripStep = kEpiThreads / kCpr;            // rows between a thread's chunks
     constexpr int kStripRows = kMBlock / kStripStep;          // chunks per thread per tile
     const int sc = threadIdx.x % kCpr, sr0 = threadIdx.x / kCpr;
-    // one 128 x n_block output tile -> staging buffer (to & 1) -> reverse scale -> one bulk store
+    // one 128 x n_block output tile -> staging buffer (to & 1) (transpose: thread = row
+    // on the TMEM side, thread = 4-column strip on the store side) -> reverse scale
+    // -> coalesced 16-byte global stores (a warp writes two whole rows of the tile).
+    // Buffer (to & 1) was last read in the strip pass of tile to-2, which every
+    // thread finished before arriving at the barrier of tile to-1.
     auto store_tile = [&](const uint32_t (&v)[kHalf], int32_t* dst, const uint8_t* crow) {
-      epi_barrier();   // staging buffer (to & 1) no longer read by the store of tile to-2
       int4* tile = reinterpret_cast<int4*>(staging + (to & 1) * kTileBytes);
 #pragma unroll
       for (int c = 0; c < kHalf; c += 4) {
@@ -305,27 +308,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tile[row * kCpr + (ch ^ (row & kSwz))] = make_int4((int)v[c], (int)v[c + 1], (int)v[c + 2], (int)v[c + 3]);
       }
       epi_barrier();
-      if (scaling) {   // M'' = rha(M m / 2^q) on this thread's 4 columns (sc*4 .. sc*4+3)
-        const uint32_t c4 = reinterpret_cast<const uint32_t*>(crow)[sc];
-        const uint32_t e0 = lut[c4 & 0x3fu], e1 = lut[(c4 >> 8) & 0x3fu], e2 = lut[(c4 >> 16) & 0x3fu],
-                       e3 = lut[(c4 >> 24) & 0x3fu];
+      // M'' = rha(M m / 2^q) on this thread's 4 columns (sc*4 .. sc*4+3)
+      const uint32_t c4 = reinterpret_cast<const uint32_t*>(crow)[sc];
+      const uint32_t e0 = lut[c4 & 0x3fu], e1 = lut[(c4 >> 8) & 0x3fu], e2 = lut[(c4 >> 16) & 0x3fu],
+                     e3 = lut[(c4 >> 24) & 0x3fu];
+      int4* gdst = reinterpret_cast<int4*>(dst);
 #pragma unroll
-        for (int k = 0; k < kStripRows; k++) {
-          const int r = sr0 + k * kStripStep;
-          int4* pch = tile + r * kCpr + (sc ^ (r & kSwz));
-          const int4 raw = *pch;
-          *pch = make_int4(rscale_e((uint32_t)raw.x, e0), rscale_e((uint32_t)raw.y, e1),
-                           rscale_e((uint32_t)raw.z, e2), rscale_e((uint32_t)raw.w, e3));
-        }
+      for (int k = 0; k < kStripRows; k++) {
+        const int r = sr0 + k * kStripStep;
+        const int slot = r * kCpr + (sc ^ (r & kSwz));
+        const int4 raw = tile[slot];
+        gdst[slot] = make_int4(rscale_e((uint32_t)raw.x, e0), rscale_e((uint32_t)raw.y, e1),
+                               rscale_e((uint32_t)raw.z, e2), rscale_e((uint32_t)raw.w, e3));
       }
-      fence_proxy_async_smem();   // generic-proxy writes -> visible to the bulk copy
-      epi_barrier();
-      if (warp == 0 && lane == 0) {
-        bulk_s2g(dst, smem_u32(tile), kTileBytes);
-        bulk_commit();
-        WINO_TRACE(pc - 1, 5);
-        bulk_wait_read1();        // every earlier tile store has finished reading its buffer
-      }
+      if (warp == 0 && lane == 0) WINO_TRACE(pc - 1, 5);
       to++;
     };
     for (int ku = 0, u = cta_unit(0); u < n_units; u = cta_unit(++ku)) {
@@ -352,7 +348,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         store_tile(v, Mraw + (long long)(kRealPlanes + kPrimaries + pidx) * ps + tile_off, crow);
       }
     }
-    if (warp == 0 && lane == 0) bulk_wait0();   // all tile stores complete before exit
   }
 #undef WINO_TRACE
   tc_fence_before();

@@ -20,7 +20,7 @@ conv.transform_filter(wd)
 S = synth.requant_shift(layer)
 y = conv(xd, 1, S)
 nsm = torch.cuda.get_device_properties(0).multi_processor_count
-WORDS = 16 * 6 + 16 * 16 * 3
+WORDS = 16 * 6
 trace = torch.zeros(nsm * WORDS, dtype=torch.int64, device="cuda")
 sp = torch.cuda.current_stream().cuda_stream
 for rep in range(3):
@@ -36,10 +36,9 @@ raw = trace.view(nsm, WORDS).cpu().numpy().astype(np.float64)
 t0 = raw[raw > 0].min()
 raw = np.where(raw > 0, (raw - t0) / 1e3, np.nan)   # us since first stamp
 t = raw[:, :96].reshape(nsm, 16, 6)
-wt = raw[:, 96:].reshape(nsm, 16, 16, 3)             # [cta][unit][epi warp][start, taken, stored]
 os.makedirs("gpurun_out", exist_ok=True)
 np.save(f"gpurun_out/trace_{cfg}.npy", t)
-names = ["prod_issue", "mma_data", "mma_tmem", "mma_commit", "epi_acc", "epi_done"]
+names = ["prod_issue", "mma_data", "mma_tmem", "mma_commit", "epi_acc", "epi_store"]
 print(f"chunks {conv.info.n_chunks}  kernel span {np.nanmax(t):.2f} us")
 for c in (0, 1, 74, 147):
     print(f"CTA {c}:")
@@ -50,14 +49,5 @@ for c in (0, 1, 74, 147):
         print("   plane %2d " % p + "  ".join(f"{n}={v:7.2f}" for n, v in zip(names, row)))
 d = lambda a, b: np.nanmean(t[:, :, b] - t[:, :, a])
 print("mean  issue->data %.2f  data->tmem %.2f  tmem->commit %.2f  commit->epi %.2f" % (d(0, 1), d(1, 2), d(2, 3), d(3, 4)))
-take = wt[..., 1] - wt[..., 0]; store = wt[..., 2] - wt[..., 1]
-print("epilogue per warp-unit: take(wait+tmem) mean %.2f us, store mean %.2f us" % (np.nanmean(take), np.nanmean(store)))
-spread = np.nanmax(wt[..., 2], axis=2) - np.nanmin(wt[..., 2], axis=2)
-print("spread of 'stored' across the 16 warps of a unit: mean %.2f us max %.2f" % (np.nanmean(spread), np.nanmax(spread)))
-for c in (0, 74):
-    for ui in range(6):
-        row = wt[c, ui]
-        print(f"  CTA {c} unit {ui}: start {np.nanmin(row[:,0]):6.2f}..{np.nanmax(row[:,0]):6.2f} "
-              f"taken {np.nanmin(row[:,1]):6.2f}..{np.nanmax(row[:,1]):6.2f} stored {np.nanmin(row[:,2]):6.2f}..{np.nanmax(row[:,2]):6.2f}")
 print("first stamps: prod_issue min %.2f max %.2f ; last epi_done max %.2f" % (
     np.nanmin(t[:, 0, 0]), np.nanmax(t[:, 0, 0]), np.nanmax(t[:, :, 5])))
