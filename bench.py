@@ -150,36 +150,49 @@ def run_ours(args):
     stream = torch.cuda.Stream(device=dev)
     sp = stream.cuda_stream
     w_wino, codes, wsp = conv.w_wino.data_ptr(), conv.codes.data_ptr(), conv.workspace.data_ptr()
+    # --streams > 1: independent batches in flight on separate streams, each with its own
+    # transformed-filter buffer, codes and workspace (no dependencies between them)
+    lanes = [(stream, conv.w_wino, conv.codes, conv.workspace)]
+    for _ in range(1, max(1, args.streams)):
+        lanes.append((torch.cuda.Stream(device=dev), torch.empty_like(conv.w_wino), torch.empty_like(conv.codes),
+                      torch.empty_like(conv.workspace)))
 
-    def step(i):
+    def step(i, lane=0):
         j = i % n_sets
-        L.wino_transform_filter(conv.plan, ws[j].data_ptr(), w_wino, codes, sp)
-        L.wino_conv2d_int8(conv.plan, xs[j].data_ptr(), w_wino, codes, 1, S, ys[j].data_ptr(), wsp, sp)
+        st_, ww_, cd_, ws_ = lanes[lane]
+        L.wino_transform_filter(conv.plan, ws[j].data_ptr(), ww_.data_ptr(), cd_.data_ptr(), st_.cuda_stream)
+        L.wino_conv2d_int8(conv.plan, xs[j].data_ptr(), ww_.data_ptr(), cd_.data_ptr(), 1, S, ys[j].data_ptr(),
+                           ws_.data_ptr(), st_.cuda_stream)
 
     launches_per_step = 1 + 3 * info.n_chunks
-    # CUDA graphs: one per rotation slot (launch-bound otherwise)
-    graphs = []
+    # CUDA graphs: one per (stream lane, rotation slot) (launch-bound otherwise)
+    graphs = {}
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
             step(i)
         stream.synchronize()
         if not args.no_graph:
-            for j in range(n_sets):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=stream):
-                    step(j)
-                graphs.append(g)
-            for j in range(max(args.warmup, 3)):
-                graphs[j % n_sets].replay()
-            stream.synchronize()
+            for ln, (st_, _, _, _) in enumerate(lanes):
+                with torch.cuda.stream(st_):
+                    for j in range(n_sets):
+                        g = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(g, stream=st_):
+                            step(j, ln)
+                        graphs[(ln, j)] = g
+                    for j in range(max(args.warmup, 3)):
+                        graphs[(ln, j % n_sets)].replay()
+            torch.cuda.synchronize()
 
     def run_steps(k, offset=0):
-        with torch.cuda.stream(stream):
-            for i in range(k):
+        n_l = len(lanes)
+        for i in range(k):
+            ln = i % n_l
+            st_ = lanes[ln][0]
+            with torch.cuda.stream(st_):
                 if graphs:
-                    graphs[(i + offset) % n_sets].replay()
+                    graphs[(ln, (i + offset) % n_sets)].replay()
                 else:
-                    step(i + offset)
+                    step(i + offset, ln)
 
     # ---------------- timed region
     if world > 1:
@@ -188,7 +201,13 @@ def run_ours(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
+        for st_, _, _, _ in lanes[1:]:
+            st_.wait_event(ev0)
         run_steps(args.steps)
+        for st_, _, _, _ in lanes[1:]:
+            e_ = torch.cuda.Event()
+            e_.record(st_)
+            stream.wait_event(e_)
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -210,8 +229,9 @@ def run_ours(args):
 
     if rank == 0:
         peaks = _peaks()
+        full = sh["n"] == layer.n and sh["co"] == layer.c_out   # the captured shape
         roof = roofline(kern, info, synth.LayerCfg(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad),
-                        peaks)
+                        peaks, load_traffic(args.config) if full else None)
         path = path_roofline(synth.LayerCfg(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad), info,
                              peaks, t_max / args.steps)
         line = {
@@ -227,7 +247,7 @@ def run_ours(args):
                 "l2": f"inputs/weights/outputs rotated over {n_sets} sets "
                       f"({n_sets * per_set / 2 ** 20:.0f} MiB > 126 MiB L2)",
                 "parallelism": f"dp{world} ({'replicated per-rank batches, weak scaling' if args.scaling == 'weak' else sh['mode'] + '-sharded, strong scaling'}; no data-path collective)",
-                "chunks": info.n_chunks, "cuda_graph": bool(graphs),
+                "chunks": info.n_chunks, "cuda_graph": bool(graphs), "streams": len(lanes),
             },
             "roofline": roof["dominant"],
             "path_roofline": path,
@@ -415,7 +435,22 @@ def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps):
     return out
 
 
-def roofline(kern, info, layer, peaks):
+def load_traffic(config):
+    """roofline.traffic: DRAM bytes per launch from the latest committed ncu --set full
+    capture of this config (profiles/rNN_traffic_<config>.json, written by
+    tools/profile_summary.py), or None when no capture exists."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                          f"r*_traffic_{config}.json")))
+    if not files:
+        return {}
+    try:
+        return json.load(open(files[-1]))["bytes"]
+    except Exception:
+        return {}
+
+
+def roofline(kern, info, layer, peaks, traffic=None):
     """Algorithmic work per launch against the measured peaks."""
     T = info.tiles
     chunk_tiles = min(info.chunk_images, layer.n) * info.tiles_h * info.tiles_w
@@ -444,7 +479,7 @@ def roofline(kern, info, layer, peaks):
         t = kern[name]["s_per_launch"]
         achieved = work / t / (1e9 if unit == "GB/s" else 1e12)
         d = {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": unit,
-             "frac": round(achieved / peak, 4), "traffic": None, "us_per_launch": round(t * 1e6, 3),
+             "frac": round(achieved / peak, 4), "traffic": (traffic or {}).get(name), "us_per_launch": round(t * 1e6, 3),
              "launches_per_step": kern[name]["launches_per_step"],
              "share_of_step": None, "algorithmic_per_launch": work}
         if name == "k3_gemm":
@@ -606,12 +641,14 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--streams", type=int, default=3,
+                    help="independent batches in flight on separate streams (own filter/workspace buffers)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
