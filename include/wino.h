@@ -72,9 +72,17 @@ typedef struct {
     int filter_scaling;   /* 0: exact (codes all 0); 1: the paper's scheme */
     int filter_target_max;/* 255 (the paper's int9 target, A6); only value supported   */
     int out_mode;         /* WINO_OUT_INT8 or WINO_OUT_INT32                           */
-    int workspace_mb;     /* batch-chunk budget for V + M in MiB; 0 = default (128, or
+    int workspace_mb;     /* batch-chunk budget for V (+ M) in MiB; 0 = default (128, or
                              env WINO_CHUNK_MB).  Larger = fewer, longer launches.     */
+    int path;             /* WINO_PATH_FUSED (0, default): K2 input transform, then ONE
+                             kernel for the GEMMs + Karatsuba + reverse scaling + output
+                             transform + store (M'' stays on chip).
+                             WINO_PATH_STAGED (1): K2, K3 GEMMs -> M'' in the workspace,
+                             K4 output transform (M'' inspectable, see wino_plan_info). */
 } wino_conv_desc;
+
+/* Hot-path kernel structure (wino_conv_desc.path). */
+enum { WINO_PATH_FUSED = 0, WINO_PATH_STAGED = 1 };
 
 typedef struct wino_plan_s *wino_plan_t;
 
@@ -92,9 +100,12 @@ typedef struct {
     int chunk_images;           /* images per workspace chunk                          */
     int n_chunks;
     long long chunk_tiles_pad;  /* tiles per chunk rounded up to m_block               */
+    int path;                   /* WINO_PATH_FUSED or WINO_PATH_STAGED                 */
+    int stages;                 /* kernels per chunk: 2 (fused) or 3 (staged)          */
     size_t v_offset, v_bytes;   /* V  = B^T d B operand planes inside the workspace    */
-    size_t m_offset, m_bytes;   /* M  = 36 int32 per (tile, cout) after Karatsuba,
-                                   before reverse scaling; swizzled tiles  */
+    size_t m_offset, m_bytes;   /* M'' = 36 int32 per (tile, cout) after Karatsuba and
+                                   reverse scaling; swizzled tiles; staged
+                                   path only (m_bytes = 0 on the fused path)           */
     size_t workspace_bytes;
     size_t filter_bytes;        /* transformed-filter buffer (w_wino)                  */
     size_t codes_bytes;         /* c_out * 36 bytes                                    */
@@ -176,10 +187,13 @@ wino_status wino_conv2d_int8_host(wino_plan_t plan, const int8_t *x_host, const 
 /* Profiling / testing entry point: enqueue ONE kernel of the hot path for
  * batch chunk `chunk` (0 <= chunk < wino_plan_info.n_chunks):
  *   stage 2 = input transform (x -> V in the workspace),
- *   stage 3 = Winograd-domain GEMMs (V, w_wino -> M in the workspace),
- *   stage 4 = output transform (M, scale_codes -> y).
- * Running stages 2, 3, 4 for every chunk in order is exactly
- * wino_conv2d_int8.  Arguments as for wino_conv2d_int8; WINO_ERR_INVALID_ARG
+ *   fused path:  stage 3 = GEMMs + Karatsuba + reverse scaling + output
+ *                transform + store (V, w_wino, scale_codes -> y);
+ *   staged path: stage 3 = Winograd-domain GEMMs + Karatsuba + reverse
+ *                scaling (V, w_wino, scale_codes -> M'' in the workspace),
+ *                stage 4 = output transform (M'' -> y).
+ * Running stages 2 .. 1 + wino_plan_info.stages for every chunk in order is
+ * exactly wino_conv2d_int8.  Arguments as for wino_conv2d_int8; WINO_ERR_INVALID_ARG
  * for a bad stage or chunk.                                               */
 wino_status wino_conv2d_int8_stage(wino_plan_t plan, int stage, int chunk, const int8_t *x,
                                    const void *w_wino, const uint8_t *scale_codes,

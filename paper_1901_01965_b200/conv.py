@@ -15,12 +15,12 @@ class WinoConv2d:
     """
 
     def __init__(self, n, h, w, c_in, c_out, pad=1, layout=L.WINO_NHWC, filter_scaling=True,
-                 out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0):
+                 out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0, path=L.WINO_PATH_FUSED):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device)
         self.desc = L.wino_conv_desc(n, h, w, c_in, c_out, pad, layout, int(bool(filter_scaling)), 255, out_mode,
-                                     workspace_mb)
+                                     workspace_mb, path)
         self.plan = L.wino_plan(self.desc, device)
         self.info = L.wino_plan_query(self.plan)
         self.layout, self.out_mode = layout, out_mode

@@ -47,6 +47,13 @@ cudaError_t setup_output_transform();
 cudaError_t launch_output_transform(const Geom& g, const int32_t* mpp, int n0, int imgs, int32_t rq_mult,
                                     int rq_shift, void* y, cudaStream_t st);
 
+// K3F: fused GEMMs + Karatsuba + reverse scaling + output transform + store (k_fused.cu);
+//   requires g.nblk == 16.  V of the chunk -> y directly (no M'' in HBM).
+cudaError_t setup_fused();
+cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
+                         const int8_t* wimg, const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y,
+                         cudaStream_t st);
+
 // misc (k_misc.cu)
 cudaError_t launch_check_codes(const uint8_t* codes, int count, int32_t* bad, cudaStream_t st);
 cudaError_t launch_maxpool2(const int8_t* x, int n, int h, int w, int c, int layout, int8_t* y, cudaStream_t st);

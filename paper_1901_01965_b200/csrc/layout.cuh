@@ -53,6 +53,7 @@ struct Geom {
   int ho, wo, th, tw, tpi;     // output size, tiles per row/col, tiles per image
   int cin_pad, cout_pad, nblk, ksteps;
   int scaling, target, out_mode;
+  int path;                    // WINO_PATH_FUSED (0) or WINO_PATH_STAGED (1)
   int chunk_imgs;
   long long chunk_tiles_pad;   // multiple of kMBlock
 };

@@ -43,6 +43,7 @@ wino_status setup_device(int device) {
   if (e == cudaSuccess) e = wino::setup_input_transform();
   if (e == cudaSuccess) e = wino::setup_gemm();
   if (e == cudaSuccess) e = wino::setup_output_transform();
+  if (e == cudaSuccess) e = wino::setup_fused();
   cudaSetDevice(old);
   if (e != cudaSuccess) return cuda_status(e);
   g_setup_done[device] = true;
@@ -93,6 +94,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   if (d.out_mode != WINO_OUT_INT8 && d.out_mode != WINO_OUT_INT32) return WINO_ERR_INVALID_ARG;
   if (d.filter_scaling != 0 && d.filter_scaling != 1) return WINO_ERR_INVALID_ARG;
   if (d.workspace_mb < 0) return WINO_ERR_INVALID_ARG;
+  if (d.path != WINO_PATH_FUSED && d.path != WINO_PATH_STAGED) return WINO_ERR_INVALID_ARG;
   if (d.n < 1 || d.h < 1 || d.w < 1 || d.c_in < 1 || d.c_out < 1) return WINO_ERR_UNSUPPORTED;
   if (d.pad != 0 && d.pad != 1) return WINO_ERR_UNSUPPORTED;
   if (d.h + 2 * d.pad < 3 || d.w + 2 * d.pad < 3) return WINO_ERR_UNSUPPORTED;
@@ -123,14 +125,17 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.tpi = g.th * g.tw;
   g.cin_pad = (int)round_up(d.c_in, wino::kKStep);
   const int cout16 = (int)round_up(d.c_out, 16);
-  g.nblk = cout16 <= 16 ? 16 : (cout16 <= 32 ? 32 : 64);
+  g.path = d.path;
+  // fused path: 16-cout units (UMMA N = 16); staged path: widest N that the cout count fills
+  g.nblk = d.path == WINO_PATH_FUSED ? 16 : (cout16 <= 16 ? 16 : (cout16 <= 32 ? 32 : 64));
   g.cout_pad = (int)round_up(d.c_out, g.nblk);
   g.ksteps = g.cin_pad / wino::kKStep;
   g.scaling = d.filter_scaling;
   g.target = d.filter_target_max;
   g.out_mode = d.out_mode;
-  // batch chunk: V + M of one chunk within the L2-sized budget
-  const size_t per_img = (size_t)g.tpi * (2 * wino::kPlanes * (size_t)g.cin_pad + wino::kSlots * 4 * (size_t)g.cout_pad);
+  // batch chunk: V (+ M on the staged path) of one chunk within the budget
+  const size_t m_per_tile = d.path == WINO_PATH_STAGED ? wino::kSlots * 4 * (size_t)g.cout_pad : 0;
+  const size_t per_img = (size_t)g.tpi * (2 * wino::kPlanes * (size_t)g.cin_pad + m_per_tile);
   long long imgs = (long long)(chunk_budget_bytes(d.workspace_mb) / (per_img ? per_img : 1));
   if (imgs < 1) imgs = 1;
   if (imgs > d.n) imgs = d.n;
@@ -138,7 +143,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.chunk_tiles_pad = round_up((long long)imgs * g.tpi, wino::kMBlock);
   p->n_chunks = (int)((d.n + imgs - 1) / imgs);
   p->v_bytes = (size_t)2 * wino::kPlanes * g.chunk_tiles_pad * g.cin_pad;
-  p->m_bytes = (size_t)wino::kSlots * g.chunk_tiles_pad * g.cout_pad * 4;
+  p->m_bytes = d.path == WINO_PATH_STAGED ? (size_t)wino::kSlots * g.chunk_tiles_pad * g.cout_pad * 4 : 0;
   p->ws_bytes = p->v_bytes + p->m_bytes;
   p->f_bytes = (size_t)2 * wino::kPlanes * g.cout_pad * g.cin_pad;
   p->x_bytes = (size_t)d.n * d.h * d.w * d.c_in;
@@ -164,6 +169,8 @@ wino_status wino_plan_query(wino_plan_t p, wino_plan_info* info) {
   info->planes = wino::kPlanes; info->pieces = wino::kPieces;
   info->chunk_images = p->g.chunk_imgs; info->n_chunks = p->n_chunks;
   info->chunk_tiles_pad = p->g.chunk_tiles_pad;
+  info->path = p->g.path;
+  info->stages = p->g.path == WINO_PATH_FUSED ? 2 : 3;
   info->v_offset = 0; info->v_bytes = p->v_bytes;
   info->m_offset = p->v_bytes; info->m_bytes = p->m_bytes;
   info->workspace_bytes = p->ws_bytes;
@@ -199,8 +206,14 @@ static wino_status run_stage(const wino_plan_s* p, int stage, int chunk, const i
   int32_t* m = reinterpret_cast<int32_t*>(static_cast<int8_t*>(workspace) + p->v_bytes);
   cudaError_t e = cudaErrorInvalidValue;
   if (stage == 2) e = wino::launch_input_transform(g, x, n0, imgs, vimg, s);
-  if (stage == 3) e = wino::launch_gemm(g, tiles_pad, vimg, static_cast<const int8_t*>(w_wino), codes, m, s);
-  if (stage == 4) e = wino::launch_output_transform(g, m, n0, imgs, rq_mult, rq_shift, y, s);
+  if (g.path == WINO_PATH_FUSED) {
+    if (stage == 3)
+      e = wino::launch_fused(g, tiles_pad, n0, imgs, vimg, static_cast<const int8_t*>(w_wino), codes, rq_mult,
+                             rq_shift, y, s);
+  } else {
+    if (stage == 3) e = wino::launch_gemm(g, tiles_pad, vimg, static_cast<const int8_t*>(w_wino), codes, m, s);
+    if (stage == 4) e = wino::launch_output_transform(g, m, n0, imgs, rq_mult, rq_shift, y, s);
+  }
   return cuda_status(e);
 }
 
@@ -217,8 +230,9 @@ wino_status wino_conv2d_int8(wino_plan_t p, const int8_t* x, const void* w_wino,
   wino_status st = check_conv_args(p, x, w_wino, codes, rq_mult, rq_shift, y, workspace);
   if (st != WINO_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int last = p->g.path == WINO_PATH_FUSED ? 3 : 4;
   for (int c = 0; c < p->n_chunks; c++)
-    for (int stage = 2; stage <= 4; stage++) {
+    for (int stage = 2; stage <= last; stage++) {
       st = run_stage(p, stage, c, x, w_wino, codes, rq_mult, rq_shift, y, workspace, s);
       if (st != WINO_OK) return st;
     }
@@ -230,7 +244,8 @@ wino_status wino_conv2d_int8_stage(wino_plan_t p, int stage, int chunk, const in
                                    void* stream) {
   wino_status st = check_conv_args(p, x, w_wino, codes, rq_mult, rq_shift, y, workspace);
   if (st != WINO_OK) return st;
-  if (stage < 2 || stage > 4 || chunk < 0 || chunk >= p->n_chunks) return WINO_ERR_INVALID_ARG;
+  const int last = p->g.path == WINO_PATH_FUSED ? 3 : 4;
+  if (stage < 2 || stage > last || chunk < 0 || chunk >= p->n_chunks) return WINO_ERR_INVALID_ARG;
   return run_stage(p, stage, chunk, x, w_wino, codes, rq_mult, rq_shift, y, workspace,
                    static_cast<cudaStream_t>(stream));
 }

@@ -18,7 +18,11 @@ def _wino():
     return W
 
 
-def _run(x, w, layout, pad=1, scaling=True, out_mode=1, M0=1, S=0, chunk_mb=None):
+FUSED, STAGED = 0, 1
+PATHS = [pytest.param(FUSED, id="fused"), pytest.param(STAGED, id="staged")]
+
+
+def _run(x, w, layout, pad=1, scaling=True, out_mode=1, M0=1, S=0, chunk_mb=None, path=FUSED):
     W = _wino()
     if chunk_mb is not None:
         os.environ["WINO_CHUNK_MB"] = str(chunk_mb)
@@ -28,7 +32,7 @@ def _run(x, w, layout, pad=1, scaling=True, out_mode=1, M0=1, S=0, chunk_mb=None
         else:
             n, h, wd, ci = x.shape
         co = w.shape[0]
-        conv = W.WinoConv2d(n, h, wd, ci, co, pad, layout, scaling, out_mode)
+        conv = W.WinoConv2d(n, h, wd, ci, co, pad, layout, scaling, out_mode, path=path)
     finally:
         os.environ.pop("WINO_CHUNK_MB", None)
     xd = torch.from_numpy(x).cuda(); wdv = torch.from_numpy(w).cuda()
@@ -38,8 +42,8 @@ def _run(x, w, layout, pad=1, scaling=True, out_mode=1, M0=1, S=0, chunk_mb=None
     return conv, y.cpu().numpy()
 
 
-def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates=True):
-    conv, y32 = _run(x, w, layout, pad, scaling, 1, chunk_mb=chunk_mb)
+def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates=True, path=FUSED):
+    conv, y32 = _run(x, w, layout, pad, scaling, 1, chunk_mb=chunk_mb, path=path)
     ref = O.wino_conv(x, w, pad, layout, scaling=scaling, want_M=intermediates)
     np.testing.assert_array_equal(y32, ref.out32)
     if not scaling:
@@ -62,6 +66,8 @@ def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates
             vpl = LD.decode_v(vbuf, T, info.cin_pad // 32, info.cin_pad)
             D = O.input_transform(x, pad, layout)
             np.testing.assert_array_equal(vpl[:, :, :ci], LD.complex_to_planes(D))
+            if path == FUSED:
+                return conv
             # K3: GEMMs + Karatsuba recombination + reverse scaling == oracle M''
             mraw = conv.m_raw().cpu().numpy()
             ms = LD.decode_m(mraw, T, co, info.cout_pad, info.n_block, info.chunk_tiles_pad)
@@ -73,13 +79,14 @@ def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates
     return conv
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("layout", [O.NHWC, O.NCHW])
 @pytest.mark.parametrize("scaling", [False, True])
-def test_c1_all_stages(layout, scaling):
+def test_c1_all_stages(layout, scaling, path):
     """BASELINE configs[0]: batch 1, 8x8, 4->4, scaling off then on; every
-    kernel's output (codes, W', V, M, y) against the oracle."""
+    kernel's output (codes, W', V, M'' on the staged path, y) against the oracle."""
     x, w = synth.config_inputs("C1", layout)
-    _check_layer(x, w, layout, 1, scaling)
+    _check_layer(x, w, layout, 1, scaling, path=path)
 
 
 @pytest.mark.parametrize("case", [
@@ -93,44 +100,50 @@ def test_c1_all_stages(layout, scaling):
     (4, 18, 18, 96, 128, 1, O.NHWC),
 ])
 @pytest.mark.parametrize("scaling", [False, True])
-def test_random_shapes_all_stages(case, scaling):
+@pytest.mark.parametrize("path", PATHS)
+def test_random_shapes_all_stages(case, scaling, path):
     n, h, wd, ci, co, pad, layout = case
-    rng = np.random.default_rng(hash((case, scaling)) % 2 ** 32)
+    rng = np.random.default_rng(abs(hash((case, scaling))) % 2 ** 32)
     x, w = synth.random_layer(rng, n, h, wd, ci, co, layout)
-    _check_layer(x, w, layout, pad, scaling)
+    _check_layer(x, w, layout, pad, scaling, path=path)
 
 
 @pytest.mark.parametrize("xv,wv", [(-128, -128), (127, 127), (-128, 127)])
 @pytest.mark.parametrize("scaling", [False, True])
-def test_extremes(xv, wv, scaling):
+@pytest.mark.parametrize("path", PATHS)
+def test_extremes(xv, wv, scaling, path):
     x = np.full((2, 12, 13, 40), xv, np.int8); w = np.full((24, 3, 3, 40), wv, np.int8)
-    _check_layer(x, w, O.NHWC, 1, scaling)
+    _check_layer(x, w, O.NHWC, 1, scaling, path=path)
 
 
-def test_multi_chunk_matches_single_chunk():
+@pytest.mark.parametrize("path", PATHS)
+def test_multi_chunk_matches_single_chunk(path):
     rng = np.random.default_rng(77)
-    x, w = synth.random_layer(rng, 7, 20, 20, 32, 48, O.NHWC)
-    conv, y = _run(x, w, O.NHWC, scaling=True, chunk_mb=1)
+    x, w = synth.random_layer(rng, 24, 20, 20, 64, 48, O.NHWC)
+    conv, y = _run(x, w, O.NHWC, scaling=True, chunk_mb=1, path=path)
     assert conv.info.n_chunks > 1
     np.testing.assert_array_equal(y, O.wino_conv(x, w, 1, O.NHWC, scaling=True).out32)
 
 
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("cout", [20, 32])
 @pytest.mark.parametrize("layout", [O.NHWC, O.NCHW])
-def test_int8_requant_output(layout):
+def test_int8_requant_output(layout, cout, path):
     rng = np.random.default_rng(5)
-    x, w = synth.random_layer(rng, 2, 15, 14, 24, 20, layout)
-    for M0, S in [(1, 0), (1, 9), (3, 11), (7, 1)]:
-        _, y8 = _run(x, w, layout, scaling=True, out_mode=0, M0=M0, S=S)
+    x, w = synth.random_layer(rng, 2, 15, 14, 24, cout, layout)
+    for M0, S in [(1, 0), (1, 9), (3, 11), (7, 1), (1, 20), (1, 24), (5, 40)]:
+        _, y8 = _run(x, w, layout, scaling=True, out_mode=0, M0=M0, S=S, path=path)
         ref = O.wino_conv(x, w, 1, layout, scaling=True, M0=M0, S=S)
         np.testing.assert_array_equal(y8, ref.y8)
 
 
-def test_max_cin_unscaled_896_and_scaled_768():
+@pytest.mark.parametrize("path", PATHS)
+def test_max_cin_unscaled_896_and_scaled_768(path):
     rng = np.random.default_rng(9)
     for ci, scaling in [(896, False), (768, True)]:
         x = rng.integers(-128, 128, (1, 6, 7, ci)).astype(np.int8)
         w = np.where(rng.integers(0, 2, (3, 3, 3, ci)) == 1, 127, -128).astype(np.int8)
-        _check_layer(x, w, O.NHWC, 1, scaling, intermediates=False)
+        _check_layer(x, w, O.NHWC, 1, scaling, intermediates=False, path=path)
 
 
 def test_plan_rejects():
@@ -199,8 +212,9 @@ def test_check_codes_and_maxpool():
         np.testing.assert_array_equal(y, O.maxpool2(x, layout))
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", ["C2", "C3", "C4"])
-def test_full_size_configs_sampled(name):
+def test_full_size_configs_sampled(name, path):
     """Full BASELINE sizes in the bench launch configuration (NHWC, int8 out,
     default chunking); whole images sampled (first, middle, last) and compared
     bit-exactly with the oracle run on those images alone."""
@@ -209,7 +223,7 @@ def test_full_size_configs_sampled(name):
     x, w = synth.config_inputs(name)
     S = synth.requant_shift(layer)
     conv = W.WinoConv2d(layer.n, layer.h, layer.w, layer.c_in, layer.c_out, 1, W.WINO_NHWC, True,
-                        W.WINO_OUT_INT8)
+                        W.WINO_OUT_INT8, path=path)
     conv.transform_filter(torch.from_numpy(w).cuda())
     y = conv(torch.from_numpy(x).cuda(), 1, S).cpu().numpy()
     for i in sorted({0, layer.n // 2, layer.n - 1}):
