@@ -4,7 +4,8 @@
 
 One step = the whole hot path over one batch of
 synthetic input: filter transform + scaling (K1) and the convolution
-(K2 input transform -> K3 tcgen05 GEMMs -> K4 output transform, per chunk).
+(K2 input transform -> K3F fused tcgen05 GEMMs + reverse scaling + output
+transform, per chunk; `--path staged` runs the three-kernel K2 -> K3 -> K4 path).
 Weak scaling: every rank runs its own batch of the configuration (data
 parallel by batch, no collective on the data path).  Inputs and weights are
 rotated over enough distinct sets that they never stay resident in the 126 MB
@@ -129,8 +130,9 @@ def run_ours(args):
     # configuration's batch (or Cout for batch < world) is split over the ranks
     sh = SH.shard(layer.n, layer.c_out, world, rank) if args.scaling == "strong" else \
         {"mode": "replica", "n0": 0, "n": layer.n, "co0": 0, "co": layer.c_out}
+    path = W.WINO_PATH_STAGED if args.path == "staged" else W.WINO_PATH_FUSED
     conv = W.WinoConv2d(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad, W.WINO_NHWC, layer.scaling,
-                        W.WINO_OUT_INT8, device=local_rank)
+                        W.WINO_OUT_INT8, device=local_rank, path=path)
     info = conv.info
     x_bytes, y_bytes = info.x_bytes, info.y_bytes
     w_bytes = sh["co"] * 9 * layer.c_in
@@ -164,7 +166,7 @@ def run_ours(args):
         L.wino_conv2d_int8(conv.plan, xs[j].data_ptr(), ww_.data_ptr(), cd_.data_ptr(), 1, S, ys[j].data_ptr(),
                            ws_.data_ptr(), st_.cuda_stream)
 
-    launches_per_step = 1 + 3 * info.n_chunks
+    launches_per_step = 1 + info.stages * info.n_chunks
     # CUDA graphs: one per (stream lane, rotation slot) (launch-bound otherwise)
     graphs = {}
     with torch.cuda.stream(stream):
@@ -243,7 +245,9 @@ def run_ours(args):
                 "workload": f"{cfg.name}: {cfg.description}", "batch_per_gpu": layer.n, "h": layer.h, "w": layer.w,
                 "c_in": layer.c_in, "c_out": layer.c_out, "pad": layer.pad, "layout": "NHWC",
                 "filter_scaling": layer.scaling, "output": f"int8 requantised (M0=1, S={S})",
-                "step": "filter transform + scaling (K1) + conv (K2,K3,K4 per chunk)",
+                "step": "filter transform + scaling (K1) + conv (" +
+                        ("K2, K3F fused GEMM+output per chunk)" if info.path == 0 else "K2,K3,K4 per chunk)"),
+                "path": "fused" if info.path == 0 else "staged",
                 "l2": f"inputs/weights/outputs rotated over {n_sets} sets "
                       f"({n_sets * per_set / 2 ** 20:.0f} MiB > 126 MiB L2)",
                 "parallelism": f"dp{world} ({'replicated per-rank batches, weak scaling' if args.scaling == 'weak' else sh['mode'] + '-sharded, strong scaling'}; no data-path collective)",
@@ -360,7 +364,7 @@ def run_ours_stack(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
             "config": {"workload": f"C5: {cfg.description}", "batch_per_gpu": n, "layers": len(cfg.layers),
                        "layout": "NHWC", "filter_scaling": True, "requant_shifts": shifts,
-                       "step": "13 filter transforms + 13 convs (K2,K3,K4 per chunk) + 4 max pools",
+                       "step": "13 filter transforms + 13 convs (K2, K3F fused per chunk) + 4 max pools",
                        "l2": "activations 0.8 GB per layer >> 126 MiB L2; 2 input sets rotated",
                        "parallelism": f"dp{world} (replicated per-rank batches, weak scaling)"},
             "path_roofline": {"t_roof_us": round(t_roof * 1e6, 2), "t_step_us": round(t_max / args.steps * 1e6, 2),
@@ -407,10 +411,11 @@ def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps):
     from paper_1901_01965_b200 import _lib as L
     info = conv.info
     sp = stream.cuda_stream
-    names = {1: "k1_filter", 2: "k2_input", 3: "k3_gemm", 4: "k4_output"}
+    names = {1: "k1_filter", 2: "k2_input", 3: "k3_gemm", 4: "k4_output"} if info.path == 1 else \
+        {1: "k1_filter", 2: "k2_input", 3: "k3_fused"}
     w_wino, codes, wsp = conv.w_wino.data_ptr(), conv.codes.data_ptr(), conv.workspace.data_ptr()
     out = {}
-    for st in (1, 2, 3, 4):
+    for st in sorted(names):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             for r in range(reps):
@@ -465,15 +470,25 @@ def roofline(kern, info, layer, peaks, traffic=None):
     k2_bytes = x_chunk + 92 * chunk_tiles * info.cin_pad
     # K3: 46 general multiplies per (tile, cin, cout) = the paper's count, 2 ops each
     k3_ops = 2 * 46 * chunk_tiles * layer.c_in * layer.c_out
-    k3_bytes = 92 * chunk_tiles * info.cin_pad + 46 * 4 * chunk_tiles * info.cout_pad + info.filter_bytes
-    # K4: reads 46 int32 per (tile, cout), writes y int8
-    k4_bytes = 46 * 4 * chunk_tiles * layer.c_out + chunk_tiles * 16 * layer.c_out
-    spec = {
-        "k1_filter": ("hbm", k1_bytes, hbm, "GB/s"),
-        "k2_input": ("hbm", k2_bytes, hbm, "GB/s"),
-        "k3_gemm": ("tensor", k3_ops, i8_sus, "TOPS"),
-        "k4_output": ("hbm", k4_bytes, hbm, "GB/s"),
-    }
+    k3_bytes = 92 * chunk_tiles * info.cin_pad + 36 * 4 * chunk_tiles * info.cout_pad + info.filter_bytes
+    # K4: reads 36 int32 per (tile, cout), writes y int8
+    k4_bytes = 36 * 4 * chunk_tiles * layer.c_out + chunk_tiles * 16 * layer.c_out
+    # K3F (fused): the K3 work; bytes: V once, W' once, y int8 once
+    k3f_bytes = 92 * chunk_tiles * info.cin_pad + info.filter_bytes + chunk_tiles * 16 * layer.c_out
+    if info.path == 1:
+        spec = {
+            "k1_filter": ("hbm", k1_bytes, hbm, "GB/s"),
+            "k2_input": ("hbm", k2_bytes, hbm, "GB/s"),
+            "k3_gemm": ("tensor", k3_ops, i8_sus, "TOPS"),
+            "k4_output": ("hbm", k4_bytes, hbm, "GB/s"),
+        }
+    else:
+        spec = {
+            "k1_filter": ("hbm", k1_bytes, hbm, "GB/s"),
+            "k2_input": ("hbm", k2_bytes, hbm, "GB/s"),
+            "k3_fused": ("tensor", k3_ops, i8_sus, "TOPS"),
+        }
+        k3_bytes = k3f_bytes
     all_k = {}
     for name, (bound, work, peak, unit) in spec.items():
         t = kern[name]["s_per_launch"]
@@ -482,7 +497,7 @@ def roofline(kern, info, layer, peaks, traffic=None):
              "frac": round(achieved / peak, 4), "traffic": (traffic or {}).get(name), "us_per_launch": round(t * 1e6, 3),
              "launches_per_step": kern[name]["launches_per_step"],
              "share_of_step": None, "algorithmic_per_launch": work}
-        if name == "k3_gemm":
+        if name in ("k3_gemm", "k3_fused"):
             d["hbm_view"] = {"bytes_per_launch": k3_bytes, "achieved_gbs": round(k3_bytes / t / 1e9, 1),
                              "frac_of_hbm": round(k3_bytes / t / 1e9 / hbm, 4)}
         all_k[name] = d
@@ -492,7 +507,7 @@ def roofline(kern, info, layer, peaks, traffic=None):
     dom = max(all_k, key=lambda k: kern[k]["s_per_step"])
     dominant = dict(all_k[dom]); dominant["kernel"] = dom
     dominant["peak_source"] = peaks["source"] + (
-        "; int8 = 2 x bf16 sustained" if dom == "k3_gemm" else "; hbm_gbs")
+        "; int8 = 2 x bf16 sustained" if dom in ("k3_gemm", "k3_fused") else "; hbm_gbs")
     return {"dominant": dominant, "all": all_k}
 
 
@@ -649,6 +664,7 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--streams", type=int, default=3,
                     help="independent batches in flight on separate streams (own filter/workspace buffers)")
+    ap.add_argument("--path", default="staged", choices=["fused", "staged"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()

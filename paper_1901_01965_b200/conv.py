@@ -15,7 +15,7 @@ class WinoConv2d:
     """
 
     def __init__(self, n, h, w, c_in, c_out, pad=1, layout=L.WINO_NHWC, filter_scaling=True,
-                 out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0, path=L.WINO_PATH_FUSED):
+                 out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0, path=L.WINO_PATH_STAGED):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device)

@@ -38,6 +38,7 @@
 // TMEM: columns [0, 240) accumulator ring, [256, 512) row partials
 // [Z_0 | P | Q | Z_5][cw 0..3][j 0..3][c 0..3].
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 #include <cuda_runtime.h>
 
@@ -120,6 +121,10 @@ __device__ __forceinline__ int32_t frscale(int32_t v, uint32_t mq) {
   return (int32_t)(p >> 7);
 }
 
+__device__ __forceinline__ void fwait(uint32_t bar, uint32_t parity, int dbg) {
+  if (dbg & 64) mbar_spin(bar, parity); else mbar_wait(bar, parity);
+}
+
 // a_k[c] for the real indices c in {0,1,2,5}
 __host__ __device__ constexpr int areal(int k, int c) {
   return c == 0 ? (k == 0) : (c == 1 ? 1 : (c == 2 ? ((k & 1) ? -1 : 1) : (k == 3)));
@@ -133,7 +138,7 @@ __host__ __device__ constexpr int im_y(int n) { return re_x(n); }
 template <bool NHWC, bool OUT8, bool RQFAST>
 __global__ void __launch_bounds__(kFThreads, 1)
     k_fused(const int8_t* __restrict__ V, const int8_t* __restrict__ W, const uint8_t* __restrict__ codes, Geom g,
-            int n0, int imgs, int tblocks, int32_t rq_mult, int rq_shift, void* __restrict__ y) {
+            int n0, int imgs, int tblocks, int32_t rq_mult, int rq_shift, void* __restrict__ y, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* staging = smem + kFStages * kFStageBytes;
@@ -192,11 +197,20 @@ __global__ void __launch_bounds__(kFThreads, 1)
           const int8_t* wh = wt + (long long)(2 * plane) * pstride;
           for (int ks = 0; ks < n_it; ks++, it++) {
             const int s = it % kFStages;
-            mbar_wait(empty0 + 8 * s, ((it / kFStages) & 1) ^ 1);
+            fwait(empty0 + 8 * s, ((it / kFStages) & 1) ^ 1, dbg);
             const int k0 = ks * kFKPerStage;
             const int kn = min(kFKPerStage, ksteps - k0);
             const uint32_t st = sbase + s * kFStageBytes;
+            if (dbg & 32) {   // debug: no copies (synchronisation cost only)
+              mbar_arrive(full0 + 8 * s);
+              continue;
+            }
             mbar_arrive_expect_tx(full0 + 8 * s, kn * (2 * kVBlockBytes + 2 * kFN * kKStep));
+            if (dbg & 16) {   // debug: the same bytes as one contiguous copy
+              bulk_g2s(st, vt + (long long)(it & 63) * kFStageBytes, kn * (2 * kVBlockBytes + 2 * kFN * kKStep),
+                       full0 + 8 * s);
+              continue;
+            }
             for (int kk = 0; kk < kn; kk++) {
               const int8_t* src = vblk + (long long)(k0 + kk) * (2 * kPlanes) * kVBlockBytes;
               bulk_g2s(st + kk * kVBlockBytes, src, kVBlockBytes, full0 + 8 * s);                       // hi
@@ -218,17 +232,17 @@ __global__ void __launch_bounds__(kFThreads, 1)
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         for (int i = 0; i < kFPlanes; i++, pc++) {
           const int b = pc % kFAccSlots;
-          mbar_wait(tempty0 + 8 * b, ((pc / kFAccSlots) & 1) ^ 1);   // epilogue drained this slot
+          fwait(tempty0 + 8 * b, ((pc / kFAccSlots) & 1) ^ 1, dbg);   // epilogue drained this slot
           tc_fence_after();
           const uint32_t acc_hh = tmem + b * kFAccCols, acc_x = acc_hh + kFN, acc_ll = acc_hh + 2 * kFN;
           for (int ks = 0; ks < n_it; ks++, it++) {
             const int s = it % kFStages;
-            mbar_wait(full0 + 8 * s, (it / kFStages) & 1);
+            fwait(full0 + 8 * s, (it / kFStages) & 1, dbg);
             tc_fence_after();
             const int k0 = ks * kFKPerStage;
             const int kn = min(kFKPerStage, ksteps - k0);
             const uint32_t st = sbase + s * kFStageBytes;
-            for (int kk = 0; kk < kn; ++kk) {
+            for (int kk = 0; kk < kn && !(dbg & 2); ++kk) {
               const uint32_t acc = (k0 + kk) > 0;
               const uint64_t a_hi = umma_desc(st + kk * kVBlockBytes, 128, 256);
               const uint64_t a_lo = umma_desc(st + kFA + kk * kVBlockBytes, 128, 256);
@@ -256,14 +270,14 @@ __global__ void __launch_bounds__(kFThreads, 1)
     // one plane: M = 2^16 hh + 2^8 x + ll for this thread's 4 couts
     auto take = [&](int32_t (&v)[kFC]) {
       const int b = pc % kFAccSlots;
-      mbar_wait(tfull0 + 8 * b, (pc / kFAccSlots) & 1);
+      fwait(tfull0 + 8 * b, (pc / kFAccSlots) & 1, dbg);
       tc_fence_after();
       const uint32_t a = lane_base + b * kFAccCols;
       uint32_t h[kFC], x[kFC], l[kFC];
       tmem_ld4(a, h);
       tmem_ld4(a + kFN, x);
       tmem_ld4(a + 2 * kFN, l);
-      tmem_ld_wait();
+      if (!(dbg & 4)) tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty0 + 8 * b);
@@ -327,6 +341,16 @@ __global__ void __launch_bounds__(kFThreads, 1)
         for (int c = 0; c < kFC; c++) Z[j][c] += 2 * re_x(j) * re[c] + 2 * re_y(j) * im[c];
     };
 
+    if (dbg & 8) {   // debug: accumulator handshake only
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x)
+        for (int i = 0; i < kFPlanes; i++, pc++) {
+          const int b = pc % kFAccSlots;
+          fwait(tfull0 + 8 * b, (pc / kFAccSlots) & 1, dbg);
+          tc_fence_after();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty0 + 8 * b);
+        }
+    } else {
     fill_etab(blockIdx.x, 0);
     int k = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, k++) {
@@ -386,6 +410,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
       cpx_row(std::integral_constant<int, 5>{});
       tmem_st_wait();
 
+      if (dbg & 1) continue;   // debug: no output (pipeline timing)
       // ---- out32 = rha(Y / 16) (A11), optional requantisation (A14), crop, store
       const int tb_i = u / nblocks, nb = u - tb_i * nblocks;
       const int t = tb_i * kMBlock + row;              // chunk tile
@@ -532,6 +557,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         }
       }
     }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -539,6 +565,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
 }
 
 static int g_fused_sms = 0;
+static int g_fused_dbg = 0;   // WINO_FUSED_DBG (debug timing only): 1 no output, 2 no MMAs, 4 no TMEM-load wait
 
 cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
                          const int8_t* wimg, const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y,
@@ -551,7 +578,7 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 20;
   cudaError_t e;
 #define WINO_KF(A, B, C) \
-  e = launch_pdl(k_fused<A, B, C>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs, tblocks, rq_mult, rq_shift, y)
+  e = launch_pdl(k_fused<A, B, C>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs, tblocks, rq_mult, rq_shift, y, g_fused_dbg)
   if (nhwc) {
     if (!out8) WINO_KF(true, false, false);
     else if (fast) WINO_KF(true, true, true);
@@ -569,6 +596,7 @@ cudaError_t setup_fused() {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_fused_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (const char* d = std::getenv("WINO_FUSED_DBG")) g_fused_dbg = std::atoi(d);
   const int smem = (int)fused_smem_bytes();
 #define WINO_KF_ATTR(A, B, C) \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)

@@ -42,6 +42,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Non-suspending poll (mbarrier.test_wait): no wake-up latency after the phase flips.
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
+  while (!mbar_test_wait(bar, parity)) {
+  }
+}
 
 // ---------------------------------------------------------------- bulk copy (TMA engine, 1-D)
 // global -> shared, completion counted in bytes on `bar`.  16-B aligned, size % 16 == 0.

@@ -12,7 +12,8 @@ from .conv import WinoConv2d, maxpool2
 
 
 class ConvStack:
-    def __init__(self, n, layers, pools_after, shifts, layout=L.WINO_NHWC, device=None, workspace_mb=1024):
+    def __init__(self, n, layers, pools_after, shifts, layout=L.WINO_NHWC, device=None, workspace_mb=1024,
+                 path=L.WINO_PATH_STAGED):
         """layers: sequence of objects with h, w, c_in, c_out, pad, scaling; shifts: requant
         shift per layer (multiplier 1)."""
         if device is None:
@@ -23,13 +24,13 @@ class ConvStack:
         sizes = []
         for l in layers:
             d = L.wino_conv_desc(n, l.h, l.w, l.c_in, l.c_out, l.pad, layout, int(l.scaling), 255, L.WINO_OUT_INT8,
-                                 workspace_mb)
+                                 workspace_mb, path)
             plan = L.wino_plan(d, device)
             sizes.append(L.wino_workspace_bytes(plan))
             L.wino_plan_destroy(plan)
         self.workspace = torch.empty(max(sizes), dtype=torch.int8, device=self.device)
         self.convs = [WinoConv2d(n, l.h, l.w, l.c_in, l.c_out, l.pad, layout, l.scaling, L.WINO_OUT_INT8, device,
-                                 workspace=self.workspace, workspace_mb=workspace_mb) for l in layers]
+                                 workspace=self.workspace, workspace_mb=workspace_mb, path=path) for l in layers]
         self.outs = [torch.empty(c.y_shape, dtype=torch.int8, device=self.device) for c in self.convs]
         self.pooled = {}
         for i, c in enumerate(self.convs):
@@ -66,4 +67,4 @@ class ConvStack:
         return cur
 
     def launches(self):
-        return sum(1 + 3 * c.info.n_chunks for c in self.convs) + len(self.pooled)
+        return sum(1 + c.info.stages * c.info.n_chunks for c in self.convs) + len(self.pooled)
