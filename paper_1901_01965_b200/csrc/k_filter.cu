@@ -94,10 +94,15 @@ __device__ __forceinline__ void load_filter(const Geom& g, const int8_t* __restr
 //   pass 2: per 32-channel group (one per warp), recompute, scale, split and
 //           stage the 92 operand bytes per channel in shared memory, then write
 //           whole 16-byte rows of the pre-tiled W image.
+//   FUSED: the fused path's group layout instead (layout.cuh): per group the rows
+//   real [W hi, W lo], complex [Wr hi, Wi hi, Wr lo, Wi lo, -Wi hi, Wr hi, -Wi lo, Wr lo]
+//   (balanced s8 pieces), 112 staged rows per channel.
+template <bool FUSED>
 __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, const int8_t* __restrict__ w,
                                                                          int8_t* __restrict__ wimg,
                                                                          uint8_t* __restrict__ codes) {
-  __shared__ __align__(16) int8_t s_stage[kFilterWarps][2 * kPlanes][32];
+  constexpr int kRows = FUSED ? 2 * kWRowUnitsF : 2 * kPlanes;
+  __shared__ __align__(16) int8_t s_stage[kFilterWarps][kRows][32];
   __shared__ int s_max[kFilterWarps][26];
   __shared__ int s_n[26], s_p[26];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -170,23 +175,60 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
 #pragma unroll
       for (int i = 0; i < 46; i++) vals[i] = 0;
     }
+    if constexpr (!FUSED) {
 #pragma unroll
-    for (int pl = 0; pl < 46; pl++) {
-      s_stage[warp][2 * pl + 0][lane] = (int8_t)(vals[pl] >> 8);             // hi, s8
-      s_stage[warp][2 * pl + 1][lane] = (int8_t)(uint8_t)(vals[pl] & 255);   // lo, u8
-    }
-    __syncwarp();
-    for (int idx = lane; idx < 2 * kPlanes * 2; idx += 32) {   // (piece-plane, 16-channel half)
-      const int pp = idx >> 1, hf = idx & 1;
-      const int4 v = *reinterpret_cast<const int4*>(&s_stage[warp][pp][hf * 16]);
-      *reinterpret_cast<int4*>(wimg + w_offset(g, pp, co, c0 + hf * 16)) = v;
+      for (int pl = 0; pl < 46; pl++) {
+        s_stage[warp][2 * pl + 0][lane] = (int8_t)(vals[pl] >> 8);             // hi, s8
+        s_stage[warp][2 * pl + 1][lane] = (int8_t)(uint8_t)(vals[pl] & 255);   // lo, u8
+      }
+      __syncwarp();
+      for (int idx = lane; idx < 2 * kPlanes * 2; idx += 32) {   // (piece-plane, 16-channel half)
+        const int pp = idx >> 1, hf = idx & 1;
+        const int4 v = *reinterpret_cast<const int4*>(&s_stage[warp][pp][hf * 16]);
+        *reinterpret_cast<int4*>(wimg + w_offset(g, pp, co, c0 + hf * 16)) = v;
+      }
+    } else {
+      // staged row 2 * wprefix(gi) + j holds piece-row j of group gi for this cout
+#pragma unroll
+      for (int s = 0; s < 16; s++) {
+        const int r0 = 2 * fg_wprefix(fg_of_real(s));
+        s_stage[warp][r0 + 0][lane] = (int8_t)bal_hi(vals[s]);
+        s_stage[warp][r0 + 1][lane] = (int8_t)bal_lo(vals[s]);
+      }
+#pragma unroll
+      for (int k = 0; k < 10; k++) {
+        const int r0 = 2 * fg_wprefix(fg_of_primary(k));
+        const int wr = vals[16 + 3 * k], wi = vals[16 + 3 * k + 1], nwi = -wi;
+        s_stage[warp][r0 + 0][lane] = (int8_t)bal_hi(wr);
+        s_stage[warp][r0 + 1][lane] = (int8_t)bal_hi(wi);
+        s_stage[warp][r0 + 2][lane] = (int8_t)bal_lo(wr);
+        s_stage[warp][r0 + 3][lane] = (int8_t)bal_lo(wi);
+        s_stage[warp][r0 + 4][lane] = (int8_t)bal_hi(nwi);
+        s_stage[warp][r0 + 5][lane] = (int8_t)bal_hi(wr);
+        s_stage[warp][r0 + 6][lane] = (int8_t)bal_lo(nwi);
+        s_stage[warp][r0 + 7][lane] = (int8_t)bal_lo(wr);
+      }
+      __syncwarp();
+      const int nb = co / kFN16, cr = co % kFN16;
+      for (int idx = lane; idx < kRows * 2; idx += 32) {   // (staged row, 16-channel half)
+        const int sr = idx >> 1, hf = idx & 1;
+        // group of staged row sr: the last group whose 2 * wprefix <= sr
+        int gi = 0;
+#pragma unroll
+        for (int q = 1; q < kFGroupsN; q++) gi += (2 * fg_wprefix(q) <= sr) ? 1 : 0;
+        const int j = sr - 2 * fg_wprefix(gi);
+        const int4 v = *reinterpret_cast<const int4*>(&s_stage[warp][sr][hf * 16]);
+        *reinterpret_cast<int4*>(wimg + wf_offset(g, gi, nb, j * kFN16 + cr, c0 + hf * 16)) = v;
+      }
     }
     __syncwarp();
   }
 }
 
 cudaError_t launch_filter_transform(const Geom& g, const int8_t* w, int8_t* wimg, uint8_t* codes, cudaStream_t st) {
-  return launch_pdl(k_filter_transform, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
+  if (g.path == 0)
+    return launch_pdl(k_filter_transform<true>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
+  return launch_pdl(k_filter_transform<false>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
 }
 
 cudaError_t setup_filter_transform() { return cudaSuccess; }

@@ -14,6 +14,7 @@
 // All 92 plane-pieces of a (tile block, K step) are 4 KB apart, so every
 // store is an immediate offset from one base pointer.
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -64,15 +65,11 @@ __device__ __forceinline__ void store_plane(int8_t* base, int v0, int v1) {
   st16(base + (2 * PL + 1) * 4096, pk);                                  // lo pair (u8)
 }
 
-__global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const int8_t* __restrict__ x, int n0,
-                                                                   int imgs, int8_t* __restrict__ vimg) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tl = lane >> 3, cp = lane & 7;                      // tile within warp, channel pair
-  const int t = blockIdx.x * kInTilesPerCta + warp * kInTilesPerWarp + tl;   // chunk tile
-  const int c = blockIdx.y * kInChPerCta + 2 * cp;              // first channel of the pair
+// Gather the zero-padded 6x6 patch of chunk tile t for channels c, c+1 and form
+// d' = B^T d column by column for both channels.
+__device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restrict__ x, int n0, int imgs, int t, int c,
+                                           Rows (&r)[2]) {
   const int tiles = imgs * g.tpi;
-  pdl_trigger();
-  pdl_wait();   // x may come from the previous kernel (layer stacks); V may still be read by the previous GEMM
 
   // ---- gather the zero-padded 6x6 patch at origin (4ty - pad, 4tx - pad): 2 channels per pixel
   uint32_t w[36];
@@ -120,7 +117,6 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
   }
 
   // ---- d' = B^T d per column, for both channels
-  Rows r[2];
 #pragma unroll
   for (int j = 0; j < 6; j++) {
 #pragma unroll
@@ -136,6 +132,18 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
       r[ch].e5[j] = d5 - d1;
     }
   }
+}
+
+__global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const int8_t* __restrict__ x, int n0,
+                                                                   int imgs, int8_t* __restrict__ vimg) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tl = lane >> 3, cp = lane & 7;                      // tile within warp, channel pair
+  const int t = blockIdx.x * kInTilesPerCta + warp * kInTilesPerWarp + tl;   // chunk tile
+  const int c = blockIdx.y * kInChPerCta + 2 * cp;              // first channel of the pair
+  pdl_trigger();
+  pdl_wait();   // x may come from the previous kernel (layer stacks); V may still be read by the previous GEMM
+  Rows r[2];
+  input_rows(g, x, n0, imgs, t, c, r);
 
   // ---- D = d' B along rows; store every plane as soon as it is formed
   const long long tb = t / kMBlock;
@@ -191,6 +199,83 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
     store_plane<43>(base, q[0][2], q[1][2]); store_plane<44>(base, q[0][3], q[1][3]);
     store_plane<45>(base, q[0][2] + q[0][3], q[1][2] + q[1][3]);
   }
+}
+
+// ---- fused-path V image (layout.cuh "fused-path operand layouts"): per group, balanced s8 pieces
+// hi = (v + 128) >> 8 (byte 1 of v + 128), lo = v - 256 hi (byte 0 of v), stored for both channels.
+__device__ __forceinline__ void st_bal(int8_t* p_hi, int v0, int v1) {
+  st16(p_hi, __byte_perm((uint32_t)(v0 + 128), (uint32_t)(v1 + 128), 0x0051));   // [hi0, hi1]
+  st16(p_hi + 4096, __byte_perm((uint32_t)v0, (uint32_t)v1, 0x0040));            // [lo0, lo1]
+}
+
+__global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, const int8_t* __restrict__ x, int n0,
+                                                                     int imgs, int8_t* __restrict__ vimg) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tl = lane >> 3, cp = lane & 7;
+  const int t = blockIdx.x * kInTilesPerCta + warp * kInTilesPerWarp + tl;
+  const int c = blockIdx.y * kInChPerCta + 2 * cp;
+  pdl_trigger();
+  pdl_wait();
+  Rows r[2];
+  input_rows(g, x, n0, imgs, t, c, r);
+
+  const long long tb = t / kMBlock;
+  const int row = t % kMBlock;
+  const long long kst = (long long)g.ksteps * kVBlockBytes;
+  int8_t* base = vimg + tb * kVPiecesF * kst + tiled_offset(row, c & 31, kMBlock);
+  const int ks = c >> 5;
+  // first (hi) piece of group gi for this K step
+  auto gp = [&](int gi) { return base + fg_vprefix(gi) * kst + (long long)(ks * fg_pieces(gi)) * kVBlockBytes; };
+  auto real_row = [&](auto ric, const int (&e0)[6], const int (&e1)[6]) {
+    constexpr int ri = decltype(ric)::value;
+    int v0[7], v1[7];
+    real_row_planes<ri>(e0, v0);
+    real_row_planes<ri>(e1, v1);
+#pragma unroll
+    for (int s = 0; s < 4; s++) st_bal(gp(fg_of_real(ri * 4 + s)), v0[s], v1[s]);
+    int8_t* pc = gp(fg_of_primary(ri));
+    st_bal(pc, v0[4], v1[4]);                      // Re (R[ri], 3)
+    st_bal(pc + 2 * kVBlockBytes, v0[5], v1[5]);   // Im
+  };
+  real_row(std::integral_constant<int, 0>{}, r[0].e0, r[1].e0);
+  real_row(std::integral_constant<int, 1>{}, r[0].e1, r[1].e1);
+  real_row(std::integral_constant<int, 2>{}, r[0].e2, r[1].e2);
+  real_row(std::integral_constant<int, 3>{}, r[0].e5, r[1].e5);
+  // complex row 3 = a + i b: (3,0) (3,1) (3,2) (3,5) -> primaries 4..7, (3,3) -> 8, (3,4) -> 9
+  int re[2][4], im[2][4], q[2][4];
+#pragma unroll
+  for (int ch = 0; ch < 2; ch++) {
+    const int* a = r[ch].ra;
+    const int* b = r[ch].rb;
+    const int as24 = a[2] + a[4], as13 = a[1] + a[3], bs24 = b[2] + b[4], bs13 = b[1] + b[3];
+    re[ch][0] = a[0] - a[4]; re[ch][1] = as13 + as24; re[ch][2] = as24 - as13; re[ch][3] = a[5] - a[1];
+    im[ch][0] = b[0] - b[4]; im[ch][1] = bs13 + bs24; im[ch][2] = bs24 - bs13; im[ch][3] = b[5] - b[1];
+    q[ch][0] = a[4] - a[2] - b[3] + b[1];
+    q[ch][1] = b[4] - b[2] + a[3] - a[1];
+    q[ch][2] = a[4] - a[2] + b[3] - b[1];
+    q[ch][3] = b[4] - b[2] - a[3] + a[1];
+  }
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    int8_t* pc = gp(fg_of_primary(4 + j));
+    st_bal(pc, re[0][j], re[1][j]);
+    st_bal(pc + 2 * kVBlockBytes, im[0][j], im[1][j]);
+  }
+  {
+    int8_t* pc = gp(fg_of_primary(8));
+    st_bal(pc, q[0][0], q[1][0]);
+    st_bal(pc + 2 * kVBlockBytes, q[0][1], q[1][1]);
+    pc = gp(fg_of_primary(9));
+    st_bal(pc, q[0][2], q[1][2]);
+    st_bal(pc + 2 * kVBlockBytes, q[0][3], q[1][3]);
+  }
+}
+
+cudaError_t launch_input_transform_f(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st) {
+  const long long tiles = (long long)imgs * g.tpi;
+  const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
+  dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
+  return launch_pdl(k_input_transform_f, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
 }
 
 cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st) {

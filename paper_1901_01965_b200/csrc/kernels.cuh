@@ -34,6 +34,8 @@ cudaError_t launch_filter_transform(const Geom& g, const int8_t* w, int8_t* wimg
 //   x: whole input tensor; images [n0, n0 + imgs) form the chunk.
 cudaError_t setup_input_transform();
 cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st);
+//   fused-path V image (group layout, balanced pieces; layout.cuh)
+cudaError_t launch_input_transform_f(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st);
 
 // K3: 46 Winograd-domain int8 GEMMs on tcgen05 + Karatsuba + reverse scaling -> M'' (k_gemm.cu)
 cudaError_t setup_gemm();
@@ -50,6 +52,7 @@ cudaError_t launch_output_transform(const Geom& g, const int32_t* mpp, int n0, i
 // K3F: fused GEMMs + Karatsuba + reverse scaling + output transform + store (k_fused.cu);
 //   requires g.nblk == 16.  V of the chunk -> y directly (no M'' in HBM).
 cudaError_t setup_fused();
+void set_fused_trace(void* buf);   // debug timeline (-DWINO_FUSED_TRACE), nullptr = off
 cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
                          const int8_t* wimg, const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y,
                          cudaStream_t st);

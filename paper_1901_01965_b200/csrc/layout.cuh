@@ -83,6 +83,60 @@ __host__ __device__ __forceinline__ long long w_offset(const Geom& g, int pp, in
          tiled_offset(r, k, g.nblk);
 }
 
+// ---------------------------------------------------------------- fused-path (K3F) operand layouts
+// The fused path stores the Winograd-domain operands by GROUP: a real position
+// (one real value) or a complex primary (Re and Im, the 4-multiplication complex
+// product Re = VrWr - ViWi, Im = VrWi + ViWr expressed as K/N-concatenated real
+// GEMMs).  Groups are numbered in the fused kernel's processing order gi:
+//   gi = 5k + s, k = 0..3 -> row R[frow(k)] (rows 0, 5, 1, 2): s < 4 real (R[ri], R[s]),
+//                                                            s = 4 primary ri
+//   gi = 20..25            -> primaries 4..9 (row 3)
+// Every value v is split into two BALANCED s8 pieces: lo = ((v + 128) & 255) - 128,
+// hi = (v - lo) / 256, so v = 256 hi + lo and one UMMA signedness (s8 x s8) fits all.
+// V (per 128-tile block): [group gi][K step][piece][128 rows x 32 B] with pieces
+//   real (hi, lo), complex (Re hi, Re lo, Im hi, Im lo)  -> 72 pieces per K step;
+//   a group's K steps are contiguous, so one bulk copy moves a whole stage.
+// W' (per 16-cout block): [group gi][K step][B rows x 32 B] with
+//   real: 32 rows [W hi (16 couts) | W lo (16)]
+//   complex: 128 rows: B0 = [Wr hi | Wi hi | Wr lo | Wi lo], B1 = [-Wi hi | Wr hi | -Wi lo | Wr lo]
+//   -> 56 x 32 rows per K step.
+constexpr int kFN16 = 16;            // couts per fused unit
+constexpr int kFGroupsN = 26;
+constexpr int kVPiecesF = 72;        // V pieces per (tile block, K step)
+constexpr int kWRowUnitsF = 56;      // 32-row W' units per (cout block, K step)
+__host__ __device__ constexpr int frow(int k) { return k == 0 ? 0 : (k == 1 ? 3 : k - 1); }
+__host__ __device__ constexpr bool fg_complex(int gi) { return gi >= 20 || gi % 5 == 4; }
+__host__ __device__ constexpr int fg_pieces(int gi) { return fg_complex(gi) ? 4 : 2; }
+__host__ __device__ constexpr int fg_wunits(int gi) { return fg_complex(gi) ? 4 : 1; }   // 32-row units
+__host__ __device__ constexpr int fg_vprefix(int gi) { return gi < 20 ? (gi / 5) * 12 + (gi % 5) * 2 : 48 + (gi - 20) * 4; }
+__host__ __device__ constexpr int fg_wprefix(int gi) { return gi < 20 ? (gi / 5) * 8 + (gi % 5) : 32 + (gi - 20) * 4; }
+// real plane index (R[ri]*... numbering of layout: ri*4 + s) or primary index of a group
+__host__ __device__ constexpr int fg_real_plane(int gi) { return frow(gi / 5) * 4 + gi % 5; }
+__host__ __device__ constexpr int fg_primary(int gi) { return gi < 20 ? frow(gi / 5) : 4 + gi - 20; }
+// group of real plane s (= ri*4 + c) / of primary k
+__host__ __device__ constexpr int fg_of_real(int s) {
+  return ((s >> 2) == 0 ? 0 : ((s >> 2) == 3 ? 1 : (s >> 2) + 1)) * 5 + (s & 3);
+}
+__host__ __device__ constexpr int fg_of_primary(int k) {
+  return k < 4 ? (k == 0 ? 0 : (k == 3 ? 1 : k + 1)) * 5 + 4 : 20 + k - 4;
+}
+// balanced s8 split
+__host__ __device__ __forceinline__ int bal_lo(int v) { return ((v + 128) & 255) - 128; }
+__host__ __device__ __forceinline__ int bal_hi(int v) { return (v - bal_lo(v)) >> 8; }
+// byte offset of V piece `piece` of group gi, chunk tile t, channel k (fused layout)
+__host__ __device__ __forceinline__ long long vf_offset(const Geom& g, int gi, int piece, long long t, int k) {
+  const long long blk = t / kMBlock;
+  const int r = (int)(t % kMBlock);
+  return ((blk * kVPiecesF + fg_vprefix(gi)) * g.ksteps + (long long)(k >> 5) * fg_pieces(gi) + piece) * kVBlockBytes +
+         tiled_offset(r, k & 31, kMBlock);
+}
+// byte offset of W' row `row` (within the group's 32- or 128-row block) of group gi, cout block nb, channel k
+__host__ __device__ __forceinline__ long long wf_offset(const Geom& g, int gi, int nb, int row, int k) {
+  const int rows = 32 * fg_wunits(gi);
+  return ((long long)(nb * kWRowUnitsF + fg_wprefix(gi)) * g.ksteps + (long long)(k >> 5) * fg_wunits(gi)) * 1024 +
+         tiled_offset(row, k & 31, rows);
+}
+
 // Position index (r*6+c) of real plane s and of complex primary k / its mirror
 // (arithmetic, so no local-memory tables; R = {0,1,2,5} -> R[i] = i + 2 (i == 3)).
 __host__ __device__ __forceinline__ int rsel(int i) { return i + (i == 3 ? 2 : 0); }

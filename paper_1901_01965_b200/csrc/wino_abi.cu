@@ -135,17 +135,19 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.out_mode = d.out_mode;
   // batch chunk: V (+ M on the staged path) of one chunk within the budget
   const size_t m_per_tile = d.path == WINO_PATH_STAGED ? wino::kSlots * 4 * (size_t)g.cout_pad : 0;
-  const size_t per_img = (size_t)g.tpi * (2 * wino::kPlanes * (size_t)g.cin_pad + m_per_tile);
+  const size_t v_per_tile_ch = d.path == WINO_PATH_STAGED ? 2 * wino::kPlanes : wino::kVPiecesF;
+  const size_t per_img = (size_t)g.tpi * (v_per_tile_ch * (size_t)g.cin_pad + m_per_tile);
   long long imgs = (long long)(chunk_budget_bytes(d.workspace_mb) / (per_img ? per_img : 1));
   if (imgs < 1) imgs = 1;
   if (imgs > d.n) imgs = d.n;
   g.chunk_imgs = (int)imgs;
   g.chunk_tiles_pad = round_up((long long)imgs * g.tpi, wino::kMBlock);
   p->n_chunks = (int)((d.n + imgs - 1) / imgs);
-  p->v_bytes = (size_t)2 * wino::kPlanes * g.chunk_tiles_pad * g.cin_pad;
+  p->v_bytes = v_per_tile_ch * g.chunk_tiles_pad * g.cin_pad;
   p->m_bytes = d.path == WINO_PATH_STAGED ? (size_t)wino::kSlots * g.chunk_tiles_pad * g.cout_pad * 4 : 0;
   p->ws_bytes = p->v_bytes + p->m_bytes;
-  p->f_bytes = (size_t)2 * wino::kPlanes * g.cout_pad * g.cin_pad;
+  // W': 92 B per (cin, cout) staged (46 planes x 2 pieces); 112 B fused (56 rows x 2 couts-halves, layout.cuh)
+  p->f_bytes = (size_t)(d.path == WINO_PATH_STAGED ? 2 * wino::kPlanes : 2 * wino::kWRowUnitsF) * g.cout_pad * g.cin_pad;
   p->x_bytes = (size_t)d.n * d.h * d.w * d.c_in;
   p->y_bytes = (size_t)d.n * g.ho * g.wo * d.c_out * (d.out_mode == WINO_OUT_INT32 ? 4 : 1);
   *out = p;
@@ -166,7 +168,8 @@ wino_status wino_plan_query(wino_plan_t p, wino_plan_info* info) {
   info->tiles = (long long)p->d.n * p->g.tpi;
   info->cin_pad = p->g.cin_pad; info->cout_pad = p->g.cout_pad;
   info->n_block = p->g.nblk; info->m_block = wino::kMBlock;
-  info->planes = wino::kPlanes; info->pieces = wino::kPieces;
+  info->planes = p->g.path == WINO_PATH_FUSED ? 36 : wino::kPlanes;   // fused: 16 real + 10 x (re, im)
+  info->pieces = wino::kPieces;
   info->chunk_images = p->g.chunk_imgs; info->n_chunks = p->n_chunks;
   info->chunk_tiles_pad = p->g.chunk_tiles_pad;
   info->path = p->g.path;
@@ -205,7 +208,9 @@ static wino_status run_stage(const wino_plan_s* p, int stage, int chunk, const i
   int8_t* vimg = static_cast<int8_t*>(workspace);
   int32_t* m = reinterpret_cast<int32_t*>(static_cast<int8_t*>(workspace) + p->v_bytes);
   cudaError_t e = cudaErrorInvalidValue;
-  if (stage == 2) e = wino::launch_input_transform(g, x, n0, imgs, vimg, s);
+  if (stage == 2)
+    e = g.path == WINO_PATH_FUSED ? wino::launch_input_transform_f(g, x, n0, imgs, vimg, s)
+                                  : wino::launch_input_transform(g, x, n0, imgs, vimg, s);
   if (g.path == WINO_PATH_FUSED) {
     if (stage == 3)
       e = wino::launch_fused(g, tiles_pad, n0, imgs, vimg, static_cast<const int8_t*>(w_wino), codes, rq_mult,
@@ -271,6 +276,7 @@ wino_status wino_check_codes(wino_plan_t p, const uint8_t* codes, int32_t* bad_f
 
 wino_status wino_debug_set_trace(void* device_buffer) {
   wino::set_gemm_trace(device_buffer);
+  wino::set_fused_trace(device_buffer);
   return WINO_OK;
 }
 

@@ -67,3 +67,79 @@ def decode_m(buf: np.ndarray, tiles: int, cout: int, cout_pad: int, nblk: int, t
     off = ((t // 128) * (cout_pad // nblk) + nb) * (128 * nblk) + r * nblk + (((cc >> 2) ^ (r & swz)) << 2) + (cc & 3)
     buf = buf.reshape(slots, tiles_pad * cout_pad)
     return np.stack([buf[p][off] for p in range(slots)], 0)
+
+
+# ------------------------------------------------------------------ fused-path layouts (DESIGN.md, layout.cuh)
+# Groups in processing order gi: gi = 5k + s for k = 0..3 over rows R[FROW[k]] (rows 0, 5, 1, 2):
+# s < 4 real (R[ri], R[s]), s = 4 the primary (R[ri], 3); gi = 20..25 primaries 4..9.
+FROW = [0, 3, 1, 2]
+
+
+def fused_groups():
+    """[(kind, index)] per gi: ("real", plane s = ri*4 + c) or ("cpx", primary k)."""
+    out = []
+    for k in range(4):
+        ri = FROW[k]
+        out += [("real", ri * 4 + s) for s in range(4)] + [("cpx", ri)]
+    return out + [("cpx", k) for k in range(4, 10)]
+
+
+def _prefixes(sizes):
+    pre, acc = [], 0
+    for s in sizes:
+        pre.append(acc); acc += s
+    return pre, acc
+
+
+def decode_v_fused(buf: np.ndarray, tiles: int, ksteps: int, cin: int):
+    """V image [tile_block][group][kstep][piece][4 KB], balanced s8 pieces -> (real [16][T][cin],
+    re [10][T][cin], im [10][T][cin]) as hi * 256 + lo."""
+    groups = fused_groups()
+    pcs = [4 if g[0] == "cpx" else 2 for g in groups]
+    pre, total = _prefixes(pcs)
+    assert total == 72
+    t = np.arange(tiles)[:, None]; k = np.arange(cin)[None, :]
+    within = tiled_offset(t % 128, k & 31, 128)
+    real = np.zeros((16, tiles, cin), np.int64); re = np.zeros((10, tiles, cin), np.int64); im = re.copy()
+    b = buf.astype(np.int64)   # int8 buffer: signed pieces
+    for gi, (kind, idx) in enumerate(groups):
+        base = ((t // 128) * 72 + pre[gi]) * ksteps + (k >> 5) * pcs[gi]
+        val = lambda p: b[(base + p) * 4096 + within] * 256 + b[(base + p + 1) * 4096 + within]
+        if kind == "real":
+            real[idx] = val(0)
+        else:
+            re[idx], im[idx] = val(0), val(2)
+    return real, re, im
+
+
+def decode_w_fused(buf: np.ndarray, cout_pad: int, ksteps: int, cin_pad: int):
+    """W' image [cout block of 16][group][kstep][rows x 32 B] -> (real [16][cout][cin], re, im [10][cout][cin],
+    consistency flag of the duplicated B1 rows: -Wi and Wr)."""
+    groups = fused_groups()
+    wu = [4 if g[0] == "cpx" else 1 for g in groups]
+    pre, total = _prefixes(wu)
+    assert total == 56
+    co = np.arange(cout_pad)[:, None]; k = np.arange(cin_pad)[None, :]
+    nb, cr = co // 16, co % 16
+    b = buf.astype(np.int64)
+    real = np.zeros((16, cout_pad, cin_pad), np.int64); re = np.zeros((10, cout_pad, cin_pad), np.int64)
+    im = re.copy(); ok = True
+    for gi, (kind, idx) in enumerate(groups):
+        base = ((nb * 56 + pre[gi]) * ksteps + (k >> 5) * wu[gi]) * 1024
+        rowv = lambda r: b[base + tiled_offset(r, k & 31, 32 * wu[gi])]
+        if kind == "real":
+            real[idx] = rowv(cr) * 256 + rowv(16 + cr)
+        else:
+            re[idx] = rowv(cr) * 256 + rowv(32 + cr)
+            im[idx] = rowv(16 + cr) * 256 + rowv(48 + cr)
+            ok &= bool(np.array_equal(rowv(64 + cr) * 256 + rowv(96 + cr), -im[idx]))
+            ok &= bool(np.array_equal(rowv(80 + cr) * 256 + rowv(112 + cr), re[idx]))
+    return real, re, im, ok
+
+
+def complex_to_values(Z: np.ndarray):
+    """Z [..., 36, 2] -> (real [16, ...], re [10, ...], im [10, ...]) in plane / primary order."""
+    real = np.stack([Z[..., p, 0] for p in REAL_POS], 0)
+    re = np.stack([Z[..., p, 0] for p in CPX_POS], 0)
+    im = np.stack([Z[..., p, 1] for p in CPX_POS], 0)
+    return real, re, im

@@ -55,19 +55,34 @@ def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates
         _, Wp, codes = O.filter_transform(w, layout, scaling=scaling)
         np.testing.assert_array_equal(conv.codes.cpu().numpy(), codes)
         wbuf = conv.w_wino.cpu().numpy()
-        wpl = LD.decode_pieces(wbuf, info.cout_pad, info.n_block, info.cin_pad // 32, info.cin_pad,
-                               info.cout_pad * info.cin_pad)
-        np.testing.assert_array_equal(wpl[:, :co, :ci], LD.complex_to_planes(Wp))
-        assert not wpl[:, co:, :].any() and not wpl[:, :, ci:].any()
+        if path == FUSED:
+            wr, wre, wim, dup_ok = LD.decode_w_fused(wbuf, info.cout_pad, info.cin_pad // 32, info.cin_pad)
+            er, ere, eim = LD.complex_to_values(Wp)
+            np.testing.assert_array_equal(wr[:, :co, :ci], er)
+            np.testing.assert_array_equal(wre[:, :co, :ci], ere)
+            np.testing.assert_array_equal(wim[:, :co, :ci], eim)
+            assert dup_ok, "B1 rows must hold -Wi and Wr"
+            for a_ in (wr, wre, wim):
+                assert not a_[:, co:, :].any() and not a_[:, :, ci:].any()
+        else:
+            wpl = LD.decode_pieces(wbuf, info.cout_pad, info.n_block, info.cin_pad // 32, info.cin_pad,
+                                   info.cout_pad * info.cin_pad)
+            np.testing.assert_array_equal(wpl[:, :co, :ci], LD.complex_to_planes(Wp))
+            assert not wpl[:, co:, :].any() and not wpl[:, :, ci:].any()
         if info.n_chunks == 1:
             # K2: V planes of every tile, byte exact
             T = int(info.tiles)
             vbuf = conv.v_image().cpu().numpy()
-            vpl = LD.decode_v(vbuf, T, info.cin_pad // 32, info.cin_pad)
             D = O.input_transform(x, pad, layout)
-            np.testing.assert_array_equal(vpl[:, :, :ci], LD.complex_to_planes(D))
             if path == FUSED:
+                vr, vre, vim = LD.decode_v_fused(vbuf, T, info.cin_pad // 32, info.cin_pad)
+                er, ere, eim = LD.complex_to_values(D)
+                np.testing.assert_array_equal(vr[:, :, :ci], er)
+                np.testing.assert_array_equal(vre[:, :, :ci], ere)
+                np.testing.assert_array_equal(vim[:, :, :ci], eim)
                 return conv
+            vpl = LD.decode_v(vbuf, T, info.cin_pad // 32, info.cin_pad)
+            np.testing.assert_array_equal(vpl[:, :, :ci], LD.complex_to_planes(D))
             # K3: GEMMs + Karatsuba recombination + reverse scaling == oracle M''
             mraw = conv.m_raw().cpu().numpy()
             ms = LD.decode_m(mraw, T, co, info.cout_pad, info.n_block, info.chunk_tiles_pad)
