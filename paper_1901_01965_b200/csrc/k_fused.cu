@@ -193,6 +193,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const int tb = u / nblocks, nb = u - tb * nblocks;
         for (int gi = 0; gi < kFGroupsN; gi++) {
           const int pcs = fg_pieces(gi), wu = fg_wunits(gi), kc = fg_kchunk(gi);
+          const int8_t* vg = V + ((long long)tb * kVPiecesF + fg_vprefix(gi)) * ksteps * kVBlockBytes;
+          const int8_t* wg = W + ((long long)nb * kWRowUnitsF + fg_wprefix(gi)) * ksteps * 1024;
           for (int k0 = 0; k0 < ksteps; k0 += kc, it++) {
             const int s = it % kFStages;
             mbar_wait(empty0 + 8 * s, ((it / kFStages) & 1) ^ 1);
