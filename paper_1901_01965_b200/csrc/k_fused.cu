@@ -56,8 +56,10 @@ namespace wino {
 constexpr int kFN = kFN16;                    // couts per unit
 constexpr int kFEpiWarps = 16;                // 4 per TMEM lane quadrant
 constexpr int kFC = 4;                        // couts per epilogue thread
-constexpr int kFProducerWarp = kFEpiWarps, kFMmaWarp = kFEpiWarps + 1;
-constexpr int kFThreads = 32 * (kFEpiWarps + 2);
+constexpr int kFProducers = 2;                // producer warps, alternating stages (the per-thread
+                                              // issue cost of a stage's bulk copies is ~0.27 us)
+constexpr int kFProducerWarp = kFEpiWarps, kFMmaWarp = kFEpiWarps + kFProducers;
+constexpr int kFThreads = 32 * (kFEpiWarps + kFProducers + 1);
 constexpr int kFStages = 4;
 constexpr uint32_t kFStageV = 32768;          // V part of a stage (<= 32 KB)
 constexpr uint32_t kFStageBytes = kFStageV + 8192;
@@ -185,9 +187,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();   // V (and W', codes) come from the kernels just before
 
-  if (warp == kFProducerWarp) {
+  if (warp >= kFProducerWarp && warp < kFProducerWarp + kFProducers) {
     if (lane == 0) {
-      // ------------------------------------------------ producer
+      // ------------------------------------------------ producers: warp p issues the stages it with it % P == p
+      const int pw = warp - kFProducerWarp;
       int it = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int tb = u / nblocks, nb = u - tb * nblocks;
@@ -196,6 +199,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           const int8_t* vg = V + ((long long)tb * kVPiecesF + fg_vprefix(gi)) * ksteps * kVBlockBytes;
           const int8_t* wg = W + ((long long)nb * kWRowUnitsF + fg_wprefix(gi)) * ksteps * 1024;
           for (int k0 = 0; k0 < ksteps; k0 += kc, it++) {
+            if (it % kFProducers != pw) continue;
             const int s = it % kFStages;
             mbar_wait(empty0 + 8 * s, ((it / kFStages) & 1) ^ 1);
             const int kn = min(kc, ksteps - k0);
