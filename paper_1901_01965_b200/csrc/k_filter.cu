@@ -178,14 +178,14 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
     if constexpr (!FUSED) {
 #pragma unroll
       for (int pl = 0; pl < 46; pl++) {
-        s_stage[warp][2 * pl + 0][lane] = (int8_t)(vals[pl] >> 8);             // hi, s8
-        s_stage[warp][2 * pl + 1][lane] = (int8_t)(uint8_t)(vals[pl] & 255);   // lo, u8
+        s_stage[warp][2 * pl + 0][lane] = (int8_t)bal_hi(vals[pl]);   // balanced s8 pieces (layout.cuh)
+        s_stage[warp][2 * pl + 1][lane] = (int8_t)bal_lo(vals[pl]);
       }
       __syncwarp();
       for (int idx = lane; idx < 2 * kPlanes * 2; idx += 32) {   // (piece-plane, 16-channel half)
         const int pp = idx >> 1, hf = idx & 1;
         const int4 v = *reinterpret_cast<const int4*>(&s_stage[warp][pp][hf * 16]);
-        *reinterpret_cast<int4*>(wimg + w_offset(g, pp, co, c0 + hf * 16)) = v;
+        *reinterpret_cast<int4*>(wimg + w_offset(g, pp >> 1, pp & 1, co, c0 + hf * 16)) = v;
       }
     } else {
       // staged row 2 * wprefix(gi) + j holds piece-row j of group gi for this cout

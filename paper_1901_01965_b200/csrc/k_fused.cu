@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
   pdl_wait();   // V (and W', codes) come from the kernels just before
 
   if (warp >= kFProducerWarp && warp < kFProducerWarp + kFProducers) {
-    if (lane == 0) {
+    {   // warp-uniform loop, one elected lane issues (operands stay in uniform registers)
       // ------------------------------------------------ producers: warp p issues the stages it with it % P == p
       const int pw = warp - kFProducerWarp;
       int it = 0;
@@ -205,16 +205,19 @@ __global__ void __launch_bounds__(kFThreads, 1)
             const int kn = min(kc, ksteps - k0);
             const uint32_t vb = (uint32_t)(kn * pcs) * kVBlockBytes, wb = (uint32_t)(kn * wu) * 1024;
             const uint32_t st = sbase + s * kFStageBytes;
-            mbar_arrive_expect_tx(full0 + 8 * s, vb + wb);
-            bulk_g2s(st, vg + (long long)k0 * pcs * kVBlockBytes, vb, full0 + 8 * s);
-            bulk_g2s(st + kFStageV, wg + (long long)k0 * wu * 1024, wb, full0 + 8 * s);
-            if (it < 64) FTRACE(it, 0);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(full0 + 8 * s, vb + wb);
+              bulk_g2s(st, vg + (long long)k0 * pcs * kVBlockBytes, vb, full0 + 8 * s);
+              bulk_g2s(st + kFStageV, wg + (long long)k0 * wu * 1024, wb, full0 + 8 * s);
+              if (it < 64) FTRACE(it, 0);
+            }
+            __syncwarp();
           }
         }
       }
     }
   } else if (warp == kFMmaWarp) {
-    if (lane == 0) {
+    {   // warp-uniform loop, one elected lane issues
       // ------------------------------------------------ MMA issuer
       const uint32_t id16 = idesc_i8(kMBlock, 16, 1, 1), id32 = idesc_i8(kMBlock, 32, 1, 1),
                      id64 = idesc_i8(kMBlock, 64, 1, 1);
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           const int b = sgc % kFSlots;
           mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);   // epilogue drained this slot
           tc_fence_after();
-          if (sgc < 32) FTRACE(64 + sgc, 0);
+          if (sgc < 32 && lane == 0) FTRACE(64 + sgc, 0);
           const int g0 = sg_first(sg), ng = sg_count(sg);
           for (int q = 0; q < ng; q++) {
             const int gi = g0 + q;
@@ -235,10 +238,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
               const int s = it % kFStages;
               mbar_wait(full0 + 8 * s, (it / kFStages) & 1);
               tc_fence_after();
-              if (it < 64) FTRACE(it, 1);
+              if (it < 64 && lane == 0) FTRACE(it, 1);
               const int kn = min(kc, ksteps - k0);
               const uint32_t st = sbase + s * kFStageBytes;
-              if (!(dbg & 2)) {
+              if (!(dbg & 2) && elect_one()) {
                 for (int kk = 0; kk < kn; ++kk) {
                   const bool first = (k0 + kk) == 0;
                   if (!cpx) {
@@ -273,11 +276,14 @@ __global__ void __launch_bounds__(kFThreads, 1)
                   }
                 }
               }
-              umma_commit(empty0 + 8 * s);   // stage reusable once these MMAs have read it
-              if (it < 64) FTRACE(it, 2);
+              __syncwarp();
+              if (elect_one()) umma_commit(empty0 + 8 * s);   // stage reusable once these MMAs have read it
+              __syncwarp();
+              if (it < 64 && lane == 0) FTRACE(it, 2);
             }
           }
-          umma_commit(tfull0 + 8 * b);       // slot complete
+          if (elect_one()) umma_commit(tfull0 + 8 * b);       // slot complete
+          __syncwarp();
         }
       }
     }

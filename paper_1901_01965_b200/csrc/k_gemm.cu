@@ -187,43 +187,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == kProducerWarp) {
-    if (lane == 0) {
-      // ------------------------------------------------ producer
+    {
+      // ------------------------------------------------ producer (warp-uniform loop, one elected lane issues)
       int it = 0, ui = 0;
       for (int ku = 0, u = cta_unit(0); u < n_units; u = cta_unit(++ku)) {
        int pidx, tb, nb;
        decode_unit(u, tblocks, nblocks, pidx, tb, nb);
        for (int pl = 0; pl < unit_planes(pidx); pl++, ui++) {
         const int plane = unit_plane0(pidx) + pl;
-        // V: one 4 KB block per (tile block, K step, plane-piece); W: contiguous K steps
-        const int8_t* vblk = V + ((long long)tb * ksteps * (2 * kPlanes) + 2 * plane) * kVBlockBytes;
-        const int8_t* wh = W + (long long)(2 * plane) * cout_pad * cin_pad + (long long)nb * ksteps * NBLK * kKStep;
-        const int8_t* wl = wh + (long long)cout_pad * cin_pad;
+        // V of the plane: [K step][hi, lo] contiguous; W': [K step][W hi | W lo rows] contiguous
+        const int8_t* vpl = V + ((long long)tb * kPlanes + plane) * ksteps * (2 * kVBlockBytes);
+        const int8_t* wpl = W + ((long long)plane * nblocks + nb) * ksteps * (2 * NBLK * kKStep);
         for (int ks = 0; ks < n_it; ks++, it++) {
           const int s = it % kStages;
           mbar_wait(empty0 + 8 * s, ((it / kStages) & 1) ^ 1);
           const int k0 = ks * kKStepsPerStage;
           const int kn = min(kKStepsPerStage, ksteps - k0);
-          const uint32_t ab = kn * kABytesPerKStep, bb = kn * (uint32_t)NBLK * kKStep;
+          const uint32_t ab = kn * 2 * kABytesPerKStep, bb = kn * 2 * (uint32_t)NBLK * kKStep;
           const uint32_t st = sbase + s * stage_bytes;
-          mbar_arrive_expect_tx(full0 + 8 * s, 2 * ab + 2 * bb);
-          for (int kk = 0; kk < kn; kk++) {
-            const int8_t* src = vblk + (long long)(k0 + kk) * (2 * kPlanes) * kVBlockBytes;
-            bulk_g2s(st + kk * kABytesPerKStep, src, kABytesPerKStep, full0 + 8 * s);                          // hi
-            bulk_g2s(st + a_bytes + kk * kABytesPerKStep, src + kVBlockBytes, kABytesPerKStep, full0 + 8 * s);  // lo
+          if (elect_one()) {
+            mbar_arrive_expect_tx(full0 + 8 * s, ab + bb);
+            bulk_g2s(st, vpl + (long long)k0 * 2 * kVBlockBytes, ab, full0 + 8 * s);
+            bulk_g2s(st + 2 * a_bytes, wpl + (long long)k0 * 2 * NBLK * kKStep, bb, full0 + 8 * s);
+            if (ks == 0) WINO_TRACE(ui, 0);
           }
-          bulk_g2s(st + 2 * a_bytes, wh + (long long)k0 * NBLK * kKStep, bb, full0 + 8 * s);
-          bulk_g2s(st + 2 * a_bytes + b_bytes, wl + (long long)k0 * NBLK * kKStep, bb, full0 + 8 * s);
-          if (ks == 0) WINO_TRACE(ui, 0);
+          __syncwarp();
         }
        }
       }
     }
   } else if (warp == kMmaWarp) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
-      const uint32_t id_ss = idesc_i8(kMBlock, NBLK, 1, 1), id_su = idesc_i8(kMBlock, NBLK, 1, 0);
-      const uint32_t id_us = idesc_i8(kMBlock, NBLK, 0, 1), id_uu = idesc_i8(kMBlock, NBLK, 0, 0);
+    {
+      // ------------------------------------------------ MMA issuer (warp-uniform loop, one elected lane issues)
+      // all pieces are balanced s8 (layout.cuh); B = [W hi | W lo] (2 NBLK rows) per K step
+      const uint32_t id_2n = idesc_i8(kMBlock, 2 * NBLK, 1, 1), id_1n = idesc_i8(kMBlock, NBLK, 1, 1);
       int it = 0, pc = 0;
       for (int ku = 0, u = cta_unit(0); u < n_units; u = cta_unit(++ku)) {
        int pidx, tbu, nbu;
@@ -243,19 +240,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int kn = min(kKStepsPerStage, ksteps - k0);
           const uint32_t st = sbase + s * stage_bytes;
           for (int kk = 0; kk < kn; ++kk) {
-            const uint32_t acc = (k0 + kk) > 0;
-            const uint64_t a_hi = umma_desc(st + kk * kABytesPerKStep, 128, 256);
-            const uint64_t a_lo = umma_desc(st + a_bytes + kk * kABytesPerKStep, 128, 256);
-            const uint64_t b_hi = umma_desc(st + 2 * a_bytes + kk * NBLK * kKStep, 128, 256);
-            const uint64_t b_lo = umma_desc(st + 2 * a_bytes + b_bytes + kk * NBLK * kKStep, 128, 256);
-            umma_i8(acc_hh, a_hi, b_hi, id_ss, acc);
-            umma_i8(acc_x, a_hi, b_lo, id_su, acc);
-            umma_i8(acc_x, a_lo, b_hi, id_us, 1);
-            umma_i8(acc_ll, a_lo, b_lo, id_uu, acc);
+            const uint64_t a_hi = umma_desc(st + (2 * kk) * kABytesPerKStep, 128, 256);
+            const uint64_t a_lo = umma_desc(st + (2 * kk + 1) * kABytesPerKStep, 128, 256);
+            const uint32_t bw = st + 2 * a_bytes + kk * 2 * NBLK * kKStep;
+            const uint64_t b_hl = umma_desc(bw, 128, 256), b_lo = umma_desc(bw + NBLK * kKStep, 128, 256);
+            if (elect_one()) {
+              if ((k0 + kk) > 0) {
+                umma_i8(acc_hh, a_hi, b_hl, id_2n, 1);   // [hh | x]  += hi . [W hi | W lo]
+                umma_i8(acc_x, a_lo, b_hl, id_2n, 1);    // [x | ll]  += lo . [W hi | W lo]
+              } else {   // first K step: initialise every column block exactly once
+                umma_i8(acc_hh, a_hi, b_hl, id_2n, 0);
+                umma_i8(acc_ll, a_lo, b_lo, id_1n, 0);
+                umma_i8(acc_x, a_lo, b_hl, id_1n, 1);
+              }
+            }
+            __syncwarp();
           }
-          umma_commit(empty0 + 8 * s);   // stage reusable once these MMAs have read it
+          if (elect_one()) umma_commit(empty0 + 8 * s);   // stage reusable once these MMAs have read it
+          __syncwarp();
         }
-        umma_commit(tfull0 + 8 * b);     // accumulator set b complete
+        if (elect_one()) umma_commit(tfull0 + 8 * b);     // accumulator set b complete
+        __syncwarp();
         WINO_TRACE(pc, 3);
        }
       }

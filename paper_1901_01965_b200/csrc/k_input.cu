@@ -57,12 +57,13 @@ __device__ __forceinline__ void real_row_planes(const int (&e)[6], int (&v)[7]) 
 
 __device__ __forceinline__ void st16(int8_t* p, uint32_t v) { *reinterpret_cast<uint16_t*>(p) = (uint16_t)v; }
 
-// Store plane `pl` for both channels: piece 0 (hi) and piece 1 (lo), 4 KB apart per piece.
+// Store plane `PL` for both channels: balanced s8 pieces hi = byte 1 of v + 128 and lo =
+// byte 0 of v (layout.cuh), hi at the plane's K-step block, lo 4 KB after it.
 template <int PL>
-__device__ __forceinline__ void store_plane(int8_t* base, int v0, int v1) {
-  const uint32_t pk = __byte_perm((uint32_t)v0, (uint32_t)v1, 0x5140);   // [lo0, lo1, hi0, hi1]
-  st16(base + (2 * PL + 0) * 4096, pk >> 16);                            // hi pair (s8)
-  st16(base + (2 * PL + 1) * 4096, pk);                                  // lo pair (u8)
+__device__ __forceinline__ void store_plane(int8_t* base, long long pstride, int v0, int v1) {
+  int8_t* p = base + PL * pstride;
+  st16(p, __byte_perm((uint32_t)(v0 + 128), (uint32_t)(v1 + 128), 0x0051));   // [hi0, hi1]
+  st16(p + 4096, __byte_perm((uint32_t)v0, (uint32_t)v1, 0x0040));            // [lo0, lo1]
 }
 
 // Gather the zero-padded 6x6 patch of chunk tile t for channels c, c+1 and form
@@ -149,26 +150,28 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
   const long long tb = t / kMBlock;
   const int row = t % kMBlock;
   const int k = c;   // channel index inside cin_pad
-  int8_t* base = vimg + (tb * g.ksteps + (k >> 5)) * (long long)(2 * kPlanes * 4096) + (row >> 3) * 256 +
-                 ((k >> 4) & 1) * 128 + (row & 7) * 16 + (k & 15);
+  // plane p, piece q of this (tile, channel) at base + p * pstride + q * 4 KB (v_offset, layout.cuh)
+  const long long pstride = (long long)g.ksteps * 2 * kVBlockBytes;
+  int8_t* base = vimg + tb * kPlanes * pstride + (long long)(k >> 5) * 2 * kVBlockBytes +
+                 tiled_offset(row, k & 31, kMBlock);
   {
     int v0[7], v1[7];
     real_row_planes<0>(r[0].e0, v0); real_row_planes<0>(r[1].e0, v1);
-    store_plane<0>(base, v0[0], v1[0]); store_plane<1>(base, v0[1], v1[1]);
-    store_plane<2>(base, v0[2], v1[2]); store_plane<3>(base, v0[3], v1[3]);
-    store_plane<16>(base, v0[4], v1[4]); store_plane<17>(base, v0[5], v1[5]); store_plane<18>(base, v0[6], v1[6]);
+    store_plane<0>(base, pstride, v0[0], v1[0]); store_plane<1>(base, pstride, v0[1], v1[1]);
+    store_plane<2>(base, pstride, v0[2], v1[2]); store_plane<3>(base, pstride, v0[3], v1[3]);
+    store_plane<16>(base, pstride, v0[4], v1[4]); store_plane<17>(base, pstride, v0[5], v1[5]); store_plane<18>(base, pstride, v0[6], v1[6]);
     real_row_planes<1>(r[0].e1, v0); real_row_planes<1>(r[1].e1, v1);
-    store_plane<4>(base, v0[0], v1[0]); store_plane<5>(base, v0[1], v1[1]);
-    store_plane<6>(base, v0[2], v1[2]); store_plane<7>(base, v0[3], v1[3]);
-    store_plane<19>(base, v0[4], v1[4]); store_plane<20>(base, v0[5], v1[5]); store_plane<21>(base, v0[6], v1[6]);
+    store_plane<4>(base, pstride, v0[0], v1[0]); store_plane<5>(base, pstride, v0[1], v1[1]);
+    store_plane<6>(base, pstride, v0[2], v1[2]); store_plane<7>(base, pstride, v0[3], v1[3]);
+    store_plane<19>(base, pstride, v0[4], v1[4]); store_plane<20>(base, pstride, v0[5], v1[5]); store_plane<21>(base, pstride, v0[6], v1[6]);
     real_row_planes<2>(r[0].e2, v0); real_row_planes<2>(r[1].e2, v1);
-    store_plane<8>(base, v0[0], v1[0]); store_plane<9>(base, v0[1], v1[1]);
-    store_plane<10>(base, v0[2], v1[2]); store_plane<11>(base, v0[3], v1[3]);
-    store_plane<22>(base, v0[4], v1[4]); store_plane<23>(base, v0[5], v1[5]); store_plane<24>(base, v0[6], v1[6]);
+    store_plane<8>(base, pstride, v0[0], v1[0]); store_plane<9>(base, pstride, v0[1], v1[1]);
+    store_plane<10>(base, pstride, v0[2], v1[2]); store_plane<11>(base, pstride, v0[3], v1[3]);
+    store_plane<22>(base, pstride, v0[4], v1[4]); store_plane<23>(base, pstride, v0[5], v1[5]); store_plane<24>(base, pstride, v0[6], v1[6]);
     real_row_planes<3>(r[0].e5, v0); real_row_planes<3>(r[1].e5, v1);
-    store_plane<12>(base, v0[0], v1[0]); store_plane<13>(base, v0[1], v1[1]);
-    store_plane<14>(base, v0[2], v1[2]); store_plane<15>(base, v0[3], v1[3]);
-    store_plane<25>(base, v0[4], v1[4]); store_plane<26>(base, v0[5], v1[5]); store_plane<27>(base, v0[6], v1[6]);
+    store_plane<12>(base, pstride, v0[0], v1[0]); store_plane<13>(base, pstride, v0[1], v1[1]);
+    store_plane<14>(base, pstride, v0[2], v1[2]); store_plane<15>(base, pstride, v0[3], v1[3]);
+    store_plane<25>(base, pstride, v0[4], v1[4]); store_plane<26>(base, pstride, v0[5], v1[5]); store_plane<27>(base, pstride, v0[6], v1[6]);
   }
   // complex row 3 = a + i b: columns 0, 1, 2, 5 -> primaries 4..7; (3,3) -> 8; (3,4) -> 9
   {
@@ -186,18 +189,18 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
       q[ch][2] = a[4] - a[2] + b[3] - b[1];
       q[ch][3] = b[4] - b[2] - a[3] + a[1];
     }
-    store_plane<28>(base, re[0][0], re[1][0]); store_plane<29>(base, im[0][0], im[1][0]);
-    store_plane<30>(base, re[0][0] + im[0][0], re[1][0] + im[1][0]);
-    store_plane<31>(base, re[0][1], re[1][1]); store_plane<32>(base, im[0][1], im[1][1]);
-    store_plane<33>(base, re[0][1] + im[0][1], re[1][1] + im[1][1]);
-    store_plane<34>(base, re[0][2], re[1][2]); store_plane<35>(base, im[0][2], im[1][2]);
-    store_plane<36>(base, re[0][2] + im[0][2], re[1][2] + im[1][2]);
-    store_plane<37>(base, re[0][3], re[1][3]); store_plane<38>(base, im[0][3], im[1][3]);
-    store_plane<39>(base, re[0][3] + im[0][3], re[1][3] + im[1][3]);
-    store_plane<40>(base, q[0][0], q[1][0]); store_plane<41>(base, q[0][1], q[1][1]);
-    store_plane<42>(base, q[0][0] + q[0][1], q[1][0] + q[1][1]);
-    store_plane<43>(base, q[0][2], q[1][2]); store_plane<44>(base, q[0][3], q[1][3]);
-    store_plane<45>(base, q[0][2] + q[0][3], q[1][2] + q[1][3]);
+    store_plane<28>(base, pstride, re[0][0], re[1][0]); store_plane<29>(base, pstride, im[0][0], im[1][0]);
+    store_plane<30>(base, pstride, re[0][0] + im[0][0], re[1][0] + im[1][0]);
+    store_plane<31>(base, pstride, re[0][1], re[1][1]); store_plane<32>(base, pstride, im[0][1], im[1][1]);
+    store_plane<33>(base, pstride, re[0][1] + im[0][1], re[1][1] + im[1][1]);
+    store_plane<34>(base, pstride, re[0][2], re[1][2]); store_plane<35>(base, pstride, im[0][2], im[1][2]);
+    store_plane<36>(base, pstride, re[0][2] + im[0][2], re[1][2] + im[1][2]);
+    store_plane<37>(base, pstride, re[0][3], re[1][3]); store_plane<38>(base, pstride, im[0][3], im[1][3]);
+    store_plane<39>(base, pstride, re[0][3] + im[0][3], re[1][3] + im[1][3]);
+    store_plane<40>(base, pstride, q[0][0], q[1][0]); store_plane<41>(base, pstride, q[0][1], q[1][1]);
+    store_plane<42>(base, pstride, q[0][0] + q[0][1], q[1][0] + q[1][1]);
+    store_plane<43>(base, pstride, q[0][2], q[1][2]); store_plane<44>(base, pstride, q[0][3], q[1][3]);
+    store_plane<45>(base, pstride, q[0][2] + q[0][3], q[1][2] + q[1][3]);
   }
 }
 

@@ -11,25 +11,25 @@
 //   plane 16+3k+0           Re of primary k   (Karatsuba P0 = Re V * Re W)
 //   plane 16+3k+1           Im of primary k   (P1 = Im V * Im W)
 //   plane 16+3k+2           Re + Im           (P2 = (Re V + Im V)(Re W + Im W))
-// Every operand value v (|v| <= 2048) is split into two int8 pieces
-//   piece 0: hi = v >> 8 (s8, in [-8, 7]);  piece 1: lo = v & 255 (u8)
-// so v = 256 hi + lo, and a plane product is
+// Every operand value v (|v| <= 2048) is split into two BALANCED s8 pieces
+//   lo = ((v + 128) & 255) - 128 (the low byte of v),  hi = (v - lo) / 256 = (v + 128) >> 8
+// so v = 256 hi + lo, both pieces s8 (hi in [-8, 8]), and a plane product is
 //   V W = 65536 hh + 256 (hl + lh) + ll     (exact mod 2^32).
 //
 // Operand images are stored pre-tiled in the UMMA canonical K-major
 // no-swizzle layout so one 1-D bulk copy moves a whole stage:
-//   block of R rows (R = 128 tiles for V, n_block couts for W) and K = cin_pad
-//   bytes; byte (row r, k) of a block lives at
-//     (k / 32) * R * 32  +  (r / 8) * 256  +  ((k % 32) / 16) * 128  +  (r % 8) * 16  +  k % 16
-//   (core matrix = 8 rows x 16 B; LBO = 128, SBO = 256; a 32-byte K step of
-//   the block is R*32 contiguous bytes, and all K steps are contiguous).
-//   V image: [tile_block][kstep][plane*2 + piece][R=128 x 32 B]  (the 92
-//            plane-pieces of one (tile block, K step) 4 KB apart, so K2 stores
-//            with immediate offsets; K3 copies one 4 KB block per piece/K step)
-//   W image: [plane][piece][cout_block][kstep][R=n_block x 32 B]
+//   block of R rows and K = 32 bytes (one K step): byte (row r, k) at
+//     (r / 8) * 256  +  (k / 16) * 128  +  (r % 8) * 16  +  k % 16
+//   (core matrix = 8 rows x 16 B; LBO = 128, SBO = 256).
+//   V image: [tile_block][plane][K step][piece hi, lo][128 rows x 32 B] -- a
+//            plane's K steps are contiguous (one bulk copy per stage)
+//   W image: [plane][cout_block][K step][2 n_block rows x 32 B], rows
+//            [W hi of the n_block couts | W lo]: the B operand of one UMMA
+//            A_piece . [W hi | W lo] (N = 2 n_block) whose two column halves
+//            land at scales 2^(8+8a) and 2^(8a) (a = 1 for the hi piece of V)
 //   M      : [slot 36][tile_block][cout_block][128 rows][n_block] int32 -- GEMM
-//            results after the Karatsuba recombination, before reverse scaling
-//            (K4): slot s < 16 real position s, 16+k = Re and 26+k = Im of
+//            results after the Karatsuba recombination and the reverse scaling
+//            (M'', read by K4): slot s < 16 real position s, 16+k = Re and 26+k = Im of
 //            complex primary k; within a 128 x n_block tile, element
 //            (r, c) sits at r * n_block + ((c / 4) ^ (r & swz)) * 4 + c % 4 with
 //            swz = min(n_block / 4, 8) - 1 (16-byte chunks XOR-swizzled by row,
@@ -63,11 +63,11 @@ __host__ __device__ __forceinline__ long long tiled_offset(int r, int k, int R) 
 }
 
 constexpr int kVBlockBytes = kMBlock * kKStep;   // one (plane-piece, tile block, K step) block = 4 KB
-// Byte offset of V piece `pp` (= plane*2 + piece), chunk tile t, channel k.
-__host__ __device__ __forceinline__ long long v_offset(const Geom& g, int pp, long long t, int k) {
+// Byte offset of V piece `piece` (0 hi, 1 lo) of plane `plane`, chunk tile t, channel k (staged path).
+__host__ __device__ __forceinline__ long long v_offset(const Geom& g, int plane, int piece, long long t, int k) {
   const long long blk = t / kMBlock;
   const int r = (int)(t % kMBlock);
-  return ((blk * g.ksteps + (k >> 5)) * (2 * kPlanes) + pp) * kVBlockBytes + tiled_offset(r, k & 31, kMBlock);
+  return (((blk * kPlanes + plane) * g.ksteps + (k >> 5)) * 2 + piece) * kVBlockBytes + tiled_offset(r, k & 31, kMBlock);
 }
 // Element offset of (chunk tile t, cout co) inside one plane of M.
 __host__ __device__ __forceinline__ long long m_offset(const Geom& g, long long t, int co) {
@@ -76,11 +76,11 @@ __host__ __device__ __forceinline__ long long m_offset(const Geom& g, long long 
   return ((t >> 7) * (long long)(g.cout_pad / g.nblk) + nb) * (kMBlock * g.nblk) + r * g.nblk +
          (((c >> 2) ^ (r & swz)) << 2) + (c & 3);
 }
-// Byte offset of W piece `pp`, output channel co, input channel k.
-__host__ __device__ __forceinline__ long long w_offset(const Geom& g, int pp, int co, int k) {
-  int blk = co / g.nblk, r = co % g.nblk;
-  return (long long)pp * g.cout_pad * g.cin_pad + (long long)blk * g.ksteps * g.nblk * 32 +
-         tiled_offset(r, k, g.nblk);
+// Byte offset of W piece `piece` (0 hi, 1 lo) of plane `plane`, output channel co, input channel k (staged).
+__host__ __device__ __forceinline__ long long w_offset(const Geom& g, int plane, int piece, int co, int k) {
+  const int nb = co / g.nblk, r = co % g.nblk;
+  return (((long long)plane * (g.cout_pad / g.nblk) + nb) * g.ksteps + (k >> 5)) * (2 * g.nblk * kKStep) +
+         tiled_offset(piece * g.nblk + r, k & 31, 2 * g.nblk);
 }
 
 // ---------------------------------------------------------------- fused-path (K3F) operand layouts

@@ -15,28 +15,30 @@ def tiled_offset(r, k, R_rows):
     return (k >> 5) * R_rows * 32 + (r >> 3) * 256 + ((k >> 4) & 1) * 128 + (r & 7) * 16 + (k & 15)
 
 
-def decode_pieces(buf: np.ndarray, rows: int, R_rows: int, ksteps: int, cin: int, pp_stride: int):
-    """buf: int8 image.  Returns int array [46][rows][cin] of hi*256 + lo."""
-    r = np.arange(rows)[:, None]; k = np.arange(cin)[None, :]
-    off = (r // R_rows) * ksteps * R_rows * 32 + tiled_offset(r % R_rows, k, R_rows)
-    out = np.zeros((46, rows, cin), np.int64)
+def decode_w_staged(buf: np.ndarray, cout_pad: int, nblk: int, ksteps: int, cin: int):
+    """W' image [plane][cout block][K step][W hi rows | W lo rows] (balanced s8 pieces) ->
+    int [46][cout_pad][cin] of hi*256 + lo."""
+    co = np.arange(cout_pad)[:, None]; k = np.arange(cin)[None, :]
+    nblocks = cout_pad // nblk
+    b = buf.astype(np.int64)
+    out = np.zeros((46, cout_pad, cin), np.int64)
     for pl in range(46):
-        hi = buf[2 * pl * pp_stride + off].astype(np.int64)
-        lo = buf[(2 * pl + 1) * pp_stride + off].astype(np.int64) & 255
+        base = ((pl * nblocks + co // nblk) * ksteps + (k >> 5)) * (2 * nblk * 32)
+        hi = b[base + tiled_offset(co % nblk, k & 31, 2 * nblk)]
+        lo = b[base + tiled_offset(nblk + co % nblk, k & 31, 2 * nblk)]
         out[pl] = hi * 256 + lo
     return out
 
 
 def decode_v(buf: np.ndarray, tiles: int, ksteps: int, cin: int):
-    """V image [tile_block][kstep][92 plane-pieces][4 KB] -> int [46][tiles][cin] (hi*256 + lo)."""
+    """V image [tile_block][plane][K step][hi, lo][4 KB] (balanced s8 pieces) -> int [46][tiles][cin]."""
     t = np.arange(tiles)[:, None]; k = np.arange(cin)[None, :]
-    blk = ((t // 128) * ksteps + (k >> 5)) * 92
     within = tiled_offset(t % 128, k & 31, 128)
+    b = buf.astype(np.int64)
     out = np.zeros((46, tiles, cin), np.int64)
     for pl in range(46):
-        hi = buf[(blk + 2 * pl) * 4096 + within].astype(np.int64)
-        lo = buf[(blk + 2 * pl + 1) * 4096 + within].astype(np.int64) & 255
-        out[pl] = hi * 256 + lo
+        blk = (((t // 128) * 46 + pl) * ksteps + (k >> 5)) * 2
+        out[pl] = b[blk * 4096 + within] * 256 + b[(blk + 1) * 4096 + within]
     return out
 
 

@@ -65,8 +65,7 @@ def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates
             for a_ in (wr, wre, wim):
                 assert not a_[:, co:, :].any() and not a_[:, :, ci:].any()
         else:
-            wpl = LD.decode_pieces(wbuf, info.cout_pad, info.n_block, info.cin_pad // 32, info.cin_pad,
-                                   info.cout_pad * info.cin_pad)
+            wpl = LD.decode_w_staged(wbuf, info.cout_pad, info.n_block, info.cin_pad // 32, info.cin_pad)
             np.testing.assert_array_equal(wpl[:, :co, :ci], LD.complex_to_planes(Wp))
             assert not wpl[:, co:, :].any() and not wpl[:, :, ci:].any()
         if info.n_chunks == 1:
