@@ -60,7 +60,7 @@ __device__ __forceinline__ int rha_mul_shift(int v, int n, int p) {  // rha(v n 
   return prod < 0 ? -r : r;
 }
 
-constexpr int kFilterWarps = 4;   // warps per CTA; one CTA per output channel
+constexpr int kFilterWarps = 8;   // warps per CTA; one CTA per output channel
 
 // Scaled operand planes of one (cout, cin) filter: 46 values.
 __device__ __forceinline__ void scaled_planes(const int t[36], const int* sn, const int* sp, int vals[46]) {

@@ -16,7 +16,8 @@ layer = synth.CONFIGS[cfg].layers[0]
 x, w = synth.config_inputs(cfg)
 conv = W.WinoConv2d(layer.n, layer.h, layer.w, layer.c_in, layer.c_out, layer.pad, W.WINO_NHWC, layer.scaling,
                     W.WINO_OUT_INT8, path=path)
-conv.transform_filter(torch.from_numpy(w).cuda())
+wdv = torch.from_numpy(w).cuda()
+conv.transform_filter(wdv)
 xd = torch.from_numpy(x).cuda()
 S = synth.requant_shift(layer)
 y = conv(xd, 1, S)
@@ -26,8 +27,11 @@ g = torch.cuda.CUDAGraph()
 with torch.cuda.stream(st):
     with torch.cuda.graph(g, stream=st):
         for r in range(reps):
-            L.wino_conv2d_int8_stage(conv.plan, stage, 0, xd.data_ptr(), conv.w_wino.data_ptr(), conv.codes.data_ptr(),
-                                     1, S, y.data_ptr(), conv.workspace.data_ptr(), sp)
+            if stage == 1:
+                L.wino_transform_filter(conv.plan, wdv.data_ptr(), conv.w_wino.data_ptr(), conv.codes.data_ptr(), sp)
+            else:
+                L.wino_conv2d_int8_stage(conv.plan, stage, 0, xd.data_ptr(), conv.w_wino.data_ptr(),
+                                         conv.codes.data_ptr(), 1, S, y.data_ptr(), conv.workspace.data_ptr(), sp)
     g.replay()
     ts = []
     for _ in range(5):
