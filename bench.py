@@ -159,12 +159,33 @@ def run_ours(args):
         lanes.append((torch.cuda.Stream(device=dev), torch.empty_like(conv.w_wino), torch.empty_like(conv.codes),
                       torch.empty_like(conv.workspace)))
 
+    # --overlap-filter: the filter transform (K1) runs on a side stream concurrently with the
+    # input transform (K2) of the same step; the GEMM waits for both (same work, fork/join inside
+    # the captured graph).  Otherwise K1 -> conv on one stream.
+    sides = [torch.cuda.Stream(device=dev) for _ in lanes]
+
     def step(i, lane=0):
         j = i % n_sets
         st_, ww_, cd_, ws_ = lanes[lane]
-        L.wino_transform_filter(conv.plan, ws[j].data_ptr(), ww_.data_ptr(), cd_.data_ptr(), st_.cuda_stream)
-        L.wino_conv2d_int8(conv.plan, xs[j].data_ptr(), ww_.data_ptr(), cd_.data_ptr(), 1, S, ys[j].data_ptr(),
-                           ws_.data_ptr(), st_.cuda_stream)
+        if not args.overlap_filter:
+            L.wino_transform_filter(conv.plan, ws[j].data_ptr(), ww_.data_ptr(), cd_.data_ptr(), st_.cuda_stream)
+            L.wino_conv2d_int8(conv.plan, xs[j].data_ptr(), ww_.data_ptr(), cd_.data_ptr(), 1, S, ys[j].data_ptr(),
+                               ws_.data_ptr(), st_.cuda_stream)
+            return
+        side = sides[lane]
+        e_fork, e_join = torch.cuda.Event(), torch.cuda.Event()
+        e_fork.record(st_)
+        side.wait_event(e_fork)
+        L.wino_transform_filter(conv.plan, ws[j].data_ptr(), ww_.data_ptr(), cd_.data_ptr(), side.cuda_stream)
+        e_join.record(side)
+        for c in range(info.n_chunks):
+            L.wino_conv2d_int8_stage(conv.plan, 2, c, xs[j].data_ptr(), ww_.data_ptr(), cd_.data_ptr(), 1, S,
+                                     ys[j].data_ptr(), ws_.data_ptr(), st_.cuda_stream)
+            if c == 0:
+                st_.wait_event(e_join)
+            for stg in range(3, 2 + info.stages):
+                L.wino_conv2d_int8_stage(conv.plan, stg, c, xs[j].data_ptr(), ww_.data_ptr(), cd_.data_ptr(), 1,
+                                         S, ys[j].data_ptr(), ws_.data_ptr(), st_.cuda_stream)
 
     launches_per_step = 1 + info.stages * info.n_chunks
     # CUDA graphs: one per (stream lane, rotation slot) (launch-bound otherwise)
@@ -252,6 +273,7 @@ def run_ours(args):
                       f"({n_sets * per_set / 2 ** 20:.0f} MiB > 126 MiB L2)",
                 "parallelism": f"dp{world} ({'replicated per-rank batches, weak scaling' if args.scaling == 'weak' else sh['mode'] + '-sharded, strong scaling'}; no data-path collective)",
                 "chunks": info.n_chunks, "cuda_graph": bool(graphs), "streams": len(lanes),
+                "filter_transform_overlapped": bool(args.overlap_filter),
             },
             "roofline": roof["dominant"],
             "path_roofline": path,
@@ -364,7 +386,7 @@ def run_ours_stack(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
             "config": {"workload": f"C5: {cfg.description}", "batch_per_gpu": n, "layers": len(cfg.layers),
                        "layout": "NHWC", "filter_scaling": True, "requant_shifts": shifts,
-                       "step": "13 filter transforms + 13 convs (K2, K3F fused per chunk) + 4 max pools",
+                       "step": "13 filter transforms + 13 convs (staged K2, K3, K4 per chunk) + 4 max pools",
                        "l2": "activations 0.8 GB per layer >> 126 MiB L2; 2 input sets rotated",
                        "parallelism": f"dp{world} (replicated per-rank batches, weak scaling)"},
             "path_roofline": {"t_roof_us": round(t_roof * 1e6, 2), "t_step_us": round(t_max / args.steps * 1e6, 2),
@@ -665,6 +687,8 @@ def main():
     ap.add_argument("--streams", type=int, default=3,
                     help="independent batches in flight on separate streams (own filter/workspace buffers)")
     ap.add_argument("--path", default="staged", choices=["fused", "staged"])
+    ap.add_argument("--overlap-filter", type=int, default=0,
+                    help="1: filter transform on a side stream concurrent with the input transform")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()

@@ -116,12 +116,119 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
   }
 }
 
+// Same transform, one thread per (tile, 4 consecutive couts): the 36 slot reads are 16-byte loads
+// (4 couts share one 16-byte chunk of an M'' tile row, layout.cuh), 16 threads cover a tile row of
+// 64 couts (256 contiguous bytes).  Requires cout % 4 == 0.
+constexpr int kOut4Quads = 16, kOut4Tiles = 16;   // 256 threads: 16 tiles x 64 couts
+template <bool NHWC, bool OUT8, bool RQFAST>
+__global__ void __launch_bounds__(256, 2) k_output_transform4(Geom g, const int32_t* __restrict__ M, int n0, int imgs,
+                                                           int32_t rq_mult, int rq_shift, void* __restrict__ y) {
+  const int tl = threadIdx.x / kOut4Quads, ql = threadIdx.x % kOut4Quads;
+  const int t = blockIdx.x * kOut4Tiles + tl;
+  const int co0 = (blockIdx.y * kOut4Quads + ql) * 4;
+  pdl_trigger();
+  pdl_wait();   // M'' comes from the GEMM just before
+  if (t >= imgs * g.tpi || co0 >= g.cout) return;
+  const long long ps = g.chunk_tiles_pad * (long long)g.cout_pad;
+  const int4* mp = reinterpret_cast<const int4*>(M + m_offset(g, t, co0));
+  const long long ps4 = ps / 4;
+  int4 v[36];
+#pragma unroll
+  for (int s = 0; s < 36; s++) v[s] = __ldg(mp + s * ps4);
+  const int img = n0 + t / g.tpi, rem = t % g.tpi;
+  const int ty = rem / g.tw, tx = rem - ty * g.tw;
+  const int oy0 = 4 * ty, ox0 = 4 * tx;
+  const int ni = min(4, g.ho - oy0), nj = min(4, g.wo - ox0);
+  const uint32_t rq_half = rq_shift > 0 ? (1u << (rq_shift - 1)) : 0u;
+  auto comp = [](const int4& q, int c) -> uint32_t {
+    return (uint32_t)(c == 0 ? q.x : (c == 1 ? q.y : (c == 2 ? q.z : q.w)));
+  };
+  auto requant = [&](uint32_t yv) -> int32_t {
+    const int32_t o32 = rha16_32(yv);
+    if (!OUT8) return o32;
+    if (RQFAST) {
+      const uint32_t a = (uint32_t)abs(o32);
+      const int32_t r = (int32_t)((a + rq_half) >> rq_shift);
+      return o32 < 0 ? max(-r, -128) : min(r, 127);
+    }
+    long long r = rq_shift > 0 ? rha_shift64((long long)o32 * rq_mult, rq_shift) : (long long)o32 * rq_mult;
+    return (int32_t)(r > 127 ? 127 : (r < -128 ? -128 : r));
+  };
+  uint32_t out[4][4][4];   // [c][i][j]
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    uint32_t Z[4][4], zr[4], zi[4];
+#pragma unroll
+    for (int ri = 0; ri < 4; ri++) {
+      const uint32_t M0 = comp(v[ri * 4], c), M1 = comp(v[ri * 4 + 1], c), M2 = comp(v[ri * 4 + 2], c),
+                     M5 = comp(v[ri * 4 + 3], c);
+      const uint32_t x2 = 2 * comp(v[16 + ri], c), y2 = 2 * comp(v[26 + ri], c);
+      Z[ri][0] = M0 + M1 + M2 + x2;
+      Z[ri][1] = M1 - M2 - y2;
+      Z[ri][2] = M1 + M2 - x2;
+      Z[ri][3] = M1 - M2 + M5 + y2;
+    }
+    {
+      const uint32_t w0r = comp(v[20], c), w1r = comp(v[21], c), w2r = comp(v[22], c), w5r = comp(v[23], c),
+                     w3r = comp(v[24], c), w4r = comp(v[25], c);
+      const uint32_t w0i = comp(v[30], c), w1i = comp(v[31], c), w2i = comp(v[32], c), w5i = comp(v[33], c),
+                     w3i = comp(v[34], c), w4i = comp(v[35], c);
+      zr[0] = w0r + w1r + w2r + w3r + w4r;        zi[0] = w0i + w1i + w2i + w3i + w4i;
+      zr[1] = w1r - w2r - w3i + w4i;              zi[1] = w1i - w2i + w3r - w4r;
+      zr[2] = w1r + w2r - w3r - w4r;              zi[2] = w1i + w2i - w3i - w4i;
+      zr[3] = w1r - w2r + w3i - w4i + w5r;        zi[3] = w1i - w2i - w3r + w4r + w5i;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      out[c][0][j] = (uint32_t)requant(Z[0][j] + Z[1][j] + Z[2][j] + 2 * zr[j]);
+      out[c][1][j] = (uint32_t)requant(Z[1][j] - Z[2][j] - 2 * zi[j]);
+      out[c][2][j] = (uint32_t)requant(Z[1][j] + Z[2][j] - 2 * zr[j]);
+      out[c][3][j] = (uint32_t)requant(Z[1][j] - Z[2][j] + Z[3][j] + 2 * zi[j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    if (i >= ni) break;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (j >= nj) break;
+      if (NHWC) {
+        const long long pix = ((long long)img * g.ho + oy0 + i) * g.wo + ox0 + j;
+        if (OUT8) {
+          *reinterpret_cast<uint32_t*>(static_cast<int8_t*>(y) + pix * g.cout + co0) =
+              (out[0][i][j] & 0xffu) | ((out[1][i][j] & 0xffu) << 8) | ((out[2][i][j] & 0xffu) << 16) |
+              (out[3][i][j] << 24);
+        } else {
+          *reinterpret_cast<int4*>(static_cast<int32_t*>(y) + pix * g.cout + co0) =
+              make_int4((int)out[0][i][j], (int)out[1][i][j], (int)out[2][i][j], (int)out[3][i][j]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          const long long off = (((long long)img * g.cout + co0 + c) * g.ho + oy0 + i) * g.wo + ox0 + j;
+          if (OUT8) static_cast<int8_t*>(y)[off] = (int8_t)out[c][i][j];
+          else static_cast<int32_t*>(y)[off] = (int32_t)out[c][i][j];
+        }
+      }
+    }
+  }
+}
+
 cudaError_t launch_output_transform(const Geom& g, const int32_t* m, int n0, int imgs, int32_t rq_mult,
                                     int rq_shift, void* y, cudaStream_t st) {
   const int tiles = imgs * g.tpi;
   dim3 grid((unsigned)((tiles + kOutTiles - 1) / kOutTiles), (unsigned)((g.cout + kOutCoBlock - 1) / kOutCoBlock));
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 30;
   cudaError_t e;
+  if (nhwc && (g.cout & 3) == 0) {   // vectorised variant (NHWC; NCHW keeps one cout per thread)
+    dim3 grid4((unsigned)((tiles + kOut4Tiles - 1) / kOut4Tiles), (unsigned)((g.cout + 63) / 64));
+#define WINO_K4V(B, C) e = launch_pdl(k_output_transform4<true, B, C>, grid4, dim3(256), 0, st, g, m, n0, imgs, rq_mult, rq_shift, y)
+    if (!out8) WINO_K4V(false, false);
+    else if (fast) WINO_K4V(true, true);
+    else WINO_K4V(true, false);
+#undef WINO_K4V
+    return e;
+  }
 #define WINO_K4(A, B, C) e = launch_pdl(k_output_transform<A, B, C>, grid, dim3(256), 0, st, g, m, n0, imgs, rq_mult, rq_shift, y)
   if (nhwc) {
     if (!out8) WINO_K4(true, false, false);

@@ -85,9 +85,9 @@ int main() {
     cudaEventRecord(e1);
     cudaError_t err = cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
-    printf("ctas %3d nprod %d R=%d V=%5d W=%5d %-7s share=%d: %6.1f ns/stage  %6.1f B/cyc/SM  (%s) %s\n", c.R, c.vb, c.wb,
-           nctas, np, c.commit ? "commit" : "arrive", c.share, ms * 1e6 / n, (double)(c.vb + c.wb) * n / (ms * 1e-3 * 1.965e9),
-           c.note, cudaGetErrorString(err));
+    printf("ctas %3d nprod %d R=%d V=%5d W=%5d %-6s share=%d: %6.1f ns/stage %6.1f B/cyc/SM (%s) %s\n", nctas, np,
+           c.R, c.vb, c.wb, c.commit ? "commit" : "arrive", c.share, ms * 1e6 / n,
+           (double)(c.vb + c.wb) * n / (ms * 1e-3 * 1.965e9), c.note, cudaGetErrorString(err));
   }
   return 0;
 }
