@@ -95,8 +95,10 @@ typedef struct {
     int cout_pad;               /* c_out rounded up to n_block                        */
     int n_block;                /* GEMM N tile (couts per CTA)                         */
     int m_block;                /* GEMM M tile (tiles per CTA) = 128                   */
-    int planes;                 /* 46 = 16 real + 10 x {re, im, re+im}        */
-    int pieces;                 /* 2 int8 pieces per operand value (hi s8, lo u8)      */
+    int planes;                 /* staged: 46 = 16 real + 10 x {re, im, re+im};
+                                   fused: 36 = 16 real + 10 x {re, im}                 */
+    int pieces;                 /* 2 balanced s8 pieces per operand value:
+                                   v = 256 hi + lo, lo = low byte of v     */
     int chunk_images;           /* images per workspace chunk                          */
     int n_chunks;
     long long chunk_tiles_pad;  /* tiles per chunk rounded up to m_block               */
