@@ -23,6 +23,7 @@
  *   - Y = A^T M'' A, full complex product, assert Im Y == 0
  *   - out32 = rha(Re Y / 16)                               P:366, A11
  *   - y8 = clamp(rha(out32 * M0 / 2^S), -128, 127)         DESIGN.md A14
+ * The rational F(2x2,3x3) pipeline of P:259-306 follows at the end.
  * No Karatsuba, conjugate shortcut, blocking or fusion is used here: those
  * are the GPU path's optimisations and are checked against this file.
  */
@@ -395,6 +396,193 @@ int oracle_wino_conv(const int8_t *x, const int8_t *w, int N, int H, int W, int 
     if (bad_range) status = status ? status : -4;
     if (bad_div) status = status ? status : -3;
     if (bad_im) status = status ? status : -2;
+    free(Wp); free(codes); free(D);
+    return status;
+}
+
+/* ==========================================================================
+ * Rational F(2x2,3x3): the configuration the paper evaluates
+ * end to end, with the same filter precision scaling.
+ *   G' = 2G, typed from P:261-268.
+ *   B^T and A^T are the standard F(2,3) matrices of the cited Lavin algorithm
+ *   (the paper prints only G', A25); pinned by the closed form
+ *   A^T[(G'gG'^T) (.) (B^T d B)]A = 4 * correlation.
+ *   Output divisor 4 ("shift right by 1 after each final transform"),
+ *   applied as one final rha(Y / 4) (A26).
+ * Positions: the 4x4 grid row-major, all 16 real.                          */
+static const int G2[4][3] = {{2, 0, 0}, {1, 1, 1}, {1, -1, 1}, {0, 0, 2}};
+static const int BT2[4][4] = {{1, 0, -1, 0}, {0, 1, 1, 0}, {0, -1, 1, 0}, {0, 1, 0, -1}};
+static const int AT2[2][4] = {{1, 1, 1, 0}, {0, 1, -1, -1}};
+#define OUT2_DIV_SHIFT 2
+
+/* W = G' g G'^T. */
+void oracle_filter_tile2(const int64_t g[3][3], int64_t W[4][4]) {
+    int64_t Gg[4][3];
+    for (int i = 0; i < 4; i++)
+        for (int j = 0; j < 3; j++) {
+            int64_t s = 0;
+            for (int k = 0; k < 3; k++) s += G2[i][k] * g[k][j];
+            Gg[i][j] = s;
+        }
+    for (int i = 0; i < 4; i++)
+        for (int j = 0; j < 4; j++) {
+            int64_t s = 0;
+            for (int k = 0; k < 3; k++) s += Gg[i][k] * G2[j][k];
+            W[i][j] = s;
+        }
+}
+/* D = B^T d B for one 4x4 patch. */
+void oracle_input_tile2(const int64_t d[4][4], int64_t D[4][4]) {
+    int64_t Bd[4][4];
+    for (int i = 0; i < 4; i++)
+        for (int j = 0; j < 4; j++) {
+            int64_t s = 0;
+            for (int k = 0; k < 4; k++) s += BT2[i][k] * d[k][j];
+            Bd[i][j] = s;
+        }
+    for (int i = 0; i < 4; i++)
+        for (int j = 0; j < 4; j++) {
+            int64_t s = 0;
+            for (int k = 0; k < 4; k++) s += Bd[i][k] * BT2[j][k];
+            D[i][j] = s;
+        }
+}
+/* Y = A^T M A (2x2). */
+void oracle_output_tile2(const int64_t M[4][4], int64_t Y[2][2]) {
+    int64_t AM[2][4];
+    for (int i = 0; i < 2; i++)
+        for (int j = 0; j < 4; j++) {
+            int64_t s = 0;
+            for (int k = 0; k < 4; k++) s += AT2[i][k] * M[k][j];
+            AM[i][j] = s;
+        }
+    for (int i = 0; i < 2; i++)
+        for (int j = 0; j < 2; j++) {
+            int64_t s = 0;
+            for (int k = 0; k < 4; k++) s += AM[i][k] * AT2[j][k];
+            Y[i][j] = s;
+        }
+}
+void oracle_filter_tile2_64(const int64_t *g9, int64_t *W16) { oracle_filter_tile2((const int64_t(*)[3])g9, (int64_t(*)[4])W16); }
+void oracle_input_tile2_64(const int64_t *d16, int64_t *D16) { oracle_input_tile2((const int64_t(*)[4])d16, (int64_t(*)[4])D16); }
+void oracle_output_tile2_64(const int64_t *M16, int64_t *Y4) { oracle_output_tile2((const int64_t(*)[4])M16, (int64_t(*)[2])Y4); }
+
+/* Offline F(2x2) filter path (P:317-330 with 16 positions):
+ *   W_out [Cout][Cin][16] (may be NULL), Wp_out [Cout][Cin][16], codes_out [Cout][16]. */
+int oracle_filter_transform2(const int8_t *w, int Cout, int Cin, int layout, int scaling, int target,
+                             int64_t *W_out, int64_t *Wp_out, uint8_t *codes_out) {
+    int status = 0;
+    int64_t *Wt = (int64_t *)malloc(sizeof(int64_t) * 16 * (size_t)(Cin > 0 ? Cin : 1));
+    for (int co = 0; co < Cout; co++) {
+        for (int ci = 0; ci < Cin; ci++) {          /* step 1: transform all weights of the OFM */
+            int64_t g[3][3], W4[4][4];
+            for (int u = 0; u < 3; u++)
+                for (int v = 0; v < 3; v++) g[u][v] = w_at(w, layout, Cout, Cin, co, ci, u, v);
+            oracle_filter_tile2(g, W4);
+            for (int pos = 0; pos < 16; pos++) Wt[(size_t)ci * 16 + pos] = W4[pos / 4][pos % 4];
+        }
+        for (int pos = 0; pos < 16; pos++) {
+            int64_t mx = 0;                          /* step 2: max magnitude across channels */
+            for (int ci = 0; ci < Cin; ci++) {
+                int64_t v = Wt[(size_t)ci * 16 + pos];
+                if (v < 0) v = -v;
+                if (v > mx) mx = v;
+            }
+            int n = 0, p = 0;
+            if (scaling && oracle_scale_factor(mx, target, &n, &p) != 0) { status = -1; n = 0; p = 0; }
+            codes_out[(size_t)co * 16 + pos] = (uint8_t)oracle_encode_code(n, p);
+            for (int ci = 0; ci < Cin; ci++) {
+                int64_t v = Wt[(size_t)ci * 16 + pos];
+                size_t o = ((size_t)co * Cin + ci) * 16 + pos;
+                if (W_out) W_out[o] = v;
+                Wp_out[o] = n ? oracle_rha_shift(v * n, p) : v;
+            }
+        }
+    }
+    free(Wt);
+    return status;
+}
+
+/* F(2x2) input transform of every tile: D_out [T][Cin][16], T = N*th*tw with
+ * th = ceil(Ho/2), patch origin (2ty - pad, 2tx - pad).                    */
+void oracle_input_transform2(const int8_t *x, int N, int H, int W, int Cin, int pad, int layout,
+                             int64_t *D_out) {
+    int Ho = H + 2 * pad - 2, Wo = W + 2 * pad - 2;
+    int th = (Ho + 1) / 2, tw = (Wo + 1) / 2;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; n++)
+        for (int ty = 0; ty < th; ty++)
+            for (int tx = 0; tx < tw; tx++)
+                for (int ci = 0; ci < Cin; ci++) {
+                    int64_t d[4][4], D[4][4];
+                    for (int a = 0; a < 4; a++)
+                        for (int b = 0; b < 4; b++)
+                            d[a][b] = x_at(x, layout, N, Cin, H, W, n, ci, 2 * ty - pad + a, 2 * tx - pad + b);
+                    oracle_input_tile2(d, D);
+                    size_t t = ((size_t)n * th + ty) * tw + tx;
+                    for (int pos = 0; pos < 16; pos++) D_out[(t * Cin + ci) * 16 + pos] = D[pos / 4][pos % 4];
+                }
+}
+
+/* The F(2x2) pipeline end to end: as oracle_wino_conv with 2x2 output tiles,
+ * out32 = rha(Y / 4).  M_out / Mpp_out [T][Cout][16] (may be NULL).
+ * Returns 0; -1 scale-factor range; -3 unscaled and 4 does not divide Y;
+ * -4 int32 range.                                                          */
+int oracle_wino2_conv(const int8_t *x, const int8_t *w, int N, int H, int W, int Cin, int Cout,
+                      int pad, int layout, int scaling, int target, int32_t M0, int S,
+                      int32_t *out32, int8_t *y8, int64_t *M_out, int64_t *Mpp_out) {
+    int Ho = H + 2 * pad - 2, Wo = W + 2 * pad - 2;
+    int th = (Ho + 1) / 2, tw = (Wo + 1) / 2;
+    size_t T = (size_t)N * th * tw;
+    int status = 0;
+    int64_t *Wp = (int64_t *)malloc(sizeof(int64_t) * 16 * (size_t)Cout * (Cin > 0 ? Cin : 1));
+    uint8_t *codes = (uint8_t *)malloc((size_t)Cout * 16);
+    int64_t *D = (int64_t *)malloc(sizeof(int64_t) * 16 * T * (Cin > 0 ? Cin : 1));
+    if (oracle_filter_transform2(w, Cout, Cin, layout, scaling, target, NULL, Wp, codes) != 0) status = -1;
+    oracle_input_transform2(x, N, H, W, Cin, pad, layout, D);
+    int bad_div = 0, bad_range = 0;
+#pragma omp parallel for collapse(2) schedule(dynamic) reduction(| : bad_div, bad_range)
+    for (long long t = 0; t < (long long)T; t++)
+        for (int co = 0; co < Cout; co++) {
+            int64_t M[4][4], Mpp[4][4];
+            memset(M, 0, sizeof(M));
+            for (int ci = 0; ci < Cin; ci++)             /* Hadamard products over channels */
+                for (int pos = 0; pos < 16; pos++)
+                    M[pos / 4][pos % 4] += Wp[((size_t)co * Cin + ci) * 16 + pos] * D[((size_t)t * Cin + ci) * 16 + pos];
+            for (int pos = 0; pos < 16; pos++) {          /* reverse scaling */
+                int64_t v = M[pos / 4][pos % 4];
+                int n, p, m = 0, q = 0;
+                oracle_decode_code(codes[(size_t)co * 16 + pos], &n, &p);
+                if (n) { oracle_reverse_factor(n, p, &m, &q); v = oracle_rha_shift(v * m, q); }
+                Mpp[pos / 4][pos % 4] = v;
+                if (v > INT32_MAX || v < INT32_MIN) bad_range = 1;
+                if (M_out) M_out[((size_t)t * Cout + co) * 16 + pos] = M[pos / 4][pos % 4];
+                if (Mpp_out) Mpp_out[((size_t)t * Cout + co) * 16 + pos] = v;
+            }
+            int64_t Y[2][2];
+            oracle_output_tile2(Mpp, Y);
+            int n_img = (int)(t / ((size_t)th * tw));
+            int rem = (int)(t % ((size_t)th * tw));
+            int ty = rem / tw, tx = rem % tw;
+            for (int i = 0; i < 2; i++)
+                for (int j = 0; j < 2; j++) {
+                    if (Y[i][j] > INT32_MAX || Y[i][j] < INT32_MIN) bad_range = 1;
+                    if (!scaling && (Y[i][j] % 4) != 0) bad_div = 1;
+                    int oy = 2 * ty + i, ox = 2 * tx + j;
+                    if (oy >= Ho || ox >= Wo) continue;
+                    int64_t o32 = oracle_rha_shift(Y[i][j], OUT2_DIV_SHIFT);
+                    int64_t yi = y_index(layout, Cout, Ho, Wo, n_img, co, oy, ox);
+                    out32[yi] = (int32_t)o32;
+                    if (y8) {
+                        int64_t r = oracle_rha_shift(o32 * (int64_t)M0, S);
+                        if (r > 127) r = 127;
+                        if (r < -128) r = -128;
+                        y8[yi] = (int8_t)r;
+                    }
+                }
+        }
+    if (bad_range) status = status ? status : -4;
+    if (bad_div) status = status ? status : -3;
     free(Wp); free(codes); free(D);
     return status;
 }

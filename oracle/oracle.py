@@ -56,6 +56,16 @@ def lib():
         L.oracle_filter_tile64.argtypes = [P, P]; L.oracle_filter_tile64.restype = None
         L.oracle_input_tile64.argtypes = [P, P]; L.oracle_input_tile64.restype = None
         L.oracle_output_tile64.argtypes = [P, P]; L.oracle_output_tile64.restype = i32
+        L.oracle_filter_tile2_64.argtypes = [P, P]; L.oracle_filter_tile2_64.restype = None
+        L.oracle_input_tile2_64.argtypes = [P, P]; L.oracle_input_tile2_64.restype = None
+        L.oracle_output_tile2_64.argtypes = [P, P]; L.oracle_output_tile2_64.restype = None
+        L.oracle_filter_transform2.argtypes = [P, i32, i32, i32, i32, i32, P, P, P]
+        L.oracle_filter_transform2.restype = i32
+        L.oracle_input_transform2.argtypes = [P, i32, i32, i32, i32, i32, i32, P]
+        L.oracle_input_transform2.restype = None
+        L.oracle_wino2_conv.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, i32, i32,
+                                        ctypes.c_int32, i32, P, P, P, P]
+        L.oracle_wino2_conv.restype = i32
         _lib = L
     return _lib
 
@@ -235,3 +245,84 @@ def maxpool2(x, layout=NHWC) -> np.ndarray:
     y = np.zeros(shape, np.int8)
     lib().oracle_maxpool2(_p(x), N, H, W, C, layout, _p(y))
     return y
+
+
+# ---------------------------------------------------------------- rational F(2x2,3x3)
+def filter_tile2(g) -> np.ndarray:
+    """W = G' g G'^T for one 3x3 filter -> (4,4) int64."""
+    g = _c(np.asarray(g).reshape(9), np.int64)
+    W = np.zeros(16, np.int64)
+    lib().oracle_filter_tile2_64(_p(g), _p(W))
+    return W.reshape(4, 4)
+
+
+def input_tile2(d) -> np.ndarray:
+    d = _c(np.asarray(d).reshape(16), np.int64)
+    D = np.zeros(16, np.int64)
+    lib().oracle_input_tile2_64(_p(d), _p(D))
+    return D.reshape(4, 4)
+
+
+def output_tile2(M) -> np.ndarray:
+    M = _c(np.asarray(M).reshape(16), np.int64)
+    Y = np.zeros(4, np.int64)
+    lib().oracle_output_tile2_64(_p(M), _p(Y))
+    return Y.reshape(2, 2)
+
+
+def tiles2(H, W, pad):
+    Ho, Wo = out_hw(H, W, pad)
+    return (Ho + 1) // 2, (Wo + 1) // 2
+
+
+def filter_transform2(w, layout=NHWC, scaling=True, target=255):
+    """F(2x2) offline filter path -> (W [Cout][Cin][16], W', codes [Cout][16])."""
+    w = _c(w, np.int8)
+    Cout = w.shape[0]
+    Cin = w.shape[1] if layout == NCHW else w.shape[3]
+    W = np.zeros((Cout, Cin, 16), np.int64); Wp = np.zeros((Cout, Cin, 16), np.int64)
+    codes = np.zeros((Cout, 16), np.uint8)
+    if lib().oracle_filter_transform2(_p(w), Cout, Cin, layout, int(bool(scaling)), target,
+                                      _p(W), _p(Wp), _p(codes)) != 0:
+        raise ValueError("scale factor out of range")
+    return W, Wp, codes
+
+
+def input_transform2(x, pad=1, layout=NHWC) -> np.ndarray:
+    """F(2x2) D for every (tile, cin) -> [T][Cin][16] int64."""
+    x = _c(x, np.int8)
+    if layout == NCHW:
+        N, Cin, H, W = x.shape
+    else:
+        N, H, W, Cin = x.shape
+    th, tw = tiles2(H, W, pad)
+    D = np.zeros((N * th * tw, Cin, 16), np.int64)
+    lib().oracle_input_transform2(_p(x), N, H, W, Cin, pad, layout, _p(D))
+    return D
+
+
+def wino2_conv(x, w, pad=1, layout=NHWC, scaling=True, target=255, M0=1, S=0,
+               want_y8=True, want_M=False) -> WinoResult:
+    """The rational F(2x2,3x3) pipeline with filter scaling; raises on
+    invariant violations (4 not dividing Y when unscaled, int32 range)."""
+    x = _c(x, np.int8); w = _c(w, np.int8)
+    if layout == NCHW:
+        N, Cin, H, W = x.shape
+    else:
+        N, H, W, Cin = x.shape
+    Cout = w.shape[0]
+    Ho, Wo = out_hw(H, W, pad)
+    th, tw = tiles2(H, W, pad)
+    T = N * th * tw
+    shape = (N, Cout, Ho, Wo) if layout == NCHW else (N, Ho, Wo, Cout)
+    out32 = np.zeros(shape, np.int32)
+    y8 = np.zeros(shape, np.int8) if want_y8 else None
+    M = np.zeros((T, Cout, 16), np.int64) if want_M else None
+    Mpp = np.zeros((T, Cout, 16), np.int64) if want_M else None
+    st = lib().oracle_wino2_conv(_p(x), _p(w), N, H, W, Cin, Cout, pad, layout, int(bool(scaling)), target,
+                                 int(M0), int(S), _p(out32), _p(y8) if y8 is not None else None,
+                                 _p(M) if M is not None else None, _p(Mpp) if Mpp is not None else None)
+    if st != 0:
+        raise ValueError(f"oracle invariant violated (status {st})")
+    return WinoResult(out32, y8, M, Mpp, st)
+
