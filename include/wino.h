@@ -79,10 +79,18 @@ typedef struct {
                              transform + store (M'' stays on chip).
                              WINO_PATH_STAGED (1): K2, K3 GEMMs -> M'' in the workspace,
                              K4 output transform (M'' inspectable, see wino_plan_info). */
+    int algorithm;        /* WINO_ALG_F4X4 (0, default): complex F(4x4,3x3) over the
+                             Gaussian integers, points {0, +-1, +-i};
+                             WINO_ALG_F2X2 (1): rational F(2x2,3x3), G' = 2G,
+                             the configuration the paper evaluates; staged path only.
+                             Codes are [c_out][36] (F4x4) or [c_out][16] (F2x2).      */
 } wino_conv_desc;
 
 /* Hot-path kernel structure (wino_conv_desc.path). */
 enum { WINO_PATH_FUSED = 0, WINO_PATH_STAGED = 1 };
+
+/* Winograd algorithm (wino_conv_desc.algorithm). */
+enum { WINO_ALG_F4X4 = 0, WINO_ALG_F2X2 = 1 };
 
 typedef struct wino_plan_s *wino_plan_t;
 
@@ -104,6 +112,9 @@ typedef struct {
     long long chunk_tiles_pad;  /* tiles per chunk rounded up to m_block               */
     int path;                   /* WINO_PATH_FUSED or WINO_PATH_STAGED                 */
     int stages;                 /* kernels per chunk: 2 (fused) or 3 (staged)          */
+    int algorithm;              /* WINO_ALG_F4X4 or WINO_ALG_F2X2                      */
+    int tile;                   /* output tile edge: 4 (F4x4) or 2 (F2x2)             */
+    int positions;              /* Winograd positions = codes per c_out: 36 or 16     */
     size_t v_offset, v_bytes;   /* V  = B^T d B operand planes inside the workspace    */
     size_t m_offset, m_bytes;   /* M'' = 36 int32 per (tile, cout) after Karatsuba and
                                    reverse scaling; swizzled tiles; staged

@@ -15,6 +15,7 @@ WINO_ERR_RANGE, WINO_ERR_CUDA, WINO_ERR_NOMEM = -4, -5, -6
 WINO_NCHW, WINO_NHWC = 0, 1
 WINO_OUT_INT8, WINO_OUT_INT32 = 0, 1
 WINO_PATH_FUSED, WINO_PATH_STAGED = 0, 1
+WINO_ALG_F4X4, WINO_ALG_F2X2 = 0, 1
 
 # every symbol include/wino.h declares
 EXPORTS = ("wino_status_string", "wino_last_cuda_error", "wino_plan", "wino_plan_destroy", "wino_plan_query", "wino_filter_bytes",
@@ -27,7 +28,7 @@ class wino_conv_desc(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("h", ctypes.c_int), ("w", ctypes.c_int), ("c_in", ctypes.c_int),
                 ("c_out", ctypes.c_int), ("pad", ctypes.c_int), ("layout", ctypes.c_int),
                 ("filter_scaling", ctypes.c_int), ("filter_target_max", ctypes.c_int), ("out_mode", ctypes.c_int),
-                ("workspace_mb", ctypes.c_int), ("path", ctypes.c_int)]
+                ("workspace_mb", ctypes.c_int), ("path", ctypes.c_int), ("algorithm", ctypes.c_int)]
 
 
 class wino_plan_info(ctypes.Structure):
@@ -36,6 +37,7 @@ class wino_plan_info(ctypes.Structure):
                 ("n_block", ctypes.c_int), ("m_block", ctypes.c_int), ("planes", ctypes.c_int),
                 ("pieces", ctypes.c_int), ("chunk_images", ctypes.c_int), ("n_chunks", ctypes.c_int),
                 ("chunk_tiles_pad", ctypes.c_longlong), ("path", ctypes.c_int), ("stages", ctypes.c_int),
+                ("algorithm", ctypes.c_int), ("tile", ctypes.c_int), ("positions", ctypes.c_int),
                 ("v_offset", ctypes.c_size_t), ("v_bytes", ctypes.c_size_t),
                 ("m_offset", ctypes.c_size_t), ("m_bytes", ctypes.c_size_t), ("workspace_bytes", ctypes.c_size_t),
                 ("filter_bytes", ctypes.c_size_t), ("codes_bytes", ctypes.c_size_t), ("x_bytes", ctypes.c_size_t),

@@ -15,12 +15,13 @@ class WinoConv2d:
     """
 
     def __init__(self, n, h, w, c_in, c_out, pad=1, layout=L.WINO_NHWC, filter_scaling=True,
-                 out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0, path=L.WINO_PATH_STAGED):
+                 out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0, path=L.WINO_PATH_STAGED,
+                 algorithm=L.WINO_ALG_F4X4):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device)
         self.desc = L.wino_conv_desc(n, h, w, c_in, c_out, pad, layout, int(bool(filter_scaling)), 255, out_mode,
-                                     workspace_mb, path)
+                                     workspace_mb, path, algorithm)
         self.plan = L.wino_plan(self.desc, device)
         self.info = L.wino_plan_query(self.plan)
         self.layout, self.out_mode = layout, out_mode
@@ -30,7 +31,7 @@ class WinoConv2d:
         self.w_shape = (c_out, c_in, 3, 3) if layout == L.WINO_NCHW else (c_out, 3, 3, c_in)
         self.y_dtype = torch.int8 if out_mode == L.WINO_OUT_INT8 else torch.int32
         self.w_wino = torch.empty(self.info.filter_bytes, dtype=torch.int8, device=self.device)
-        self.codes = torch.empty((c_out, 36), dtype=torch.uint8, device=self.device)
+        self.codes = torch.empty((c_out, self.info.positions), dtype=torch.uint8, device=self.device)
         if workspace is not None:   # caller-shared scratch (e.g. one buffer for a layer stack)
             assert workspace.numel() >= self.info.workspace_bytes and workspace.dtype == torch.int8
             self.workspace = workspace

@@ -225,7 +225,106 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
   }
 }
 
+// ---- rational F(2x2,3x3): W = G' g G'^T, G' = 2G, 16 real positions
+// (row-major 4x4), the same per-(OFM, position) scaling, staged W' layout with 16 planes.
+__device__ __forceinline__ void filter_tile_transform2(const int g[3][3], int out[16]) {
+  int u[4][3];   // G' g: rows 2 g0 | g0 + g1 + g2 | g0 - g1 + g2 | 2 g2
+#pragma unroll
+  for (int j = 0; j < 3; j++) {
+    u[0][j] = 2 * g[0][j];
+    u[1][j] = g[0][j] + g[1][j] + g[2][j];
+    u[2][j] = g[0][j] - g[1][j] + g[2][j];
+    u[3][j] = 2 * g[2][j];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {   // (G' g) G'^T row by row
+    out[i * 4 + 0] = 2 * u[i][0];
+    out[i * 4 + 1] = u[i][0] + u[i][1] + u[i][2];
+    out[i * 4 + 2] = u[i][0] - u[i][1] + u[i][2];
+    out[i * 4 + 3] = 2 * u[i][2];
+  }
+}
+
+__global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform2(Geom g, const int8_t* __restrict__ w,
+                                                                          int8_t* __restrict__ wimg,
+                                                                          uint8_t* __restrict__ codes) {
+  __shared__ __align__(16) int8_t s_stage[kFilterWarps][32][32];   // 16 planes x 2 pieces per channel
+  __shared__ int s_max[kFilterWarps][16];
+  __shared__ int s_n[16], s_p[16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int co = blockIdx.x;
+  const bool live = co < g.cout;
+  pdl_trigger();
+  pdl_wait();
+  int mx[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) mx[i] = 0;
+  if (live) {
+    for (int ci = threadIdx.x; ci < g.cin; ci += blockDim.x) {   // steps 1-2: transform, max magnitude
+      int gg[3][3], t[16];
+      load_filter(g, w, co, ci, gg);
+      filter_tile_transform2(gg, t);
+#pragma unroll
+      for (int s = 0; s < 16; s++) mx[s] = max(mx[s], abs(t[s]));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 16; i++) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx[i] = max(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
+    if (lane == 0) s_max[warp][i] = mx[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < 16) {   // steps 3-4 (read as DESIGN.md A3)
+    int m = 0;
+#pragma unroll
+    for (int wv = 0; wv < kFilterWarps; wv++) m = max(m, s_max[wv][threadIdx.x]);
+    int n = 0, p = 0;
+    if (g.scaling && m > g.target) {
+      const int x = (g.target * 128) / m;
+      const int y = 31 - __clz(x);
+      n = y >= 3 ? (x >> (y - 3)) : (x << (3 - y));
+      p = 10 - y;
+    }
+    s_n[threadIdx.x] = n;
+    s_p[threadIdx.x] = p;
+    if (live) codes[co * 16 + threadIdx.x] = (uint8_t)(n ? ((n << 2) | (p - 4)) : 0);
+  }
+  __syncthreads();
+  int sn[16], sp[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) { sn[i] = s_n[i]; sp[i] = s_p[i]; }
+  for (int c0 = warp * 32; c0 < g.cin_pad; c0 += kFilterWarps * 32) {
+    const int ci = c0 + lane;
+    int vals[16];
+    if (live && ci < g.cin) {
+      int gg[3][3];
+      load_filter(g, w, co, ci, gg);
+      filter_tile_transform2(gg, vals);
+#pragma unroll
+      for (int s = 0; s < 16; s++) vals[s] = sn[s] ? rha_mul_shift(vals[s], sn[s], sp[s]) : vals[s];
+    } else {
+#pragma unroll
+      for (int s = 0; s < 16; s++) vals[s] = 0;
+    }
+#pragma unroll
+    for (int s = 0; s < 16; s++) {
+      s_stage[warp][2 * s + 0][lane] = (int8_t)bal_hi(vals[s]);
+      s_stage[warp][2 * s + 1][lane] = (int8_t)bal_lo(vals[s]);
+    }
+    __syncwarp();
+    for (int idx = lane; idx < 32 * 2; idx += 32) {   // (piece-plane, 16-channel half)
+      const int pp = idx >> 1, hf = idx & 1;
+      const int4 v = *reinterpret_cast<const int4*>(&s_stage[warp][pp][hf * 16]);
+      *reinterpret_cast<int4*>(wimg + w_offset(g, pp >> 1, pp & 1, co, c0 + hf * 16)) = v;
+    }
+    __syncwarp();
+  }
+}
+
 cudaError_t launch_filter_transform(const Geom& g, const int8_t* w, int8_t* wimg, uint8_t* codes, cudaStream_t st) {
+  if (g.alg == 1)
+    return launch_pdl(k_filter_transform2, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
   if (g.path == 0)
     return launch_pdl(k_filter_transform<true>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
   return launch_pdl(k_filter_transform<false>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);

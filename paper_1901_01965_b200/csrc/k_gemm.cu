@@ -64,9 +64,18 @@ __device__ __forceinline__ void decode_unit(int u, int tblocks, int nblocks, int
 __device__ __forceinline__ int cta_unit(int k) {
   return k * (int)gridDim.x + ((k & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
 }
-__device__ __forceinline__ int unit_planes(int pidx) { return pidx < kPrimaries ? 3 : 1; }
+// F2: rational F(2x2,3x3): 16 single-plane real units, unit = plane = position = M'' slot.
+template <bool F2> struct Alg {
+  static constexpr int kPrim = F2 ? 0 : kPrimaries;            // complex (3-plane) units, first
+  static constexpr int kUnits = F2 ? 16 : kPositions;           // unit kinds per (tile block, cout block)
+  static constexpr int kPlanesV = F2 ? 16 : kPlanes;            // planes per tile block in V
+  static constexpr int kPos = F2 ? 16 : 36;                     // codes per cout
+};
+template <bool F2>
+__device__ __forceinline__ int unit_planes(int pidx) { return pidx < Alg<F2>::kPrim ? 3 : 1; }
+template <bool F2>
 __device__ __forceinline__ int unit_plane0(int pidx) {
-  return pidx < kPrimaries ? kRealPlanes + 3 * pidx : pidx - kPrimaries;
+  return pidx < Alg<F2>::kPrim ? kRealPlanes + 3 * pidx : pidx - Alg<F2>::kPrim;
 }
 
 // Debug timeline (wino_debug_set_trace; compiled in with -DWINO_K3_TRACE): per CTA,
@@ -113,7 +122,7 @@ __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync %0, %1;" ::"n"(kEpiBarrier), "n"(kEpiWarps * 32) : "memory");
 }
 
-template <int NBLK>
+template <int NBLK, bool F2>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ Mraw,
            const uint8_t* __restrict__ codes, int cout, int scaling, int ksteps, long long tiles_pad, int tblocks,
@@ -150,7 +159,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
   const int nblocks = cout_pad / NBLK;
-  const int n_units = tblocks * nblocks * kPositions;
+  const int n_units = tblocks * nblocks * Alg<F2>::kUnits;
   const int n_it = (ksteps + kKStepsPerStage - 1) / kKStepsPerStage;
 
   if (warp == 0) {
@@ -176,10 +185,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     lut[threadIdx.x] = (uint32_t)m | ((uint32_t)q << 8) | ((q ? (1u << (q - 1)) : 0u) << 16);
   }
   pdl_wait();   // V, W' and the codes come from the kernels just before
-  for (int i = threadIdx.x; i < kPositions * cout_pad; i += blockDim.x) {   // codes, position-major
+  for (int i = threadIdx.x; i < Alg<F2>::kUnits * cout_pad; i += blockDim.x) {   // codes, position-major
     const int pidx = i / cout_pad, co = i - pidx * cout_pad;
-    const int pos = pidx < kPrimaries ? cpx_pos(pidx) : real_pos(pidx - kPrimaries);
-    s_codes[i] = (scaling && co < cout) ? codes[(long long)co * 36 + pos] : 0;
+    const int pos = F2 ? pidx : (pidx < kPrimaries ? cpx_pos(pidx) : real_pos(pidx - kPrimaries));
+    s_codes[i] = (scaling && co < cout) ? codes[(long long)co * Alg<F2>::kPos + pos] : 0;
   }
   tc_fence_before();
   __syncthreads();
@@ -193,10 +202,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int ku = 0, u = cta_unit(0); u < n_units; u = cta_unit(++ku)) {
        int pidx, tb, nb;
        decode_unit(u, tblocks, nblocks, pidx, tb, nb);
-       for (int pl = 0; pl < unit_planes(pidx); pl++, ui++) {
-        const int plane = unit_plane0(pidx) + pl;
+       for (int pl = 0; pl < unit_planes<F2>(pidx); pl++, ui++) {
+        const int plane = unit_plane0<F2>(pidx) + pl;
         // V of the plane: [K step][hi, lo] contiguous; W': [K step][W hi | W lo rows] contiguous
-        const int8_t* vpl = V + ((long long)tb * kPlanes + plane) * ksteps * (2 * kVBlockBytes);
+        const int8_t* vpl = V + ((long long)tb * Alg<F2>::kPlanesV + plane) * ksteps * (2 * kVBlockBytes);
         const int8_t* wpl = W + ((long long)plane * nblocks + nb) * ksteps * (2 * NBLK * kKStep);
         for (int ks = 0; ks < n_it; ks++, it++) {
           const int s = it % kStages;
@@ -225,7 +234,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int ku = 0, u = cta_unit(0); u < n_units; u = cta_unit(++ku)) {
        int pidx, tbu, nbu;
        decode_unit(u, tblocks, nblocks, pidx, tbu, nbu);
-       for (int pl = 0; pl < unit_planes(pidx); pl++, pc++) {
+       for (int pl = 0; pl < unit_planes<F2>(pidx); pl++, pc++) {
         const int b = pc & 1;
         mbar_wait(tempty0 + 8 * b, ((pc >> 1) & 1) ^ 1);   // epilogue drained this buffer
         tc_fence_after();
@@ -334,10 +343,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       decode_unit(u, tblocks, nblocks, pidx, tb, nb);
       const long long tile_off = ((long long)tb * nblocks + nb) * (kMBlock * NBLK);
       const uint8_t* crow = s_codes + pidx * cout_pad + nb * NBLK;
-      if (pidx >= kPrimaries) {                    // real position: one plane
+      if (pidx >= Alg<F2>::kPrim) {                // real position: one plane
         uint32_t v[kHalf];
         take_plane(v);
-        store_tile(v, Mraw + (long long)(pidx - kPrimaries) * ps + tile_off, crow);
+        store_tile(v, Mraw + (long long)(pidx - Alg<F2>::kPrim) * ps + tile_off, crow);
       } else {                                     // complex primary: Karatsuba P0, P1, P2
         uint32_t re[kHalf], sm[kHalf], v[kHalf];
         take_plane(re);                            // P0
@@ -368,12 +377,14 @@ cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t*
                         const uint8_t* codes, int32_t* mraw, cudaStream_t st) {
   // tile blocks of this launch; M strides use the full chunk geometry (K4 reads with it)
   const int tblocks = (int)(tiles_pad_launch / kMBlock);
-  const int n_units = tblocks * (g.cout_pad / g.nblk) * kPositions;
+  const int n_units = tblocks * (g.cout_pad / g.nblk) * (g.alg == 1 ? 16 : kPositions);
   const int grid = n_units < g_num_sms ? n_units : g_num_sms;
   const size_t smem = gemm_smem_bytes(g.nblk, g.cout_pad);
   cudaError_t e;
 #define WINO_LAUNCH_GEMM(N)                                                                                  \
-  e = launch_pdl(k_gemm<N>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw, codes, g.cout, g.scaling, \
+  e = g.alg == 1 ? launch_pdl(k_gemm<N, true>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw, codes, g.cout, g.scaling, \
+                 g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad, g_trace) \
+                 : launch_pdl(k_gemm<N, false>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw, codes, g.cout, g.scaling, \
                  g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad, g_trace)
   switch (g.nblk) {
     case 16: WINO_LAUNCH_GEMM(16); break;
@@ -389,9 +400,12 @@ cudaError_t setup_gemm() {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(16, kMaxCoutPad));
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(32, kMaxCoutPad));
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(64, kMaxCoutPad));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(16, kMaxCoutPad));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(16, kMaxCoutPad));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(32, kMaxCoutPad));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(32, kMaxCoutPad));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(64, kMaxCoutPad));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(64, kMaxCoutPad));
   return e;
 }
 

@@ -281,10 +281,77 @@ cudaError_t launch_input_transform_f(const Geom& g, const int8_t* x, int n0, int
   return launch_pdl(k_input_transform_f, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
 }
 
+// ---- rational F(2x2,3x3): 4x4 patch at (2ty - pad, 2tx - pad), D = B^T d B with the
+// F(2,3) matrix B^T = [[1,0,-1,0],[0,1,1,0],[0,-1,1,0],[0,1,0,-1]] (A25), 16 real planes
+// (position i*4 + j), balanced pieces, staged V layout (plane stride = g.planes = 16).
+__global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, const int8_t* __restrict__ x, int n0,
+                                                                    int imgs, int8_t* __restrict__ vimg) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tl = lane >> 3, cp = lane & 7;
+  const int t = blockIdx.x * kInTilesPerCta + warp * kInTilesPerWarp + tl;
+  const int c = blockIdx.y * kInChPerCta + 2 * cp;
+  pdl_trigger();
+  pdl_wait();
+  uint32_t w[16];   // 2 channels per pixel
+  {
+    int img = 0, iy0 = -1000000, ix0 = -1000000;
+    if (t < imgs * g.tpi) {
+      const int rem = t % g.tpi, ty = rem / g.tw;
+      img = n0 + t / g.tpi;
+      iy0 = 2 * ty - g.pad;
+      ix0 = 2 * (rem - ty * g.tw) - g.pad;
+    }
+    const bool cok = c < g.cin;
+    const long long cstep = g.layout == 1 ? 1 : (long long)g.h * g.w;
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        const int iy = iy0 + a, ix = ix0 + b;
+        uint32_t v = 0;
+        if (cok && iy >= 0 && iy < g.h && ix >= 0 && ix < g.w) {
+          const long long i0 = g.layout == 1 ? (((long long)img * g.h + iy) * g.w + ix) * g.cin + c
+                                             : (((long long)img * g.cin + c) * g.h + iy) * g.w + ix;
+          v = (uint8_t)__ldg(x + i0);
+          if (c + 1 < g.cin) v |= (uint32_t)(uint8_t)__ldg(x + i0 + cstep) << 8;
+        }
+        w[a * 4 + b] = v;
+      }
+  }
+  const long long pstride = (long long)g.ksteps * 2 * kVBlockBytes;
+  int8_t* base = vimg + (t / kMBlock) * g.planes * pstride + (long long)(c >> 5) * 2 * kVBlockBytes +
+                 tiled_offset(t % kMBlock, c & 31, kMBlock);
+  int Dv[2][16];
+#pragma unroll
+  for (int ch = 0; ch < 2; ch++) {
+    int r[4][4];   // d' = B^T d, column by column
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int d0 = sbyte(w[0 * 4 + j], ch), d1 = sbyte(w[1 * 4 + j], ch), d2 = sbyte(w[2 * 4 + j], ch),
+                d3 = sbyte(w[3 * 4 + j], ch);
+      r[0][j] = d0 - d2; r[1][j] = d1 + d2; r[2][j] = d2 - d1; r[3][j] = d1 - d3;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {   // D = d' B, row by row
+      Dv[ch][i * 4 + 0] = r[i][0] - r[i][2];
+      Dv[ch][i * 4 + 1] = r[i][1] + r[i][2];
+      Dv[ch][i * 4 + 2] = r[i][2] - r[i][1];
+      Dv[ch][i * 4 + 3] = r[i][1] - r[i][3];
+    }
+  }
+#pragma unroll
+  for (int pos = 0; pos < 16; pos++) {
+    int8_t* p = base + pos * pstride;
+    st16(p, __byte_perm((uint32_t)(Dv[0][pos] + 128), (uint32_t)(Dv[1][pos] + 128), 0x0051));   // [hi0, hi1]
+    st16(p + kVBlockBytes, __byte_perm((uint32_t)Dv[0][pos], (uint32_t)Dv[1][pos], 0x0040));      // [lo0, lo1]
+  }
+}
+
 cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st) {
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
   dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
+  if (g.alg == 1) return launch_pdl(k_input_transform2, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
   return launch_pdl(k_input_transform, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
 }
 

@@ -214,12 +214,78 @@ __global__ void __launch_bounds__(256, 2) k_output_transform4(Geom g, const int3
   }
 }
 
+// ---- rational F(2x2,3x3): Y = A^T M'' A with A^T = [[1,1,1,0],[0,1,-1,-1]] (A25)
+// on the 16 M'' slots (position i*4 + j), out32 = rha(Y / 4) (A26), requantisation, 2x2 store.
+template <bool NHWC, bool OUT8, bool RQFAST>
+__global__ void __launch_bounds__(256) k_output_transform2(Geom g, const int32_t* __restrict__ M, int n0, int imgs,
+                                                           int32_t rq_mult, int rq_shift, void* __restrict__ y) {
+  const int tl = threadIdx.x / kOutCoBlock, cl = threadIdx.x % kOutCoBlock;
+  const int t = blockIdx.x * kOutTiles + tl;
+  const int co = blockIdx.y * kOutCoBlock + cl;
+  pdl_trigger();
+  pdl_wait();
+  if (t >= imgs * g.tpi || co >= g.cout) return;
+  const long long ps = g.chunk_tiles_pad * (long long)g.cout_pad;
+  const int32_t* mp = M + m_offset(g, t, co);
+  uint32_t m[16];
+#pragma unroll
+  for (int s = 0; s < 16; s++) m[s] = (uint32_t)__ldg(mp + s * ps);
+  uint32_t Z[2][4];   // A^T M''
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    Z[0][j] = m[0 * 4 + j] + m[1 * 4 + j] + m[2 * 4 + j];
+    Z[1][j] = m[1 * 4 + j] - m[2 * 4 + j] - m[3 * 4 + j];
+  }
+  const int img = n0 + t / g.tpi, rem = t % g.tpi;
+  const int ty = rem / g.tw, tx = rem - ty * g.tw;
+  const int oy0 = 2 * ty, ox0 = 2 * tx;
+  const int ni = min(2, g.ho - oy0), nj = min(2, g.wo - ox0);
+  const uint32_t rq_half = rq_shift > 0 ? (1u << (rq_shift - 1)) : 0u;
+#pragma unroll
+  for (int i = 0; i < 2; i++) {
+    if (i >= ni) break;
+    const uint32_t Yr[2] = {Z[i][0] + Z[i][1] + Z[i][2], Z[i][1] - Z[i][2] - Z[i][3]};   // (A^T M'') A
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      if (j >= nj) break;
+      const int32_t yv = (int32_t)Yr[j];
+      const int32_t o32 = (yv + 2 + (yv >> 31)) >> 2;   // rha(Y / 4), |Y| < 2^31 - 2
+      const long long yi = NHWC ? (((long long)img * g.ho + oy0 + i) * g.wo + ox0 + j) * g.cout + co
+                                : (((long long)img * g.cout + co) * g.ho + oy0 + i) * g.wo + ox0 + j;
+      if (!OUT8) {
+        static_cast<int32_t*>(y)[yi] = o32;
+      } else if (RQFAST) {
+        const uint32_t a = (uint32_t)abs(o32);
+        const int32_t r = (int32_t)((a + rq_half) >> rq_shift);
+        static_cast<int8_t*>(y)[yi] = (int8_t)(o32 < 0 ? max(-r, -128) : min(r, 127));
+      } else {
+        long long r = rq_shift > 0 ? rha_shift64((long long)o32 * rq_mult, rq_shift) : (long long)o32 * rq_mult;
+        static_cast<int8_t*>(y)[yi] = (int8_t)(r > 127 ? 127 : (r < -128 ? -128 : r));
+      }
+    }
+  }
+}
+
 cudaError_t launch_output_transform(const Geom& g, const int32_t* m, int n0, int imgs, int32_t rq_mult,
                                     int rq_shift, void* y, cudaStream_t st) {
   const int tiles = imgs * g.tpi;
   dim3 grid((unsigned)((tiles + kOutTiles - 1) / kOutTiles), (unsigned)((g.cout + kOutCoBlock - 1) / kOutCoBlock));
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 30;
   cudaError_t e;
+  if (g.alg == 1) {   // rational F(2x2)
+#define WINO_K42(A, B, C) e = launch_pdl(k_output_transform2<A, B, C>, grid, dim3(256), 0, st, g, m, n0, imgs, rq_mult, rq_shift, y)
+    if (nhwc) {
+      if (!out8) WINO_K42(true, false, false);
+      else if (fast) WINO_K42(true, true, true);
+      else WINO_K42(true, true, false);
+    } else {
+      if (!out8) WINO_K42(false, false, false);
+      else if (fast) WINO_K42(false, true, true);
+      else WINO_K42(false, true, false);
+    }
+#undef WINO_K42
+    return e;
+  }
   if (nhwc && (g.cout & 3) == 0) {   // vectorised variant (NHWC; NCHW keeps one cout per thread)
     dim3 grid4((unsigned)((tiles + kOut4Tiles - 1) / kOut4Tiles), (unsigned)((g.cout + 63) / 64));
 #define WINO_K4V(B, C) e = launch_pdl(k_output_transform4<true, B, C>, grid4, dim3(256), 0, st, g, m, n0, imgs, rq_mult, rq_shift, y)

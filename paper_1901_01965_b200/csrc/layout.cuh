@@ -54,6 +54,10 @@ struct Geom {
   int cin_pad, cout_pad, nblk, ksteps;
   int scaling, target, out_mode;
   int path;                    // WINO_PATH_FUSED (0) or WINO_PATH_STAGED (1)
+  int alg;                     // WINO_ALG_F4X4 (0) or WINO_ALG_F2X2 (1)
+  int tile;                    // output tile edge (4 or 2)
+  int npos;                    // Winograd positions = M'' slots = codes per cout (36 or 16)
+  int planes;                  // staged GEMM planes per (tile, channel) (46 or 16)
   int chunk_imgs;
   long long chunk_tiles_pad;   // multiple of kMBlock
 };
@@ -67,7 +71,7 @@ constexpr int kVBlockBytes = kMBlock * kKStep;   // one (plane-piece, tile block
 __host__ __device__ __forceinline__ long long v_offset(const Geom& g, int plane, int piece, long long t, int k) {
   const long long blk = t / kMBlock;
   const int r = (int)(t % kMBlock);
-  return (((blk * kPlanes + plane) * g.ksteps + (k >> 5)) * 2 + piece) * kVBlockBytes + tiled_offset(r, k & 31, kMBlock);
+  return (((blk * g.planes + plane) * g.ksteps + (k >> 5)) * 2 + piece) * kVBlockBytes + tiled_offset(r, k & 31, kMBlock);
 }
 // Element offset of (chunk tile t, cout co) inside one plane of M.
 __host__ __device__ __forceinline__ long long m_offset(const Geom& g, long long t, int co) {

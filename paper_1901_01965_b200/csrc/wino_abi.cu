@@ -95,6 +95,8 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   if (d.filter_scaling != 0 && d.filter_scaling != 1) return WINO_ERR_INVALID_ARG;
   if (d.workspace_mb < 0) return WINO_ERR_INVALID_ARG;
   if (d.path != WINO_PATH_FUSED && d.path != WINO_PATH_STAGED) return WINO_ERR_INVALID_ARG;
+  if (d.algorithm != WINO_ALG_F4X4 && d.algorithm != WINO_ALG_F2X2) return WINO_ERR_INVALID_ARG;
+  if (d.algorithm == WINO_ALG_F2X2 && d.path != WINO_PATH_STAGED) return WINO_ERR_UNSUPPORTED;
   if (d.n < 1 || d.h < 1 || d.w < 1 || d.c_in < 1 || d.c_out < 1) return WINO_ERR_UNSUPPORTED;
   if (d.pad != 0 && d.pad != 1) return WINO_ERR_UNSUPPORTED;
   if (d.h + 2 * d.pad < 3 || d.w + 2 * d.pad < 3) return WINO_ERR_UNSUPPORTED;
@@ -120,8 +122,12 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.n = d.n; g.h = d.h; g.w = d.w; g.cin = d.c_in; g.cout = d.c_out; g.pad = d.pad; g.layout = d.layout;
   g.ho = d.h + 2 * d.pad - 2;
   g.wo = d.w + 2 * d.pad - 2;
-  g.th = (g.ho + 3) / 4;
-  g.tw = (g.wo + 3) / 4;
+  g.alg = d.algorithm;
+  g.tile = d.algorithm == WINO_ALG_F2X2 ? 2 : 4;
+  g.npos = d.algorithm == WINO_ALG_F2X2 ? 16 : 36;
+  g.planes = d.algorithm == WINO_ALG_F2X2 ? 16 : wino::kPlanes;
+  g.th = (g.ho + g.tile - 1) / g.tile;
+  g.tw = (g.wo + g.tile - 1) / g.tile;
   g.tpi = g.th * g.tw;
   g.cin_pad = (int)round_up(d.c_in, wino::kKStep);
   const int cout16 = (int)round_up(d.c_out, 16);
@@ -134,8 +140,8 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.target = d.filter_target_max;
   g.out_mode = d.out_mode;
   // batch chunk: V (+ M on the staged path) of one chunk within the budget
-  const size_t m_per_tile = d.path == WINO_PATH_STAGED ? wino::kSlots * 4 * (size_t)g.cout_pad : 0;
-  const size_t v_per_tile_ch = d.path == WINO_PATH_STAGED ? 2 * wino::kPlanes : wino::kVPiecesF;
+  const size_t m_per_tile = d.path == WINO_PATH_STAGED ? (size_t)g.npos * 4 * (size_t)g.cout_pad : 0;
+  const size_t v_per_tile_ch = d.path == WINO_PATH_STAGED ? 2 * (size_t)g.planes : wino::kVPiecesF;
   const size_t per_img = (size_t)g.tpi * (v_per_tile_ch * (size_t)g.cin_pad + m_per_tile);
   long long imgs = (long long)(chunk_budget_bytes(d.workspace_mb) / (per_img ? per_img : 1));
   if (imgs < 1) imgs = 1;
@@ -144,10 +150,10 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.chunk_tiles_pad = round_up((long long)imgs * g.tpi, wino::kMBlock);
   p->n_chunks = (int)((d.n + imgs - 1) / imgs);
   p->v_bytes = v_per_tile_ch * g.chunk_tiles_pad * g.cin_pad;
-  p->m_bytes = d.path == WINO_PATH_STAGED ? (size_t)wino::kSlots * g.chunk_tiles_pad * g.cout_pad * 4 : 0;
+  p->m_bytes = d.path == WINO_PATH_STAGED ? (size_t)g.npos * g.chunk_tiles_pad * g.cout_pad * 4 : 0;
   p->ws_bytes = p->v_bytes + p->m_bytes;
   // W': 92 B per (cin, cout) staged (46 planes x 2 pieces); 112 B fused (56 rows x 2 couts-halves, layout.cuh)
-  p->f_bytes = (size_t)(d.path == WINO_PATH_STAGED ? 2 * wino::kPlanes : 2 * wino::kWRowUnitsF) * g.cout_pad * g.cin_pad;
+  p->f_bytes = (size_t)(d.path == WINO_PATH_STAGED ? 2 * g.planes : 2 * wino::kWRowUnitsF) * g.cout_pad * g.cin_pad;
   p->x_bytes = (size_t)d.n * d.h * d.w * d.c_in;
   p->y_bytes = (size_t)d.n * g.ho * g.wo * d.c_out * (d.out_mode == WINO_OUT_INT32 ? 4 : 1);
   *out = p;
@@ -168,7 +174,8 @@ wino_status wino_plan_query(wino_plan_t p, wino_plan_info* info) {
   info->tiles = (long long)p->d.n * p->g.tpi;
   info->cin_pad = p->g.cin_pad; info->cout_pad = p->g.cout_pad;
   info->n_block = p->g.nblk; info->m_block = wino::kMBlock;
-  info->planes = p->g.path == WINO_PATH_FUSED ? 36 : wino::kPlanes;   // fused: 16 real + 10 x (re, im)
+  info->planes = p->g.path == WINO_PATH_FUSED ? 36 : p->g.planes;   // fused: 16 real + 10 x (re, im)
+  info->algorithm = p->g.alg; info->tile = p->g.tile; info->positions = p->g.npos;
   info->pieces = wino::kPieces;
   info->chunk_images = p->g.chunk_imgs; info->n_chunks = p->n_chunks;
   info->chunk_tiles_pad = p->g.chunk_tiles_pad;
@@ -178,13 +185,13 @@ wino_status wino_plan_query(wino_plan_t p, wino_plan_info* info) {
   info->m_offset = p->v_bytes; info->m_bytes = p->m_bytes;
   info->workspace_bytes = p->ws_bytes;
   info->filter_bytes = p->f_bytes;
-  info->codes_bytes = (size_t)p->d.c_out * 36;
+  info->codes_bytes = (size_t)p->d.c_out * p->g.npos;
   info->x_bytes = p->x_bytes; info->y_bytes = p->y_bytes;
   return WINO_OK;
 }
 
 size_t wino_filter_bytes(wino_plan_t p) { return p ? p->f_bytes : 0; }
-size_t wino_codes_bytes(wino_plan_t p) { return p ? (size_t)p->d.c_out * 36 : 0; }
+size_t wino_codes_bytes(wino_plan_t p) { return p ? (size_t)p->d.c_out * p->g.npos : 0; }
 size_t wino_workspace_bytes(wino_plan_t p) { return p ? p->ws_bytes : 0; }
 size_t wino_output_bytes(wino_plan_t p) { return p ? p->y_bytes : 0; }
 
@@ -271,7 +278,7 @@ wino_status wino_conv2d_int8_host(wino_plan_t p, const int8_t* x_host, const voi
 
 wino_status wino_check_codes(wino_plan_t p, const uint8_t* codes, int32_t* bad_flag, void* stream) {
   if (!p || !codes || !bad_flag) return WINO_ERR_INVALID_ARG;
-  return cuda_status(wino::launch_check_codes(codes, p->d.c_out * 36, bad_flag, static_cast<cudaStream_t>(stream)));
+  return cuda_status(wino::launch_check_codes(codes, p->d.c_out * p->g.npos, bad_flag, static_cast<cudaStream_t>(stream)));
 }
 
 wino_status wino_debug_set_trace(void* device_buffer) {

@@ -15,14 +15,14 @@ def tiled_offset(r, k, R_rows):
     return (k >> 5) * R_rows * 32 + (r >> 3) * 256 + ((k >> 4) & 1) * 128 + (r & 7) * 16 + (k & 15)
 
 
-def decode_w_staged(buf: np.ndarray, cout_pad: int, nblk: int, ksteps: int, cin: int):
+def decode_w_staged(buf: np.ndarray, cout_pad: int, nblk: int, ksteps: int, cin: int, nplanes: int = 46):
     """W' image [plane][cout block][K step][W hi rows | W lo rows] (balanced s8 pieces) ->
-    int [46][cout_pad][cin] of hi*256 + lo."""
+    int [nplanes][cout_pad][cin] of hi*256 + lo."""
     co = np.arange(cout_pad)[:, None]; k = np.arange(cin)[None, :]
     nblocks = cout_pad // nblk
     b = buf.astype(np.int64)
-    out = np.zeros((46, cout_pad, cin), np.int64)
-    for pl in range(46):
+    out = np.zeros((nplanes, cout_pad, cin), np.int64)
+    for pl in range(nplanes):
         base = ((pl * nblocks + co // nblk) * ksteps + (k >> 5)) * (2 * nblk * 32)
         hi = b[base + tiled_offset(co % nblk, k & 31, 2 * nblk)]
         lo = b[base + tiled_offset(nblk + co % nblk, k & 31, 2 * nblk)]
@@ -30,14 +30,14 @@ def decode_w_staged(buf: np.ndarray, cout_pad: int, nblk: int, ksteps: int, cin:
     return out
 
 
-def decode_v(buf: np.ndarray, tiles: int, ksteps: int, cin: int):
-    """V image [tile_block][plane][K step][hi, lo][4 KB] (balanced s8 pieces) -> int [46][tiles][cin]."""
+def decode_v(buf: np.ndarray, tiles: int, ksteps: int, cin: int, nplanes: int = 46):
+    """V image [tile_block][plane][K step][hi, lo][4 KB] (balanced s8 pieces) -> int [nplanes][tiles][cin]."""
     t = np.arange(tiles)[:, None]; k = np.arange(cin)[None, :]
     within = tiled_offset(t % 128, k & 31, 128)
     b = buf.astype(np.int64)
-    out = np.zeros((46, tiles, cin), np.int64)
-    for pl in range(46):
-        blk = (((t // 128) * 46 + pl) * ksteps + (k >> 5)) * 2
+    out = np.zeros((nplanes, tiles, cin), np.int64)
+    for pl in range(nplanes):
+        blk = (((t // 128) * nplanes + pl) * ksteps + (k >> 5)) * 2
         out[pl] = b[blk * 4096 + within] * 256 + b[(blk + 1) * 4096 + within]
     return out
 
