@@ -131,8 +131,9 @@ def run_ours(args):
     sh = SH.shard(layer.n, layer.c_out, world, rank) if args.scaling == "strong" else \
         {"mode": "replica", "n0": 0, "n": layer.n, "co0": 0, "co": layer.c_out}
     path = W.WINO_PATH_STAGED if args.path == "staged" else W.WINO_PATH_FUSED
+    alg = W.WINO_ALG_F2X2 if args.alg == "f2" else W.WINO_ALG_F4X4
     conv = W.WinoConv2d(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad, W.WINO_NHWC, layer.scaling,
-                        W.WINO_OUT_INT8, device=local_rank, path=path)
+                        W.WINO_OUT_INT8, device=local_rank, path=path, algorithm=alg)
     info = conv.info
     x_bytes, y_bytes = info.x_bytes, info.y_bytes
     w_bytes = sh["co"] * 9 * layer.c_in
@@ -269,6 +270,8 @@ def run_ours(args):
                 "step": "filter transform + scaling (K1) + conv (" +
                         ("K2, K3F fused GEMM+output per chunk)" if info.path == 0 else "K2,K3,K4 per chunk)"),
                 "path": "fused" if info.path == 0 else "staged",
+                "algorithm": "F(2x2,3x3) rational (SURVEY f1)" if info.algorithm == 1 else
+                             "F(4x4,3x3) complex (Gaussian integers)",
                 "l2": f"inputs/weights/outputs rotated over {n_sets} sets "
                       f"({n_sets * per_set / 2 ** 20:.0f} MiB > 126 MiB L2)",
                 "parallelism": f"dp{world} ({'replicated per-rank batches, weak scaling' if args.scaling == 'weak' else sh['mode'] + '-sharded, strong scaling'}; no data-path collective)",
@@ -484,19 +487,22 @@ def roofline(kern, info, layer, peaks, traffic=None):
     nch = info.n_chunks
     hbm = peaks["hbm_gbs"]
     i8_sus = 2.0 * peaks["bf16_tflops_sustained"]   # int8 dense = 2 x bf16 (nominal ratio 4.5/2.25)
-    x_chunk = chunk_tiles * 16 * layer.c_in        # ~ bytes of x per chunk (16 px per tile)
+    px = info.tile * info.tile                     # output pixels per tile (16 F4x4, 4 F2x2)
+    mults = alg_mults(info)                        # general multiplications per (tile, cin, cout)
+    vpc = 2 * info.planes if info.path == 1 else 72   # V bytes per (tile, channel)
+    x_chunk = chunk_tiles * px * layer.c_in        # ~ bytes of x per chunk
     res = {}
-    # K1: reads w (9 Cin Cout B), writes W' image (92 Cin_pad Cout_pad B) + codes
-    k1_bytes = 9 * layer.c_in * layer.c_out + info.filter_bytes + 36 * layer.c_out
-    # K2: reads x of the chunk, writes V (92 B per tile and channel)
-    k2_bytes = x_chunk + 92 * chunk_tiles * info.cin_pad
-    # K3: 46 general multiplies per (tile, cin, cout) = the paper's count, 2 ops each
-    k3_ops = 2 * 46 * chunk_tiles * layer.c_in * layer.c_out
-    k3_bytes = 92 * chunk_tiles * info.cin_pad + 36 * 4 * chunk_tiles * info.cout_pad + info.filter_bytes
-    # K4: reads 36 int32 per (tile, cout), writes y int8
-    k4_bytes = 36 * 4 * chunk_tiles * layer.c_out + chunk_tiles * 16 * layer.c_out
+    # K1: reads w (9 Cin Cout B), writes the W' image + codes
+    k1_bytes = 9 * layer.c_in * layer.c_out + info.filter_bytes + info.positions * layer.c_out
+    # K2: reads x of the chunk, writes V
+    k2_bytes = x_chunk + vpc * chunk_tiles * info.cin_pad
+    # K3: the method's general multiplies per (tile, cin, cout) (46 = P:228; 16 for F(2x2)), 2 ops each
+    k3_ops = 2 * mults * chunk_tiles * layer.c_in * layer.c_out
+    k3_bytes = vpc * chunk_tiles * info.cin_pad + info.positions * 4 * chunk_tiles * info.cout_pad + info.filter_bytes
+    # K4: reads the M'' int32 per (tile, cout), writes y int8
+    k4_bytes = info.positions * 4 * chunk_tiles * layer.c_out + chunk_tiles * px * layer.c_out
     # K3F (fused): the K3 work; bytes: V once, W' once, y int8 once
-    k3f_bytes = 92 * chunk_tiles * info.cin_pad + info.filter_bytes + chunk_tiles * 16 * layer.c_out
+    k3f_bytes = vpc * chunk_tiles * info.cin_pad + info.filter_bytes + chunk_tiles * px * layer.c_out
     if info.path == 1:
         spec = {
             "k1_filter": ("hbm", k1_bytes, hbm, "GB/s"),
@@ -533,12 +539,19 @@ def roofline(kern, info, layer, peaks, traffic=None):
     return {"dominant": dominant, "all": all_k}
 
 
+def alg_mults(info):
+    """The method's general multiplications per (tile, input channel, output channel): 46 for the
+    complex F(4x4) (the fused path's 4-multiplication form is an implementation choice), 16 for
+    the rational F(2x2)."""
+    return 16 if info.algorithm == 1 else 46
+
+
 def path_roofline(layer, info, peaks, t_step):
-    """t_roof = max(2*46*T*Cin*Cout / P_int8, (x + y + W') / HBM) for one
+    """t_roof = max(2*mults*T*Cin*Cout / P_int8, (x + y + W') / HBM) for one
     rank's step, and the achieved fraction of it."""
     T = info.tiles
-    ops46 = 2 * 46 * T * layer.c_in * layer.c_out
-    byts = info.x_bytes + info.y_bytes + 92 * layer.c_in * layer.c_out + 9 * layer.c_in * layer.c_out
+    ops46 = 2 * alg_mults(info) * T * layer.c_in * layer.c_out
+    byts = info.x_bytes + info.y_bytes + info.filter_bytes + 9 * layer.c_in * layer.c_out
     i8 = 2.0 * peaks["bf16_tflops_sustained"] * 1e12
     t_roof = max(ops46 / i8, byts / (peaks["hbm_gbs"] * 1e9))
     return {"t_roof_us": round(t_roof * 1e6, 3), "t_step_us": round(t_step * 1e6, 3),
@@ -687,6 +700,8 @@ def main():
     ap.add_argument("--streams", type=int, default=3,
                     help="independent batches in flight on separate streams (own filter/workspace buffers)")
     ap.add_argument("--path", default="staged", choices=["fused", "staged"])
+    ap.add_argument("--alg", default="f4", choices=["f4", "f2"],
+                    help="f4: complex F(4x4,3x3) (the north star); f2: rational F(2x2,3x3) (SURVEY f1, staged only)")
     ap.add_argument("--overlap-filter", type=int, default=0,
                     help="1: filter transform on a side stream concurrent with the input transform")
     ap.add_argument("--no-cpu", action="store_true")
