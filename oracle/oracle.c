@@ -111,10 +111,12 @@ void oracle_decode_code(int code, int *n, int *p) {
     *n = code >> 2; *p = (code & 3) + 4;
 }
 
-/* Inverse factor (A8): the largest q in {7,6,5,4} with
- * m = rha(2^(q+p) / n) <= 255.  Returns -1 if none exists.               */
+/* Inverse factor (A8/A27): the largest q in {7,...,3} with
+ * m = rha(2^(q+p) / n) <= 255.  q = 3 is needed only by n/2^p = 8/128, which
+ * int9 weights (uint8 - zero point, f2) reach and int8 weights never do.
+ * Returns -1 if none exists.                                             */
 int oracle_reverse_factor(int n, int p, int *m, int *q) {
-    for (int qq = 7; qq >= 4; qq--) {
+    for (int qq = 7; qq >= 3; qq--) {
         int64_t num = (int64_t)1 << (qq + p);
         /* rha(num / n) for positive num, n: floor((2 num + n) / (2 n)) */
         int64_t mm = (2 * num + n) / (2 * (int64_t)n);
@@ -126,14 +128,16 @@ int oracle_reverse_factor(int n, int p, int *m, int *q) {
 /* ---- layouts --------------------------------------------------------------
  * layout 0 = NCHW (x [N][C][H][W], w [Cout][Cin][3][3], y [N][Cout][Ho][Wo])
  * layout 1 = NHWC (x [N][H][W][C], w [Cout][3][3][Cin], y [N][Ho][Wo][Cout]) */
-static inline int64_t x_at(const int8_t *x, int layout, int N, int C, int H, int W,
+/* Element accessors on int16 tensors: the int8 entry points below widen their
+ * inputs, the uint8 ones (f2) store x - zx and w - zw (int9).        */
+static inline int64_t x_at(const int16_t *x, int layout, int N, int C, int H, int W,
                            int n, int c, int h, int w) {
     (void)N;
     if (h < 0 || h >= H || w < 0 || w >= W) return 0;   /* zero padding */
     if (layout == 0) return x[(((int64_t)n * C + c) * H + h) * W + w];
     return x[(((int64_t)n * H + h) * W + w) * C + c];
 }
-static inline int64_t w_at(const int8_t *w, int layout, int Cout, int Cin,
+static inline int64_t w_at(const int16_t *w, int layout, int Cout, int Cin,
                            int co, int ci, int u, int v) {
     (void)Cout;
     if (layout == 0) return w[(((int64_t)co * Cin + ci) * 3 + u) * 3 + v];
@@ -145,8 +149,8 @@ static inline int64_t y_index(int layout, int Cout, int Ho, int Wo, int n, int c
 }
 
 /* O1: direct correlation, int64 accumulation (A1, A12). */
-void oracle_direct_conv(const int8_t *x, const int8_t *w, int N, int H, int W,
-                        int Cin, int Cout, int pad, int layout, int64_t *out) {
+void oracle_direct_conv16(const int16_t *x, const int16_t *w, int N, int H, int W,
+                          int Cin, int Cout, int pad, int layout, int64_t *out) {
     int Ho = H + 2 * pad - 2, Wo = W + 2 * pad - 2;
 #pragma omp parallel for collapse(2) schedule(dynamic)
     for (int n = 0; n < N; n++)
@@ -246,8 +250,8 @@ static inline int64_t max_abs_component(gint v) {
  *   codes_out [Cout][36]          6-bit codes, 0 = unscaled
  * scaling == 0: every code is 0 and W' = W.   Returns 0, or -1 if a
  * factor falls outside p in [4,7] (cannot happen for int8 weights).       */
-int oracle_filter_transform(const int8_t *w, int Cout, int Cin, int layout, int scaling,
-                            int target, int64_t *W_out, int64_t *Wp_out, uint8_t *codes_out) {
+int oracle_filter_transform16(const int16_t *w, int Cout, int Cin, int layout, int scaling,
+                              int target, int64_t *W_out, int64_t *Wp_out, uint8_t *codes_out) {
     int status = 0;
     gint *Wt = (gint *)malloc(sizeof(gint) * 36 * (size_t)(Cin > 0 ? Cin : 1));
     for (int co = 0; co < Cout; co++) {
@@ -291,8 +295,8 @@ int oracle_filter_transform(const int8_t *w, int Cout, int Cin, int layout, int 
 
 /* Input transform of every tile (O1, O2).  D_out [T][Cin][36][2], T = N*th*tw,
  * tile t = (n*th + ty)*tw + tx with patch origin (4ty - pad, 4tx - pad).   */
-void oracle_input_transform(const int8_t *x, int N, int H, int W, int Cin, int pad,
-                            int layout, int64_t *D_out) {
+void oracle_input_transform16(const int16_t *x, int N, int H, int W, int Cin, int pad,
+                              int layout, int64_t *D_out) {
     int Ho = H + 2 * pad - 2, Wo = W + 2 * pad - 2;
     int th = (Ho + 3) / 4, tw = (Wo + 3) / 4;
 #pragma omp parallel for collapse(2) schedule(static)
@@ -323,9 +327,9 @@ void oracle_input_transform(const int8_t *x, int N, int H, int W, int Cin, int p
  * Returns 0; -1 on a scale-factor range error; -2 if Im Y != 0 anywhere;
  * -3 if scaling is off and 16 does not divide Y; -4 if |M''| or |Y| would
  * leave int32 (the GPU stores int32, A23).                     */
-int oracle_wino_conv(const int8_t *x, const int8_t *w, int N, int H, int W, int Cin, int Cout,
-                     int pad, int layout, int scaling, int target, int32_t M0, int S,
-                     int32_t *out32, int8_t *y8, int64_t *M_out, int64_t *Mpp_out) {
+int oracle_wino_conv16(const int16_t *x, const int16_t *w, int N, int H, int W, int Cin, int Cout,
+                       int pad, int layout, int scaling, int target, int32_t M0, int S,
+                       int32_t *out32, int8_t *y8, int64_t *M_out, int64_t *Mpp_out) {
     int Ho = H + 2 * pad - 2, Wo = W + 2 * pad - 2;
     int th = (Ho + 3) / 4, tw = (Wo + 3) / 4;
     size_t T = (size_t)N * th * tw;
@@ -333,8 +337,8 @@ int oracle_wino_conv(const int8_t *x, const int8_t *w, int N, int H, int W, int 
     int64_t *Wp = (int64_t *)malloc(sizeof(int64_t) * 72 * (size_t)Cout * (Cin > 0 ? Cin : 1));
     uint8_t *codes = (uint8_t *)malloc((size_t)Cout * 36);
     int64_t *D = (int64_t *)malloc(sizeof(int64_t) * 72 * T * (Cin > 0 ? Cin : 1));
-    if (oracle_filter_transform(w, Cout, Cin, layout, scaling, target, NULL, Wp, codes) != 0) status = -1;
-    oracle_input_transform(x, N, H, W, Cin, pad, layout, D);
+    if (oracle_filter_transform16(w, Cout, Cin, layout, scaling, target, NULL, Wp, codes) != 0) status = -1;
+    oracle_input_transform16(x, N, H, W, Cin, pad, layout, D);
     int bad_im = 0, bad_div = 0, bad_range = 0;
 #pragma omp parallel for collapse(2) schedule(dynamic) reduction(| : bad_im, bad_div, bad_range)
     for (long long t = 0; t < (long long)T; t++)
@@ -469,8 +473,8 @@ void oracle_output_tile2_64(const int64_t *M16, int64_t *Y4) { oracle_output_til
 
 /* Offline F(2x2) filter path (P:317-330 with 16 positions):
  *   W_out [Cout][Cin][16] (may be NULL), Wp_out [Cout][Cin][16], codes_out [Cout][16]. */
-int oracle_filter_transform2(const int8_t *w, int Cout, int Cin, int layout, int scaling, int target,
-                             int64_t *W_out, int64_t *Wp_out, uint8_t *codes_out) {
+int oracle_filter_transform2_16(const int16_t *w, int Cout, int Cin, int layout, int scaling, int target,
+                                int64_t *W_out, int64_t *Wp_out, uint8_t *codes_out) {
     int status = 0;
     int64_t *Wt = (int64_t *)malloc(sizeof(int64_t) * 16 * (size_t)(Cin > 0 ? Cin : 1));
     for (int co = 0; co < Cout; co++) {
@@ -505,8 +509,8 @@ int oracle_filter_transform2(const int8_t *w, int Cout, int Cin, int layout, int
 
 /* F(2x2) input transform of every tile: D_out [T][Cin][16], T = N*th*tw with
  * th = ceil(Ho/2), patch origin (2ty - pad, 2tx - pad).                    */
-void oracle_input_transform2(const int8_t *x, int N, int H, int W, int Cin, int pad, int layout,
-                             int64_t *D_out) {
+void oracle_input_transform2_16(const int16_t *x, int N, int H, int W, int Cin, int pad, int layout,
+                                int64_t *D_out) {
     int Ho = H + 2 * pad - 2, Wo = W + 2 * pad - 2;
     int th = (Ho + 1) / 2, tw = (Wo + 1) / 2;
 #pragma omp parallel for collapse(2) schedule(static)
@@ -528,9 +532,9 @@ void oracle_input_transform2(const int8_t *x, int N, int H, int W, int Cin, int 
  * out32 = rha(Y / 4).  M_out / Mpp_out [T][Cout][16] (may be NULL).
  * Returns 0; -1 scale-factor range; -3 unscaled and 4 does not divide Y;
  * -4 int32 range.                                                          */
-int oracle_wino2_conv(const int8_t *x, const int8_t *w, int N, int H, int W, int Cin, int Cout,
-                      int pad, int layout, int scaling, int target, int32_t M0, int S,
-                      int32_t *out32, int8_t *y8, int64_t *M_out, int64_t *Mpp_out) {
+int oracle_wino2_conv16(const int16_t *x, const int16_t *w, int N, int H, int W, int Cin, int Cout,
+                        int pad, int layout, int scaling, int target, int32_t M0, int S,
+                        int32_t *out32, int8_t *y8, int64_t *M_out, int64_t *Mpp_out) {
     int Ho = H + 2 * pad - 2, Wo = W + 2 * pad - 2;
     int th = (Ho + 1) / 2, tw = (Wo + 1) / 2;
     size_t T = (size_t)N * th * tw;
@@ -538,8 +542,8 @@ int oracle_wino2_conv(const int8_t *x, const int8_t *w, int N, int H, int W, int
     int64_t *Wp = (int64_t *)malloc(sizeof(int64_t) * 16 * (size_t)Cout * (Cin > 0 ? Cin : 1));
     uint8_t *codes = (uint8_t *)malloc((size_t)Cout * 16);
     int64_t *D = (int64_t *)malloc(sizeof(int64_t) * 16 * T * (Cin > 0 ? Cin : 1));
-    if (oracle_filter_transform2(w, Cout, Cin, layout, scaling, target, NULL, Wp, codes) != 0) status = -1;
-    oracle_input_transform2(x, N, H, W, Cin, pad, layout, D);
+    if (oracle_filter_transform2_16(w, Cout, Cin, layout, scaling, target, NULL, Wp, codes) != 0) status = -1;
+    oracle_input_transform2_16(x, N, H, W, Cin, pad, layout, D);
     int bad_div = 0, bad_range = 0;
 #pragma omp parallel for collapse(2) schedule(dynamic) reduction(| : bad_div, bad_range)
     for (long long t = 0; t < (long long)T; t++)
@@ -644,3 +648,102 @@ int oracle_output_tile64(const int64_t *M72, int64_t *Y16) {
     for (int i = 0; i < 16; i++) Y16[i] = Y[i / 4][i % 4];
     return r;
 }
+
+/* ---- entry points on int8 tensors (widened to int16) and on uint8 tensors with
+ * zero points (f2: the paper's affine uint8 model: values x - zx, w - zw
+ * in [-255, 255]; padding is the real value 0, i.e. x - zx = 0).           */
+static int16_t *widen8(const int8_t *a, size_t n) {
+    int16_t *r = (int16_t *)malloc(sizeof(int16_t) * (n ? n : 1));
+    for (size_t i = 0; i < n; i++) r[i] = a[i];
+    return r;
+}
+static int16_t *widen_u8(const uint8_t *a, size_t n, int z) {
+    int16_t *r = (int16_t *)malloc(sizeof(int16_t) * (n ? n : 1));
+    for (size_t i = 0; i < n; i++) r[i] = (int16_t)((int)a[i] - z);
+    return r;
+}
+#define XN ((size_t)N * H * W * Cin)
+#define WN ((size_t)Cout * Cin * 9)
+
+void oracle_direct_conv(const int8_t *x, const int8_t *w, int N, int H, int W,
+                        int Cin, int Cout, int pad, int layout, int64_t *out) {
+    int16_t *x16 = widen8(x, XN), *w16 = widen8(w, WN);
+    oracle_direct_conv16(x16, w16, N, H, W, Cin, Cout, pad, layout, out);
+    free(x16); free(w16);
+}
+int oracle_filter_transform(const int8_t *w, int Cout, int Cin, int layout, int scaling,
+                            int target, int64_t *W_out, int64_t *Wp_out, uint8_t *codes_out) {
+    int16_t *w16 = widen8(w, WN);
+    int r = oracle_filter_transform16(w16, Cout, Cin, layout, scaling, target, W_out, Wp_out, codes_out);
+    free(w16);
+    return r;
+}
+void oracle_input_transform(const int8_t *x, int N, int H, int W, int Cin, int pad,
+                            int layout, int64_t *D_out) {
+    int16_t *x16 = widen8(x, XN);
+    oracle_input_transform16(x16, N, H, W, Cin, pad, layout, D_out);
+    free(x16);
+}
+int oracle_wino_conv(const int8_t *x, const int8_t *w, int N, int H, int W, int Cin, int Cout,
+                     int pad, int layout, int scaling, int target, int32_t M0, int S,
+                     int32_t *out32, int8_t *y8, int64_t *M_out, int64_t *Mpp_out) {
+    int16_t *x16 = widen8(x, XN), *w16 = widen8(w, WN);
+    int r = oracle_wino_conv16(x16, w16, N, H, W, Cin, Cout, pad, layout, scaling, target, M0, S,
+                               out32, y8, M_out, Mpp_out);
+    free(x16); free(w16);
+    return r;
+}
+int oracle_filter_transform2(const int8_t *w, int Cout, int Cin, int layout, int scaling, int target,
+                             int64_t *W_out, int64_t *Wp_out, uint8_t *codes_out) {
+    int16_t *w16 = widen8(w, WN);
+    int r = oracle_filter_transform2_16(w16, Cout, Cin, layout, scaling, target, W_out, Wp_out, codes_out);
+    free(w16);
+    return r;
+}
+void oracle_input_transform2(const int8_t *x, int N, int H, int W, int Cin, int pad, int layout,
+                             int64_t *D_out) {
+    int16_t *x16 = widen8(x, XN);
+    oracle_input_transform2_16(x16, N, H, W, Cin, pad, layout, D_out);
+    free(x16);
+}
+int oracle_wino2_conv(const int8_t *x, const int8_t *w, int N, int H, int W, int Cin, int Cout,
+                      int pad, int layout, int scaling, int target, int32_t M0, int S,
+                      int32_t *out32, int8_t *y8, int64_t *M_out, int64_t *Mpp_out) {
+    int16_t *x16 = widen8(x, XN), *w16 = widen8(w, WN);
+    int r = oracle_wino2_conv16(x16, w16, N, H, W, Cin, Cout, pad, layout, scaling, target, M0, S,
+                                out32, y8, M_out, Mpp_out);
+    free(x16); free(w16);
+    return r;
+}
+/* uint8 + zero points (f2) */
+void oracle_direct_conv_u8(const uint8_t *x, const uint8_t *w, int zx, int zw, int N, int H, int W,
+                           int Cin, int Cout, int pad, int layout, int64_t *out) {
+    int16_t *x16 = widen_u8(x, XN, zx), *w16 = widen_u8(w, WN, zw);
+    oracle_direct_conv16(x16, w16, N, H, W, Cin, Cout, pad, layout, out);
+    free(x16); free(w16);
+}
+int oracle_filter_transform_u8(const uint8_t *w, int zw, int Cout, int Cin, int layout, int scaling, int target,
+                               int64_t *W_out, int64_t *Wp_out, uint8_t *codes_out) {
+    int16_t *w16 = widen_u8(w, WN, zw);
+    int r = oracle_filter_transform16(w16, Cout, Cin, layout, scaling, target, W_out, Wp_out, codes_out);
+    free(w16);
+    return r;
+}
+void oracle_input_transform_u8(const uint8_t *x, int zx, int N, int H, int W, int Cin, int pad, int layout,
+                               int64_t *D_out) {
+    int16_t *x16 = widen_u8(x, XN, zx);
+    oracle_input_transform16(x16, N, H, W, Cin, pad, layout, D_out);
+    free(x16);
+}
+int oracle_wino_conv_u8(const uint8_t *x, const uint8_t *w, int zx, int zw, int N, int H, int W, int Cin,
+                        int Cout, int pad, int layout, int scaling, int target, int32_t M0, int S,
+                        int32_t *out32, int8_t *y8, int64_t *M_out, int64_t *Mpp_out) {
+    int16_t *x16 = widen_u8(x, XN, zx), *w16 = widen_u8(w, WN, zw);
+    int r = oracle_wino_conv16(x16, w16, N, H, W, Cin, Cout, pad, layout, scaling, target, M0, S,
+                               out32, y8, M_out, Mpp_out);
+    free(x16); free(w16);
+    return r;
+}
+#undef XN
+#undef WN
+

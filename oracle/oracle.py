@@ -66,6 +66,15 @@ def lib():
         L.oracle_wino2_conv.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, i32, i32,
                                         ctypes.c_int32, i32, P, P, P, P]
         L.oracle_wino2_conv.restype = i32
+        L.oracle_direct_conv_u8.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, i32, i32, P]
+        L.oracle_direct_conv_u8.restype = None
+        L.oracle_filter_transform_u8.argtypes = [P, i32, i32, i32, i32, i32, i32, P, P, P]
+        L.oracle_filter_transform_u8.restype = i32
+        L.oracle_input_transform_u8.argtypes = [P, i32, i32, i32, i32, i32, i32, i32, P]
+        L.oracle_input_transform_u8.restype = None
+        L.oracle_wino_conv_u8.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32,
+                                          ctypes.c_int32, i32, P, P, P, P]
+        L.oracle_wino_conv_u8.restype = i32
         _lib = L
     return _lib
 
@@ -104,7 +113,7 @@ def decode_code(code: int):
 
 
 def reverse_factor(n: int, p: int):
-    """(m, q) per P:366 read as DESIGN.md A8."""
+    """(m, q) per P:366 read as DESIGN.md A8 / A27 (q in [3, 7]; q = 3 only for 8/128)."""
     m, q = ctypes.c_int(), ctypes.c_int()
     if lib().oracle_reverse_factor(int(n), int(p), ctypes.byref(m), ctypes.byref(q)) != 0:
         raise ValueError("no 8-bit inverse")
@@ -322,6 +331,71 @@ def wino2_conv(x, w, pad=1, layout=NHWC, scaling=True, target=255, M0=1, S=0,
     st = lib().oracle_wino2_conv(_p(x), _p(w), N, H, W, Cin, Cout, pad, layout, int(bool(scaling)), target,
                                  int(M0), int(S), _p(out32), _p(y8) if y8 is not None else None,
                                  _p(M) if M is not None else None, _p(Mpp) if Mpp is not None else None)
+    if st != 0:
+        raise ValueError(f"oracle invariant violated (status {st})")
+    return WinoResult(out32, y8, M, Mpp, st)
+
+
+# ---------------------------------------------------------------- uint8 + zero points
+def _dims(x, w, layout):
+    if layout == NCHW:
+        N, Cin, H, W = x.shape
+    else:
+        N, H, W, Cin = x.shape
+    return N, H, W, Cin, w.shape[0]
+
+
+def direct_conv_u8(x, w, zx, zw, pad=1, layout=NHWC) -> np.ndarray:
+    """Exact correlation of (x - zx) with (w - zw) (int64), uint8 tensors (O1 on int9 values)."""
+    x = _c(x, np.uint8); w = _c(w, np.uint8)
+    N, H, W, Cin, Cout = _dims(x, w, layout)
+    Ho, Wo = out_hw(H, W, pad)
+    out = np.zeros((N, Cout, Ho, Wo) if layout == NCHW else (N, Ho, Wo, Cout), np.int64)
+    lib().oracle_direct_conv_u8(_p(x), _p(w), int(zx), int(zw), N, H, W, Cin, Cout, pad, layout, _p(out))
+    return out
+
+
+def filter_transform_u8(w, zw, layout=NHWC, scaling=True, target=255):
+    w = _c(w, np.uint8)
+    Cout = w.shape[0]
+    Cin = w.shape[1] if layout == NCHW else w.shape[3]
+    W = np.zeros((Cout, Cin, 36, 2), np.int64); Wp = np.zeros((Cout, Cin, 36, 2), np.int64)
+    codes = np.zeros((Cout, 36), np.uint8)
+    if lib().oracle_filter_transform_u8(_p(w), int(zw), Cout, Cin, layout, int(bool(scaling)), target,
+                                        _p(W), _p(Wp), _p(codes)) != 0:
+        raise ValueError("scale factor out of range")
+    return W, Wp, codes
+
+
+def input_transform_u8(x, zx, pad=1, layout=NHWC) -> np.ndarray:
+    x = _c(x, np.uint8)
+    if layout == NCHW:
+        N, Cin, H, W = x.shape
+    else:
+        N, H, W, Cin = x.shape
+    th, tw = tiles(H, W, pad)
+    D = np.zeros((N * th * tw, Cin, 36, 2), np.int64)
+    lib().oracle_input_transform_u8(_p(x), int(zx), N, H, W, Cin, pad, layout, _p(D))
+    return D
+
+
+def wino_conv_u8(x, w, zx, zw, pad=1, layout=NHWC, scaling=True, target=255, M0=1, S=0,
+                 want_y8=True, want_M=False) -> WinoResult:
+    """The complex F(4x4) pipeline on uint8 tensors with zero points (int9 values)."""
+    x = _c(x, np.uint8); w = _c(w, np.uint8)
+    N, H, W, Cin, Cout = _dims(x, w, layout)
+    Ho, Wo = out_hw(H, W, pad)
+    th, tw = tiles(H, W, pad)
+    T = N * th * tw
+    shape = (N, Cout, Ho, Wo) if layout == NCHW else (N, Ho, Wo, Cout)
+    out32 = np.zeros(shape, np.int32)
+    y8 = np.zeros(shape, np.int8) if want_y8 else None
+    M = np.zeros((T, Cout, 36, 2), np.int64) if want_M else None
+    Mpp = np.zeros((T, Cout, 36, 2), np.int64) if want_M else None
+    st = lib().oracle_wino_conv_u8(_p(x), _p(w), int(zx), int(zw), N, H, W, Cin, Cout, pad, layout,
+                                   int(bool(scaling)), target, int(M0), int(S), _p(out32),
+                                   _p(y8) if y8 is not None else None, _p(M) if M is not None else None,
+                                   _p(Mpp) if Mpp is not None else None)
     if st != 0:
         raise ValueError(f"oracle invariant violated (status {st})")
     return WinoResult(out32, y8, M, Mpp, st)
