@@ -132,8 +132,13 @@ def run_ours(args):
         {"mode": "replica", "n0": 0, "n": layer.n, "co0": 0, "co": layer.c_out}
     path = W.WINO_PATH_STAGED if args.path == "staged" else W.WINO_PATH_FUSED
     alg = W.WINO_ALG_F2X2 if args.alg == "f2" else W.WINO_ALG_F4X4
+    # --input u8: the same synthetic values as uint8 tensors with zero points 128
+    u8 = args.input == "u8"
+    zp = 128 if u8 else 0
     conv = W.WinoConv2d(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad, W.WINO_NHWC, layer.scaling,
-                        W.WINO_OUT_INT8, device=local_rank, path=path, algorithm=alg)
+                        W.WINO_OUT_INT8, device=local_rank, path=path, algorithm=alg,
+                        input_type=W.WINO_IN_UINT8 if u8 else W.WINO_IN_INT8, x_zero_point=zp, w_zero_point=zp)
+    to_in = (lambda a: (a.astype(np.int16) + 128).astype(np.uint8)) if u8 else (lambda a: a)
     info = conv.info
     x_bytes, y_bytes = info.x_bytes, info.y_bytes
     w_bytes = sh["co"] * 9 * layer.c_in
@@ -148,7 +153,8 @@ def run_ours(args):
             w = np.ascontiguousarray(w[sh["co0"]: sh["co0"] + sh["co"]])
         else:
             x, w = synth.config_inputs(args.config, rank=rank * 1000 + i)
-        xs.append(torch.from_numpy(np.ascontiguousarray(x)).to(dev)); ws.append(torch.from_numpy(w).to(dev))
+        xs.append(torch.from_numpy(np.ascontiguousarray(to_in(x))).to(dev))
+        ws.append(torch.from_numpy(np.ascontiguousarray(to_in(w))).to(dev))
         ys.append(torch.empty(conv.y_shape, dtype=torch.int8, device=dev))
     stream = torch.cuda.Stream(device=dev)
     sp = stream.cuda_stream
@@ -270,6 +276,7 @@ def run_ours(args):
                 "step": "filter transform + scaling (K1) + conv (" +
                         ("K2, K3F fused GEMM+output per chunk)" if info.path == 0 else "K2,K3,K4 per chunk)"),
                 "path": "fused" if info.path == 0 else "staged",
+                "input": "uint8, zero points 128 (SURVEY f2)" if u8 else "int8",
                 "algorithm": "F(2x2,3x3) rational (SURVEY f1)" if info.algorithm == 1 else
                              "F(4x4,3x3) complex (Gaussian integers)",
                 "l2": f"inputs/weights/outputs rotated over {n_sets} sets "
@@ -700,6 +707,8 @@ def main():
     ap.add_argument("--streams", type=int, default=3,
                     help="independent batches in flight on separate streams (own filter/workspace buffers)")
     ap.add_argument("--path", default="staged", choices=["fused", "staged"])
+    ap.add_argument("--input", default="i8", choices=["i8", "u8"],
+                    help="u8: uint8 tensors with zero points (SURVEY f2, staged F(4x4), c_in <= 224)")
     ap.add_argument("--alg", default="f4", choices=["f4", "f2"],
                     help="f4: complex F(4x4,3x3) (the north star); f2: rational F(2x2,3x3) (SURVEY f1, staged only)")
     ap.add_argument("--overlap-filter", type=int, default=0,

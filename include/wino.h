@@ -84,6 +84,13 @@ typedef struct {
                              WINO_ALG_F2X2 (1): rational F(2x2,3x3), G' = 2G,
                              the configuration the paper evaluates; staged path only.
                              Codes are [c_out][36] (F4x4) or [c_out][16] (F2x2).      */
+    int input_type;       /* WINO_IN_INT8 (0, default) or WINO_IN_UINT8 (1): x and w are
+                             uint8 with the zero points below (the paper's affine model,
+                             P:251); the convolution is that of the int9 values x - zx,
+                             w - zw, padding = real 0 (A28).  uint8 needs the
+                             staged path, F4x4 and c_in <= 224 (int32 exactness).     */
+    int x_zero_point;     /* [0, 255], uint8 input only                                  */
+    int w_zero_point;     /* [0, 255], uint8 input only                                  */
 } wino_conv_desc;
 
 /* Hot-path kernel structure (wino_conv_desc.path). */
@@ -91,6 +98,9 @@ enum { WINO_PATH_FUSED = 0, WINO_PATH_STAGED = 1 };
 
 /* Winograd algorithm (wino_conv_desc.algorithm). */
 enum { WINO_ALG_F4X4 = 0, WINO_ALG_F2X2 = 1 };
+
+/* Element type of x and w (wino_conv_desc.input_type). */
+enum { WINO_IN_INT8 = 0, WINO_IN_UINT8 = 1 };
 
 typedef struct wino_plan_s *wino_plan_t;
 

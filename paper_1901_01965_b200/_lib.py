@@ -16,6 +16,7 @@ WINO_NCHW, WINO_NHWC = 0, 1
 WINO_OUT_INT8, WINO_OUT_INT32 = 0, 1
 WINO_PATH_FUSED, WINO_PATH_STAGED = 0, 1
 WINO_ALG_F4X4, WINO_ALG_F2X2 = 0, 1
+WINO_IN_INT8, WINO_IN_UINT8 = 0, 1
 
 # every symbol include/wino.h declares
 EXPORTS = ("wino_status_string", "wino_last_cuda_error", "wino_plan", "wino_plan_destroy", "wino_plan_query", "wino_filter_bytes",
@@ -28,7 +29,8 @@ class wino_conv_desc(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("h", ctypes.c_int), ("w", ctypes.c_int), ("c_in", ctypes.c_int),
                 ("c_out", ctypes.c_int), ("pad", ctypes.c_int), ("layout", ctypes.c_int),
                 ("filter_scaling", ctypes.c_int), ("filter_target_max", ctypes.c_int), ("out_mode", ctypes.c_int),
-                ("workspace_mb", ctypes.c_int), ("path", ctypes.c_int), ("algorithm", ctypes.c_int)]
+                ("workspace_mb", ctypes.c_int), ("path", ctypes.c_int), ("algorithm", ctypes.c_int),
+                ("input_type", ctypes.c_int), ("x_zero_point", ctypes.c_int), ("w_zero_point", ctypes.c_int)]
 
 
 class wino_plan_info(ctypes.Structure):

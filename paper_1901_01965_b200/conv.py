@@ -16,12 +16,13 @@ class WinoConv2d:
 
     def __init__(self, n, h, w, c_in, c_out, pad=1, layout=L.WINO_NHWC, filter_scaling=True,
                  out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0, path=L.WINO_PATH_STAGED,
-                 algorithm=L.WINO_ALG_F4X4):
+                 algorithm=L.WINO_ALG_F4X4, input_type=L.WINO_IN_INT8, x_zero_point=0, w_zero_point=0):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device)
         self.desc = L.wino_conv_desc(n, h, w, c_in, c_out, pad, layout, int(bool(filter_scaling)), 255, out_mode,
-                                     workspace_mb, path, algorithm)
+                                     workspace_mb, path, algorithm, input_type, x_zero_point, w_zero_point)
+        self.in_dtype = torch.uint8 if input_type == L.WINO_IN_UINT8 else torch.int8
         self.plan = L.wino_plan(self.desc, device)
         self.info = L.wino_plan_query(self.plan)
         self.layout, self.out_mode = layout, out_mode
@@ -52,13 +53,13 @@ class WinoConv2d:
         return (stream or torch.cuda.current_stream()).cuda_stream
 
     def transform_filter(self, w: torch.Tensor, stream=None):
-        assert w.dtype == torch.int8 and w.is_cuda and tuple(w.shape) == self.w_shape and w.is_contiguous()
+        assert w.dtype == self.in_dtype and w.is_cuda and tuple(w.shape) == self.w_shape and w.is_contiguous()
         L.wino_transform_filter(self.plan, w.data_ptr(), self.w_wino.data_ptr(), self.codes.data_ptr(),
                                 self._stream(stream))
         return self.codes
 
     def __call__(self, x: torch.Tensor, requant_mult=1, requant_shift=0, y=None, codes=None, stream=None):
-        assert x.dtype == torch.int8 and x.is_cuda and tuple(x.shape) == self.x_shape and x.is_contiguous()
+        assert x.dtype == self.in_dtype and x.is_cuda and tuple(x.shape) == self.x_shape and x.is_contiguous()
         if y is None:
             y = torch.empty(self.y_shape, dtype=self.y_dtype, device=self.device)
         c = self.codes if codes is None else codes

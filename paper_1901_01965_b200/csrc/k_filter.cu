@@ -77,13 +77,16 @@ __device__ __forceinline__ void scaled_planes(const int t[36], const int* sn, co
   }
 }
 
+// One 3x3 filter as int values: int8 w, or uint8 w minus its zero point (int9, f2, A28).
 __device__ __forceinline__ void load_filter(const Geom& g, const int8_t* __restrict__ w, int co, int ci, int gg[3][3]) {
 #pragma unroll
   for (int u = 0; u < 3; u++)
 #pragma unroll
-    for (int v = 0; v < 3; v++)
-      gg[u][v] = g.layout == 0 ? w[((long long)co * g.cin + ci) * 9 + u * 3 + v]
-                               : w[((long long)co * 9 + u * 3 + v) * g.cin + ci];
+    for (int v = 0; v < 3; v++) {
+      const int8_t raw = g.layout == 0 ? w[((long long)co * g.cin + ci) * 9 + u * 3 + v]
+                                       : w[((long long)co * 9 + u * 3 + v) * g.cin + ci];
+      gg[u][v] = g.in_u8 ? (int)(uint8_t)raw - g.zw : (int)raw;
+    }
 }
 
 // One CTA per output channel (the unit the paper scales: "applied to

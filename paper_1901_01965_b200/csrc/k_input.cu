@@ -37,6 +37,14 @@ __device__ __forceinline__ int sbyte(uint32_t w, int b) {
   return (int)r;
 }
 
+// Activation value of channel byte `ch` of a gathered pixel pair: int8, or uint8 minus the zero
+// point (int9, f2).
+template <bool U8>
+__device__ __forceinline__ int dval(const Geom& g, uint32_t w, int ch) {
+  if constexpr (U8) return (int)((w >> (8 * ch)) & 0xffu) - g.zx;
+  else return sbyte(w, ch);
+}
+
 // The 46 operand-plane values of one channel from d' rows (e0, e1, e2, e5 real;
 // row 3 = ra + i rb), in plane order (layout.cuh).
 struct Rows {
@@ -68,11 +76,15 @@ __device__ __forceinline__ void store_plane(int8_t* base, long long pstride, int
 
 // Gather the zero-padded 6x6 patch of chunk tile t for channels c, c+1 and form
 // d' = B^T d column by column for both channels.
+template <bool U8>
 __device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restrict__ x, int n0, int imgs, int t, int c,
                                            Rows (&r)[2]) {
   const int tiles = imgs * g.tpi;
 
-  // ---- gather the zero-padded 6x6 patch at origin (4ty - pad, 4tx - pad): 2 channels per pixel
+  // ---- gather the zero-padded 6x6 patch at origin (4ty - pad, 4tx - pad): 2 channels per pixel.
+  // uint8 input (f2): out-of-map pixels and channels past Cin read the zero point, so that
+  // d = u8 - zx = 0 there (padding is the real value 0, A28).
+  const uint32_t zpair = U8 ? (uint32_t)(g.zx | (g.zx << 8)) : 0u;
   uint32_t w[36];
   {
     int img = 0, iy0 = -1000000, ix0 = -1000000;   // padding tiles read nothing
@@ -95,7 +107,7 @@ __device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restri
         const bool vy = iy0 + a >= 0 && iy0 + a < g.h;
         const uint16_t* rp = reinterpret_cast<const uint16_t*>(p0 + a * rstride);
 #pragma unroll
-        for (int b = 0; b < 6; b++) w[a * 6 + b] = (vy && vx[b]) ? (uint32_t)__ldg(rp + (b * g.cin >> 1)) : 0u;
+        for (int b = 0; b < 6; b++) w[a * 6 + b] = (vy && vx[b]) ? (uint32_t)__ldg(rp + (b * g.cin >> 1)) : zpair;
       }
     } else {
       // generic path (NCHW or odd Cin): byte loads
@@ -105,12 +117,12 @@ __device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restri
 #pragma unroll
         for (int b = 0; b < 6; b++) {
           const int iy = iy0 + a, ix = ix0 + b;
-          uint32_t v = 0;
+          uint32_t v = zpair;
           if (vx[b] && iy >= 0 && iy < g.h) {
             const long long i0 = g.layout == 1 ? (((long long)img * g.h + iy) * g.w + ix) * g.cin + c
                                                : (((long long)img * g.cin + c) * g.h + iy) * g.w + ix;
             v = (uint8_t)__ldg(x + i0);
-            if (c + 1 < g.cin) v |= (uint32_t)(uint8_t)__ldg(x + i0 + cstep) << 8;
+            v |= (c + 1 < g.cin) ? (uint32_t)(uint8_t)__ldg(x + i0 + cstep) << 8 : (zpair & 0xff00u);
           }
           w[a * 6 + b] = v;
         }
@@ -122,8 +134,8 @@ __device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restri
   for (int j = 0; j < 6; j++) {
 #pragma unroll
     for (int ch = 0; ch < 2; ch++) {
-      const int d0 = sbyte(w[0 * 6 + j], ch), d1 = sbyte(w[1 * 6 + j], ch), d2 = sbyte(w[2 * 6 + j], ch);
-      const int d3 = sbyte(w[3 * 6 + j], ch), d4 = sbyte(w[4 * 6 + j], ch), d5 = sbyte(w[5 * 6 + j], ch);
+      const int d0 = dval<U8>(g, w[0 * 6 + j], ch), d1 = dval<U8>(g, w[1 * 6 + j], ch), d2 = dval<U8>(g, w[2 * 6 + j], ch);
+      const int d3 = dval<U8>(g, w[3 * 6 + j], ch), d4 = dval<U8>(g, w[4 * 6 + j], ch), d5 = dval<U8>(g, w[5 * 6 + j], ch);
       const int s24 = d2 + d4, s13 = d1 + d3;
       r[ch].e0[j] = d0 - d4;
       r[ch].e1[j] = s13 + s24;
@@ -135,6 +147,7 @@ __device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restri
   }
 }
 
+template <bool U8>
 __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const int8_t* __restrict__ x, int n0,
                                                                    int imgs, int8_t* __restrict__ vimg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -144,7 +157,7 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
   pdl_trigger();
   pdl_wait();   // x may come from the previous kernel (layer stacks); V may still be read by the previous GEMM
   Rows r[2];
-  input_rows(g, x, n0, imgs, t, c, r);
+  input_rows<U8>(g, x, n0, imgs, t, c, r);
 
   // ---- D = d' B along rows; store every plane as soon as it is formed
   const long long tb = t / kMBlock;
@@ -220,7 +233,7 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, con
   pdl_trigger();
   pdl_wait();
   Rows r[2];
-  input_rows(g, x, n0, imgs, t, c, r);
+  input_rows<false>(g, x, n0, imgs, t, c, r);
 
   const long long tb = t / kMBlock;
   const int row = t % kMBlock;
@@ -352,7 +365,8 @@ cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int i
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
   dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
   if (g.alg == 1) return launch_pdl(k_input_transform2, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
-  return launch_pdl(k_input_transform, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
+  if (g.in_u8) return launch_pdl(k_input_transform<true>, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
+  return launch_pdl(k_input_transform<false>, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
 }
 
 cudaError_t setup_input_transform() { return cudaSuccess; }

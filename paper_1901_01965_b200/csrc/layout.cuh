@@ -58,6 +58,7 @@ struct Geom {
   int tile;                    // output tile edge (4 or 2)
   int npos;                    // Winograd positions = M'' slots = codes per cout (36 or 16)
   int planes;                  // staged GEMM planes per (tile, channel) (46 or 16)
+  int in_u8, zx, zw;           // uint8 x/w with zero points (f2, A28); 0, 0, 0 for int8
   int chunk_imgs;
   long long chunk_tiles_pad;   // multiple of kMBlock
 };
@@ -164,9 +165,10 @@ __device__ __forceinline__ void decode_code(int code, int& n, int& p) {
   n = code >> 2;
   p = (code & 3) + 4;
 }
-// Inverse factor: the largest q in {7..4} with m = rha(2^(q+p)/n) <= 255.
+// Inverse factor (A8/A27): the largest q in {7..3} with m = rha(2^(q+p)/n) <= 255
+// (q = 3 only for the 8/128 factor that int9 weights reach).
 __device__ __forceinline__ void inverse_factor(int n, int p, int& m, int& q) {
-  for (q = 7; q >= 4; --q) {
+  for (q = 7; q >= 3; --q) {
     long long num = 1ll << (q + p);
     m = (int)((2 * num + n) / (2 * n));
     if (m <= 255) return;

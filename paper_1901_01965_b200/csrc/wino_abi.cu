@@ -97,6 +97,12 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   if (d.path != WINO_PATH_FUSED && d.path != WINO_PATH_STAGED) return WINO_ERR_INVALID_ARG;
   if (d.algorithm != WINO_ALG_F4X4 && d.algorithm != WINO_ALG_F2X2) return WINO_ERR_INVALID_ARG;
   if (d.algorithm == WINO_ALG_F2X2 && d.path != WINO_PATH_STAGED) return WINO_ERR_UNSUPPORTED;
+  if (d.input_type != WINO_IN_INT8 && d.input_type != WINO_IN_UINT8) return WINO_ERR_INVALID_ARG;
+  if (d.input_type == WINO_IN_UINT8) {
+    if (d.x_zero_point < 0 || d.x_zero_point > 255 || d.w_zero_point < 0 || d.w_zero_point > 255)
+      return WINO_ERR_INVALID_ARG;
+    if (d.path != WINO_PATH_STAGED || d.algorithm != WINO_ALG_F4X4 || d.c_in > 224) return WINO_ERR_UNSUPPORTED;
+  }
   if (d.n < 1 || d.h < 1 || d.w < 1 || d.c_in < 1 || d.c_out < 1) return WINO_ERR_UNSUPPORTED;
   if (d.pad != 0 && d.pad != 1) return WINO_ERR_UNSUPPORTED;
   if (d.h + 2 * d.pad < 3 || d.w + 2 * d.pad < 3) return WINO_ERR_UNSUPPORTED;
@@ -126,6 +132,9 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.tile = d.algorithm == WINO_ALG_F2X2 ? 2 : 4;
   g.npos = d.algorithm == WINO_ALG_F2X2 ? 16 : 36;
   g.planes = d.algorithm == WINO_ALG_F2X2 ? 16 : wino::kPlanes;
+  g.in_u8 = d.input_type == WINO_IN_UINT8;
+  g.zx = g.in_u8 ? d.x_zero_point : 0;
+  g.zw = g.in_u8 ? d.w_zero_point : 0;
   g.th = (g.ho + g.tile - 1) / g.tile;
   g.tw = (g.wo + g.tile - 1) / g.tile;
   g.tpi = g.th * g.tw;
