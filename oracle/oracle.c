@@ -93,19 +93,30 @@ int64_t oracle_rha_shift(int64_t v, int k) {
 int oracle_scale_factor(int64_t mx, int target, int *n, int *p) {
     *n = 0; *p = 0;
     if (mx <= target) return 0;
-    int64_t x = ((int64_t)target * 128) / mx;
+    /* the paper's 128; the int8-native target (f3, A29) takes one more bit, 256 with
+     * p = 11 - y, so that x keeps 4 significant bits down to factor 8/256 (exactly the largest
+     * n/2^p <= target/mx, pinned by brute force)                                              */
+    const int f3 = target < 255;
+    int64_t x = ((int64_t)target * (f3 ? 256 : 128)) / mx;
     if (x <= 0) return -1;
     int y = 0;
     while (((int64_t)1 << (y + 1)) <= x) y++;
-    int nn, pp = 10 - y;
+    int nn, pp = (f3 ? 11 : 10) - y;
     if (y >= 3) nn = (int)(x >> (y - 3)); else nn = (int)(x << (3 - y));
-    if (pp < 4 || pp > 7) return -1;
+    /* p in [4,7] for the paper's target 255; the int8-native target (f3, A29) reaches p = 8 */
+    if (pp < 4 || pp > (target < 255 ? 8 : 7)) return -1;
     *n = nn; *p = pp;
     return 0;
 }
 
 /* 6-bit code (A4): (n << 2) | (p - 4); 0 = unscaled.   */
 int oracle_encode_code(int n, int p) { return n == 0 ? 0 : ((n << 2) | (p - 4)); }
+/* 7-bit code of the int8-native target (f3, A29): (n << 3) | (p - 4), p in [4,8]. */
+int oracle_encode_code7(int n, int p) { return n == 0 ? 0 : ((n << 3) | (p - 4)); }
+void oracle_decode_code7(int code, int *n, int *p) {
+    if (code == 0) { *n = 0; *p = 0; return; }
+    *n = code >> 3; *p = (code & 7) + 4;
+}
 void oracle_decode_code(int code, int *n, int *p) {
     if (code == 0) { *n = 0; *p = 0; return; }
     *n = code >> 2; *p = (code & 3) + 4;
@@ -239,6 +250,11 @@ int oracle_output_tile(const gint M[6][6], int64_t Y[4][4]) {
     return ok;
 }
 
+/* position (r, c) of the 6x6 grid involves +-i (rows/columns 3, 4) */
+static inline int Wt_is_complex_pos(int pos) {
+    int r = pos / 6, c = pos % 6;
+    return r == 3 || r == 4 || c == 3 || c == 4;
+}
 static inline int64_t max_abs_component(gint v) {
     int64_t a = v.re < 0 ? -v.re : v.re, b = v.im < 0 ? -v.im : v.im;
     return a > b ? a : b;   /* DESIGN.md A5 */
@@ -265,17 +281,24 @@ int oracle_filter_transform16(const int16_t *w, int Cout, int Cin, int layout, i
             for (int pos = 0; pos < 36; pos++) Wt[(size_t)ci * 36 + pos] = Wt6[pos / 6][pos % 6];
         }
         for (int pos = 0; pos < 36; pos++) {
+            /* int8-native target (f3, A29): complex positions bound |Re| + |Im| by 126 so that
+             * after rounding Re', Im' and Re' + Im' all fit s8; real positions bound |W| by 127.   */
+            const int f3 = target == 127;
+            const int is_cpx = Wt_is_complex_pos(pos);
+            const int tgt = f3 && is_cpx ? 126 : target;
             /* step 2: max magnitude at this X-Y location across channels */
             int64_t mx = 0;
             for (int ci = 0; ci < Cin; ci++) {
-                int64_t m = max_abs_component(Wt[(size_t)ci * 36 + pos]);
+                gint v = Wt[(size_t)ci * 36 + pos];
+                int64_t m = f3 ? (v.re < 0 ? -v.re : v.re) + (v.im < 0 ? -v.im : v.im)
+                               : max_abs_component(v);
                 if (m > mx) mx = m;
             }
             int n = 0, p = 0;
             if (scaling) {      /* steps 3-4 */
-                if (oracle_scale_factor(mx, target, &n, &p) != 0) { status = -1; n = 0; p = 0; }
+                if (oracle_scale_factor(mx, tgt, &n, &p) != 0) { status = -1; n = 0; p = 0; }
             }
-            codes_out[(size_t)co * 36 + pos] = (uint8_t)oracle_encode_code(n, p);
+            codes_out[(size_t)co * 36 + pos] = (uint8_t)(f3 ? oracle_encode_code7(n, p) : oracle_encode_code(n, p));
             for (int ci = 0; ci < Cin; ci++) {
                 gint v = Wt[(size_t)ci * 36 + pos];
                 size_t o = (((size_t)co * Cin + ci) * 36 + pos) * 2;
@@ -358,7 +381,8 @@ int oracle_wino_conv16(const int16_t *x, const int16_t *w, int N, int H, int W, 
             for (int pos = 0; pos < 36; pos++) {
                 gint v = M[pos / 6][pos % 6];
                 int n, p, m = 0, q = 0;
-                oracle_decode_code(codes[(size_t)co * 36 + pos], &n, &p);
+                if (target == 127) oracle_decode_code7(codes[(size_t)co * 36 + pos], &n, &p);
+                else oracle_decode_code(codes[(size_t)co * 36 + pos], &n, &p);
                 if (n) {
                     oracle_reverse_factor(n, p, &m, &q);
                     v.re = oracle_rha_shift(v.re * m, q);

@@ -39,6 +39,8 @@ def lib():
         L.oracle_rha_shift.argtypes = [i64, i32]; L.oracle_rha_shift.restype = i64
         L.oracle_scale_factor.argtypes = [i64, i32, P, P]; L.oracle_scale_factor.restype = i32
         L.oracle_encode_code.argtypes = [i32, i32]; L.oracle_encode_code.restype = i32
+        L.oracle_encode_code7.argtypes = [i32, i32]; L.oracle_encode_code7.restype = i32
+        L.oracle_decode_code7.argtypes = [i32, P, P]; L.oracle_decode_code7.restype = None
         L.oracle_decode_code.argtypes = [i32, P, P]; L.oracle_decode_code.restype = None
         L.oracle_reverse_factor.argtypes = [i32, i32, P, P]; L.oracle_reverse_factor.restype = i32
         L.oracle_direct_conv.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, P]
@@ -104,6 +106,17 @@ def scale_factor(mx: int, target: int = 255):
 
 def encode_code(n: int, p: int) -> int:
     return int(lib().oracle_encode_code(int(n), int(p)))
+
+
+def encode_code7(n: int, p: int) -> int:
+    """7-bit code of the int8-native target (f3, A29)."""
+    return int(lib().oracle_encode_code7(int(n), int(p)))
+
+
+def decode_code7(code: int):
+    n, p = ctypes.c_int(), ctypes.c_int()
+    lib().oracle_decode_code7(int(code), ctypes.byref(n), ctypes.byref(p))
+    return n.value, p.value
 
 
 def decode_code(code: int):
