@@ -137,7 +137,8 @@ def run_ours(args):
     zp = 128 if u8 else 0
     conv = W.WinoConv2d(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad, W.WINO_NHWC, layer.scaling,
                         W.WINO_OUT_INT8, device=local_rank, path=path, algorithm=alg,
-                        input_type=W.WINO_IN_UINT8 if u8 else W.WINO_IN_INT8, x_zero_point=zp, w_zero_point=zp)
+                        input_type=W.WINO_IN_UINT8 if u8 else W.WINO_IN_INT8, x_zero_point=zp, w_zero_point=zp,
+                        filter_target_max=args.target)
     to_in = (lambda a: (a.astype(np.int16) + 128).astype(np.uint8)) if u8 else (lambda a: a)
     info = conv.info
     x_bytes, y_bytes = info.x_bytes, info.y_bytes
@@ -259,7 +260,9 @@ def run_ours(args):
 
     if rank == 0:
         peaks = _peaks()
-        full = sh["n"] == layer.n and sh["co"] == layer.c_out   # the captured shape
+        # the captured shape and variant (default staged int8 F(4x4), target 255)
+        full = sh["n"] == layer.n and sh["co"] == layer.c_out and args.path == "staged" and args.alg == "f4" and \
+            args.input == "i8" and args.target == 255
         roof = roofline(kern, info, synth.LayerCfg(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad),
                         peaks, load_traffic(args.config) if full else None)
         path = path_roofline(synth.LayerCfg(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad), info,
@@ -277,6 +280,7 @@ def run_ours(args):
                         ("K2, K3F fused GEMM+output per chunk)" if info.path == 0 else "K2,K3,K4 per chunk)"),
                 "path": "fused" if info.path == 0 else "staged",
                 "input": "uint8, zero points 128 (SURVEY f2)" if u8 else "int8",
+                "filter_target_max": args.target if layer.scaling else None,
                 "algorithm": "F(2x2,3x3) rational (SURVEY f1)" if info.algorithm == 1 else
                              "F(4x4,3x3) complex (Gaussian integers)",
                 "l2": f"inputs/weights/outputs rotated over {n_sets} sets "
@@ -711,6 +715,9 @@ def main():
                     help="u8: uint8 tensors with zero points (SURVEY f2, staged F(4x4), c_in <= 224)")
     ap.add_argument("--alg", default="f4", choices=["f4", "f2"],
                     help="f4: complex F(4x4,3x3) (the north star); f2: rational F(2x2,3x3) (SURVEY f1, staged only)")
+    ap.add_argument("--target", type=int, default=255, choices=[255, 127],
+                    help="filter scaling target: 255 = the paper's (two-piece W'); 127 = int8-native single-piece "
+                         "W' (SURVEY f3, staged F(4x4) int8)")
     ap.add_argument("--overlap-filter", type=int, default=0,
                     help="1: filter transform on a side stream concurrent with the input transform")
     ap.add_argument("--no-cpu", action="store_true")

@@ -16,12 +16,14 @@ class WinoConv2d:
 
     def __init__(self, n, h, w, c_in, c_out, pad=1, layout=L.WINO_NHWC, filter_scaling=True,
                  out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0, path=L.WINO_PATH_STAGED,
-                 algorithm=L.WINO_ALG_F4X4, input_type=L.WINO_IN_INT8, x_zero_point=0, w_zero_point=0):
+                 algorithm=L.WINO_ALG_F4X4, input_type=L.WINO_IN_INT8, x_zero_point=0, w_zero_point=0,
+                 filter_target_max=255):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device)
-        self.desc = L.wino_conv_desc(n, h, w, c_in, c_out, pad, layout, int(bool(filter_scaling)), 255, out_mode,
-                                     workspace_mb, path, algorithm, input_type, x_zero_point, w_zero_point)
+        # filter_target_max: 255 = the paper's two-piece W'; 127 = int8-native single-piece W' (f3, A29)
+        self.desc = L.wino_conv_desc(n, h, w, c_in, c_out, pad, layout, int(bool(filter_scaling)), filter_target_max,
+                                     out_mode, workspace_mb, path, algorithm, input_type, x_zero_point, w_zero_point)
         self.in_dtype = torch.uint8 if input_type == L.WINO_IN_UINT8 else torch.int8
         self.plan = L.wino_plan(self.desc, device)
         self.info = L.wino_plan_query(self.plan)

@@ -100,11 +100,14 @@ __device__ __forceinline__ void load_filter(const Geom& g, const int8_t* __restr
 //   FUSED: the fused path's group layout instead (layout.cuh): per group the rows
 //   real [W hi, W lo], complex [Wr hi, Wi hi, Wr lo, Wi lo, -Wi hi, Wr hi, -Wi lo, Wr lo]
 //   (balanced s8 pieces), 112 staged rows per channel.
-template <bool FUSED>
+//   W1: the int8-native target (A29): real positions bound |W| by 127,
+//   complex ones |Re| + |Im| by 126, x = floor(target 256 / max), p = 11 - y, 7-bit codes; each
+//   of the 46 planes is ONE s8 operand (w1_offset), 46 staged rows per channel.
+template <bool FUSED, bool W1 = false>
 __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, const int8_t* __restrict__ w,
                                                                          int8_t* __restrict__ wimg,
                                                                          uint8_t* __restrict__ codes) {
-  constexpr int kRows = FUSED ? 2 * kWRowUnitsF : 2 * kPlanes;
+  constexpr int kRows = FUSED ? 2 * kWRowUnitsF : (W1 ? kPlanes : 2 * kPlanes);
   __shared__ __align__(16) int8_t s_stage[kFilterWarps][kRows][32];
   __shared__ int s_max[kFilterWarps][26];
   __shared__ int s_n[26], s_p[26];
@@ -125,7 +128,9 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
 #pragma unroll
       for (int s = 0; s < 16; s++) mx[s] = max(mx[s], abs(t[s]));
 #pragma unroll
-      for (int k = 0; k < 10; k++) mx[16 + k] = max(mx[16 + k], max(abs(t[16 + 2 * k]), abs(t[17 + 2 * k])));
+      for (int k = 0; k < 10; k++)
+        mx[16 + k] = max(mx[16 + k], W1 ? abs(t[16 + 2 * k]) + abs(t[17 + 2 * k])
+                                        : max(abs(t[16 + 2 * k]), abs(t[17 + 2 * k])));
     }
   }
 #pragma unroll
@@ -140,19 +145,22 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
 #pragma unroll
     for (int wv = 0; wv < kFilterWarps; wv++) m = max(m, s_max[wv][threadIdx.x]);
     int n = 0, p = 0;
-    if (g.scaling && m > g.target) {
+    const int tgt = W1 ? (threadIdx.x < 16 ? 127 : 126) : g.target;
+    if (g.scaling && m > tgt) {
       // P:322-329 read per DESIGN.md A3: x = floor(255*128/max), y = floor(log2 x),
-      // n = x >> (y - 3) (4-bit, in [8, 15]), p = 10 - y (in [4, 7]).
-      const int x = (g.target * 128) / m;
+      // n = x >> (y - 3) (4-bit, in [8, 15]), p = 10 - y (in [4, 7]).  W1 (A29): one more
+      // bit, x = floor(tgt*256/max), p = 11 - y (in [4, 8]).
+      const int x = (tgt * (W1 ? 256 : 128)) / m;
       const int y = 31 - __clz(x);
       n = y >= 3 ? (x >> (y - 3)) : (x << (3 - y));
-      p = 10 - y;
+      p = (W1 ? 11 : 10) - y;
     }
     s_n[threadIdx.x] = n;
     s_p[threadIdx.x] = p;
     if (live) {
       const int i = threadIdx.x;
-      const uint8_t code = (uint8_t)(n ? ((n << 2) | (p - 4)) : 0);   // 6-bit code, 0 = unscaled
+      // 6-bit code, W1 7-bit (A29); 0 = unscaled
+      const uint8_t code = (uint8_t)(n ? (W1 ? ((n << 3) | (p - 4)) : ((n << 2) | (p - 4))) : 0);
       if (i < 16) {
         codes[co * 36 + real_pos(i)] = code;
       } else {
@@ -178,7 +186,16 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
 #pragma unroll
       for (int i = 0; i < 46; i++) vals[i] = 0;
     }
-    if constexpr (!FUSED) {
+    if constexpr (W1) {
+#pragma unroll
+      for (int pl = 0; pl < 46; pl++) s_stage[warp][pl][lane] = (int8_t)vals[pl];   // |W'| <= 127 (A29)
+      __syncwarp();
+      for (int idx = lane; idx < kPlanes * 2; idx += 32) {   // (plane, 16-channel half)
+        const int pl = idx >> 1, hf = idx & 1;
+        const int4 v = *reinterpret_cast<const int4*>(&s_stage[warp][pl][hf * 16]);
+        *reinterpret_cast<int4*>(wimg + w1_offset(g, pl, co, c0 + hf * 16)) = v;
+      }
+    } else if constexpr (!FUSED) {
 #pragma unroll
       for (int pl = 0; pl < 46; pl++) {
         s_stage[warp][2 * pl + 0][lane] = (int8_t)bal_hi(vals[pl]);   // balanced s8 pieces (layout.cuh)
@@ -330,6 +347,9 @@ cudaError_t launch_filter_transform(const Geom& g, const int8_t* w, int8_t* wimg
     return launch_pdl(k_filter_transform2, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
   if (g.path == 0)
     return launch_pdl(k_filter_transform<true>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
+  if (g.w1)
+    return launch_pdl(k_filter_transform<false, true>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg,
+                      codes);
   return launch_pdl(k_filter_transform<false>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
 }
 

@@ -17,6 +17,9 @@
 // Then the reverse scaling M'' = rha(M m / 2^q) with (m, q)
 // derived on the device from the per-(cout, position) 6-bit codes.  The output
 // is M'' = 36 int32 per (tile, cout) (16 real values, 10 Re, 10 Im).
+// W1 (int8-native target, A29): W' is ONE s8 piece, so a plane is two
+// UMMAs per K step (B = W', N = n_block) into acc_h, acc_l and M_p = 2^8 acc_h + acc_l; the
+// codes are 7-bit (n << 3 | p - 4).
 // Persistent CTA per SM, warp-specialised (10 warps):
 //   warps 0..7   epilogue: warp w reads TMEM lanes 32(w%4).. (its quadrant),
 //                column half w/4; combines the pieces (and the Karatsuba planes),
@@ -122,7 +125,7 @@ __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync %0, %1;" ::"n"(kEpiBarrier), "n"(kEpiWarps * 32) : "memory");
 }
 
-template <int NBLK, bool F2>
+template <int NBLK, bool F2, bool W1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ Mraw,
            const uint8_t* __restrict__ codes, int cout, int scaling, int ksteps, long long tiles_pad, int tblocks,
@@ -131,7 +134,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int kHalf = NBLK / 2;                 // columns per epilogue warp (8, 16 or 32)
   constexpr int kCpr = NBLK / 4;                  // 16-byte chunks per tile row
   constexpr int kSwz = (kCpr < 8 ? kCpr : 8) - 1; // chunk XOR mask (row & kSwz)
-  constexpr uint32_t kAccCols = 3 * NBLK;         // hh, x, ll
+  constexpr uint32_t kAccCols = (W1 ? 2 : 3) * NBLK;   // hh, x, ll  (W1: h, l)
+  constexpr int kWRows = W1 ? 1 : 2;                   // W' pieces (rows of NBLK) per K step
   constexpr uint32_t kTmemCols = 512;
   constexpr uint32_t kTileBytes = kMBlock * NBLK * 4;
   static_assert(2 * kAccCols <= kTmemCols, "double-buffered accumulators must fit TMEM");
@@ -153,8 +157,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* staging = smem + kStages * stage_bytes;                       // 2 x kTileBytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(staging + 2 * kTileBytes);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
-  uint32_t* lut = tmem_slot + 4;                                         // 64: code -> (m, q, half)
-  uint8_t* s_codes = reinterpret_cast<uint8_t*>(lut + 64);               // [26 positions][cout_pad]
+  uint32_t* lut = tmem_slot + 4;                                         // 128: code -> (m, q, half)
+  uint8_t* s_codes = reinterpret_cast<uint8_t*>(lut + 128);              // [26 positions][cout_pad]
   const uint32_t sbase = smem_u32(smem);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * kStages), tempty0 = smem_u32(bars + 2 * kStages + 2);
@@ -178,9 +182,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_mbar_init();
   }
   pdl_trigger();
-  if (threadIdx.x < 64) {   // inverse factor of every 6-bit code (A8); code 0 -> identity
+  if (threadIdx.x < 128) {   // inverse factor of every 6-bit (W1: 7-bit) code (A8); code 0 -> identity
     int n, p, m = 1, q = 0;
-    decode_code(threadIdx.x, n, p);
+    if (W1) decode_code7(threadIdx.x, n, p);
+    else decode_code(threadIdx.x & 63, n, p);
     if (n >= 8) inverse_factor(n, p, m, q);
     lut[threadIdx.x] = (uint32_t)m | ((uint32_t)q << 8) | ((q ? (1u << (q - 1)) : 0u) << 16);
   }
@@ -206,18 +211,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int plane = unit_plane0<F2>(pidx) + pl;
         // V of the plane: [K step][hi, lo] contiguous; W': [K step][W hi | W lo rows] contiguous
         const int8_t* vpl = V + ((long long)tb * Alg<F2>::kPlanesV + plane) * ksteps * (2 * kVBlockBytes);
-        const int8_t* wpl = W + ((long long)plane * nblocks + nb) * ksteps * (2 * NBLK * kKStep);
+        const int8_t* wpl = W + ((long long)plane * nblocks + nb) * ksteps * (kWRows * NBLK * kKStep);
         for (int ks = 0; ks < n_it; ks++, it++) {
           const int s = it % kStages;
           mbar_wait(empty0 + 8 * s, ((it / kStages) & 1) ^ 1);
           const int k0 = ks * kKStepsPerStage;
           const int kn = min(kKStepsPerStage, ksteps - k0);
-          const uint32_t ab = kn * 2 * kABytesPerKStep, bb = kn * 2 * (uint32_t)NBLK * kKStep;
+          const uint32_t ab = kn * 2 * kABytesPerKStep, bb = kn * kWRows * (uint32_t)NBLK * kKStep;
           const uint32_t st = sbase + s * stage_bytes;
           if (elect_one()) {
             mbar_arrive_expect_tx(full0 + 8 * s, ab + bb);
             bulk_g2s(st, vpl + (long long)k0 * 2 * kVBlockBytes, ab, full0 + 8 * s);
-            bulk_g2s(st + 2 * a_bytes, wpl + (long long)k0 * 2 * NBLK * kKStep, bb, full0 + 8 * s);
+            bulk_g2s(st + 2 * a_bytes, wpl + (long long)k0 * kWRows * NBLK * kKStep, bb, full0 + 8 * s);
             if (ks == 0) WINO_TRACE(ui, 0);
           }
           __syncwarp();
@@ -251,9 +256,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int kk = 0; kk < kn; ++kk) {
             const uint64_t a_hi = umma_desc(st + (2 * kk) * kABytesPerKStep, 128, 256);
             const uint64_t a_lo = umma_desc(st + (2 * kk + 1) * kABytesPerKStep, 128, 256);
-            const uint32_t bw = st + 2 * a_bytes + kk * 2 * NBLK * kKStep;
+            const uint32_t bw = st + 2 * a_bytes + kk * kWRows * NBLK * kKStep;
             const uint64_t b_hl = umma_desc(bw, 128, 256), b_lo = umma_desc(bw + NBLK * kKStep, 128, 256);
-            if (elect_one()) {
+            if (W1) {   // single W' piece: acc_h += hi . W',  acc_l += lo . W'
+              if (elect_one()) {
+                const uint32_t accum = (k0 + kk) > 0 ? 1u : 0u;
+                umma_i8(acc_hh, a_hi, b_hl, id_1n, accum);
+                umma_i8(acc_hh + NBLK, a_lo, b_hl, id_1n, accum);
+              }
+            } else if (elect_one()) {
               if ((k0 + kk) > 0) {
                 umma_i8(acc_hh, a_hi, b_hl, id_2n, 1);   // [hh | x]  += hi . [W hi | W lo]
                 umma_i8(acc_x, a_lo, b_hl, id_2n, 1);    // [x | ll]  += lo . [W hi | W lo]
@@ -291,6 +302,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t acc = lane_base + b * kAccCols;
 #pragma unroll
       for (int c = 0; c < kHalf; c += 8) {
+        if constexpr (W1) {
+          uint32_t h[8], l[8];
+          tmem_ld<8>(acc + c, h);
+          tmem_ld<8>(acc + NBLK + c, l);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; j++) v[c + j] = (h[j] << 8) + l[j];
+          continue;
+        }
         uint32_t h[8], x[8], l[8];
         tmem_ld<8>(acc + c, h);
         tmem_ld<8>(acc + NBLK + c, x);
@@ -324,8 +344,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       epi_barrier();
       // M'' = rha(M m / 2^q) on this thread's 4 columns (sc*4 .. sc*4+3)
       const uint32_t c4 = reinterpret_cast<const uint32_t*>(crow)[sc];
-      const uint32_t e0 = lut[c4 & 0x3fu], e1 = lut[(c4 >> 8) & 0x3fu], e2 = lut[(c4 >> 16) & 0x3fu],
-                     e3 = lut[(c4 >> 24) & 0x3fu];
+      constexpr uint32_t kCm = W1 ? 0x7fu : 0x3fu;
+      const uint32_t e0 = lut[c4 & kCm], e1 = lut[(c4 >> 8) & kCm], e2 = lut[(c4 >> 16) & kCm],
+                     e3 = lut[(c4 >> 24) & kCm];
       int4* gdst = reinterpret_cast<int4*>(dst);
 #pragma unroll
       for (int k = 0; k < kStripRows; k++) {
@@ -381,11 +402,16 @@ cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t*
   const int grid = n_units < g_num_sms ? n_units : g_num_sms;
   const size_t smem = gemm_smem_bytes(g.nblk, g.cout_pad);
   cudaError_t e;
-#define WINO_LAUNCH_GEMM(N)                                                                                  \
-  e = g.alg == 1 ? launch_pdl(k_gemm<N, true>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw, codes, g.cout, g.scaling, \
-                 g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad, g_trace) \
-                 : launch_pdl(k_gemm<N, false>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw, codes, g.cout, g.scaling, \
-                 g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad, g_trace)
+#define WINO_LAUNCH_GEMM(N)                                                                                 \
+  e = g.alg == 1 ? launch_pdl(k_gemm<N, true, false>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw,  \
+                              codes, g.cout, g.scaling, g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad,         \
+                              g.cin_pad, g_trace)                                                                 \
+      : g.w1 ? launch_pdl(k_gemm<N, false, true>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw,     \
+                          codes, g.cout, g.scaling, g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad,  \
+                          g_trace)                                                                                \
+             : launch_pdl(k_gemm<N, false, false>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw,    \
+                          codes, g.cout, g.scaling, g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad,  \
+                          g_trace)
   switch (g.nblk) {
     case 16: WINO_LAUNCH_GEMM(16); break;
     case 32: WINO_LAUNCH_GEMM(32); break;
@@ -400,12 +426,19 @@ cudaError_t setup_gemm() {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(16, kMaxCoutPad));
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(16, kMaxCoutPad));
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(32, kMaxCoutPad));
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(32, kMaxCoutPad));
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(64, kMaxCoutPad));
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(64, kMaxCoutPad));
+  auto attr = [&](const void* f, int nblk) {
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes(nblk, kMaxCoutPad));
+  };
+  attr((const void*)k_gemm<16, false, false>, 16);
+  attr((const void*)k_gemm<16, true, false>, 16);
+  attr((const void*)k_gemm<16, false, true>, 16);
+  attr((const void*)k_gemm<32, false, false>, 32);
+  attr((const void*)k_gemm<32, true, false>, 32);
+  attr((const void*)k_gemm<32, false, true>, 32);
+  attr((const void*)k_gemm<64, false, false>, 64);
+  attr((const void*)k_gemm<64, true, false>, 64);
+  attr((const void*)k_gemm<64, false, true>, 64);
   return e;
 }
 

@@ -312,15 +312,17 @@ cudaError_t launch_output_transform(const Geom& g, const int32_t* m, int n0, int
 cudaError_t setup_output_transform() { return cudaSuccess; }
 
 // ------------------------------------------------------------------ misc
-__global__ void k_check_codes(const uint8_t* __restrict__ codes, int count, int32_t* bad) {
+// valid: 0, or a 6-bit code with n in [8,15]; int8-native target (f3): a 7-bit code with n in [8,15], p in [4,8]
+__global__ void k_check_codes(const uint8_t* __restrict__ codes, int count, int code7, int32_t* bad) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) {
     int c = codes[i];
-    if (c != 0 && (c >= 64 || (c >> 2) < 8)) atomicOr(bad, 1);
+    const bool ok = c == 0 || (code7 ? (c < 128 && (c >> 3) >= 8 && (c & 7) <= 4) : (c < 64 && (c >> 2) >= 8));
+    if (!ok) atomicOr(bad, 1);
   }
 }
-cudaError_t launch_check_codes(const uint8_t* codes, int count, int32_t* bad, cudaStream_t st) {
-  k_check_codes<<<(count + 255) / 256, 256, 0, st>>>(codes, count, bad);
+cudaError_t launch_check_codes(const uint8_t* codes, int count, int code7, int32_t* bad, cudaStream_t st) {
+  k_check_codes<<<(count + 255) / 256, 256, 0, st>>>(codes, count, code7, bad);
   return cudaGetLastError();
 }
 

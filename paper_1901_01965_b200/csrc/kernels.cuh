@@ -79,7 +79,7 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
                          cudaStream_t st);
 
 // misc (k_misc.cu)
-cudaError_t launch_check_codes(const uint8_t* codes, int count, int32_t* bad, cudaStream_t st);
+cudaError_t launch_check_codes(const uint8_t* codes, int count, int code7, int32_t* bad, cudaStream_t st);
 cudaError_t launch_maxpool2(const int8_t* x, int n, int h, int w, int c, int layout, int8_t* y, cudaStream_t st);
 
 }  // namespace wino

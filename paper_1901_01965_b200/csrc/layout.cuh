@@ -59,6 +59,7 @@ struct Geom {
   int npos;                    // Winograd positions = M'' slots = codes per cout (36 or 16)
   int planes;                  // staged GEMM planes per (tile, channel) (46 or 16)
   int in_u8, zx, zw;           // uint8 x/w with zero points (f2, A28); 0, 0, 0 for int8
+  int w1;                      // int8-native target (f3, A29): W' is ONE s8 piece per plane, 7-bit codes
   int chunk_imgs;
   long long chunk_tiles_pad;   // multiple of kMBlock
 };
@@ -142,6 +143,14 @@ __host__ __device__ __forceinline__ long long wf_offset(const Geom& g, int gi, i
          tiled_offset(row, k & 31, rows);
 }
 
+// Byte offset of the single s8 W' piece (int8-native target, f3) of plane `plane`, cout co, channel k:
+// [plane][cout block][K step][n_block rows x 32 B].
+__host__ __device__ __forceinline__ long long w1_offset(const Geom& g, int plane, int co, int k) {
+  const int nb = co / g.nblk, r = co % g.nblk;
+  return (((long long)plane * (g.cout_pad / g.nblk) + nb) * g.ksteps + (k >> 5)) * (g.nblk * kKStep) +
+         tiled_offset(r, k & 31, g.nblk);
+}
+
 // Position index (r*6+c) of real plane s and of complex primary k / its mirror
 // (arithmetic, so no local-memory tables; R = {0,1,2,5} -> R[i] = i + 2 (i == 3)).
 __host__ __device__ __forceinline__ int rsel(int i) { return i + (i == 3 ? 2 : 0); }
@@ -164,6 +173,11 @@ __device__ __forceinline__ long long rha_shift64(long long v, int k) {
 __device__ __forceinline__ void decode_code(int code, int& n, int& p) {
   n = code >> 2;
   p = (code & 3) + 4;
+}
+// Decode a 7-bit code of the int8-native target (f3, A29): (n << 3) | (p - 4), p in [4,8].
+__device__ __forceinline__ void decode_code7(int code, int& n, int& p) {
+  n = code >> 3;
+  p = (code & 7) + 4;
 }
 // Inverse factor (A8/A27): the largest q in {7..3} with m = rha(2^(q+p)/n) <= 255
 // (q = 3 only for the 8/128 factor that int9 weights reach).

@@ -108,7 +108,11 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   if (d.h + 2 * d.pad < 3 || d.w + 2 * d.pad < 3) return WINO_ERR_UNSUPPORTED;
   // int32 exactness of M'' and Y (A23): 896 unscaled, 768 scaled
   if (d.c_in > (d.filter_scaling ? 768 : 896)) return WINO_ERR_UNSUPPORTED;
-  if (d.filter_target_max != 255) return WINO_ERR_UNSUPPORTED;
+  if (d.filter_target_max != 255 && d.filter_target_max != 127) return WINO_ERR_UNSUPPORTED;
+  // int8-native target (f3, A29): single-piece W' needs scaling, the staged complex F(4x4), int8 input
+  if (d.filter_target_max == 127 && (!d.filter_scaling || d.path != WINO_PATH_STAGED || d.algorithm != WINO_ALG_F4X4 ||
+                                     d.input_type != WINO_IN_INT8))
+    return WINO_ERR_UNSUPPORTED;
   if (d.c_out > 2048 || (long long)d.n * d.h * d.w > (1ll << 40)) return WINO_ERR_UNSUPPORTED;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess) return WINO_ERR_CUDA;
@@ -132,6 +136,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.tile = d.algorithm == WINO_ALG_F2X2 ? 2 : 4;
   g.npos = d.algorithm == WINO_ALG_F2X2 ? 16 : 36;
   g.planes = d.algorithm == WINO_ALG_F2X2 ? 16 : wino::kPlanes;
+  g.w1 = d.filter_target_max == 127;
   g.in_u8 = d.input_type == WINO_IN_UINT8;
   g.zx = g.in_u8 ? d.x_zero_point : 0;
   g.zw = g.in_u8 ? d.w_zero_point : 0;
@@ -162,7 +167,8 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   p->m_bytes = d.path == WINO_PATH_STAGED ? (size_t)g.npos * g.chunk_tiles_pad * g.cout_pad * 4 : 0;
   p->ws_bytes = p->v_bytes + p->m_bytes;
   // W': 92 B per (cin, cout) staged (46 planes x 2 pieces); 112 B fused (56 rows x 2 couts-halves, layout.cuh)
-  p->f_bytes = (size_t)(d.path == WINO_PATH_STAGED ? 2 * g.planes : 2 * wino::kWRowUnitsF) * g.cout_pad * g.cin_pad;
+  p->f_bytes = (size_t)(d.path == WINO_PATH_STAGED ? (g.w1 ? 1 : 2) * g.planes : 2 * wino::kWRowUnitsF) * g.cout_pad *
+               g.cin_pad;
   p->x_bytes = (size_t)d.n * d.h * d.w * d.c_in;
   p->y_bytes = (size_t)d.n * g.ho * g.wo * d.c_out * (d.out_mode == WINO_OUT_INT32 ? 4 : 1);
   *out = p;
@@ -287,7 +293,8 @@ wino_status wino_conv2d_int8_host(wino_plan_t p, const int8_t* x_host, const voi
 
 wino_status wino_check_codes(wino_plan_t p, const uint8_t* codes, int32_t* bad_flag, void* stream) {
   if (!p || !codes || !bad_flag) return WINO_ERR_INVALID_ARG;
-  return cuda_status(wino::launch_check_codes(codes, p->d.c_out * p->g.npos, bad_flag, static_cast<cudaStream_t>(stream)));
+  return cuda_status(wino::launch_check_codes(codes, p->d.c_out * p->g.npos, p->g.w1, bad_flag,
+                                              static_cast<cudaStream_t>(stream)));
 }
 
 wino_status wino_debug_set_trace(void* device_buffer) {

@@ -30,6 +30,19 @@ def decode_w_staged(buf: np.ndarray, cout_pad: int, nblk: int, ksteps: int, cin:
     return out
 
 
+def decode_w1(buf: np.ndarray, cout_pad: int, nblk: int, ksteps: int, cin: int, nplanes: int = 46):
+    """Single-piece W' image of the int8-native target (f3) [plane][cout block][K step][n_block rows]
+    -> int [nplanes][cout_pad][cin]."""
+    co = np.arange(cout_pad)[:, None]; k = np.arange(cin)[None, :]
+    nblocks = cout_pad // nblk
+    b = buf.astype(np.int64)
+    out = np.zeros((nplanes, cout_pad, cin), np.int64)
+    for pl in range(nplanes):
+        base = ((pl * nblocks + co // nblk) * ksteps + (k >> 5)) * (nblk * 32)
+        out[pl] = b[base + tiled_offset(co % nblk, k & 31, nblk)]
+    return out
+
+
 def decode_v(buf: np.ndarray, tiles: int, ksteps: int, cin: int, nplanes: int = 46):
     """V image [tile_block][plane][K step][hi, lo][4 KB] (balanced s8 pieces) -> int [nplanes][tiles][cin]."""
     t = np.arange(tiles)[:, None]; k = np.arange(cin)[None, :]

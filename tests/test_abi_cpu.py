@@ -42,7 +42,11 @@ def test_status_strings_and_pre_cuda_validation():
                        (dict(input_type=2), L.WINO_ERR_INVALID_ARG),
                        (dict(input_type=1, x_zero_point=256, path=1), L.WINO_ERR_INVALID_ARG),
                        (dict(input_type=1, path=0), L.WINO_ERR_UNSUPPORTED),
-                       (dict(input_type=1, path=1, c_in=225), L.WINO_ERR_UNSUPPORTED)]:
+                       (dict(input_type=1, path=1, c_in=225), L.WINO_ERR_UNSUPPORTED),
+                       (dict(filter_target_max=126, path=1), L.WINO_ERR_UNSUPPORTED),
+                       (dict(filter_target_max=127, path=1, filter_scaling=0), L.WINO_ERR_UNSUPPORTED),
+                       (dict(filter_target_max=127, path=1, algorithm=1), L.WINO_ERR_UNSUPPORTED),
+                       (dict(filter_target_max=127, path=1, input_type=1), L.WINO_ERR_UNSUPPORTED)]:
         d = dict(base); d.update(kw)
         with pytest.raises(L.WinoError) as e:
             L.wino_plan(L.wino_conv_desc(**d), 0)

@@ -1,6 +1,8 @@
 """GPU parity of the rational F(2x2,3x3) path (staged kernels with
 algorithm = WINO_ALG_F2X2) against the oracle's F(2x2) pipeline, element by element:
 codes, W' planes, V planes and M'' byte/int exact, y bit-exact."""
+import zlib
+
 import numpy as np
 import pytest
 import torch
@@ -64,7 +66,7 @@ def test_f2_c1_shape(layout, scaling):
 @pytest.mark.parametrize("scaling", [False, True])
 def test_f2_random_shapes(case, scaling):
     n, h, wd, ci, co, pad, layout = case
-    rng = np.random.default_rng(abs(hash((case, scaling, "f2"))) % 2 ** 32)
+    rng = np.random.default_rng(zlib.crc32(repr((case, scaling, "f2")).encode()))
     x, w = synth.random_layer(rng, n, h, wd, ci, co, layout)
     _check(x, w, layout, pad, scaling)
 

@@ -1,6 +1,7 @@
 """GPU parity: the CUDA path through the C ABI against the CPU oracle,
 element by element on the same seeded inputs.  Integer work => bit-exact."""
 import os
+import zlib
 
 import numpy as np
 import pytest
@@ -117,7 +118,7 @@ def test_c1_all_stages(layout, scaling, path):
 @pytest.mark.parametrize("path", PATHS)
 def test_random_shapes_all_stages(case, scaling, path):
     n, h, wd, ci, co, pad, layout = case
-    rng = np.random.default_rng(abs(hash((case, scaling))) % 2 ** 32)
+    rng = np.random.default_rng(zlib.crc32(repr((case, scaling)).encode()))
     x, w = synth.random_layer(rng, n, h, wd, ci, co, layout)
     _check_layer(x, w, layout, pad, scaling, path=path)
 

@@ -1,5 +1,7 @@
 """GPU parity of the uint8 + zero-point mode (staged complex F(4x4))
 against the oracle's uint8 pipeline: codes, W', V and M'' exact, y bit-exact."""
+import zlib
+
 import numpy as np
 import pytest
 import torch
@@ -58,7 +60,7 @@ def _check(x, w, zx, zw, layout, pad=1, scaling=True, intermediates=True):
 @pytest.mark.parametrize("scaling", [False, True])
 def test_u8_random_shapes(case, scaling):
     n, h, wd, ci, co, pad, layout, zx, zw = case
-    rng = np.random.default_rng(abs(hash((case, scaling, "u8"))) % 2 ** 32)
+    rng = np.random.default_rng(zlib.crc32(repr((case, scaling, "u8")).encode()))
     x, w = _layer(rng, n, h, wd, ci, co, layout)
     _check(x, w, zx, zw, layout, pad, scaling)
 
