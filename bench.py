@@ -514,20 +514,18 @@ def roofline(kern, info, layer, peaks, traffic=None):
     k4_bytes = info.positions * 4 * chunk_tiles * layer.c_out + chunk_tiles * px * layer.c_out
     # K3F (fused): the K3 work; bytes: V once, W' once, y int8 once
     k3f_bytes = vpc * chunk_tiles * info.cin_pad + info.filter_bytes + chunk_tiles * px * layer.c_out
-    if info.path == 1:
-        spec = {
-            "k1_filter": ("hbm", k1_bytes, hbm, "GB/s"),
-            "k2_input": ("hbm", k2_bytes, hbm, "GB/s"),
-            "k3_gemm": ("tensor", k3_ops, i8_sus, "TOPS"),
-            "k4_output": ("hbm", k4_bytes, hbm, "GB/s"),
-        }
-    else:
-        spec = {
-            "k1_filter": ("hbm", k1_bytes, hbm, "GB/s"),
-            "k2_input": ("hbm", k2_bytes, hbm, "GB/s"),
-            "k3_fused": ("tensor", k3_ops, i8_sus, "TOPS"),
-        }
+    # The GEMM kernel has two roofs: its algorithmic int ops against the int8 tensor peak, and its own
+    # HBM bytes (V in, W' in, M'' or y out) against the HBM peak.  The binding roof is the one with the
+    # larger minimum time (the kernel's arithmetic intensity against the ridge point); the bench line
+    # reports that one and keeps the other as a second view.
+    gemm = "k3_gemm" if info.path == 1 else "k3_fused"
+    if info.path != 1:
         k3_bytes = k3f_bytes
+    t_tc, t_hbm = k3_ops / (i8_sus * 1e12), k3_bytes / (hbm * 1e9)
+    gemm_spec = ("hbm", k3_bytes, hbm, "GB/s") if t_hbm >= t_tc else ("tensor", k3_ops, i8_sus, "TOPS")
+    spec = {"k1_filter": ("hbm", k1_bytes, hbm, "GB/s"), "k2_input": ("hbm", k2_bytes, hbm, "GB/s"), gemm: gemm_spec}
+    if info.path == 1:
+        spec["k4_output"] = ("hbm", k4_bytes, hbm, "GB/s")
     all_k = {}
     for name, (bound, work, peak, unit) in spec.items():
         t = kern[name]["s_per_launch"]
@@ -536,7 +534,10 @@ def roofline(kern, info, layer, peaks, traffic=None):
              "frac": round(achieved / peak, 4), "traffic": (traffic or {}).get(name), "us_per_launch": round(t * 1e6, 3),
              "launches_per_step": kern[name]["launches_per_step"],
              "share_of_step": None, "algorithmic_per_launch": work}
-        if name in ("k3_gemm", "k3_fused"):
+        if name == gemm:
+            d["roof_times_us"] = {"tensor": round(t_tc * 1e6, 3), "hbm": round(t_hbm * 1e6, 3)}
+            d["tensor_view"] = {"int_ops_per_launch": k3_ops, "achieved_tops": round(k3_ops / t / 1e12, 2),
+                                "peak_tops": round(i8_sus, 1), "frac": round(k3_ops / t / 1e12 / i8_sus, 4)}
             d["hbm_view"] = {"bytes_per_launch": k3_bytes, "achieved_gbs": round(k3_bytes / t / 1e9, 1),
                              "frac_of_hbm": round(k3_bytes / t / 1e9 / hbm, 4)}
         all_k[name] = d
@@ -546,7 +547,7 @@ def roofline(kern, info, layer, peaks, traffic=None):
     dom = max(all_k, key=lambda k: kern[k]["s_per_step"])
     dominant = dict(all_k[dom]); dominant["kernel"] = dom
     dominant["peak_source"] = peaks["source"] + (
-        "; int8 = 2 x bf16 sustained" if dom in ("k3_gemm", "k3_fused") else "; hbm_gbs")
+        "; int8 = 2 x bf16 sustained" if dominant["bound"] == "tensor" else "; hbm_gbs")
     return {"dominant": dominant, "all": all_k}
 
 
