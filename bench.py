@@ -130,7 +130,7 @@ def run_ours(args):
     # configuration's batch (or Cout for batch < world) is split over the ranks
     sh = SH.shard(layer.n, layer.c_out, world, rank) if args.scaling == "strong" else \
         {"mode": "replica", "n0": 0, "n": layer.n, "co0": 0, "co": layer.c_out}
-    path = W.WINO_PATH_STAGED if args.path == "staged" else W.WINO_PATH_FUSED
+    path = {"staged": W.WINO_PATH_STAGED, "fused": W.WINO_PATH_FUSED, "auto": W.WINO_PATH_AUTO}[args.path]
     alg = W.WINO_ALG_F2X2 if args.alg == "f2" else W.WINO_ALG_F4X4
     # --input u8: the same synthetic values as uint8 tensors with zero points 128
     u8 = args.input == "u8"
@@ -260,11 +260,11 @@ def run_ours(args):
 
     if rank == 0:
         peaks = _peaks()
-        # the captured shape and variant (default staged int8 F(4x4), target 255)
-        full = sh["n"] == layer.n and sh["co"] == layer.c_out and args.path == "staged" and args.alg == "f4" and \
-            args.input == "i8" and args.target == 255
+        # the captured shape and variant (int8 F(4x4), target 255; per kernel path)
+        full = sh["n"] == layer.n and sh["co"] == layer.c_out and args.alg == "f4" and args.input == "i8" and \
+            args.target == 255
         roof = roofline(kern, info, synth.LayerCfg(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad),
-                        peaks, load_traffic(args.config) if full else None)
+                        peaks, load_traffic(args.config, "staged" if info.path == 1 else "fused") if full else None)
         path = path_roofline(synth.LayerCfg(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad), info,
                              peaks, t_max / args.steps)
         line = {
@@ -476,13 +476,13 @@ def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps):
     return out
 
 
-def load_traffic(config):
+def load_traffic(config, path):
     """roofline.traffic: DRAM bytes per launch from the latest committed ncu --set full
-    capture of this config (profiles/rNN_traffic_<config>.json, written by
-    tools/profile_summary.py), or None when no capture exists."""
+    capture of this config and kernel path (profiles/rNN_traffic_<config>_<path>.json, written
+    by tools/profile_summary.py), or {} when no capture exists."""
     import glob
     files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                          f"r*_traffic_{config}.json")))
+                                          f"r*_traffic_{config}_{path}.json")))
     if not files:
         return {}
     try:
@@ -711,7 +711,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--streams", type=int, default=3,
                     help="independent batches in flight on separate streams (own filter/workspace buffers)")
-    ap.add_argument("--path", default="staged", choices=["fused", "staged"])
+    ap.add_argument("--path", default="auto", choices=["auto", "fused", "staged"],
+                    help="auto: the plan picks fused for c_in*c_out <= 128*128 (C2, C3), staged otherwise")
     ap.add_argument("--input", default="i8", choices=["i8", "u8"],
                     help="u8: uint8 tensors with zero points (SURVEY f2, staged F(4x4), c_in <= 224)")
     ap.add_argument("--alg", default="f4", choices=["f4", "f2"],

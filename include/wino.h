@@ -78,7 +78,10 @@ typedef struct {
                              kernel for the GEMMs + Karatsuba + reverse scaling + output
                              transform + store (M'' stays on chip).
                              WINO_PATH_STAGED (1): K2, K3 GEMMs -> M'' in the workspace,
-                             K4 output transform (M'' inspectable, see wino_plan_info). */
+                             K4 output transform (M'' inspectable, see wino_plan_info).
+                             WINO_PATH_AUTO (2): fused when c_in * c_out <= 128 * 128 and
+                             the variant allows it (F4x4, int8, target 255), else
+                             staged; wino_plan_info.path reports the choice.           */
     int algorithm;        /* WINO_ALG_F4X4 (0, default): complex F(4x4,3x3) over the
                              Gaussian integers, points {0, +-1, +-i};
                              WINO_ALG_F2X2 (1): rational F(2x2,3x3), G' = 2G,
@@ -94,7 +97,7 @@ typedef struct {
 } wino_conv_desc;
 
 /* Hot-path kernel structure (wino_conv_desc.path). */
-enum { WINO_PATH_FUSED = 0, WINO_PATH_STAGED = 1 };
+enum { WINO_PATH_FUSED = 0, WINO_PATH_STAGED = 1, WINO_PATH_AUTO = 2 };
 
 /* Winograd algorithm (wino_conv_desc.algorithm). */
 enum { WINO_ALG_F4X4 = 0, WINO_ALG_F2X2 = 1 };

@@ -14,7 +14,7 @@ WINO_OK, WINO_ERR_INVALID_ARG, WINO_ERR_UNSUPPORTED, WINO_ERR_SHAPE = 0, -1, -2,
 WINO_ERR_RANGE, WINO_ERR_CUDA, WINO_ERR_NOMEM = -4, -5, -6
 WINO_NCHW, WINO_NHWC = 0, 1
 WINO_OUT_INT8, WINO_OUT_INT32 = 0, 1
-WINO_PATH_FUSED, WINO_PATH_STAGED = 0, 1
+WINO_PATH_FUSED, WINO_PATH_STAGED, WINO_PATH_AUTO = 0, 1, 2
 WINO_ALG_F4X4, WINO_ALG_F2X2 = 0, 1
 WINO_IN_INT8, WINO_IN_UINT8 = 0, 1
 

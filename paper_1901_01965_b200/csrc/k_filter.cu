@@ -5,6 +5,7 @@
 // One warp per output channel (see k_filter_transform); the transform is
 // recomputed in the second pass instead of being stored.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -120,11 +121,20 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
   int mx[26];
 #pragma unroll
   for (int i = 0; i < 26; i++) mx[i] = 0;
+  // the transform of this thread's first channel (ci = threadIdx.x) stays in registers for pass 2,
+  // whose first iteration handles the same channel (every channel when cin <= blockDim)
+  int t0[36];
+#pragma unroll
+  for (int i = 0; i < 36; i++) t0[i] = 0;
   if (live) {
     for (int ci = threadIdx.x; ci < g.cin; ci += blockDim.x) {
       int gg[3][3], t[36];
       load_filter(g, w, co, ci, gg);
       filter_tile_transform(gg, t);
+      if (ci == (int)threadIdx.x) {
+#pragma unroll
+        for (int i = 0; i < 36; i++) t0[i] = t[i];
+      }
 #pragma unroll
       for (int s = 0; s < 16; s++) mx[s] = max(mx[s], abs(t[s]));
 #pragma unroll
@@ -178,10 +188,14 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
     const int ci = c0 + lane;
     int vals[46];
     if (live && ci < g.cin) {
-      int gg[3][3], t[36];
-      load_filter(g, w, co, ci, gg);
-      filter_tile_transform(gg, t);
-      scaled_planes(t, sn, sp, vals);
+      if (c0 == warp * 32) {   // ci == threadIdx.x: transformed in pass 1
+        scaled_planes(t0, sn, sp, vals);
+      } else {
+        int gg[3][3], t[36];
+        load_filter(g, w, co, ci, gg);
+        filter_tile_transform(gg, t);
+        scaled_planes(t, sn, sp, vals);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 46; i++) vals[i] = 0;
@@ -342,17 +356,22 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform2(Geom g,
   }
 }
 
+static int g_carve_filter = kCarveFilter;
+
 cudaError_t launch_filter_transform(const Geom& g, const int8_t* w, int8_t* wimg, uint8_t* codes, cudaStream_t st) {
   if (g.alg == 1)
-    return launch_pdl(k_filter_transform2, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
+    return launch_pdl_co(k_filter_transform2, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g_carve_filter, g, w, wimg, codes);
   if (g.path == 0)
-    return launch_pdl(k_filter_transform<true>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
+    return launch_pdl_co(k_filter_transform<true>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g_carve_filter, g, w, wimg, codes);
   if (g.w1)
-    return launch_pdl(k_filter_transform<false, true>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg,
+    return launch_pdl_co(k_filter_transform<false, true>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g_carve_filter, g, w, wimg,
                       codes);
-  return launch_pdl(k_filter_transform<false>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g, w, wimg, codes);
+  return launch_pdl_co(k_filter_transform<false>, dim3(g.cout_pad), dim3(kFilterWarps * 32), 0, st, g_carve_filter, g, w, wimg, codes);
 }
 
-cudaError_t setup_filter_transform() { return cudaSuccess; }
+cudaError_t setup_filter_transform() {
+  if (const char* c = std::getenv("WINO_CARVE_K1")) g_carve_filter = std::atoi(c);   // experiments
+  return cudaSuccess;
+}
 
 }  // namespace wino

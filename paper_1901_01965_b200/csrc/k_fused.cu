@@ -146,6 +146,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
 #define FTRACE(i, ev) do { } while (0)
 #endif
   extern __shared__ __align__(1024) uint8_t smem[];
+#ifndef WINO_FUSED_DBG
+  dbg = 0;   // the WINO_FUSED_DBG ablation modes exist only in debug builds (-DWINO_FUSED_DBG)
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* part = smem + kFStages * kFStageBytes;                            // Z_0 / Z_5 | output staging
   uint32_t* etab = reinterpret_cast<uint32_t*>(part + kFPartBytes);          // [26 groups][16 couts] m'
@@ -606,7 +609,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
 static int g_fused_sms = 0;
 static uint64_t* g_fused_trace = nullptr;
 void set_fused_trace(void* buf) { g_fused_trace = static_cast<uint64_t*>(buf); }
-static int g_fused_dbg = 0;   // WINO_FUSED_DBG (debug timing only): 2 no MMAs, 8 epilogue handshake only
+// WINO_FUSED_DBG env (debug builds with -DWINO_FUSED_DBG only): 2 no MMAs, 8 epilogue handshake only
+static int g_fused_dbg = 0;
 
 cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
                          const int8_t* wimg, const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y,

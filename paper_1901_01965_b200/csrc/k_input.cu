@@ -14,6 +14,7 @@
 // All 92 plane-pieces of a (tile block, K step) are 4 KB apart, so every
 // store is an immediate offset from one base pointer.
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 #include <cuda_runtime.h>
 
@@ -291,7 +292,7 @@ cudaError_t launch_input_transform_f(const Geom& g, const int8_t* x, int n0, int
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
   dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
-  return launch_pdl(k_input_transform_f, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
+  return launch_pdl_co(k_input_transform_f, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
 }
 
 // ---- rational F(2x2,3x3): 4x4 patch at (2ty - pad, 2tx - pad), D = B^T d B with the
@@ -364,9 +365,9 @@ cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int i
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
   dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
-  if (g.alg == 1) return launch_pdl(k_input_transform2, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
-  if (g.in_u8) return launch_pdl(k_input_transform<true>, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
-  return launch_pdl(k_input_transform<false>, grid, dim3(kInWarps * 32), 0, st, g, x, n0, imgs, vimg);
+  if (g.alg == 1) return launch_pdl_co(k_input_transform2, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
+  if (g.in_u8) return launch_pdl_co(k_input_transform<true>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
+  return launch_pdl_co(k_input_transform<false>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
 }
 
 cudaError_t setup_input_transform() { return cudaSuccess; }

@@ -18,6 +18,7 @@
 //   Y[2][j] = Z1+Z2-2Re Z3      Y[3][j] = Z1-Z2+Z5+2Im Z3.
 // All sums are int32 with wrap-around: exact because the true Y fits (A23).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -273,7 +274,7 @@ cudaError_t launch_output_transform(const Geom& g, const int32_t* m, int n0, int
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 30;
   cudaError_t e;
   if (g.alg == 1) {   // rational F(2x2)
-#define WINO_K42(A, B, C) e = launch_pdl(k_output_transform2<A, B, C>, grid, dim3(256), 0, st, g, m, n0, imgs, rq_mult, rq_shift, y)
+#define WINO_K42(A, B, C) e = launch_pdl_co(k_output_transform2<A, B, C>, grid, dim3(256), 0, st, kCarveL1, g, m, n0, imgs, rq_mult, rq_shift, y)
     if (nhwc) {
       if (!out8) WINO_K42(true, false, false);
       else if (fast) WINO_K42(true, true, true);
@@ -288,14 +289,14 @@ cudaError_t launch_output_transform(const Geom& g, const int32_t* m, int n0, int
   }
   if (nhwc && (g.cout & 3) == 0) {   // vectorised variant (NHWC; NCHW keeps one cout per thread)
     dim3 grid4((unsigned)((tiles + kOut4Tiles - 1) / kOut4Tiles), (unsigned)((g.cout + 63) / 64));
-#define WINO_K4V(B, C) e = launch_pdl(k_output_transform4<true, B, C>, grid4, dim3(256), 0, st, g, m, n0, imgs, rq_mult, rq_shift, y)
+#define WINO_K4V(B, C) e = launch_pdl_co(k_output_transform4<true, B, C>, grid4, dim3(256), 0, st, kCarveL1, g, m, n0, imgs, rq_mult, rq_shift, y)
     if (!out8) WINO_K4V(false, false);
     else if (fast) WINO_K4V(true, true);
     else WINO_K4V(true, false);
 #undef WINO_K4V
     return e;
   }
-#define WINO_K4(A, B, C) e = launch_pdl(k_output_transform<A, B, C>, grid, dim3(256), 0, st, g, m, n0, imgs, rq_mult, rq_shift, y)
+#define WINO_K4(A, B, C) e = launch_pdl_co(k_output_transform<A, B, C>, grid, dim3(256), 0, st, kCarveL1, g, m, n0, imgs, rq_mult, rq_shift, y)
   if (nhwc) {
     if (!out8) WINO_K4(true, false, false);
     else if (fast) WINO_K4(true, true, true);

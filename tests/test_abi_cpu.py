@@ -36,7 +36,7 @@ def test_status_strings_and_pre_cuda_validation():
     for kw, status in [(dict(pad=2), L.WINO_ERR_UNSUPPORTED), (dict(c_in=897, filter_scaling=0), L.WINO_ERR_UNSUPPORTED),
                        (dict(c_in=769), L.WINO_ERR_UNSUPPORTED), (dict(layout=5), L.WINO_ERR_INVALID_ARG),
                        (dict(out_mode=9), L.WINO_ERR_INVALID_ARG), (dict(h=1, pad=0), L.WINO_ERR_UNSUPPORTED),
-                       (dict(filter_target_max=127), L.WINO_ERR_UNSUPPORTED), (dict(path=2), L.WINO_ERR_INVALID_ARG),
+                       (dict(filter_target_max=127), L.WINO_ERR_UNSUPPORTED), (dict(path=3), L.WINO_ERR_INVALID_ARG),
                        (dict(algorithm=2), L.WINO_ERR_INVALID_ARG),
                        (dict(algorithm=1, path=0), L.WINO_ERR_UNSUPPORTED),
                        (dict(input_type=2), L.WINO_ERR_INVALID_ARG),

@@ -277,3 +277,21 @@ def test_vgg16_stack_full_size_sampled():
     # the activations stay informative (requant shifts neither saturate nor vanish)
     last = (st.pooled.get(len(ws) - 1, st.outs[-1])).cpu().numpy()
     assert 4 < np.abs(last.astype(np.int32)).mean() < 100
+
+
+def test_auto_path_choice_and_parity():
+    """WINO_PATH_AUTO resolves to fused for c_in*c_out <= 128*128 with the fused path's variants,
+    staged otherwise (info.path reports it), and either way the result is the oracle's."""
+    W = _wino()
+    for (ci, co, kw, want) in [(64, 64, {}, W.WINO_PATH_FUSED), (128, 128, {}, W.WINO_PATH_FUSED),
+                               (128, 160, {}, W.WINO_PATH_STAGED), (256, 256, {}, W.WINO_PATH_STAGED),
+                               (64, 64, dict(algorithm=W.WINO_ALG_F2X2), W.WINO_PATH_STAGED),
+                               (64, 64, dict(filter_target_max=127), W.WINO_PATH_STAGED)]:
+        conv = W.WinoConv2d(1, 9, 10, ci, co, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=W.WINO_PATH_AUTO, **kw)
+        assert conv.info.path == want, (ci, co, kw)
+    rng = np.random.default_rng(77)
+    x, w = synth.random_layer(rng, 2, 13, 11, 40, 24, O.NHWC)
+    conv = W.WinoConv2d(2, 13, 11, 40, 24, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=W.WINO_PATH_AUTO)
+    conv.transform_filter(torch.from_numpy(w).cuda())
+    np.testing.assert_array_equal(conv(torch.from_numpy(x).cuda()).cpu().numpy(),
+                                  O.wino_conv(x, w, 1, O.NHWC, True).out32)

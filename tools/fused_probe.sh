@@ -1,0 +1,7 @@
+python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
+for cfg in C2 C3 C4; do python tools/time_stage.py $cfg fused 3 50; done
+WINO_NVCC_FLAGS=-DWINO_FUSED_DBG python -c "from paper_1901_01965_b200 import build as B; B.build(force=True)"
+for d in 0 2 8 10; do WINO_FUSED_DBG=$d python tools/time_stage.py C2 fused 3 50; done
+python -c "from paper_1901_01965_b200 import build as B; B.build(force=True)"
+for cfg in C2 C3; do python bench.py --no-cpu --config $cfg --steps 1000 > /tmp/s.json 2>&1; python -c "
+import json; d=json.load(open('/tmp/s.json')); k=d['kernels']; print('$cfg', d['value'], d['ms_per_step'], d['config']['path'], ' '.join(f\"{n}={v['us_per_launch']}\" for n,v in k.items()))"; done

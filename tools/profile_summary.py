@@ -14,7 +14,8 @@ import sys
 
 launches, reps, bench, out = sys.argv[1:5]
 traffic_out = sys.argv[5] if len(sys.argv) > 5 else None
-KEYS = {"k_filter": "k1_filter", "k_input": "k2_input", "k_gemm": "k3_gemm", "k_output": "k4_output"}
+KEYS = {"k_filter": "k1_filter", "k_input": "k2_input", "k_gemm": "k3_gemm", "k_output": "k4_output",
+        "k_fused": "k3_fused"}
 
 
 def bench_key(name):

@@ -1,0 +1,5 @@
+python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+for cfg in C2 C3 C4; do python bench.py --no-cpu --config $cfg --steps 1000 > /tmp/s.json 2>&1; python -c "
+import json; d=json.load(open('/tmp/s.json')); k=d['kernels']; print('$cfg', d['value'], d['ms_per_step'], ' '.join(f\"{n}={v['us_per_launch']}\" for n,v in k.items()))"; done
+python bench.py --no-cpu --config C2 --path fused --steps 1000 > /tmp/s.json 2>&1; python -c "
+import json; d=json.load(open('/tmp/s.json')); k=d['kernels']; print('C2 fused', d['value'], d['ms_per_step'], ' '.join(f\"{n}={v['us_per_launch']}\" for n,v in k.items()))"
