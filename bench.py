@@ -321,7 +321,8 @@ def run_ours_stack(args):
     cfg = synth.CONFIGS["C5"]
     shifts = synth.stack_shifts("C5")
     n = cfg.layers[0].n
-    st = ConvStack(n, cfg.layers, cfg.pools_after, shifts, device=local_rank)
+    path = {"staged": L.WINO_PATH_STAGED, "fused": L.WINO_PATH_FUSED, "auto": L.WINO_PATH_AUTO}[args.path]
+    st = ConvStack(n, cfg.layers, cfg.pools_after, shifts, device=local_rank, path=path)
     n_sets = 2
     xs, wss = [], []
     for i in range(n_sets):
@@ -374,6 +375,18 @@ def run_ours_stack(args):
         ops46 = 2 * 46 * c.info.tiles * l.c_in * l.c_out
         byts = c.info.x_bytes + c.info.y_bytes + 92 * l.c_in * l.c_out
         t_roof += max(ops46 / i8, byts / (peaks["hbm_gbs"] * 1e9))
+    # roofline of the stack's dominant kernel: every layer's kernels timed alone (as for C2-C4) on the
+    # stack's own buffers; the (layer, kernel) with the largest time per step is reported
+    kern_l, cur = [], xs[0]
+    for i, c in enumerate(st.convs):
+        kern_l.append(profile_kernels(c, [cur], [wss[0][i]], [st.outs[i]], shifts[i], stream, 1, 10))
+        cur = st.pooled.get(i, st.outs[i])
+    dom_l = max(range(len(st.convs)), key=lambda i: max(k["s_per_step"] for k in kern_l[i].values()))
+    lay = cfg.layers[dom_l]
+    roof = roofline(kern_l[dom_l], st.convs[dom_l].info, synth.LayerCfg(n, lay.h, lay.w, lay.c_in, lay.c_out, lay.pad),
+                    peaks, None)
+    roof["dominant"]["layer"] = dom_l + 1
+    stack_kernel_us = sum(k["s_per_step"] for kl in kern_l for k in kl.values()) * 1e6
     # e2e: host x in, host final activation out, through the C ABI calls
     xh = xs[0].cpu().pin_memory()
     out = st(xs[0], stream)
@@ -400,12 +413,15 @@ def run_ours_stack(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
             "config": {"workload": f"C5: {cfg.description}", "batch_per_gpu": n, "layers": len(cfg.layers),
                        "layout": "NHWC", "filter_scaling": True, "requant_shifts": shifts,
-                       "step": "13 filter transforms + 13 convs (staged K2, K3, K4 per chunk) + 4 max pools",
+                       "step": "13 filter transforms + 13 convs + 4 max pools",
+                       "paths": ["fused" if c.info.path == 0 else "staged" for c in st.convs],
                        "l2": "activations 0.8 GB per layer >> 126 MiB L2; 2 input sets rotated",
                        "parallelism": f"dp{world} (replicated per-rank batches, weak scaling)"},
             "path_roofline": {"t_roof_us": round(t_roof * 1e6, 2), "t_step_us": round(t_max / args.steps * 1e6, 2),
                               "frac": round(t_roof / (t_max / args.steps), 4),
                               "roofline_effective_tops": round(ops_step / t_roof / 1e12, 1)},
+            "roofline": roof["dominant"],
+            "kernel_sum_vs_step": round(stack_kernel_us / (t_max / args.steps * 1e6), 3),
             "gpu_launches": st.launches() * args.steps + len(cfg.layers) * args.steps,
             "clocks": clk.summary(),
             "e2e": {"value": round(world * ops_step * reps / te / 1e12, 3), "unit": "TOPS",
