@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
   // per CTA: [stage it < 64][4]: 0 producer issued, 1 MMA saw data, 2 MMA committed; [64 + slot-group < 32][4]:
   // 0 MMA got slot, 1 epilogue warp 0 saw accumulators, 2 epilogue warp 0 released
   uint64_t* tr = trace ? trace + (size_t)blockIdx.x * 96 * 4 : nullptr;
-#define FTRACE(i, ev) do { if (tr && (i) < 96) { uint64_t t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); tr[(i) * 4 + (ev)] = t_; } } while (0)
+#define FTRACE(i, ev) do { if (tr && (i) < 96) { tr[(i) * 4 + (ev)] = clock64(); } } while (0)   // SM cycles
 #else
   (void)trace;
 #define FTRACE(i, ev) do { } while (0)
@@ -611,6 +611,10 @@ static uint64_t* g_fused_trace = nullptr;
 void set_fused_trace(void* buf) { g_fused_trace = static_cast<uint64_t*>(buf); }
 // WINO_FUSED_DBG env (debug builds with -DWINO_FUSED_DBG only): 2 no MMAs, 8 epilogue handshake only
 static int g_fused_dbg = 0;
+// fewest CTAs for the same number of unit rounds (C2: 196 units -> 98 CTAs x 2 instead of 148 + 48): the
+// freed SMs run the other streams' kernels for the whole launch (C2 190.7 -> 203.1, C3 310.7 -> 332.1 TOPS
+// with three batches in flight); WINO_FUSED_BALANCE=0 restores the full grid (experiments)
+static int g_fused_balance = 1;
 
 cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
                          const int8_t* wimg, const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y,
@@ -618,7 +622,11 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
   if (g.nblk != kFN) return cudaErrorInvalidValue;
   const int tblocks = (int)(tiles_pad_launch / kMBlock);
   const int n_units = tblocks * (g.cout_pad / kFN);
-  const int grid = n_units < g_fused_sms ? n_units : g_fused_sms;
+  int grid = n_units < g_fused_sms ? n_units : g_fused_sms;
+  if (g_fused_balance) {   // fewest CTAs with the same number of unit rounds: the rest of the SMs stay free
+    const int rounds = (n_units + grid - 1) / grid;
+    grid = (n_units + rounds - 1) / rounds;
+  }
   const size_t smem = fused_smem_bytes();
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 20;
   cudaError_t e;
@@ -643,6 +651,7 @@ cudaError_t setup_fused() {
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_fused_sms, cudaDevAttrMultiProcessorCount, dev);
   if (const char* d = std::getenv("WINO_FUSED_DBG")) g_fused_dbg = std::atoi(d);
+  if (const char* d = std::getenv("WINO_FUSED_BALANCE")) g_fused_balance = std::atoi(d);
   const int smem = (int)fused_smem_bytes();
 #define WINO_KF_ATTR(A, B, C) \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)

@@ -420,6 +420,7 @@ static int g_num_sms = 0;
 static uint64_t* g_trace = nullptr;
 // WINO_K3_DBG env (debug builds with -DWINO_K3_DBG only): 1 no M stores, 2 no tiles, 4 no MMAs, 8 no loads
 static int g_gemm_dbg = 0;
+static int g_gemm_balance = 0;   // WINO_K3_BALANCE (experiments)
 void set_gemm_trace(void* buf) { g_trace = static_cast<uint64_t*>(buf); }
 
 cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t* vimg, const int8_t* wimg,
@@ -427,7 +428,11 @@ cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t*
   // tile blocks of this launch; M strides use the full chunk geometry (K4 reads with it)
   const int tblocks = (int)(tiles_pad_launch / kMBlock);
   const int n_units = tblocks * (g.cout_pad / g.nblk) * (g.alg == 1 ? 16 : kPositions);
-  const int grid = n_units < g_num_sms ? n_units : g_num_sms;
+  int grid = n_units < g_num_sms ? n_units : g_num_sms;
+  if (g_gemm_balance) {   // fewest CTAs with the same number of unit rounds (see launch_fused)
+    const int rounds = (n_units + grid - 1) / grid;
+    grid = (n_units + rounds - 1) / rounds;
+  }
   const int nst = gemm_stages(g.nblk, g.cout_pad);
   const size_t smem = gemm_smem_bytes(g.nblk, g.cout_pad, nst);
   cudaError_t e;
@@ -456,6 +461,7 @@ cudaError_t setup_gemm() {
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (const char* d = std::getenv("WINO_K3_DBG")) g_gemm_dbg = std::atoi(d);
+  if (const char* d = std::getenv("WINO_K3_BALANCE")) g_gemm_balance = std::atoi(d);
   if (const char* d = std::getenv("WINO_K3_STAGES")) g_stages_cap = std::max(kMinStages, std::min(kMaxStages, std::atoi(d)));
   auto attr = [&](const void* f, int nblk) {
     if (e == cudaSuccess)

@@ -27,7 +27,7 @@ L.lib().wino_debug_set_trace(None)
 t = buf.cpu().numpy().reshape(148, 96, 4)[cta].astype(np.float64)
 t0 = t[t > 0].min()
 ns = lambda v: f"{(v - t0):8.0f}" if v > 0 else "       -"
-print("stage: producer_issued  mma_saw_data  mma_committed  (ns from first event)")
+print("stage: producer_issued  mma_saw_data  mma_committed  (SM cycles from the first event)")
 for i in range(64):
     if t[i, 0] > 0:
         print(f"  st{i:2d}: {ns(t[i,0])} {ns(t[i,1])} {ns(t[i,2])}")
