@@ -380,13 +380,19 @@ __global__ void __launch_bounds__(kFThreads, 1)
 #pragma unroll
         for (int c = 0; c < 4; c++) Z[j][c] += 2 * re_x(j) * m0[c] + 2 * re_y(j) * m1[c];
     };
-    auto fill_etab = [&](int u) {
+    // this thread's etab entry (group etid / 16, cout etid % 16) of unit u: the code is loaded from
+    // global memory one unit ahead (load_code at the start of a unit, fill_etab at its end), so the
+    // load latency never stalls the epilogue
+    auto load_code = [&](int u) -> int {
       if (u < n_units && etid < kFGroupsN * kFN) {
         const int gi = etid / kFN, c = etid % kFN;
         const int co = (u % nblocks) * kFN + c;
-        const int code = (g.scaling && co < g.cout) ? codes[(long long)co * 36 + fg_pos(gi)] : 0;
-        etab[etid] = lut[code & 63];
+        return (g.scaling && co < g.cout) ? codes[(long long)co * 36 + fg_pos(gi)] : 0;
       }
+      return 0;
+    };
+    auto fill_etab = [&](int code) {
+      if (etid < kFGroupsN * kFN) etab[etid] = lut[code & 63];
     };
 
     if (dbg & 8) {   // debug: accumulator handshake only
@@ -396,9 +402,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
           slot_release();
         }
     } else {
-      fill_etab(blockIdx.x);
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      fill_etab(load_code(blockIdx.x));
+      int uc = 0;   // units done (trace index)
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, uc++) {
         fepi_barrier();                                // etab visible; staging of the previous unit drained
+        const int next_code = load_code(u + gridDim.x);
         {
           int32_t Z[4][4];
           real_row(0, Z);                              // row 0 -> Z_0
@@ -453,6 +461,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         cpx_row(std::integral_constant<int, 3>{});
         cpx_row(std::integral_constant<int, 4>{});
         cpx_row(std::integral_constant<int, 5>{});
+        if (warp == 0 && lane == 0) FTRACE(uc * 8 + 0, 3);
         tmem_st_wait();
 
         // ---- Y rows: Y0 = Z_0 + P + 2 Re Z_3, Y2 = P - 2 Re Z_3, Y1 = Q - 2 Im Z_3, Y3 = Q + Z_5 + 2 Im Z_3
@@ -473,8 +482,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
             Y1[j][c] -= i2;
           }
         }
+        if (warp == 0 && lane == 0) FTRACE(uc * 8 + 1, 3);
         fepi_barrier();                                // every Z_0 / Z_5 read before the staging overwrites them
-        fill_etab(u + gridDim.x);                      // this unit's reverse scales are all done
+        if (warp == 0 && lane == 0) FTRACE(uc * 8 + 2, 3);
+        fill_etab(next_code);                          // this unit's reverse scales are all done
 
         // ---- out32 = rha(Y / 16) (A11), optional requantisation (A14), crop, store
         const int tb_i = u / nblocks, nb = u - tb_i * nblocks;
@@ -515,8 +526,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
           if (stage8) {   // stage [px][tile][16 couts] bytes; 16-byte chunks leave after the barrier
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-              const uint32_t w = ((uint32_t)outv(Yi[j][0]) & 0xffu) | (((uint32_t)outv(Yi[j][1]) & 0xffu) << 8) |
-                                 (((uint32_t)outv(Yi[j][2]) & 0xffu) << 16) | ((uint32_t)outv(Yi[j][3]) << 24);
+              const uint32_t w = __byte_perm(__byte_perm((uint32_t)outv(Yi[j][0]), (uint32_t)outv(Yi[j][1]), 0x0040),
+                                             __byte_perm((uint32_t)outv(Yi[j][2]), (uint32_t)outv(Yi[j][3]), 0x0040),
+                                             0x5410);
               *reinterpret_cast<uint32_t*>(part + ((i * 4 + j) * kMBlock + row) * 16 + cw * kFC) = w;
             }
             return;
@@ -580,23 +592,29 @@ __global__ void __launch_bounds__(kFThreads, 1)
         emit_row(1, Y1);
         emit_row(2, Y2);
         emit_row(3, Y3);
+        if (warp == 0 && lane == 0) FTRACE(uc * 8 + 3, 3);
         fepi_barrier();                                // staging complete; etab of the next unit visible
+        if (warp == 0 && lane == 0) FTRACE(uc * 8 + 4, 3);
         if (stage8) {
-#pragma unroll
-          for (int q = 0; q < (16 * kMBlock) / (kFEpiWarps * 32); q++) {
-            const int ch = etid + q * kFEpiWarps * 32;
-            const int px = ch >> 7, rr = ch & (kMBlock - 1);
-            const int tt = tb_i * kMBlock + rr;
-            if (tt >= imgs * g.tpi) continue;
+          // chunk ch = etid + q * 512: tile rr = etid % 128 for every q (512 = 4 x 128), pixel px = ch / 128
+          const int rr = etid & (kMBlock - 1);
+          const int tt = tb_i * kMBlock + rr;
+          if (tt < imgs * g.tpi) {
             const int rem = tt % g.tpi, ty = rem / g.tw;
-            const int oy = 4 * ty + (px >> 2), ox = 4 * (rem - ty * g.tw) + (px & 3);
-            if (oy >= g.ho || ox >= g.wo) continue;
-            const uint4 val = *reinterpret_cast<const uint4*>(part + ch * 16);
-            int8_t* dst = static_cast<int8_t*>(y) +
-                          (((long long)(n0 + tt / g.tpi) * g.ho + oy) * g.wo + ox) * g.cout + nb * kFN;
-            *reinterpret_cast<uint4*>(dst) = val;
+            const int oyb = 4 * ty, oxb = 4 * (rem - ty * g.tw);
+            int8_t* base = static_cast<int8_t*>(y) + (long long)(n0 + tt / g.tpi) * g.ho * g.wo * g.cout + nb * kFN;
+#pragma unroll
+            for (int q = 0; q < (16 * kMBlock) / (kFEpiWarps * 32); q++) {
+              const int ch = etid + q * kFEpiWarps * 32;
+              const int px = ch >> 7;
+              const int oy = oyb + (px >> 2), ox = oxb + (px & 3);
+              if (oy >= g.ho || ox >= g.wo) continue;
+              const uint4 val = *reinterpret_cast<const uint4*>(part + ch * 16);
+              *reinterpret_cast<uint4*>(base + ((long long)oy * g.wo + ox) * g.cout) = val;
+            }
           }
         }
+        if (warp == 0 && lane == 0) FTRACE(uc * 8 + 5, 3);
       }
     }
   }

@@ -35,3 +35,8 @@ print("slot-group: mma_got_slot  epi_saw_acc  epi_released")
 for i in range(32):
     if t[64 + i, 0] > 0:
         print(f"  sg{i:2d}: {ns(t[64+i,0])} {ns(t[64+i,1])} {ns(t[64+i,2])}")
+print("unit end (warp 0): last slot taken, Y formed, barrier 1 passed, rows staged, barrier 2 passed, stored")
+for u in range(4):
+    row = t[u * 8: u * 8 + 6, 3]
+    if row[0] > 0:
+        print(f"  unit {u}: " + " ".join(ns(v) for v in row))
