@@ -258,14 +258,18 @@ def _oracle_stack(x, ws, shifts, pools):
     return outs
 
 
-def test_vgg16_stack_full_size_sampled():
+@pytest.mark.parametrize("path", [pytest.param(STAGED, id="staged"), pytest.param(2, id="auto")])
+def test_vgg16_stack_full_size_sampled(path):
     """BASELINE configs[4] at full size (13 layers, 224x224, batch 256, requantised,
-    max-pooled): images 0 and 255 compared layer by layer with the oracle."""
+    max-pooled): images 0 and 255 compared layer by layer with the oracle; all layers staged,
+    and per-layer AUTO as bench.py runs it (fused for the four 64/128-channel layers)."""
     from paper_1901_01965_b200.stack import ConvStack
     cfg = synth.CONFIGS["C5"]
     shifts = synth.stack_shifts("C5")
     x, ws = synth.stack_inputs("C5")
-    st = ConvStack(x.shape[0], cfg.layers, cfg.pools_after, shifts)
+    st = ConvStack(x.shape[0], cfg.layers, cfg.pools_after, shifts, path=path)
+    if path == 2:
+        assert [c.info.path for c in st.convs] == [FUSED] * 4 + [STAGED] * 9
     st.transform_filters([torch.from_numpy(w).cuda() for w in ws])
     st(torch.from_numpy(x).cuda())
     torch.cuda.synchronize()
