@@ -743,7 +743,8 @@ def main():
     ap.add_argument("--e2e-streams", type=int, default=3,
                     help="host-buffer (e2e) leg: steps in flight on separate streams, so copies overlap compute")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=24.0,
+                    help="CPU oracle baseline budget (about half of it is the timed sample)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
