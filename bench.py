@@ -254,6 +254,8 @@ def run_ours(args):
 
     # ---------------- per-kernel durations (roofline), same stream, outside the timed region
     kern = profile_kernels(conv, xs, ws, ys, S, stream, n_sets, 60)
+    # ---------------- scaling-induced error against direct convolution (outside the timed region)
+    scal_err = scaling_error(W, conv, layer, xs[0], ws[0], S, path, dev) if rank == 0 else None
     # ---------------- e2e through the C ABI with host buffers (pinned), copies inside the region
     e2e = run_e2e(conv, xs, ws, S, stream, n_sets, max(3, min(args.steps, 100)), world, dist if world > 1 else None,
                   dev, job_ops, n_streams=args.e2e_streams)
@@ -296,6 +298,7 @@ def run_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "e2e": e2e,
+            "scaling_error": scal_err,
         }
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_seconds)
@@ -451,6 +454,45 @@ def cpu_baseline_stack(shifts):
     cores = len(os.sched_getaffinity(0))
     return {"value": round(ops / t / 1e12, 6), "unit": "TOPS", "cores": cores, "kind": "oracle",
             "sample": f"oracle stack (13 layers + pools) on image 0 of C5 ({ops:.3e} direct ops); {t:.2f} s"}
+
+
+def scaling_error(W, conv, layer, x, w, S, path, dev, images=4):
+    """BASELINE north_star: the scaling-induced error against direct convolution, max-abs and mean-abs
+    in output LSBs, on the first `images` images: out32 of the same kernels (an int32-output plan) against
+    the exact direct convolution (torch float64 conv2d on the GPU: exact, |sums| < 2^53), and the bench's
+    own int8 output against the direct result requantised with the same rule (rha(v / 2^S), clamp)."""
+    import torch
+    import torch.nn.functional as F
+    if not layer.scaling:
+        return None
+    ne = min(images, x.shape[0])
+    xs = x[:ne].contiguous()
+    c32 = W.WinoConv2d(ne, layer.h, layer.w, layer.c_in, conv.w_shape[0], layer.pad, W.WINO_NHWC, True,
+                       W.WINO_OUT_INT32, device=dev.index, path=path, algorithm=conv.desc.algorithm,
+                       input_type=conv.desc.input_type, x_zero_point=conv.desc.x_zero_point,
+                       w_zero_point=conv.desc.w_zero_point, filter_target_max=conv.desc.filter_target_max)
+    c32.transform_filter(w)
+    y32 = c32(xs).long()
+    zx, zw = conv.desc.x_zero_point, conv.desc.w_zero_point
+    xf = (xs.to(torch.float64) if xs.dtype == torch.int8 else xs.to(torch.float64) - zx).permute(0, 3, 1, 2)
+    wf = (w.to(torch.float64) if w.dtype == torch.int8 else w.to(torch.float64) - zw).permute(0, 3, 1, 2)
+    ref = F.conv2d(xf, wf, padding=layer.pad).permute(0, 2, 3, 1).round().long()
+    conv.transform_filter(w)
+    y8 = conv(x, 1, S)[:ne].long()
+
+    def requant(v):
+        a = v.abs()
+        r = (a + (1 << (S - 1))) >> S if S > 0 else a
+        return torch.clamp(torch.where(v < 0, -r, r), -128, 127)
+
+    e32 = (y32 - ref).abs().double()
+    e8 = (y8 - requant(ref)).abs().double()
+    return {"images": ne, "reference": "direct convolution (torch float64 conv2d, exact)",
+            "out32_lsb": {"max_abs": int(e32.max()), "mean_abs": round(float(e32.mean()), 4),
+                          "mean_abs_ref": round(float(ref.abs().double().mean()), 2),
+                          "mean_rel": round(float(e32.mean() / ref.abs().double().mean()), 6)},
+            "y8_lsb": {"max_abs": int(e8.max()), "mean_abs": round(float(e8.mean()), 5),
+                       "frac_differing": round(float((e8 > 0).double().mean()), 5), "requant_shift": S}}
 
 
 def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps):
