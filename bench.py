@@ -254,6 +254,24 @@ def run_ours(args):
 
     # ---------------- per-kernel durations (roofline), same stream, outside the timed region
     kern = profile_kernels(conv, xs, ws, ys, S, stream, n_sets, 60)
+    # ---------------- strong scaling: gather the sharded outputs of set 0 over NCCL (checking only,
+    # outside the timed region) and compare them with rank 0's single-GPU run of the whole problem
+    sharded_check = None
+    if world > 1 and args.scaling == "strong":
+        y_loc = conv(xs[0], 1, S)
+        full_shape = (layer.n, conv.y_shape[1], conv.y_shape[2], layer.c_out)
+        y_all = SH.gather_nhwc(y_loc, full_shape, sh, world, dev)
+        if rank == 0:
+            xf, wf = synth.config_inputs(args.config, rank=0)
+            cf = W.WinoConv2d(layer.n, layer.h, layer.w, layer.c_in, layer.c_out, layer.pad, W.WINO_NHWC,
+                              layer.scaling, W.WINO_OUT_INT8, device=local_rank, path=path, algorithm=alg,
+                              input_type=conv.desc.input_type, x_zero_point=zp, w_zero_point=zp,
+                              filter_target_max=args.target)
+            cf.transform_filter(torch.from_numpy(np.ascontiguousarray(to_in(wf))).to(dev))
+            y_one = cf(torch.from_numpy(np.ascontiguousarray(to_in(xf))).to(dev), 1, S)
+            sharded_check = {"mode": sh["mode"], "gathered_bytes": int(y_all.numel()),
+                             "collective": "all_gather_into_tensor (NCCL), checking only",
+                             "equal_to_single_gpu": bool(torch.equal(y_all, y_one))}
     # ---------------- scaling-induced error against direct convolution (outside the timed region)
     scal_err = scaling_error(W, conv, layer, xs[0], ws[0], S, path, dev) if rank == 0 else None
     # ---------------- e2e through the C ABI with host buffers (pinned), copies inside the region
@@ -299,6 +317,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "e2e": e2e,
             "scaling_error": scal_err,
+            "sharded_check": sharded_check,
         }
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_seconds)
