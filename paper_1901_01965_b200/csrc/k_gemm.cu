@@ -46,8 +46,8 @@
 
 namespace wino {
 
-constexpr int kMinStages = 4, kMaxStages = 8;   // ring depth: as deep as shared memory allows
-constexpr int kKStepsPerStage = 2;
+constexpr int kMinStages = 2, kMaxStages = 8;   // ring depth: as deep as shared memory allows
+constexpr int kMaxKStepsPerStage = 4;   // K steps per ring stage: 2 or 4 (gemm_ksteps_per_stage)
 constexpr int kEpiWarps = 8;                             // 2 per TMEM lane quadrant
 constexpr int kProducerWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr int kGemmThreads = 32 * (kEpiWarps + 2);
@@ -94,22 +94,29 @@ __device__ __forceinline__ uint64_t gtimer() {
   return t;
 }
 
-__host__ __device__ inline uint32_t gemm_stage_bytes(int nblk) {
-  return 2u * kKStepsPerStage * kABytesPerKStep + 2u * kKStepsPerStage * (uint32_t)nblk * kKStep;
+__host__ __device__ inline uint32_t gemm_stage_bytes(int nblk, int kps) {
+  return 2u * kps * kABytesPerKStep + 2u * kps * (uint32_t)nblk * kKStep;
 }
 // stages + 2 staging tiles (128 x nblk int32) + barriers/LUT (1 KB) + codes [26][cout_pad]
-inline size_t gemm_smem_bytes(int nblk, int cout_pad, int stages) {
-  return (size_t)stages * gemm_stage_bytes(nblk) + 2 * (size_t)kMBlock * nblk * 4 + 1024 +
+inline size_t gemm_smem_bytes(int nblk, int cout_pad, int stages, int kps) {
+  return (size_t)stages * gemm_stage_bytes(nblk, kps) + 2 * (size_t)kMBlock * nblk * 4 + 1024 +
          (size_t)(kPrimaries + kRealPlanes) * cout_pad;
 }
 constexpr int kMaxCoutPad = 2048;
 constexpr size_t kSmemLimit = 227 * 1024;
 // ring depth: loads in flight per SM are what hides the L2/HBM latency under load
 static int g_stages_cap = kMaxStages;   // WINO_K3_STAGES (experiments): cap on the ring depth
-inline int gemm_stages(int nblk, int cout_pad) {
+inline int gemm_stages(int nblk, int cout_pad, int kps) {
   int st = g_stages_cap;
-  while (st > kMinStages && gemm_smem_bytes(nblk, cout_pad, st) > kSmemLimit) --st;
+  while (st > kMinStages && gemm_smem_bytes(nblk, cout_pad, st, kps) > kSmemLimit) --st;
   return st;
+}
+// K steps per stage: 4 when the plane has that many (fewer stages and commits per plane: C4 K3
+// 43.8 -> 38.9 us), else the plane's whole K range (2 at C2).  WINO_K3_KPS overrides (experiments).
+static int g_kps_override = 0;
+inline int gemm_ksteps_per_stage(int ksteps) {
+  if (g_kps_override == 2 || g_kps_override == 4) return g_kps_override;
+  return ksteps >= 4 ? 4 : 2;
 }
 
 template <int C>
@@ -139,7 +146,7 @@ template <int NBLK, bool F2, bool W1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ Mraw,
            const uint8_t* __restrict__ codes, int cout, int scaling, int ksteps, long long tiles_pad, int tblocks,
-           int cout_pad, int cin_pad, int nst, uint64_t* __restrict__ trace, int dbg) {
+           int cout_pad, int cin_pad, int nst, int kps, uint64_t* __restrict__ trace, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem[];
 #ifndef WINO_K3_DBG
   dbg = 0;   // the WINO_K3_DBG ablation modes exist only in debug builds (-DWINO_K3_DBG)
@@ -164,8 +171,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #endif
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t a_bytes = kKStepsPerStage * kABytesPerKStep;
-  const uint32_t b_bytes = kKStepsPerStage * (uint32_t)NBLK * kKStep;
+  const uint32_t a_bytes = kps * kABytesPerKStep;
+  const uint32_t b_bytes = kps * (uint32_t)NBLK * kKStep;
   const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
   uint8_t* staging = smem + nst * stage_bytes;                           // 2 x kTileBytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(staging + 2 * kTileBytes);
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tfull0 = smem_u32(bars + 2 * kMaxStages), tempty0 = smem_u32(bars + 2 * kMaxStages + 2);
   const int nblocks = cout_pad / NBLK;
   const int n_units = tblocks * nblocks * Alg<F2>::kUnits;
-  const int n_it = (ksteps + kKStepsPerStage - 1) / kKStepsPerStage;
+  const int n_it = (ksteps + kps - 1) / kps;
 
   if (warp == 0) {
     tmem_alloc(smem_u32(tmem_slot), kTmemCols);
@@ -227,8 +234,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int8_t* wpl = W + ((long long)plane * nblocks + nb) * ksteps * (kWRows * NBLK * kKStep);
         for (int ks = 0; ks < n_it; ks++) {
           mbar_wait(empty0 + 8 * s, ph ^ 1);
-          const int k0 = ks * kKStepsPerStage;
-          const int kn = min(kKStepsPerStage, ksteps - k0);
+          const int k0 = ks * kps;
+          const int kn = min(kps, ksteps - k0);
           const uint32_t ab = kn * 2 * kABytesPerKStep, bb = kn * kWRows * (uint32_t)NBLK * kKStep;
           const uint32_t st = sbase + s * stage_bytes;
           if (dbg & 8) {   // debug timing only (WINO_K3_DBG): no loads
@@ -264,8 +271,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(full0 + 8 * s, ph);
           tc_fence_after();
           if (ks == 0) WINO_TRACE(pc, 1);
-          const int k0 = ks * kKStepsPerStage;
-          const int kn = min(kKStepsPerStage, ksteps - k0);
+          const int k0 = ks * kps;
+          const int kn = min(kps, ksteps - k0);
           const uint32_t st = sbase + s * stage_bytes;
           for (int kk = 0; kk < kn; ++kk) {
             const uint64_t a_hi = umma_desc(st + (2 * kk) * kABytesPerKStep, 128, 256);
@@ -433,19 +440,20 @@ cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t*
     const int rounds = (n_units + grid - 1) / grid;
     grid = (n_units + rounds - 1) / rounds;
   }
-  const int nst = gemm_stages(g.nblk, g.cout_pad);
-  const size_t smem = gemm_smem_bytes(g.nblk, g.cout_pad, nst);
+  const int kps = gemm_ksteps_per_stage(g.ksteps);
+  const int nst = gemm_stages(g.nblk, g.cout_pad, kps);
+  const size_t smem = gemm_smem_bytes(g.nblk, g.cout_pad, nst, kps);
   cudaError_t e;
 #define WINO_LAUNCH_GEMM(N)                                                                                 \
   e = g.alg == 1 ? launch_pdl(k_gemm<N, true, false>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw,  \
                               codes, g.cout, g.scaling, g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad,         \
-                              g.cin_pad, nst, g_trace, g_gemm_dbg)                                                                 \
+                              g.cin_pad, nst, kps, g_trace, g_gemm_dbg)                                                                 \
       : g.w1 ? launch_pdl(k_gemm<N, false, true>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw,     \
                           codes, g.cout, g.scaling, g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad,  \
-                          nst, g_trace, g_gemm_dbg)                                                                                \
+                          nst, kps, g_trace, g_gemm_dbg)                                                                                \
              : launch_pdl(k_gemm<N, false, false>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw,    \
                           codes, g.cout, g.scaling, g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad,  \
-                          nst, g_trace, g_gemm_dbg)
+                          nst, kps, g_trace, g_gemm_dbg)
   switch (g.nblk) {
     case 16: WINO_LAUNCH_GEMM(16); break;
     case 32: WINO_LAUNCH_GEMM(32); break;
@@ -462,6 +470,7 @@ cudaError_t setup_gemm() {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (const char* d = std::getenv("WINO_K3_DBG")) g_gemm_dbg = std::atoi(d);
   if (const char* d = std::getenv("WINO_K3_BALANCE")) g_gemm_balance = std::atoi(d);
+  if (const char* d = std::getenv("WINO_K3_KPS")) g_kps_override = std::atoi(d);
   if (const char* d = std::getenv("WINO_K3_STAGES")) g_stages_cap = std::max(kMinStages, std::min(kMaxStages, std::atoi(d)));
   auto attr = [&](const void* f, int nblk) {
     if (e == cudaSuccess)
