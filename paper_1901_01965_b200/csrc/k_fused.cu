@@ -131,7 +131,10 @@ __host__ __device__ constexpr int re_y(int n) { return (n & 3) == 1 ? -1 : ((n &
 __host__ __device__ constexpr int im_x(int n) { return (n & 3) == 1 ? 1 : ((n & 3) == 3 ? -1 : 0); }
 __host__ __device__ constexpr int im_y(int n) { return re_x(n); }
 
-template <bool NHWC, bool OUT8, bool RQFAST>
+// MG (c_in <= 64, i.e. ksteps <= 2): a real pair's whole K range is ONE ring stage (its two groups'
+// V and W' are contiguous), 18 stages per unit instead of 26 -- each stage costs ~350 cycles of
+// copy issue.  The MG loops are separate code, so the general loops stay as they are.
+template <bool NHWC, bool OUT8, bool RQFAST, bool MG>
 __global__ void __launch_bounds__(kFThreads, 1)
     k_fused(const int8_t* __restrict__ V, const int8_t* __restrict__ W, const uint8_t* __restrict__ codes, Geom g,
             int n0, int imgs, int tblocks, int32_t rq_mult, int rq_shift, void* __restrict__ y, int dbg,
@@ -195,6 +198,32 @@ __global__ void __launch_bounds__(kFThreads, 1)
       // ------------------------------------------------ producers: warp p issues the stages it with it % P == p
       const int pw = warp - kFProducerWarp;
       int it = 0;
+      if constexpr (MG) {
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+          const int tb = u / nblocks, nb = u - tb * nblocks;
+          for (int sg = 0; sg < kFSlotGroups; sg++) {
+            const int g0 = sg_first(sg), ng = sg_count(sg);
+            for (int q = 0; q < (ng == 2 ? 1 : ng); q++, it++) {   // one stage per slot-group
+              if (it % kFProducers != pw) continue;
+              const int gi = g0 + q;
+              const int8_t* vg = V + ((long long)tb * kVPiecesF + fg_vprefix(gi)) * ksteps * kVBlockBytes;
+              const int8_t* wg = W + ((long long)nb * kWRowUnitsF + fg_wprefix(gi)) * ksteps * 1024;
+              const int s = it % kFStages;
+              mbar_wait(empty0 + 8 * s, ((it / kFStages) & 1) ^ 1);
+              // pair: pieces 2 + 2, W' units 1 + 1; complex group: 4 pieces, 4 W' units (all K steps)
+              const int pcs = ng == 2 ? 4 : fg_pieces(gi), wu = ng == 2 ? 2 : fg_wunits(gi);
+              const uint32_t vb = (uint32_t)(ksteps * pcs) * kVBlockBytes, wb = (uint32_t)(ksteps * wu) * 1024;
+              const uint32_t st = sbase + s * kFStageBytes;
+              if (elect_one()) {
+                mbar_arrive_expect_tx(full0 + 8 * s, vb + wb);
+                bulk_g2s(st, vg, vb, full0 + 8 * s);
+                bulk_g2s(st + kFStageV, wg, wb, full0 + 8 * s);
+              }
+              __syncwarp();
+            }
+          }
+        }
+      } else
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int tb = u / nblocks, nb = u - tb * nblocks;
         for (int gi = 0; gi < kFGroupsN; gi++) {
@@ -225,6 +254,64 @@ __global__ void __launch_bounds__(kFThreads, 1)
       const uint32_t id16 = idesc_i8(kMBlock, 16, 1, 1), id32 = idesc_i8(kMBlock, 32, 1, 1),
                      id64 = idesc_i8(kMBlock, 64, 1, 1);
       int it = 0, sgc = 0;
+      if constexpr (MG) {
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+          for (int sg = 0; sg < kFSlotGroups; sg++, sgc++, it++) {   // one stage per slot-group
+            const int b = sgc % kFSlots;
+            mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
+            tc_fence_after();
+            const int g0 = sg_first(sg), ng = sg_count(sg);
+            const int s = it % kFStages;
+            mbar_wait(full0 + 8 * s, (it / kFStages) & 1);
+            tc_fence_after();
+            const uint32_t st = sbase + s * kFStageBytes;
+            const uint32_t d0 = tmem + b * kFSlotCols;
+            if (elect_one()) {
+              if (ng == 2) {   // real pair: group q's V at q * 2 ksteps blocks, W' at q * ksteps KB
+                for (int q = 0; q < 2; ++q) {
+                  const uint32_t d = d0 + q * 48;
+                  const uint32_t va = st + (uint32_t)(q * 2 * ksteps) * kVBlockBytes;
+                  const uint32_t wa = st + kFStageV + (uint32_t)(q * ksteps) * 1024;
+                  for (int kk = 0; kk < ksteps; ++kk) {
+                    const uint64_t ah = umma_desc(va + (2 * kk) * kVBlockBytes, 128, 256);
+                    const uint64_t al = umma_desc(va + (2 * kk + 1) * kVBlockBytes, 128, 256);
+                    const uint64_t bb = umma_desc(wa + kk * 1024, 128, 256), bl = umma_desc(wa + kk * 1024 + 512, 128, 256);
+                    umma_i8(d, ah, bb, id32, kk == 0 ? 0u : 1u);             // [s16 | s8]
+                    if (kk == 0) {
+                      umma_i8(d + 32, al, bl, id16, 0u);                     // s0
+                      umma_i8(d + 16, al, bb, id16, 1u);                     // s8 += lo.hi
+                    } else {
+                      umma_i8(d + 16, al, bb, id32, 1u);                     // [s8 | s0]
+                    }
+                  }
+                }
+              } else {         // complex group: all K steps in the stage
+                for (int kk = 0; kk < ksteps; ++kk) {
+                  const uint32_t a0 = st + (4 * kk) * kVBlockBytes;
+                  const uint64_t rh = umma_desc(a0, 128, 256), rl = umma_desc(a0 + kVBlockBytes, 128, 256);
+                  const uint64_t ih = umma_desc(a0 + 2 * kVBlockBytes, 128, 256),
+                                 il = umma_desc(a0 + 3 * kVBlockBytes, 128, 256);
+                  const uint32_t bw = st + kFStageV + kk * 4096;
+                  const uint64_t b0 = umma_desc(bw, 128, 256), b0l = umma_desc(bw + 1024, 128, 256);
+                  const uint64_t b1 = umma_desc(bw + 2048, 128, 256);
+                  umma_i8(d0, rh, b0, id64, kk == 0 ? 0u : 1u);
+                  if (kk == 0) {
+                    umma_i8(d0 + 64, rl, b0l, id32, 0u);
+                    umma_i8(d0 + 32, rl, b0, id32, 1u);
+                  } else {
+                    umma_i8(d0 + 32, rl, b0, id64, 1u);
+                  }
+                  umma_i8(d0, ih, b1, id64, 1u);
+                  umma_i8(d0 + 32, il, b1, id64, 1u);
+                }
+              }
+              umma_commit(empty0 + 8 * s);    // stage reusable once these MMAs have read it
+              umma_commit(tfull0 + 8 * b);    // slot complete
+            }
+            __syncwarp();
+          }
+        }
+      } else
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         for (int sg = 0; sg < kFSlotGroups; sg++, sgc++) {
           const int b = sgc % kFSlots;
@@ -633,6 +720,7 @@ static int g_fused_dbg = 0;
 // freed SMs run the other streams' kernels for the whole launch (C2 190.7 -> 203.1, C3 310.7 -> 332.1 TOPS
 // with three batches in flight); WINO_FUSED_BALANCE=0 restores the full grid (experiments)
 static int g_fused_balance = 1;
+static int g_fused_merge = 1;   // WINO_FUSED_MERGE=0: the general loops at c_in <= 64 too (experiments)
 
 cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
                          const int8_t* wimg, const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y,
@@ -649,8 +737,11 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 20;
   cudaError_t e;
 #define WINO_KF(A, B, C)                                                                                       \
-  e = launch_pdl(k_fused<A, B, C>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs, tblocks, \
-                 rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)
+  e = g.ksteps <= 2 && g_fused_merge                                                                             \
+          ? launch_pdl(k_fused<A, B, C, true>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs, \
+                       tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
+          : launch_pdl(k_fused<A, B, C, false>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0,     \
+                       imgs, tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)
   if (nhwc) {
     if (!out8) WINO_KF(true, false, false);
     else if (fast) WINO_KF(true, true, true);
@@ -670,9 +761,11 @@ cudaError_t setup_fused() {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_fused_sms, cudaDevAttrMultiProcessorCount, dev);
   if (const char* d = std::getenv("WINO_FUSED_DBG")) g_fused_dbg = std::atoi(d);
   if (const char* d = std::getenv("WINO_FUSED_BALANCE")) g_fused_balance = std::atoi(d);
+  if (const char* d = std::getenv("WINO_FUSED_MERGE")) g_fused_merge = std::atoi(d);
   const int smem = (int)fused_smem_bytes();
-#define WINO_KF_ATTR(A, B, C) \
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+#define WINO_KF_ATTR(A, B, C)                                                                                     \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
   WINO_KF_ATTR(true, false, false);
   WINO_KF_ATTR(true, true, true);
   WINO_KF_ATTR(true, true, false);
