@@ -209,7 +209,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
               const int8_t* vg = V + ((long long)tb * kVPiecesF + fg_vprefix(gi)) * ksteps * kVBlockBytes;
               const int8_t* wg = W + ((long long)nb * kWRowUnitsF + fg_wprefix(gi)) * ksteps * 1024;
               const int s = it % kFStages;
-              mbar_wait(empty0 + 8 * s, ((it / kFStages) & 1) ^ 1);
+              // stage s last held slot-group it - kFStages: its accumulator commit (tfull) also covers the
+              // MMAs that read the stage, so no separate stage commit is needed (tfull cannot have moved on:
+              // its next commit is slot-group it's, whose operands are loaded here)
+              static_assert(kFStages == kFSlots, "one stage per slot-group: stage s <-> slot s");
+              if (it >= kFStages) mbar_wait(tfull0 + 8 * s, ((it - kFStages) / kFSlots) & 1);
               // pair: pieces 2 + 2, W' units 1 + 1; complex group: 4 pieces, 4 W' units (all K steps)
               const int pcs = ng == 2 ? 4 : fg_pieces(gi), wu = ng == 2 ? 2 : fg_wunits(gi);
               const uint32_t vb = (uint32_t)(ksteps * pcs) * kVBlockBytes, wb = (uint32_t)(ksteps * wu) * 1024;
@@ -305,8 +309,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
                   umma_i8(d0 + 32, il, b1, id64, 1u);
                 }
               }
-              umma_commit(empty0 + 8 * s);    // stage reusable once these MMAs have read it
-              umma_commit(tfull0 + 8 * b);    // slot complete
+              umma_commit(tfull0 + 8 * b);    // slot complete (and stage s free, see the producer)
             }
             __syncwarp();
           }
