@@ -131,10 +131,12 @@ __host__ __device__ constexpr int re_y(int n) { return (n & 3) == 1 ? -1 : ((n &
 __host__ __device__ constexpr int im_x(int n) { return (n & 3) == 1 ? 1 : ((n & 3) == 3 ? -1 : 0); }
 __host__ __device__ constexpr int im_y(int n) { return re_x(n); }
 
-// MG (c_in <= 64, i.e. ksteps <= 2): a real pair's whole K range is ONE ring stage (its two groups'
-// V and W' are contiguous), 18 stages per unit instead of 26 -- each stage costs ~350 cycles of
-// copy issue.  The MG loops are separate code, so the general loops stay as they are.
-template <bool NHWC, bool OUT8, bool RQFAST, bool MG>
+// MG > 0: ONE ring stage per slot-group (a real pair's or a complex group's whole K range; the pair's
+// V and W' are contiguous), 18 stages per unit instead of 26 (c_in <= 64) or 36 (c_in <= 128) -- each
+// stage costs ~350 cycles of copy issue plus a commit.  MG = 1 (c_in <= 64): 4 stages of
+// 40 KB; MG = 2 (c_in <= 128): 2 stages of 80 KB (the same 160 KB).  The MG loops are separate code, so
+// the general loops (MG = 0) stay as they are.
+template <bool NHWC, bool OUT8, bool RQFAST, int MG>
 __global__ void __launch_bounds__(kFThreads, 1)
     k_fused(const int8_t* __restrict__ V, const int8_t* __restrict__ W, const uint8_t* __restrict__ codes, Geom g,
             int n0, int imgs, int tblocks, int32_t rq_mult, int rq_shift, void* __restrict__ y, int dbg,
@@ -198,7 +200,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
       // ------------------------------------------------ producers: warp p issues the stages it with it % P == p
       const int pw = warp - kFProducerWarp;
       int it = 0;
-      if constexpr (MG) {
+      if constexpr (MG > 0) {
+        constexpr int kMgStages = MG == 2 ? 2 : 4;
+        constexpr uint32_t kMgStageBytes = kFStages * kFStageBytes / kMgStages, kMgStageV = MG == 2 ? 65536 : kFStageV;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
           const int tb = u / nblocks, nb = u - tb * nblocks;
           for (int sg = 0; sg < kFSlotGroups; sg++) {
@@ -208,20 +212,21 @@ __global__ void __launch_bounds__(kFThreads, 1)
               const int gi = g0 + q;
               const int8_t* vg = V + ((long long)tb * kVPiecesF + fg_vprefix(gi)) * ksteps * kVBlockBytes;
               const int8_t* wg = W + ((long long)nb * kWRowUnitsF + fg_wprefix(gi)) * ksteps * 1024;
-              const int s = it % kFStages;
-              // stage s last held slot-group it - kFStages: its accumulator commit (tfull) also covers the
+              const int s = it % kMgStages;
+              // stage s last held slot-group it - kMgStages: its accumulator commit (tfull) also covers the
               // MMAs that read the stage, so no separate stage commit is needed (tfull cannot have moved on:
-              // its next commit is slot-group it's, whose operands are loaded here)
-              static_assert(kFStages == kFSlots, "one stage per slot-group: stage s <-> slot s");
-              if (it >= kFStages) mbar_wait(tfull0 + 8 * s, ((it - kFStages) / kFSlots) & 1);
+              // its next commit is slot-group it - kMgStages + 4 >= it's, whose operands are loaded here)
+              static_assert(kMgStages <= kFSlots, "stage reuse must precede the slot's next commit");
+              if (it >= kMgStages)
+                mbar_wait(tfull0 + 8 * ((it - kMgStages) % kFSlots), ((it - kMgStages) / kFSlots) & 1);
               // pair: pieces 2 + 2, W' units 1 + 1; complex group: 4 pieces, 4 W' units (all K steps)
               const int pcs = ng == 2 ? 4 : fg_pieces(gi), wu = ng == 2 ? 2 : fg_wunits(gi);
               const uint32_t vb = (uint32_t)(ksteps * pcs) * kVBlockBytes, wb = (uint32_t)(ksteps * wu) * 1024;
-              const uint32_t st = sbase + s * kFStageBytes;
+              const uint32_t st = sbase + s * kMgStageBytes;
               if (elect_one()) {
                 mbar_arrive_expect_tx(full0 + 8 * s, vb + wb);
                 bulk_g2s(st, vg, vb, full0 + 8 * s);
-                bulk_g2s(st + kFStageV, wg, wb, full0 + 8 * s);
+                bulk_g2s(st + kMgStageV, wg, wb, full0 + 8 * s);
               }
               __syncwarp();
             }
@@ -258,24 +263,26 @@ __global__ void __launch_bounds__(kFThreads, 1)
       const uint32_t id16 = idesc_i8(kMBlock, 16, 1, 1), id32 = idesc_i8(kMBlock, 32, 1, 1),
                      id64 = idesc_i8(kMBlock, 64, 1, 1);
       int it = 0, sgc = 0;
-      if constexpr (MG) {
+      if constexpr (MG > 0) {
+        constexpr int kMgStages = MG == 2 ? 2 : 4;
+        constexpr uint32_t kMgStageBytes = kFStages * kFStageBytes / kMgStages, kMgStageV = MG == 2 ? 65536 : kFStageV;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
           for (int sg = 0; sg < kFSlotGroups; sg++, sgc++, it++) {   // one stage per slot-group
             const int b = sgc % kFSlots;
             mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
             tc_fence_after();
             const int g0 = sg_first(sg), ng = sg_count(sg);
-            const int s = it % kFStages;
-            mbar_wait(full0 + 8 * s, (it / kFStages) & 1);
+            const int s = it % kMgStages;
+            mbar_wait(full0 + 8 * s, (it / kMgStages) & 1);
             tc_fence_after();
-            const uint32_t st = sbase + s * kFStageBytes;
+            const uint32_t st = sbase + s * kMgStageBytes;
             const uint32_t d0 = tmem + b * kFSlotCols;
             if (elect_one()) {
               if (ng == 2) {   // real pair: group q's V at q * 2 ksteps blocks, W' at q * ksteps KB
                 for (int q = 0; q < 2; ++q) {
                   const uint32_t d = d0 + q * 48;
                   const uint32_t va = st + (uint32_t)(q * 2 * ksteps) * kVBlockBytes;
-                  const uint32_t wa = st + kFStageV + (uint32_t)(q * ksteps) * 1024;
+                  const uint32_t wa = st + kMgStageV + (uint32_t)(q * ksteps) * 1024;
                   for (int kk = 0; kk < ksteps; ++kk) {
                     const uint64_t ah = umma_desc(va + (2 * kk) * kVBlockBytes, 128, 256);
                     const uint64_t al = umma_desc(va + (2 * kk + 1) * kVBlockBytes, 128, 256);
@@ -295,7 +302,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
                   const uint64_t rh = umma_desc(a0, 128, 256), rl = umma_desc(a0 + kVBlockBytes, 128, 256);
                   const uint64_t ih = umma_desc(a0 + 2 * kVBlockBytes, 128, 256),
                                  il = umma_desc(a0 + 3 * kVBlockBytes, 128, 256);
-                  const uint32_t bw = st + kFStageV + kk * 4096;
+                  const uint32_t bw = st + kMgStageV + kk * 4096;
                   const uint64_t b0 = umma_desc(bw, 128, 256), b0l = umma_desc(bw + 1024, 128, 256);
                   const uint64_t b1 = umma_desc(bw + 2048, 128, 256);
                   umma_i8(d0, rh, b0, id64, kk == 0 ? 0u : 1u);
@@ -723,7 +730,8 @@ static int g_fused_dbg = 0;
 // freed SMs run the other streams' kernels for the whole launch (C2 190.7 -> 203.1, C3 310.7 -> 332.1 TOPS
 // with three batches in flight); WINO_FUSED_BALANCE=0 restores the full grid (experiments)
 static int g_fused_balance = 1;
-static int g_fused_merge = 1;   // WINO_FUSED_MERGE=0: the general loops at c_in <= 64 too (experiments)
+static int g_fused_merge = 2;   // WINO_FUSED_MERGE: 0 general loops only, 1 merged stages at c_in <= 64,
+                                // 2 also at c_in <= 128 (experiments)
 
 cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
                          const int8_t* wimg, const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y,
@@ -740,11 +748,14 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 20;
   cudaError_t e;
 #define WINO_KF(A, B, C)                                                                                       \
-  e = g.ksteps <= 2 && g_fused_merge                                                                             \
-          ? launch_pdl(k_fused<A, B, C, true>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs, \
+  e = g.ksteps <= 2 && g_fused_merge >= 1                                                                        \
+          ? launch_pdl(k_fused<A, B, C, 1>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
                        tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
-          : launch_pdl(k_fused<A, B, C, false>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0,     \
-                       imgs, tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)
+      : g.ksteps <= 4 && g_fused_merge >= 2                                                                      \
+          ? launch_pdl(k_fused<A, B, C, 2>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
+                       tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
+          : launch_pdl(k_fused<A, B, C, 0>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
+                       tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)
   if (nhwc) {
     if (!out8) WINO_KF(true, false, false);
     else if (fast) WINO_KF(true, true, true);
@@ -767,8 +778,9 @@ cudaError_t setup_fused() {
   if (const char* d = std::getenv("WINO_FUSED_MERGE")) g_fused_merge = std::atoi(d);
   const int smem = (int)fused_smem_bytes();
 #define WINO_KF_ATTR(A, B, C)                                                                                     \
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
   WINO_KF_ATTR(true, false, false);
   WINO_KF_ATTR(true, true, true);
   WINO_KF_ATTR(true, true, false);
