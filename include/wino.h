@@ -79,9 +79,9 @@ typedef struct {
                              transform + store (M'' stays on chip).
                              WINO_PATH_STAGED (1): K2, K3 GEMMs -> M'' in the workspace,
                              K4 output transform (M'' inspectable, see wino_plan_info).
-                             WINO_PATH_AUTO (2): fused when c_in * c_out <= 128 * 128 and
-                             the variant allows it (F4x4, int8, target 255), else
-                             staged; wino_plan_info.path reports the choice.           */
+                             WINO_PATH_AUTO (2): fused when c_in <= 128 and the variant
+                             allows it (F4x4, int8, target 255), else staged;
+                             wino_plan_info.path reports the choice.                   */
     int algorithm;        /* WINO_ALG_F4X4 (0, default): complex F(4x4,3x3) over the
                              Gaussian integers, points {0, +-1, +-i};
                              WINO_ALG_F2X2 (1): rational F(2x2,3x3), G' = 2G,

@@ -91,12 +91,13 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   *out = nullptr;
   if (desc->path != WINO_PATH_FUSED && desc->path != WINO_PATH_STAGED && desc->path != WINO_PATH_AUTO)
     return WINO_ERR_INVALID_ARG;
-  // WINO_PATH_AUTO: the fused kernel where it measured faster (C2/C3: c_in c_out <= 128 x 128 and the
-  // variants it implements: F(4x4), int8, target 255), else staged
+  // WINO_PATH_AUTO: the fused kernel where it measured faster -- c_in <= 128, where its ring holds one
+  // stage per slot-group (tools/path_ab.py: 64..128 -> 64..256 channels), for the variants it implements
+  // (F(4x4), int8, target 255) -- else staged
   wino_conv_desc dr = *desc;
   if (dr.path == WINO_PATH_AUTO)
     dr.path = (dr.algorithm == WINO_ALG_F4X4 && dr.input_type == WINO_IN_INT8 && dr.filter_target_max == 255 &&
-               (long long)dr.c_in * dr.c_out <= 128ll * 128)
+               dr.c_in <= 128)
                   ? WINO_PATH_FUSED
                   : WINO_PATH_STAGED;
   const wino_conv_desc& d = dr;
