@@ -200,7 +200,49 @@ __global__ void __launch_bounds__(kFThreads, 1)
       // ------------------------------------------------ producers: warp p issues the stages it with it % P == p
       const int pw = warp - kFProducerWarp;
       int it = 0;
-      if constexpr (MG > 0) {
+      if constexpr (MG == 3) {
+        // two 80 KB stages, each 4 K steps of one slot-group (a pair: both groups' chunks, 2 + 2 copies),
+        // released by stage commits as in the general loops
+        constexpr uint32_t kSB = kFStages * kFStageBytes / 2, kSV = 65536;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+          const int tb = u / nblocks, nb = u - tb * nblocks;
+          for (int sg = 0; sg < kFSlotGroups; sg++) {
+            const int g0 = sg_first(sg), ng = sg_count(sg);
+            for (int k0 = 0; k0 < ksteps; k0 += 4, it++) {
+              if (it % kFProducers != pw) continue;
+              const int s = it & 1;
+              mbar_wait(empty0 + 8 * s, ((it >> 1) & 1) ^ 1);
+              const int kn = min(4, ksteps - k0);
+              const uint32_t st = sbase + s * kSB;
+              if (elect_one()) {
+                if (ng == 2) {   // group q: V at q * 32 KB, W' at kSV + q * 4 KB
+                  const uint32_t vbq = (uint32_t)(kn * 2) * kVBlockBytes, wbq = (uint32_t)kn * 1024;
+                  mbar_arrive_expect_tx(full0 + 8 * s, 2 * (vbq + wbq));
+                  for (int q = 0; q < 2; q++) {
+                    const int gi = g0 + q;
+                    const int8_t* vg = V + ((long long)tb * kVPiecesF + fg_vprefix(gi)) * ksteps * kVBlockBytes +
+                                       (long long)k0 * 2 * kVBlockBytes;
+                    const int8_t* wg = W + ((long long)nb * kWRowUnitsF + fg_wprefix(gi)) * ksteps * 1024 +
+                                       (long long)k0 * 1024;
+                    bulk_g2s(st + q * 32768u, vg, vbq, full0 + 8 * s);
+                    bulk_g2s(st + kSV + q * 4096u, wg, wbq, full0 + 8 * s);
+                  }
+                } else {
+                  const uint32_t vb = (uint32_t)(kn * 4) * kVBlockBytes, wb = (uint32_t)(kn * 4) * 1024;
+                  const int8_t* vg = V + ((long long)tb * kVPiecesF + fg_vprefix(g0)) * ksteps * kVBlockBytes +
+                                     (long long)k0 * 4 * kVBlockBytes;
+                  const int8_t* wg = W + ((long long)nb * kWRowUnitsF + fg_wprefix(g0)) * ksteps * 1024 +
+                                     (long long)k0 * 4 * 1024;
+                  mbar_arrive_expect_tx(full0 + 8 * s, vb + wb);
+                  bulk_g2s(st, vg, vb, full0 + 8 * s);
+                  bulk_g2s(st + kSV, wg, wb, full0 + 8 * s);
+                }
+              }
+              __syncwarp();
+            }
+          }
+        }
+      } else if constexpr (MG > 0) {
         constexpr int kMgStages = MG == 2 ? 2 : 4;
         constexpr uint32_t kMgStageBytes = kFStages * kFStageBytes / kMgStages, kMgStageV = MG == 2 ? 65536 : kFStageV;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -263,7 +305,70 @@ __global__ void __launch_bounds__(kFThreads, 1)
       const uint32_t id16 = idesc_i8(kMBlock, 16, 1, 1), id32 = idesc_i8(kMBlock, 32, 1, 1),
                      id64 = idesc_i8(kMBlock, 64, 1, 1);
       int it = 0, sgc = 0;
-      if constexpr (MG > 0) {
+      if constexpr (MG == 3) {
+        constexpr uint32_t kSB = kFStages * kFStageBytes / 2, kSV = 65536;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+          for (int sg = 0; sg < kFSlotGroups; sg++, sgc++) {
+            const int b = sgc % kFSlots;
+            mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
+            tc_fence_after();
+            const int g0 = sg_first(sg), ng = sg_count(sg);
+            const uint32_t d0 = tmem + b * kFSlotCols;
+            for (int k0 = 0; k0 < ksteps; k0 += 4, it++) {
+              const int s = it & 1;
+              mbar_wait(full0 + 8 * s, (it >> 1) & 1);
+              tc_fence_after();
+              const int kn = min(4, ksteps - k0);
+              const uint32_t st = sbase + s * kSB;
+              if (elect_one()) {
+                if (ng == 2) {
+                  for (int q = 0; q < 2; ++q) {
+                    const uint32_t d = d0 + q * 48;
+                    const uint32_t va = st + q * 32768u, wa = st + kSV + q * 4096u;
+                    for (int kk = 0; kk < kn; ++kk) {
+                      const bool first = k0 + kk == 0;
+                      const uint64_t ah = umma_desc(va + (2 * kk) * kVBlockBytes, 128, 256);
+                      const uint64_t al = umma_desc(va + (2 * kk + 1) * kVBlockBytes, 128, 256);
+                      const uint64_t bb = umma_desc(wa + kk * 1024, 128, 256), bl = umma_desc(wa + kk * 1024 + 512, 128, 256);
+                      umma_i8(d, ah, bb, id32, first ? 0u : 1u);
+                      if (first) {
+                        umma_i8(d + 32, al, bl, id16, 0u);
+                        umma_i8(d + 16, al, bb, id16, 1u);
+                      } else {
+                        umma_i8(d + 16, al, bb, id32, 1u);
+                      }
+                    }
+                  }
+                } else {
+                  for (int kk = 0; kk < kn; ++kk) {
+                    const bool first = k0 + kk == 0;
+                    const uint32_t a0 = st + (4 * kk) * kVBlockBytes;
+                    const uint64_t rh = umma_desc(a0, 128, 256), rl = umma_desc(a0 + kVBlockBytes, 128, 256);
+                    const uint64_t ih = umma_desc(a0 + 2 * kVBlockBytes, 128, 256),
+                                   il = umma_desc(a0 + 3 * kVBlockBytes, 128, 256);
+                    const uint32_t bw = st + kSV + kk * 4096;
+                    const uint64_t b0 = umma_desc(bw, 128, 256), b0l = umma_desc(bw + 1024, 128, 256);
+                    const uint64_t b1 = umma_desc(bw + 2048, 128, 256);
+                    umma_i8(d0, rh, b0, id64, first ? 0u : 1u);
+                    if (first) {
+                      umma_i8(d0 + 64, rl, b0l, id32, 0u);
+                      umma_i8(d0 + 32, rl, b0, id32, 1u);
+                    } else {
+                      umma_i8(d0 + 32, rl, b0, id64, 1u);
+                    }
+                    umma_i8(d0, ih, b1, id64, 1u);
+                    umma_i8(d0 + 32, il, b1, id64, 1u);
+                  }
+                }
+                umma_commit(empty0 + 8 * s);   // stage reusable once these MMAs have read it
+              }
+              __syncwarp();
+            }
+            if (elect_one()) umma_commit(tfull0 + 8 * b);   // slot complete
+            __syncwarp();
+          }
+        }
+      } else if constexpr (MG > 0) {
         constexpr int kMgStages = MG == 2 ? 2 : 4;
         constexpr uint32_t kMgStageBytes = kFStages * kFStageBytes / kMgStages, kMgStageV = MG == 2 ? 65536 : kFStageV;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -730,8 +835,8 @@ static int g_fused_dbg = 0;
 // freed SMs run the other streams' kernels for the whole launch (C2 190.7 -> 203.1, C3 310.7 -> 332.1 TOPS
 // with three batches in flight); WINO_FUSED_BALANCE=0 restores the full grid (experiments)
 static int g_fused_balance = 1;
-static int g_fused_merge = 2;   // WINO_FUSED_MERGE: 0 general loops only, 1 merged stages at c_in <= 64,
-                                // 2 also at c_in <= 128 (experiments)
+static int g_fused_merge = 3;   // WINO_FUSED_MERGE: 0 general loops only, 1 merged stages at c_in <= 64,
+                                // 2 also at c_in <= 128, 3 also 4-K-step slot-group stages at c_in <= 256
 
 cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
                          const int8_t* wimg, const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y,
@@ -753,6 +858,9 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
                        tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
       : g.ksteps <= 4 && g_fused_merge >= 2                                                                      \
           ? launch_pdl(k_fused<A, B, C, 2>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
+                       tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
+      : g.ksteps <= 8 && g_fused_merge >= 3                                                                      \
+          ? launch_pdl(k_fused<A, B, C, 3>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
                        tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
           : launch_pdl(k_fused<A, B, C, 0>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
                        tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)
@@ -780,7 +888,8 @@ cudaError_t setup_fused() {
 #define WINO_KF_ATTR(A, B, C)                                                                                     \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
   WINO_KF_ATTR(true, false, false);
   WINO_KF_ATTR(true, true, true);
   WINO_KF_ATTR(true, true, false);
