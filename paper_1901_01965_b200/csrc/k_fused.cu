@@ -111,6 +111,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[4][4]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// zero 4 columns of this warp's lane quadrant (accumulators of the MG variants start from zero, so every
+// UMMA accumulates and the first K step needs no split)
+__device__ __forceinline__ void tmem_zero4(uint32_t taddr) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %1, %1, %1};" ::"r"(taddr), "r"(0) : "memory");
+}
 
 // M'' = rha(v m / 2^q) (A9) evaluated as rha(v m' / 2^7) with
 // m' = m 2^(7-q) (q in [4,7], so m' <= 2040): one constant per (position, cout)
@@ -193,6 +198,18 @@ __global__ void __launch_bounds__(kFThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if constexpr (MG > 0) {   // every accumulator slot starts at zero (the epilogue re-zeroes each after reading)
+    if (warp < kFEpiWarps) {
+      const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * kFC;
+      for (int b = 0; b < kFSlots; b++)
+#pragma unroll
+        for (int blk = 0; blk < 6; blk++) tmem_zero4(lb + b * kFSlotCols + blk * 16);
+      tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   pdl_wait();   // V (and W', codes) come from the kernels just before
 
   if (warp >= kFProducerWarp && warp < kFProducerWarp + kFProducers) {
@@ -269,6 +286,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 mbar_arrive_expect_tx(full0 + 8 * s, vb + wb);
                 bulk_g2s(st, vg, vb, full0 + 8 * s);
                 bulk_g2s(st + kMgStageV, wg, wb, full0 + 8 * s);
+                if (it < 64) FTRACE(it, 0);
               }
               __syncwarp();
             }
@@ -325,37 +343,24 @@ __global__ void __launch_bounds__(kFThreads, 1)
                   for (int q = 0; q < 2; ++q) {
                     const uint32_t d = d0 + q * 48;
                     const uint32_t va = st + q * 32768u, wa = st + kSV + q * 4096u;
-                    for (int kk = 0; kk < kn; ++kk) {
-                      const bool first = k0 + kk == 0;
+                    for (int kk = 0; kk < kn; ++kk) {   // slots start at zero: every UMMA accumulates
                       const uint64_t ah = umma_desc(va + (2 * kk) * kVBlockBytes, 128, 256);
                       const uint64_t al = umma_desc(va + (2 * kk + 1) * kVBlockBytes, 128, 256);
-                      const uint64_t bb = umma_desc(wa + kk * 1024, 128, 256), bl = umma_desc(wa + kk * 1024 + 512, 128, 256);
-                      umma_i8(d, ah, bb, id32, first ? 0u : 1u);
-                      if (first) {
-                        umma_i8(d + 32, al, bl, id16, 0u);
-                        umma_i8(d + 16, al, bb, id16, 1u);
-                      } else {
-                        umma_i8(d + 16, al, bb, id32, 1u);
-                      }
+                      const uint64_t bb = umma_desc(wa + kk * 1024, 128, 256);
+                      umma_i8(d, ah, bb, id32, 1u);
+                      umma_i8(d + 16, al, bb, id32, 1u);
                     }
                   }
                 } else {
                   for (int kk = 0; kk < kn; ++kk) {
-                    const bool first = k0 + kk == 0;
                     const uint32_t a0 = st + (4 * kk) * kVBlockBytes;
                     const uint64_t rh = umma_desc(a0, 128, 256), rl = umma_desc(a0 + kVBlockBytes, 128, 256);
                     const uint64_t ih = umma_desc(a0 + 2 * kVBlockBytes, 128, 256),
                                    il = umma_desc(a0 + 3 * kVBlockBytes, 128, 256);
                     const uint32_t bw = st + kSV + kk * 4096;
-                    const uint64_t b0 = umma_desc(bw, 128, 256), b0l = umma_desc(bw + 1024, 128, 256);
-                    const uint64_t b1 = umma_desc(bw + 2048, 128, 256);
-                    umma_i8(d0, rh, b0, id64, first ? 0u : 1u);
-                    if (first) {
-                      umma_i8(d0 + 64, rl, b0l, id32, 0u);
-                      umma_i8(d0 + 32, rl, b0, id32, 1u);
-                    } else {
-                      umma_i8(d0 + 32, rl, b0, id64, 1u);
-                    }
+                    const uint64_t b0 = umma_desc(bw, 128, 256), b1 = umma_desc(bw + 2048, 128, 256);
+                    umma_i8(d0, rh, b0, id64, 1u);
+                    umma_i8(d0 + 32, rl, b0, id64, 1u);
                     umma_i8(d0, ih, b1, id64, 1u);
                     umma_i8(d0 + 32, il, b1, id64, 1u);
                   }
@@ -376,10 +381,12 @@ __global__ void __launch_bounds__(kFThreads, 1)
             const int b = sgc % kFSlots;
             mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
             tc_fence_after();
+            if (sgc < 32 && lane == 0) FTRACE(64 + sgc, 0);
             const int g0 = sg_first(sg), ng = sg_count(sg);
             const int s = it % kMgStages;
             mbar_wait(full0 + 8 * s, (it / kMgStages) & 1);
             tc_fence_after();
+            if (it < 64 && lane == 0) FTRACE(it, 1);
             const uint32_t st = sbase + s * kMgStageBytes;
             const uint32_t d0 = tmem + b * kFSlotCols;
             if (elect_one()) {
@@ -388,17 +395,12 @@ __global__ void __launch_bounds__(kFThreads, 1)
                   const uint32_t d = d0 + q * 48;
                   const uint32_t va = st + (uint32_t)(q * 2 * ksteps) * kVBlockBytes;
                   const uint32_t wa = st + kMgStageV + (uint32_t)(q * ksteps) * 1024;
-                  for (int kk = 0; kk < ksteps; ++kk) {
+                  for (int kk = 0; kk < ksteps; ++kk) {   // slots start at zero: every UMMA accumulates
                     const uint64_t ah = umma_desc(va + (2 * kk) * kVBlockBytes, 128, 256);
                     const uint64_t al = umma_desc(va + (2 * kk + 1) * kVBlockBytes, 128, 256);
-                    const uint64_t bb = umma_desc(wa + kk * 1024, 128, 256), bl = umma_desc(wa + kk * 1024 + 512, 128, 256);
-                    umma_i8(d, ah, bb, id32, kk == 0 ? 0u : 1u);             // [s16 | s8]
-                    if (kk == 0) {
-                      umma_i8(d + 32, al, bl, id16, 0u);                     // s0
-                      umma_i8(d + 16, al, bb, id16, 1u);                     // s8 += lo.hi
-                    } else {
-                      umma_i8(d + 16, al, bb, id32, 1u);                     // [s8 | s0]
-                    }
+                    const uint64_t bb = umma_desc(wa + kk * 1024, 128, 256);
+                    umma_i8(d, ah, bb, id32, 1u);                             // [s16 | s8] += hi . [W hi | W lo]
+                    umma_i8(d + 16, al, bb, id32, 1u);                        // [s8 | s0]  += lo . [W hi | W lo]
                   }
                 }
               } else {         // complex group: all K steps in the stage
@@ -408,20 +410,15 @@ __global__ void __launch_bounds__(kFThreads, 1)
                   const uint64_t ih = umma_desc(a0 + 2 * kVBlockBytes, 128, 256),
                                  il = umma_desc(a0 + 3 * kVBlockBytes, 128, 256);
                   const uint32_t bw = st + kMgStageV + kk * 4096;
-                  const uint64_t b0 = umma_desc(bw, 128, 256), b0l = umma_desc(bw + 1024, 128, 256);
-                  const uint64_t b1 = umma_desc(bw + 2048, 128, 256);
-                  umma_i8(d0, rh, b0, id64, kk == 0 ? 0u : 1u);
-                  if (kk == 0) {
-                    umma_i8(d0 + 64, rl, b0l, id32, 0u);
-                    umma_i8(d0 + 32, rl, b0, id32, 1u);
-                  } else {
-                    umma_i8(d0 + 32, rl, b0, id64, 1u);
-                  }
+                  const uint64_t b0 = umma_desc(bw, 128, 256), b1 = umma_desc(bw + 2048, 128, 256);
+                  umma_i8(d0, rh, b0, id64, 1u);        // [Re16 Im16 Re8 Im8] += Vr hi . B0
+                  umma_i8(d0 + 32, rl, b0, id64, 1u);   // [Re8 Im8 Re0 Im0]   += Vr lo . B0
                   umma_i8(d0, ih, b1, id64, 1u);
                   umma_i8(d0 + 32, il, b1, id64, 1u);
                 }
               }
               umma_commit(tfull0 + 8 * b);    // slot complete (and stage s free, see the producer)
+              if (it < 64) FTRACE(it, 2);
             }
             __syncwarp();
           }
@@ -515,6 +512,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
       if (warp == 0 && lane == 0 && sgc < 32) FTRACE(64 + sgc, 1);
       return lane_base + b * kFSlotCols;
     };
+    auto zero_slot = [&](uint32_t a) {   // MG variants: the columns this warp read, back to zero
+      if constexpr (MG > 0) {
+#pragma unroll
+        for (int blk = 0; blk < 6; blk++) tmem_zero4(a + blk * 16);
+        tmem_st_wait();
+      }
+    };
     auto slot_release = [&]() {
       tc_fence_before();
       __syncwarp();
@@ -540,6 +544,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
       tmem_ld4(a + 64, x1);
       tmem_ld4(a + 80, l1);
       tmem_ld_wait();
+      zero_slot(a);
       slot_release();
       combine(h0, x0, l0, m0);
       combine(h1, x1, l1, m1);
@@ -556,6 +561,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
       tmem_ld4(a + 64, rl);
       tmem_ld4(a + 80, il);
       tmem_ld_wait();
+      zero_slot(a);
       slot_release();
       combine(rh, rx, rl, re);
       combine(ih, ix, il, im);
