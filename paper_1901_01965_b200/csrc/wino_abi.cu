@@ -60,6 +60,12 @@ wino_status check_device(const wino_plan_s* p) {
 
 long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 
+// WINO_PATH_AUTO's c_in limit for the fused path; WINO_AUTO_FUSED_CIN overrides (experiments)
+int auto_fused_max_cin() {
+  const char* env = std::getenv("WINO_AUTO_FUSED_CIN");
+  return env ? std::atoi(env) : 128;
+}
+
 size_t chunk_budget_bytes(int desc_mb) {
   const char* env = std::getenv("WINO_CHUNK_MB");
   long mb = desc_mb > 0 ? desc_mb : (env ? std::atol(env) : 128);
@@ -97,7 +103,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   wino_conv_desc dr = *desc;
   if (dr.path == WINO_PATH_AUTO)
     dr.path = (dr.algorithm == WINO_ALG_F4X4 && dr.input_type == WINO_IN_INT8 && dr.filter_target_max == 255 &&
-               dr.c_in <= 128)
+               dr.c_in <= auto_fused_max_cin())
                   ? WINO_PATH_FUSED
                   : WINO_PATH_STAGED;
   const wino_conv_desc& d = dr;
