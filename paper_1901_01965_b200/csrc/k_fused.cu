@@ -569,6 +569,31 @@ __global__ void __launch_bounds__(kFThreads, 1)
       rscale(im, gi);
     };
     // Z of real row R[ri] (processing slot k): real (r, cc) adds a_j[cc] M''; the pair adds 2 Re(i^j z)
+    // int8 NHWC output of a unit, staged in `part` as [px][tile][16 couts]: 16-byte chunks to global.
+    // Deferred into the NEXT unit's row 0 (after its first two slot-groups, before Z_0 overwrites the
+    // staging), so the accumulators of that unit are drained meanwhile instead of stalling its MMAs.
+    const bool stage8 = NHWC && OUT8 && (g.cout & 15) == 0;
+    bool pending = false;
+    int pend_tb = 0, pend_nb = 0;
+    auto store_staged = [&](int tb_i, int nb) {
+      // chunk ch = etid + q * 512: tile rr = etid % 128 for every q (512 = 4 x 128), pixel px = ch / 128
+      const int rr = etid & (kMBlock - 1);
+      const int tt = tb_i * kMBlock + rr;
+      if (tt < imgs * g.tpi) {
+        const int rem = tt % g.tpi, ty = rem / g.tw;
+        const int oyb = 4 * ty, oxb = 4 * (rem - ty * g.tw);
+        int8_t* base = static_cast<int8_t*>(y) + (long long)(n0 + tt / g.tpi) * g.ho * g.wo * g.cout + nb * kFN;
+#pragma unroll
+        for (int q = 0; q < (16 * kMBlock) / (kFEpiWarps * 32); q++) {
+          const int ch = etid + q * kFEpiWarps * 32;
+          const int px = ch >> 7;
+          const int oy = oyb + (px >> 2), ox = oxb + (px & 3);
+          if (oy >= g.ho || ox >= g.wo) continue;
+          const uint4 val = *reinterpret_cast<const uint4*>(part + ch * 16);
+          *reinterpret_cast<uint4*>(base + ((long long)oy * g.wo + ox) * g.cout) = val;
+        }
+      }
+    };
     auto real_row = [&](int k, int32_t (&Z)[4][4]) {
       const int gb = 5 * k;
       int32_t m0[4], m1[4];
@@ -578,6 +603,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
 #pragma unroll
         for (int c = 0; c < 4; c++) Z[j][c] = areal(j, 0) * m0[c] + areal(j, 1) * m1[c];
       take_real2(gb + 2, m0, m1);   // cc = 2, 5
+      if (k == 0 && pending) {      // the previous unit's output, then nobody reads the staging any more
+        store_staged(pend_tb, pend_nb);
+        fepi_barrier();
+        pending = false;
+      }
 #pragma unroll
       for (int j = 0; j < 4; j++)
 #pragma unroll
@@ -728,7 +758,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
           }
           return (int32_t)(r > 127 ? 127 : (r < -128 ? -128 : r));
         };
-        const bool stage8 = NHWC && OUT8 && (g.cout & 15) == 0;
         // store output row i (Yi[j][c] = Y[i][j] of couts co0 + c)
         auto emit_row = [&](int i, const int32_t (&Yi)[4][4]) {
           if (stage8) {   // stage [px][tile][16 couts] bytes; 16-byte chunks leave after the barrier
@@ -803,27 +832,14 @@ __global__ void __launch_bounds__(kFThreads, 1)
         if (warp == 0 && lane == 0) FTRACE(uc * 8 + 3, 3);
         fepi_barrier();                                // staging complete; etab of the next unit visible
         if (warp == 0 && lane == 0) FTRACE(uc * 8 + 4, 3);
-        if (stage8) {
-          // chunk ch = etid + q * 512: tile rr = etid % 128 for every q (512 = 4 x 128), pixel px = ch / 128
-          const int rr = etid & (kMBlock - 1);
-          const int tt = tb_i * kMBlock + rr;
-          if (tt < imgs * g.tpi) {
-            const int rem = tt % g.tpi, ty = rem / g.tw;
-            const int oyb = 4 * ty, oxb = 4 * (rem - ty * g.tw);
-            int8_t* base = static_cast<int8_t*>(y) + (long long)(n0 + tt / g.tpi) * g.ho * g.wo * g.cout + nb * kFN;
-#pragma unroll
-            for (int q = 0; q < (16 * kMBlock) / (kFEpiWarps * 32); q++) {
-              const int ch = etid + q * kFEpiWarps * 32;
-              const int px = ch >> 7;
-              const int oy = oyb + (px >> 2), ox = oxb + (px & 3);
-              if (oy >= g.ho || ox >= g.wo) continue;
-              const uint4 val = *reinterpret_cast<const uint4*>(part + ch * 16);
-              *reinterpret_cast<uint4*>(base + ((long long)oy * g.wo + ox) * g.cout) = val;
-            }
-          }
+        if (stage8) {   // stored during the next unit's row 0 (or after the last unit)
+          pending = true;
+          pend_tb = tb_i;
+          pend_nb = nb;
         }
         if (warp == 0 && lane == 0) FTRACE(uc * 8 + 5, 3);
       }
+      if (pending) store_staged(pend_tb, pend_nb);
     }
   }
   tc_fence_before();
