@@ -113,6 +113,11 @@ def test_c1_all_stages(layout, scaling, path):
     (2, 1, 1, 2, 3, 1, O.NCHW),
     (1, 57, 11, 40, 33, 1, O.NCHW),
     (4, 18, 18, 96, 128, 1, O.NHWC),
+    # the fused kernel's stage variants: 3 K steps (one 80 KB stage per slot-group), 7 K steps (two
+    # 4-K-step stages, the second a tail), 10 K steps (the general ring)
+    (2, 14, 10, 80, 48, 1, O.NCHW),
+    (2, 11, 13, 200, 24, 1, O.NHWC),
+    (1, 9, 9, 300, 20, 1, O.NHWC),
 ])
 @pytest.mark.parametrize("scaling", [False, True])
 @pytest.mark.parametrize("path", PATHS)
