@@ -409,6 +409,7 @@ def run_ours_stack(args):
                     peaks, None)
     roof["dominant"]["layer"] = dom_l + 1
     stack_kernel_us = sum(k["s_per_step"] for kl in kern_l for k in kl.values()) * 1e6
+    layers_us = [round(sum(k["s_per_step"] for k in kl.values()) * 1e6, 1) for kl in kern_l]
     # e2e: host x in, host final activation out, through the C ABI calls
     xh = xs[0].cpu().pin_memory()
     out = st(xs[0], stream)
@@ -444,6 +445,7 @@ def run_ours_stack(args):
                               "roofline_effective_tops": round(ops_step / t_roof / 1e12, 1)},
             "roofline": roof["dominant"],
             "kernel_sum_vs_step": round(stack_kernel_us / (t_max / args.steps * 1e6), 3),
+            "layers_kernel_us": layers_us,
             "gpu_launches": st.launches() * args.steps + len(cfg.layers) * args.steps,
             "clocks": clk.summary(),
             "e2e": {"value": round(world * ops_step * reps / te / 1e12, 3), "unit": "TOPS",
