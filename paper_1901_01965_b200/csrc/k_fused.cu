@@ -36,11 +36,14 @@
 //   Y[3] = Q + Z_5 + 2 Im Z_3,  P = Z_1 + Z_2, Q = Z_1 - Z_2   (row 4 never formed)
 // Z_0, Z_5 are parked in shared memory, P, Q in TMEM, Re/Im Z_3 in registers.
 //
-// Persistent CTA per SM, warp-specialised (18 warps, <= 96 registers):
+// Persistent CTAs (the fewest that keep the number of unit rounds), warp-specialised (19 warps,
+// <= 96 registers):
 //   warps 0..15  epilogue: TMEM lane quadrant w % 4 (32 tiles), couts 4 (w / 4) .. +3
-//   warp 16      producer (1 lane): bulk copies into a kFStages-deep ring
-//   warp 17      MMA issuer (1 lane): tcgen05.mma into 4 TMEM accumulator slots of 96
+//   warps 16, 17 producers (one elected lane each, alternate stages): bulk copies into the ring
+//   warp 18      MMA issuer (one elected lane): tcgen05.mma into 4 TMEM accumulator slots of 96
 //                columns (one complex group or two real groups each)
+// Ring (160 KB): MG = 0 four 40 KB stages (a group's K chunk each), MG = 1 four 40 KB stages and
+// MG = 2 two 80 KB stages (one slot-group each), MG = 3 two 80 KB stages (4 K steps of a slot-group).
 // TMEM: [0, 384) accumulator slots, [384, 448) P, [448, 512) Q.
 #include <cstdint>
 #include <cstdlib>
