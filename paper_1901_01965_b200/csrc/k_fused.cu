@@ -761,14 +761,28 @@ __global__ void __launch_bounds__(kFThreads, 1)
           }
           return (int32_t)(r > 127 ? 127 : (r < -128 ? -128 : r));
         };
+        // RQFAST without the clamp: cvt.pack.sat saturates while packing four values into bytes
+        auto outv_unclamped = [&](int32_t yv) -> int32_t {
+          const int32_t kpos = rq_shift > 0 ? 8 + (1 << (rq_shift + 3)) : 8;
+          const int32_t kneg = rq_shift > 0 ? 17 : 1;
+          return (yv + kpos + (yv >> 31) * kneg) >> (rq_shift + 4);
+        };
+        auto pack_sat4 = [](int32_t a, int32_t b, int32_t c, int32_t d) -> uint32_t {   // bytes [a, b, c, d]
+          uint32_t hi, w;
+          asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
+          asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(w) : "r"(b), "r"(a), "r"(hi));
+          return w;
+        };
         // store output row i (Yi[j][c] = Y[i][j] of couts co0 + c)
         auto emit_row = [&](int i, const int32_t (&Yi)[4][4]) {
           if (stage8) {   // stage [px][tile][16 couts] bytes; 16-byte chunks leave after the barrier
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-              const uint32_t w = __byte_perm(__byte_perm((uint32_t)outv(Yi[j][0]), (uint32_t)outv(Yi[j][1]), 0x0040),
-                                             __byte_perm((uint32_t)outv(Yi[j][2]), (uint32_t)outv(Yi[j][3]), 0x0040),
-                                             0x5410);
+              const uint32_t w = RQFAST ? pack_sat4(outv_unclamped(Yi[j][0]), outv_unclamped(Yi[j][1]),
+                                                    outv_unclamped(Yi[j][2]), outv_unclamped(Yi[j][3]))
+                                        : __byte_perm(__byte_perm((uint32_t)outv(Yi[j][0]), (uint32_t)outv(Yi[j][1]), 0x0040),
+                                                      __byte_perm((uint32_t)outv(Yi[j][2]), (uint32_t)outv(Yi[j][3]), 0x0040),
+                                                      0x5410);
               *reinterpret_cast<uint32_t*>(part + ((i * 4 + j) * kMBlock + row) * 16 + cw * kFC) = w;
             }
             return;
