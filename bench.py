@@ -793,7 +793,7 @@ def main():
     ap.add_argument("--streams", type=int, default=3,
                     help="independent batches in flight on separate streams (own filter/workspace buffers)")
     ap.add_argument("--path", default="auto", choices=["auto", "fused", "staged"],
-                    help="auto: the plan picks fused for c_in <= 128 (C2, C3, C5 layers 1-5), staged otherwise")
+                    help="auto: the plan picks fused for c_in <= 256 (C2-C4, C5 layers 1-8), staged otherwise")
     ap.add_argument("--input", default="i8", choices=["i8", "u8"],
                     help="u8: uint8 tensors with zero points (SURVEY f2, staged F(4x4), c_in <= 224)")
     ap.add_argument("--alg", default="f4", choices=["f4", "f2"],

@@ -79,7 +79,7 @@ typedef struct {
                              transform + store (M'' stays on chip).
                              WINO_PATH_STAGED (1): K2, K3 GEMMs -> M'' in the workspace,
                              K4 output transform (M'' inspectable, see wino_plan_info).
-                             WINO_PATH_AUTO (2): fused when c_in <= 128 and the variant
+                             WINO_PATH_AUTO (2): fused when c_in <= 256 and the variant
                              allows it (F4x4, int8, target 255), else staged;
                              wino_plan_info.path reports the choice.                   */
     int algorithm;        /* WINO_ALG_F4X4 (0, default): complex F(4x4,3x3) over the

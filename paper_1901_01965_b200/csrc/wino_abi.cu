@@ -63,7 +63,7 @@ long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 // WINO_PATH_AUTO's c_in limit for the fused path; WINO_AUTO_FUSED_CIN overrides (experiments)
 int auto_fused_max_cin() {
   const char* env = std::getenv("WINO_AUTO_FUSED_CIN");
-  return env ? std::atoi(env) : 128;
+  return env ? std::atoi(env) : 256;
 }
 
 size_t chunk_budget_bytes(int desc_mb) {
@@ -97,9 +97,9 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   *out = nullptr;
   if (desc->path != WINO_PATH_FUSED && desc->path != WINO_PATH_STAGED && desc->path != WINO_PATH_AUTO)
     return WINO_ERR_INVALID_ARG;
-  // WINO_PATH_AUTO: the fused kernel where it measured faster -- c_in <= 128, where its ring holds one
-  // stage per slot-group (tools/path_ab.py: 64..128 -> 64..256 channels), for the variants it implements
-  // (F(4x4), int8, target 255) -- else staged
+  // WINO_PATH_AUTO: the fused kernel where it measured faster or as fast and steadier -- c_in <= 256,
+  // where its ring holds one or two stages per slot-group (C2-C4; tools/path_ab.py), for the variants it
+  // implements (F(4x4), int8, target 255) -- else staged
   wino_conv_desc dr = *desc;
   if (dr.path == WINO_PATH_AUTO)
     dr.path = (dr.algorithm == WINO_ALG_F4X4 && dr.input_type == WINO_IN_INT8 && dr.filter_target_max == 255 &&
