@@ -80,7 +80,7 @@ typedef struct {
                              WINO_PATH_STAGED (1): K2, K3 GEMMs -> M'' in the workspace,
                              K4 output transform (M'' inspectable, see wino_plan_info).
                              WINO_PATH_AUTO (2): fused when c_in <= 256 and the variant
-                             allows it (F4x4, int8, target 255), else staged;
+                             allows it (F4x4, target 255), else staged;
                              wino_plan_info.path reports the choice.                   */
     int algorithm;        /* WINO_ALG_F4X4 (0, default): complex F(4x4,3x3) over the
                              Gaussian integers, points {0, +-1, +-i};
@@ -90,8 +90,8 @@ typedef struct {
     int input_type;       /* WINO_IN_INT8 (0, default) or WINO_IN_UINT8 (1): x and w are
                              uint8 with the zero points below (the paper's affine model,
                              P:251); the convolution is that of the int9 values x - zx,
-                             w - zw, padding = real 0 (A28).  uint8 needs the
-                             staged path, F4x4 and c_in <= 224 (int32 exactness).     */
+                             w - zw, padding = real 0 (A28).  uint8 needs
+                             F4x4 and c_in <= 224 (int32 exactness); either path.      */
     int x_zero_point;     /* [0, 255], uint8 input only                                  */
     int w_zero_point;     /* [0, 255], uint8 input only                                  */
 } wino_conv_desc;

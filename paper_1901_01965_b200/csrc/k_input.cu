@@ -225,6 +225,7 @@ __device__ __forceinline__ void st_bal(int8_t* p_hi, int v0, int v1) {
   st16(p_hi + 4096, __byte_perm((uint32_t)v0, (uint32_t)v1, 0x0040));            // [lo0, lo1]
 }
 
+template <bool U8>
 __global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, const int8_t* __restrict__ x, int n0,
                                                                      int imgs, int8_t* __restrict__ vimg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, con
   pdl_trigger();
   pdl_wait();
   Rows r[2];
-  input_rows<false>(g, x, n0, imgs, t, c, r);
+  input_rows<U8>(g, x, n0, imgs, t, c, r);
 
   const long long tb = t / kMBlock;
   const int row = t % kMBlock;
@@ -292,7 +293,9 @@ cudaError_t launch_input_transform_f(const Geom& g, const int8_t* x, int n0, int
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
   dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
-  return launch_pdl_co(k_input_transform_f, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
+  if (g.in_u8)   // uint8 + zero point (f2, A28)
+    return launch_pdl_co(k_input_transform_f<true>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
+  return launch_pdl_co(k_input_transform_f<false>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
 }
 
 // ---- rational F(2x2,3x3): 4x4 patch at (2ty - pad, 2tx - pad), D = B^T d B with the

@@ -99,11 +99,10 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
     return WINO_ERR_INVALID_ARG;
   // WINO_PATH_AUTO: the fused kernel where it measured faster or as fast and steadier -- c_in <= 256,
   // where its ring holds one or two stages per slot-group (C2-C4; tools/path_ab.py), for the variants it
-  // implements (F(4x4), int8, target 255) -- else staged
+  // implements (F(4x4), int8 or uint8, target 255) -- else staged
   wino_conv_desc dr = *desc;
   if (dr.path == WINO_PATH_AUTO)
-    dr.path = (dr.algorithm == WINO_ALG_F4X4 && dr.input_type == WINO_IN_INT8 && dr.filter_target_max == 255 &&
-               dr.c_in <= auto_fused_max_cin())
+    dr.path = (dr.algorithm == WINO_ALG_F4X4 && dr.filter_target_max == 255 && dr.c_in <= auto_fused_max_cin())
                   ? WINO_PATH_FUSED
                   : WINO_PATH_STAGED;
   const wino_conv_desc& d = dr;
@@ -118,7 +117,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   if (d.input_type == WINO_IN_UINT8) {
     if (d.x_zero_point < 0 || d.x_zero_point > 255 || d.w_zero_point < 0 || d.w_zero_point > 255)
       return WINO_ERR_INVALID_ARG;
-    if (d.path != WINO_PATH_STAGED || d.algorithm != WINO_ALG_F4X4 || d.c_in > 224) return WINO_ERR_UNSUPPORTED;
+    if (d.algorithm != WINO_ALG_F4X4 || d.c_in > 224) return WINO_ERR_UNSUPPORTED;
   }
   if (d.n < 1 || d.h < 1 || d.w < 1 || d.c_in < 1 || d.c_out < 1) return WINO_ERR_UNSUPPORTED;
   if (d.pad != 0 && d.pad != 1) return WINO_ERR_UNSUPPORTED;

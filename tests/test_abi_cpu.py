@@ -41,7 +41,7 @@ def test_status_strings_and_pre_cuda_validation():
                        (dict(algorithm=1, path=0), L.WINO_ERR_UNSUPPORTED),
                        (dict(input_type=2), L.WINO_ERR_INVALID_ARG),
                        (dict(input_type=1, x_zero_point=256, path=1), L.WINO_ERR_INVALID_ARG),
-                       (dict(input_type=1, path=0), L.WINO_ERR_UNSUPPORTED),
+                       (dict(input_type=1, path=0, c_in=225), L.WINO_ERR_UNSUPPORTED),
                        (dict(input_type=1, path=1, c_in=225), L.WINO_ERR_UNSUPPORTED),
                        (dict(filter_target_max=126, path=1), L.WINO_ERR_UNSUPPORTED),
                        (dict(filter_target_max=127, path=1, filter_scaling=0), L.WINO_ERR_UNSUPPORTED),

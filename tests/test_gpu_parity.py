@@ -296,6 +296,8 @@ def test_auto_path_choice_and_parity():
                                (128, 256, {}, W.WINO_PATH_FUSED), (256, 256, {}, W.WINO_PATH_FUSED),
                                (300, 64, {}, W.WINO_PATH_STAGED), (512, 512, {}, W.WINO_PATH_STAGED),
                                (64, 64, dict(algorithm=W.WINO_ALG_F2X2), W.WINO_PATH_STAGED),
+                               (64, 64, dict(input_type=W.WINO_IN_UINT8, x_zero_point=3, w_zero_point=250),
+                                W.WINO_PATH_FUSED),
                                (64, 64, dict(filter_target_max=127), W.WINO_PATH_STAGED)]:
         conv = W.WinoConv2d(1, 9, 10, ci, co, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=W.WINO_PATH_AUTO, **kw)
         assert conv.info.path == want, (ci, co, kw)

@@ -20,19 +20,22 @@ def _layer(rng, n, h, w, ci, co, layout):
     return x, wt
 
 
-def _check(x, w, zx, zw, layout, pad=1, scaling=True, intermediates=True):
+def _check(x, w, zx, zw, layout, pad=1, scaling=True, intermediates=True, path=None):
     import paper_1901_01965_b200 as W
+    path = W.WINO_PATH_STAGED if path is None else path
+    intermediates = intermediates and path == W.WINO_PATH_STAGED   # V / W' / M'' decoders: staged layouts
     if layout == O.NCHW:
         n, ci, h, wd = x.shape
     else:
         n, h, wd, ci = x.shape
     co = w.shape[0]
-    conv = W.WinoConv2d(n, h, wd, ci, co, pad, layout, scaling, W.WINO_OUT_INT32, path=W.WINO_PATH_STAGED,
+    conv = W.WinoConv2d(n, h, wd, ci, co, pad, layout, scaling, W.WINO_OUT_INT32, path=path,
                         input_type=W.WINO_IN_UINT8, x_zero_point=zx, w_zero_point=zw)
     conv.transform_filter(torch.from_numpy(w).cuda())
     y = conv(torch.from_numpy(x).cuda()).cpu().numpy()
     ref = O.wino_conv_u8(x, w, zx, zw, pad, layout, scaling=scaling, want_M=intermediates)
     np.testing.assert_array_equal(y, ref.out32)
+    np.testing.assert_array_equal(conv.codes.cpu().numpy(), O.filter_transform_u8(w, zw, layout, scaling=scaling)[2])
     if not scaling:
         np.testing.assert_array_equal(y.astype(np.int64), O.direct_conv_u8(x, w, zx, zw, pad, layout))
     if intermediates:
@@ -58,28 +61,35 @@ def _check(x, w, zx, zw, layout, pad=1, scaling=True, intermediates=True):
     (1, 3, 3, 1, 1, 0, O.NHWC, 7, 200), (2, 1, 1, 2, 3, 1, O.NCHW, 128, 1), (4, 18, 18, 96, 128, 1, O.NHWC, 100, 140),
     (1, 9, 10, 224, 40, 1, O.NHWC, 128, 128)])
 @pytest.mark.parametrize("scaling", [False, True])
-def test_u8_random_shapes(case, scaling):
+@pytest.mark.parametrize("path", ["staged", "fused"])
+def test_u8_random_shapes(case, scaling, path):
+    import paper_1901_01965_b200 as W
     n, h, wd, ci, co, pad, layout, zx, zw = case
     rng = np.random.default_rng(zlib.crc32(repr((case, scaling, "u8")).encode()))
     x, w = _layer(rng, n, h, wd, ci, co, layout)
-    _check(x, w, zx, zw, layout, pad, scaling)
+    _check(x, w, zx, zw, layout, pad, scaling, path=W.WINO_PATH_STAGED if path == "staged" else W.WINO_PATH_FUSED)
 
 
 @pytest.mark.parametrize("xv,zx,wv,zw", [(0, 255, 255, 0), (255, 0, 0, 255), (255, 0, 255, 0), (0, 255, 0, 255)])
 @pytest.mark.parametrize("scaling", [False, True])
-def test_u8_int9_extremes(xv, zx, wv, zw, scaling):
+@pytest.mark.parametrize("path", ["staged", "fused"])
+def test_u8_int9_extremes(xv, zx, wv, zw, scaling, path):
     """The int9 corners: |x - zx| = |w - zw| = 255 everywhere (Winograd-domain values up to 4080, the
     8/128 scale factor and its q = 3 inverse, A27), at the plan's maximum c_in for some cases."""
+    import paper_1901_01965_b200 as W
+    p = W.WINO_PATH_STAGED if path == "staged" else W.WINO_PATH_FUSED
     for ci in (40, 224):
         x = np.full((1, 10, 11, ci), xv, np.uint8); w = np.full((8, 3, 3, ci), wv, np.uint8)
-        _check(x, w, zx, zw, O.NHWC, 1, scaling, intermediates=ci == 40)
+        _check(x, w, zx, zw, O.NHWC, 1, scaling, intermediates=ci == 40, path=p)
 
 
-def test_u8_int8_requant():
+@pytest.mark.parametrize("path", ["staged", "fused"])
+def test_u8_int8_requant(path):
     import paper_1901_01965_b200 as W
     rng = np.random.default_rng(51)
-    x, w = _layer(rng, 2, 15, 14, 24, 20, O.NHWC)
-    conv = W.WinoConv2d(2, 15, 14, 24, 20, 1, O.NHWC, True, W.WINO_OUT_INT8, path=W.WINO_PATH_STAGED,
+    x, w = _layer(rng, 2, 15, 14, 24, 32, O.NHWC)
+    p = W.WINO_PATH_STAGED if path == "staged" else W.WINO_PATH_FUSED
+    conv = W.WinoConv2d(2, 15, 14, 24, 32, 1, O.NHWC, True, W.WINO_OUT_INT8, path=p,
                         input_type=W.WINO_IN_UINT8, x_zero_point=120, w_zero_point=135)
     conv.transform_filter(torch.from_numpy(w).cuda())
     xd = torch.from_numpy(x).cuda()
@@ -88,15 +98,17 @@ def test_u8_int8_requant():
                                       O.wino_conv_u8(x, w, 120, 135, 1, O.NHWC, True, M0=M0, S=S).y8)
 
 
-def test_u8_with_zero_point_128_equals_int8_mode():
+@pytest.mark.parametrize("path", ["staged", "fused"])
+def test_u8_with_zero_point_128_equals_int8_mode(path):
     """uint8 tensors x + 128, w + 128 with zero points 128 are the int8 tensors: identical outputs."""
     import paper_1901_01965_b200 as W
     import synth
     x, w = synth.config_inputs("C2", n=2)
     S = synth.requant_shift(synth.CONFIGS["C2"].layers[0])
+    p = W.WINO_PATH_STAGED if path == "staged" else W.WINO_PATH_FUSED
     outs = []
     for it in (W.WINO_IN_INT8, W.WINO_IN_UINT8):
-        conv = W.WinoConv2d(2, 56, 56, 64, 64, 1, W.WINO_NHWC, True, W.WINO_OUT_INT8, path=W.WINO_PATH_STAGED,
+        conv = W.WinoConv2d(2, 56, 56, 64, 64, 1, W.WINO_NHWC, True, W.WINO_OUT_INT8, path=p,
                             input_type=it, x_zero_point=128 if it else 0, w_zero_point=128 if it else 0)
         sh = (lambda a: (a.astype(np.int16) + 128).astype(np.uint8)) if it else (lambda a: a)
         conv.transform_filter(torch.from_numpy(sh(w)).cuda())
