@@ -142,8 +142,9 @@ __host__ __device__ constexpr int im_y(int n) { return re_x(n); }
 // MG > 0: ONE ring stage per slot-group (a real pair's or a complex group's whole K range; the pair's
 // V and W' are contiguous), 18 stages per unit instead of 26 (c_in <= 64) or 36 (c_in <= 128) -- each
 // stage costs ~350 cycles of copy issue plus a commit.  MG = 1 (c_in <= 64): 4 stages of
-// 40 KB; MG = 2 (c_in <= 128): 2 stages of 80 KB (the same 160 KB).  The MG loops are separate code, so
-// the general loops (MG = 0) stay as they are.
+// 40 KB; MG = 2 (c_in <= 128): 2 stages of 80 KB (the same 160 KB); MG = 3 (c_in > 128): 2 stages of 80 KB,
+// each 4 K steps of a slot-group (faster than the general loops at every c_in measured, 256..768).  The MG
+// loops are separate code; the general loops (MG = 0) remain for WINO_FUSED_MERGE=0 (experiments).
 template <bool NHWC, bool OUT8, bool RQFAST, int MG>
 __global__ void __launch_bounds__(kFThreads, 1)
     k_fused(const int8_t* __restrict__ V, const int8_t* __restrict__ W, const uint8_t* __restrict__ codes, Geom g,
@@ -875,7 +876,7 @@ static int g_fused_dbg = 0;
 // with three batches in flight); WINO_FUSED_BALANCE=0 restores the full grid (experiments)
 static int g_fused_balance = 1;
 static int g_fused_merge = 3;   // WINO_FUSED_MERGE: 0 general loops only, 1 merged stages at c_in <= 64,
-                                // 2 also at c_in <= 128, 3 also 4-K-step slot-group stages at c_in <= 256
+                                // 2 also at c_in <= 128, 3 also 4-K-step slot-group stages above
 
 cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
                          const int8_t* wimg, const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y,
@@ -898,7 +899,7 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
       : g.ksteps <= 4 && g_fused_merge >= 2                                                                      \
           ? launch_pdl(k_fused<A, B, C, 2>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
                        tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
-      : g.ksteps <= 8 && g_fused_merge >= 3                                                                      \
+      : g_fused_merge >= 3                                                                                       \
           ? launch_pdl(k_fused<A, B, C, 3>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
                        tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
           : launch_pdl(k_fused<A, B, C, 0>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \

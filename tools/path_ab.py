@@ -31,9 +31,18 @@ def t_conv(n, h, w, ci, co, path, reps=20):
     return float(np.median(ts)), ops
 
 
-for shape in [(32, 56, 56, 64, 64), (64, 28, 28, 128, 128), (32, 56, 56, 64, 128), (32, 56, 56, 128, 128),
+SHAPES = [(32, 56, 56, 64, 64), (64, 28, 28, 128, 128), (32, 56, 56, 64, 128), (32, 56, 56, 128, 128),
               (16, 56, 56, 128, 256), (64, 28, 28, 128, 256), (64, 28, 28, 256, 128), (128, 14, 14, 256, 256),
-              (8, 112, 112, 64, 128), (8, 112, 112, 128, 128)]:
+              (8, 112, 112, 64, 128), (8, 112, 112, 128, 128), (64, 28, 28, 256, 512), (64, 28, 28, 512, 512),
+              (256, 14, 14, 512, 512)]
+if len(sys.argv) > 1:   # e.g. python tools/path_ab.py fused 64,28,28,512,512 256,14,14,512,512
+    paths = {"fused": W.WINO_PATH_FUSED, "staged": W.WINO_PATH_STAGED}
+    for sh in sys.argv[2:]:
+        shape = tuple(int(v) for v in sh.split(","))
+        t, ops = t_conv(*shape, paths[sys.argv[1]])
+        print(f"{shape}: {sys.argv[1]} {ops / t / 1e6:7.1f} TOPS (one stream)")
+    sys.exit(0)
+for shape in SHAPES:
     r = {}
     for name, p in (("fused", W.WINO_PATH_FUSED), ("staged", W.WINO_PATH_STAGED)):
         t, ops = t_conv(*shape, p)
