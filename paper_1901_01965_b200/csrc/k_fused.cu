@@ -394,7 +394,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
             const uint32_t st = sbase + s * kMgStageBytes;
             const uint32_t d0 = tmem + b * kFSlotCols;
             if (elect_one()) {
-              if (ng == 2) {   // real pair: group q's V at q * 2 ksteps blocks, W' at q * ksteps KB
+              if (dbg & 2) {   // debug builds only: no UMMAs
+              } else if (ng == 2) {   // real pair: group q's V at q * 2 ksteps blocks, W' at q * ksteps KB
                 for (int q = 0; q < 2; ++q) {
                   const uint32_t d = d0 + q * 48;
                   const uint32_t va = st + (uint32_t)(q * 2 * ksteps) * kVBlockBytes;
