@@ -319,21 +319,37 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, cons
       ix0 = 2 * (rem - ty * g.tw) - g.pad;
     }
     const bool cok = c < g.cin;
-    const long long cstep = g.layout == 1 ? 1 : (long long)g.h * g.w;
+    bool vx[4];
 #pragma unroll
-    for (int a = 0; a < 4; a++)
+    for (int b = 0; b < 4; b++) vx[b] = cok && ix0 + b >= 0 && ix0 + b < g.w;
+    if (g.layout == 1 && (g.cin & 1) == 0) {
+      // NHWC, even Cin: one 16-bit load per pixel; row pointer hoisted, column offsets b*Cin (as in K2)
+      const int8_t* p0 = x + ((long long)img * g.h * g.w + (long long)iy0 * g.w + ix0) * g.cin + c;
+      const long long rstride = (long long)g.w * g.cin;
 #pragma unroll
-      for (int b = 0; b < 4; b++) {
-        const int iy = iy0 + a, ix = ix0 + b;
-        uint32_t v = 0;
-        if (cok && iy >= 0 && iy < g.h && ix >= 0 && ix < g.w) {
-          const long long i0 = g.layout == 1 ? (((long long)img * g.h + iy) * g.w + ix) * g.cin + c
-                                             : (((long long)img * g.cin + c) * g.h + iy) * g.w + ix;
-          v = (uint8_t)__ldg(x + i0);
-          if (c + 1 < g.cin) v |= (uint32_t)(uint8_t)__ldg(x + i0 + cstep) << 8;
-        }
-        w[a * 4 + b] = v;
+      for (int a = 0; a < 4; a++) {
+        const bool vy = iy0 + a >= 0 && iy0 + a < g.h;
+        const uint16_t* rp = reinterpret_cast<const uint16_t*>(p0 + a * rstride);
+#pragma unroll
+        for (int b = 0; b < 4; b++) w[a * 4 + b] = (vy && vx[b]) ? (uint32_t)__ldg(rp + (b * g.cin >> 1)) : 0u;
       }
+    } else {
+      const long long cstep = g.layout == 1 ? 1 : (long long)g.h * g.w;
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+          const int iy = iy0 + a, ix = ix0 + b;
+          uint32_t v = 0;
+          if (vx[b] && iy >= 0 && iy < g.h) {
+            const long long i0 = g.layout == 1 ? (((long long)img * g.h + iy) * g.w + ix) * g.cin + c
+                                               : (((long long)img * g.cin + c) * g.h + iy) * g.w + ix;
+            v = (uint8_t)__ldg(x + i0);
+            if (c + 1 < g.cin) v |= (uint32_t)(uint8_t)__ldg(x + i0 + cstep) << 8;
+          }
+          w[a * 4 + b] = v;
+        }
+    }
   }
   const long long pstride = (long long)g.ksteps * 2 * kVBlockBytes;
   int8_t* base = vimg + (t / kMBlock) * g.planes * pstride + (long long)(c >> 5) * 2 * kVBlockBytes +

@@ -85,6 +85,11 @@ cudaError_t launch_output_transform(const Geom& g, const int32_t* mpp, int n0, i
 
 // K3F: fused GEMMs + Karatsuba + reverse scaling + output transform + store (k_fused.cu);
 //   requires g.nblk == 16.  V of the chunk -> y directly (no M'' in HBM).
+// K3F2: fused rational F(2x2) GEMMs + reverse scaling + output transform + store (k_fused2.cu)
+cudaError_t setup_fused2();
+cudaError_t launch_fused2(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
+                          const int8_t* wimg, const uint8_t* codes, int32_t rq_mult, int rq_shift, void* y,
+                          cudaStream_t st);
 cudaError_t setup_fused();
 void set_fused_trace(void* buf);   // debug timeline (-DWINO_FUSED_TRACE), nullptr = off
 cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,

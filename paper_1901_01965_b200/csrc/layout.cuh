@@ -83,10 +83,12 @@ __host__ __device__ __forceinline__ long long m_offset(const Geom& g, long long 
          (((c >> 2) ^ (r & swz)) << 2) + (c & 3);
 }
 // Byte offset of W piece `piece` (0 hi, 1 lo) of plane `plane`, output channel co, input channel k (staged).
+// Staged path: [plane][cout block][K step][W hi rows | W lo rows]; the fused F(2x2) path (k_fused2.cu)
+// orders [cout block][plane][K step][...] so that the two planes of a pair are contiguous.
 __host__ __device__ __forceinline__ long long w_offset(const Geom& g, int plane, int piece, int co, int k) {
   const int nb = co / g.nblk, r = co % g.nblk;
-  return (((long long)plane * (g.cout_pad / g.nblk) + nb) * g.ksteps + (k >> 5)) * (2 * g.nblk * kKStep) +
-         tiled_offset(piece * g.nblk + r, k & 31, 2 * g.nblk);
+  const long long blk = g.path == 0 ? (long long)nb * g.planes + plane : (long long)plane * (g.cout_pad / g.nblk) + nb;
+  return (blk * g.ksteps + (k >> 5)) * (2 * g.nblk * kKStep) + tiled_offset(piece * g.nblk + r, k & 31, 2 * g.nblk);
 }
 
 // ---------------------------------------------------------------- fused-path (K3F) operand layouts

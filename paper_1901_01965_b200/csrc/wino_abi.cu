@@ -44,6 +44,7 @@ wino_status setup_device(int device) {
   if (e == cudaSuccess) e = wino::setup_gemm();
   if (e == cudaSuccess) e = wino::setup_output_transform();
   if (e == cudaSuccess) e = wino::setup_fused();
+  if (e == cudaSuccess) e = wino::setup_fused2();
   cudaSetDevice(old);
   if (e != cudaSuccess) return cuda_status(e);
   g_setup_done[device] = true;
@@ -112,7 +113,6 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   if (d.workspace_mb < 0) return WINO_ERR_INVALID_ARG;
   if (d.path != WINO_PATH_FUSED && d.path != WINO_PATH_STAGED) return WINO_ERR_INVALID_ARG;
   if (d.algorithm != WINO_ALG_F4X4 && d.algorithm != WINO_ALG_F2X2) return WINO_ERR_INVALID_ARG;
-  if (d.algorithm == WINO_ALG_F2X2 && d.path != WINO_PATH_STAGED) return WINO_ERR_UNSUPPORTED;
   if (d.input_type != WINO_IN_INT8 && d.input_type != WINO_IN_UINT8) return WINO_ERR_INVALID_ARG;
   if (d.input_type == WINO_IN_UINT8) {
     if (d.x_zero_point < 0 || d.x_zero_point > 255 || d.w_zero_point < 0 || d.w_zero_point > 255)
@@ -163,7 +163,8 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   const int cout16 = (int)round_up(d.c_out, 16);
   g.path = d.path;
   // fused path: 16-cout units (UMMA N = 16); staged path: widest N that the cout count fills
-  g.nblk = d.path == WINO_PATH_FUSED ? 16 : (cout16 <= 16 ? 16 : (cout16 <= 32 ? 32 : 64));
+  g.nblk = d.path == WINO_PATH_FUSED ? (d.algorithm == WINO_ALG_F2X2 ? 32 : 16)
+                                     : (cout16 <= 16 ? 16 : (cout16 <= 32 ? 32 : 64));
   g.cout_pad = (int)round_up(d.c_out, g.nblk);
   g.ksteps = g.cin_pad / wino::kKStep;
   g.scaling = d.filter_scaling;
@@ -171,7 +172,8 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.out_mode = d.out_mode;
   // batch chunk: V (+ M on the staged path) of one chunk within the budget
   const size_t m_per_tile = d.path == WINO_PATH_STAGED ? (size_t)g.npos * 4 * (size_t)g.cout_pad : 0;
-  const size_t v_per_tile_ch = d.path == WINO_PATH_STAGED ? 2 * (size_t)g.planes : wino::kVPiecesF;
+  const bool fused_f4 = d.path == WINO_PATH_FUSED && d.algorithm == WINO_ALG_F4X4;
+  const size_t v_per_tile_ch = fused_f4 ? wino::kVPiecesF : 2 * (size_t)g.planes;
   const size_t per_img = (size_t)g.tpi * (v_per_tile_ch * (size_t)g.cin_pad + m_per_tile);
   long long imgs = (long long)(chunk_budget_bytes(d.workspace_mb) / (per_img ? per_img : 1));
   if (imgs < 1) imgs = 1;
@@ -183,8 +185,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   p->m_bytes = d.path == WINO_PATH_STAGED ? (size_t)g.npos * g.chunk_tiles_pad * g.cout_pad * 4 : 0;
   p->ws_bytes = p->v_bytes + p->m_bytes;
   // W': 92 B per (cin, cout) staged (46 planes x 2 pieces); 112 B fused (56 rows x 2 couts-halves, layout.cuh)
-  p->f_bytes = (size_t)(d.path == WINO_PATH_STAGED ? (g.w1 ? 1 : 2) * g.planes : 2 * wino::kWRowUnitsF) * g.cout_pad *
-               g.cin_pad;
+  p->f_bytes = (size_t)(fused_f4 ? 2 * wino::kWRowUnitsF : (g.w1 ? 1 : 2) * g.planes) * g.cout_pad * g.cin_pad;
   p->x_bytes = (size_t)d.n * d.h * d.w * d.c_in;
   p->y_bytes = (size_t)d.n * g.ho * g.wo * d.c_out * (d.out_mode == WINO_OUT_INT32 ? 4 : 1);
   *out = p;
@@ -205,7 +206,7 @@ wino_status wino_plan_query(wino_plan_t p, wino_plan_info* info) {
   info->tiles = (long long)p->d.n * p->g.tpi;
   info->cin_pad = p->g.cin_pad; info->cout_pad = p->g.cout_pad;
   info->n_block = p->g.nblk; info->m_block = wino::kMBlock;
-  info->planes = p->g.path == WINO_PATH_FUSED ? 36 : p->g.planes;   // fused: 16 real + 10 x (re, im)
+  info->planes = p->g.path == WINO_PATH_FUSED && p->g.alg == 0 ? 36 : p->g.planes;   // fused F4: 16 + 10 x (re, im)
   info->algorithm = p->g.alg; info->tile = p->g.tile; info->positions = p->g.npos;
   info->pieces = wino::kPieces;
   info->chunk_images = p->g.chunk_imgs; info->n_chunks = p->n_chunks;
@@ -247,12 +248,14 @@ static wino_status run_stage(const wino_plan_s* p, int stage, int chunk, const i
   int32_t* m = reinterpret_cast<int32_t*>(static_cast<int8_t*>(workspace) + p->v_bytes);
   cudaError_t e = cudaErrorInvalidValue;
   if (stage == 2)
-    e = g.path == WINO_PATH_FUSED ? wino::launch_input_transform_f(g, x, n0, imgs, vimg, s)
+    e = g.path == WINO_PATH_FUSED && g.alg == 0 ? wino::launch_input_transform_f(g, x, n0, imgs, vimg, s)
                                   : wino::launch_input_transform(g, x, n0, imgs, vimg, s);
   if (g.path == WINO_PATH_FUSED) {
     if (stage == 3)
-      e = wino::launch_fused(g, tiles_pad, n0, imgs, vimg, static_cast<const int8_t*>(w_wino), codes, rq_mult,
-                             rq_shift, y, s);
+      e = g.alg == 1 ? wino::launch_fused2(g, tiles_pad, n0, imgs, vimg, static_cast<const int8_t*>(w_wino), codes,
+                                           rq_mult, rq_shift, y, s)
+                     : wino::launch_fused(g, tiles_pad, n0, imgs, vimg, static_cast<const int8_t*>(w_wino), codes,
+                                          rq_mult, rq_shift, y, s);
   } else {
     if (stage == 3) e = wino::launch_gemm(g, tiles_pad, vimg, static_cast<const int8_t*>(w_wino), codes, m, s);
     if (stage == 4) e = wino::launch_output_transform(g, m, n0, imgs, rq_mult, rq_shift, y, s);

@@ -1,6 +1,6 @@
-"""GPU parity of the rational F(2x2,3x3) path (staged kernels with
-algorithm = WINO_ALG_F2X2) against the oracle's F(2x2) pipeline, element by element:
-codes, W' planes, V planes and M'' byte/int exact, y bit-exact."""
+"""GPU parity of the rational F(2x2,3x3) path (algorithm = WINO_ALG_F2X2, the staged
+kernels and the fused k_fused2) against the oracle's F(2x2) pipeline, element by element: codes, W'
+planes, V planes and M'' byte/int exact (staged), y bit-exact (both)."""
 import zlib
 
 import numpy as np
@@ -14,23 +14,28 @@ import layout_decode as LD
 pytestmark = pytest.mark.gpu
 
 
-def _conv(n, h, w, ci, co, pad, layout, scaling, out_mode=1, chunk_mb=0):
+PATHS = [pytest.param(1, id="staged"), pytest.param(0, id="fused")]
+
+
+def _conv(n, h, w, ci, co, pad, layout, scaling, out_mode=1, chunk_mb=0, path=1):
     import paper_1901_01965_b200 as W
     return W.WinoConv2d(n, h, w, ci, co, pad, layout, scaling, out_mode, workspace_mb=chunk_mb,
-                        path=W.WINO_PATH_STAGED, algorithm=W.WINO_ALG_F2X2)
+                        path=path, algorithm=W.WINO_ALG_F2X2)
 
 
-def _check(x, w, layout, pad=1, scaling=True, intermediates=True):
+def _check(x, w, layout, pad=1, scaling=True, intermediates=True, path=1):
+    intermediates = intermediates and path == 1   # V / W' / M'' decoders: staged layouts
     if layout == O.NCHW:
         n, ci, h, wd = x.shape
     else:
         n, h, wd, ci = x.shape
     co = w.shape[0]
-    conv = _conv(n, h, wd, ci, co, pad, layout, scaling)
+    conv = _conv(n, h, wd, ci, co, pad, layout, scaling, path=path)
     conv.transform_filter(torch.from_numpy(w).cuda())
     y = conv(torch.from_numpy(x).cuda()).cpu().numpy()
     ref = O.wino2_conv(x, w, pad, layout, scaling=scaling, want_M=intermediates)
     np.testing.assert_array_equal(y, ref.out32)
+    np.testing.assert_array_equal(conv.codes.cpu().numpy(), O.filter_transform2(w, layout, scaling=scaling)[2])
     if not scaling:
         np.testing.assert_array_equal(y.astype(np.int64), O.direct_conv(x, w, pad, layout))
     if intermediates:
@@ -54,43 +59,48 @@ def _check(x, w, layout, pad=1, scaling=True, intermediates=True):
 
 @pytest.mark.parametrize("layout", [O.NHWC, O.NCHW])
 @pytest.mark.parametrize("scaling", [False, True])
-def test_f2_c1_shape(layout, scaling):
+@pytest.mark.parametrize("path", PATHS)
+def test_f2_c1_shape(layout, scaling, path):
     x, w = synth.config_inputs("C1", layout)
-    _check(x, w, layout, 1, scaling)
+    _check(x, w, layout, 1, scaling, path=path)
 
 
 @pytest.mark.parametrize("case", [
     (2, 40, 37, 17, 70, 1, O.NHWC), (1, 23, 30, 64, 16, 0, O.NHWC), (3, 13, 9, 3, 5, 1, O.NCHW),
     (1, 3, 3, 1, 1, 0, O.NHWC), (2, 1, 1, 2, 3, 1, O.NCHW), (1, 57, 11, 40, 33, 1, O.NCHW),
-    (4, 18, 18, 96, 128, 1, O.NHWC)])
+    (4, 18, 18, 96, 128, 1, O.NHWC), (2, 11, 13, 200, 24, 1, O.NHWC), (1, 9, 9, 300, 40, 1, O.NCHW)])
 @pytest.mark.parametrize("scaling", [False, True])
-def test_f2_random_shapes(case, scaling):
+@pytest.mark.parametrize("path", PATHS)
+def test_f2_random_shapes(case, scaling, path):
     n, h, wd, ci, co, pad, layout = case
     rng = np.random.default_rng(zlib.crc32(repr((case, scaling, "f2")).encode()))
     x, w = synth.random_layer(rng, n, h, wd, ci, co, layout)
-    _check(x, w, layout, pad, scaling)
+    _check(x, w, layout, pad, scaling, path=path)
 
 
 @pytest.mark.parametrize("xv,wv", [(-128, -128), (127, 127), (-128, 127)])
 @pytest.mark.parametrize("scaling", [False, True])
-def test_f2_extremes(xv, wv, scaling):
+@pytest.mark.parametrize("path", PATHS)
+def test_f2_extremes(xv, wv, scaling, path):
     x = np.full((2, 12, 13, 40), xv, np.int8); w = np.full((24, 3, 3, 40), wv, np.int8)
-    _check(x, w, O.NHWC, 1, scaling)
+    _check(x, w, O.NHWC, 1, scaling, path=path)
 
 
-def test_f2_max_cin():
+@pytest.mark.parametrize("path", PATHS)
+def test_f2_max_cin(path):
     rng = np.random.default_rng(31)
     for ci, scaling in [(896, False), (768, True)]:
         x = rng.integers(-128, 128, (1, 6, 7, ci)).astype(np.int8)
         w = np.where(rng.integers(0, 2, (3, 3, 3, ci)) == 1, 127, -128).astype(np.int8)
-        _check(x, w, O.NHWC, 1, scaling, intermediates=False)
+        _check(x, w, O.NHWC, 1, scaling, intermediates=False, path=path)
 
 
 @pytest.mark.parametrize("layout", [O.NHWC, O.NCHW])
-def test_f2_int8_requant_and_chunks(layout):
+@pytest.mark.parametrize("path", PATHS)
+def test_f2_int8_requant_and_chunks(layout, path):
     rng = np.random.default_rng(32)
     x, w = synth.random_layer(rng, 24, 20, 20, 64, 48, layout)
-    conv = _conv(24, 20, 20, 64, 48, 1, layout, True, out_mode=0, chunk_mb=1)
+    conv = _conv(24, 20, 20, 64, 48, 1, layout, True, out_mode=0, chunk_mb=1, path=path)
     assert conv.info.n_chunks > 1
     conv.transform_filter(torch.from_numpy(w).cuda())
     xd = torch.from_numpy(x).cuda()
@@ -100,13 +110,14 @@ def test_f2_int8_requant_and_chunks(layout):
 
 
 @pytest.mark.parametrize("name", ["C2", "C3", "C4"])
-def test_f2_full_size_configs_sampled(name):
+@pytest.mark.parametrize("path", PATHS)
+def test_f2_full_size_configs_sampled(name, path):
     """BASELINE config shapes with the F(2x2) algorithm, NHWC, int8 out: first, middle and last
     images compared bit-exactly with the oracle run on those images alone."""
     layer = synth.CONFIGS[name].layers[0]
     x, w = synth.config_inputs(name)
     S = synth.requant_shift(layer)
-    conv = _conv(layer.n, layer.h, layer.w, layer.c_in, layer.c_out, 1, O.NHWC, True, out_mode=0)
+    conv = _conv(layer.n, layer.h, layer.w, layer.c_in, layer.c_out, 1, O.NHWC, True, out_mode=0, path=path)
     conv.transform_filter(torch.from_numpy(w).cuda())
     y = conv(torch.from_numpy(x).cuda(), 1, S).cpu().numpy()
     for i in sorted({0, layer.n // 2, layer.n - 1}):
@@ -114,8 +125,9 @@ def test_f2_full_size_configs_sampled(name):
     np.testing.assert_array_equal(conv.codes.cpu().numpy(), O.filter_transform2(w, O.NHWC, True)[2])
 
 
-def test_f2_fused_plan_rejected():
+def test_f2_fused_plan_reports_its_shape():
     import paper_1901_01965_b200 as W
-    with pytest.raises(W.WinoError):
-        W.WinoConv2d(1, 8, 8, 4, 4, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=W.WINO_PATH_FUSED,
-                     algorithm=W.WINO_ALG_F2X2)
+    conv = W.WinoConv2d(1, 8, 8, 4, 4, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=W.WINO_PATH_FUSED,
+                        algorithm=W.WINO_ALG_F2X2)
+    i = conv.info
+    assert i.path == 0 and i.stages == 2 and i.positions == 16 and i.tile == 2 and i.n_block == 32
