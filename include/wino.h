@@ -79,13 +79,13 @@ typedef struct {
                              transform + store (M'' stays on chip).
                              WINO_PATH_STAGED (1): K2, K3 GEMMs -> M'' in the workspace,
                              K4 output transform (M'' inspectable, see wino_plan_info).
-                             WINO_PATH_AUTO (2): fused when c_in <= 256 and the variant
-                             allows it (F4x4, target 255), else staged;
+                             WINO_PATH_AUTO (2): fused for F2x2, and for F4x4 when
+                             c_in <= 256 (target 255 only), else staged;
                              wino_plan_info.path reports the choice.                   */
     int algorithm;        /* WINO_ALG_F4X4 (0, default): complex F(4x4,3x3) over the
                              Gaussian integers, points {0, +-1, +-i};
                              WINO_ALG_F2X2 (1): rational F(2x2,3x3), G' = 2G,
-                             the configuration the paper evaluates; staged path only.
+                             the configuration the paper evaluates; either path.
                              Codes are [c_out][36] (F4x4) or [c_out][16] (F2x2).      */
     int input_type;       /* WINO_IN_INT8 (0, default) or WINO_IN_UINT8 (1): x and w are
                              uint8 with the zero points below (the paper's affine model,

@@ -98,12 +98,13 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   *out = nullptr;
   if (desc->path != WINO_PATH_FUSED && desc->path != WINO_PATH_STAGED && desc->path != WINO_PATH_AUTO)
     return WINO_ERR_INVALID_ARG;
-  // WINO_PATH_AUTO: the fused kernel where it measured faster or as fast and steadier -- c_in <= 256,
-  // where its ring holds one or two stages per slot-group (C2-C4; tools/path_ab.py), for the variants it
-  // implements (F(4x4), int8 or uint8, target 255) -- else staged
+  // WINO_PATH_AUTO: the fused kernels where they measured faster -- the complex F(4x4) one at c_in <= 256
+  // (C2-C4; tools/path_ab.py), the rational F(2x2) one everywhere (C2-C4: 1.4-1.7x the staged path) --
+  // for target 255; else staged
   wino_conv_desc dr = *desc;
   if (dr.path == WINO_PATH_AUTO)
-    dr.path = (dr.algorithm == WINO_ALG_F4X4 && dr.filter_target_max == 255 && dr.c_in <= auto_fused_max_cin())
+    dr.path = (dr.filter_target_max == 255 &&
+               (dr.algorithm == WINO_ALG_F2X2 || dr.c_in <= auto_fused_max_cin()))
                   ? WINO_PATH_FUSED
                   : WINO_PATH_STAGED;
   const wino_conv_desc& d = dr;

@@ -289,13 +289,14 @@ def test_vgg16_stack_full_size_sampled(path):
 
 
 def test_auto_path_choice_and_parity():
-    """WINO_PATH_AUTO resolves to fused for c_in <= 256 with the fused path's variants, staged
+    """WINO_PATH_AUTO resolves to fused for F(2x2) and for F(4x4) at c_in <= 256 (target 255), staged
     otherwise (info.path reports it), and either way the result is the oracle's."""
     W = _wino()
     for (ci, co, kw, want) in [(64, 64, {}, W.WINO_PATH_FUSED), (128, 128, {}, W.WINO_PATH_FUSED),
                                (128, 256, {}, W.WINO_PATH_FUSED), (256, 256, {}, W.WINO_PATH_FUSED),
                                (300, 64, {}, W.WINO_PATH_STAGED), (512, 512, {}, W.WINO_PATH_STAGED),
-                               (64, 64, dict(algorithm=W.WINO_ALG_F2X2), W.WINO_PATH_STAGED),
+                               (64, 64, dict(algorithm=W.WINO_ALG_F2X2), W.WINO_PATH_FUSED),
+                               (512, 64, dict(algorithm=W.WINO_ALG_F2X2), W.WINO_PATH_FUSED),
                                (64, 64, dict(input_type=W.WINO_IN_UINT8, x_zero_point=3, w_zero_point=250),
                                 W.WINO_PATH_FUSED),
                                (64, 64, dict(filter_target_max=127), W.WINO_PATH_STAGED)]:
