@@ -768,6 +768,30 @@ int oracle_wino_conv_u8(const uint8_t *x, const uint8_t *w, int zx, int zw, int 
     free(x16); free(w16);
     return r;
 }
+/* the rational F(2x2) pipeline on uint8 tensors with zero points (f1 x f2: the paper's own evaluated
+ * configuration) -- the same int16 core as the int8 entry points                    */
+int oracle_filter_transform2_u8(const uint8_t *w, int zw, int Cout, int Cin, int layout, int scaling, int target,
+                                int64_t *W_out, int64_t *Wp_out, uint8_t *codes_out) {
+    int16_t *w16 = widen_u8(w, WN, zw);
+    int r = oracle_filter_transform2_16(w16, Cout, Cin, layout, scaling, target, W_out, Wp_out, codes_out);
+    free(w16);
+    return r;
+}
+void oracle_input_transform2_u8(const uint8_t *x, int zx, int N, int H, int W, int Cin, int pad, int layout,
+                                int64_t *D_out) {
+    int16_t *x16 = widen_u8(x, XN, zx);
+    oracle_input_transform2_16(x16, N, H, W, Cin, pad, layout, D_out);
+    free(x16);
+}
+int oracle_wino2_conv_u8(const uint8_t *x, const uint8_t *w, int zx, int zw, int N, int H, int W, int Cin,
+                         int Cout, int pad, int layout, int scaling, int target, int32_t M0, int S,
+                         int32_t *out32, int8_t *y8, int64_t *M_out, int64_t *Mpp_out) {
+    int16_t *x16 = widen_u8(x, XN, zx), *w16 = widen_u8(w, WN, zw);
+    int r = oracle_wino2_conv16(x16, w16, N, H, W, Cin, Cout, pad, layout, scaling, target, M0, S,
+                                out32, y8, M_out, Mpp_out);
+    free(x16); free(w16);
+    return r;
+}
 #undef XN
 #undef WN
 

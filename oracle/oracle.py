@@ -77,6 +77,13 @@ def lib():
         L.oracle_wino_conv_u8.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32,
                                           ctypes.c_int32, i32, P, P, P, P]
         L.oracle_wino_conv_u8.restype = i32
+        L.oracle_filter_transform2_u8.argtypes = [P, i32, i32, i32, i32, i32, i32, P, P, P]
+        L.oracle_filter_transform2_u8.restype = i32
+        L.oracle_input_transform2_u8.argtypes = [P, i32, i32, i32, i32, i32, i32, i32, P]
+        L.oracle_input_transform2_u8.restype = None
+        L.oracle_wino2_conv_u8.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32,
+                                           ctypes.c_int32, i32, P, P, P, P]
+        L.oracle_wino2_conv_u8.restype = i32
         _lib = L
     return _lib
 
@@ -413,3 +420,51 @@ def wino_conv_u8(x, w, zx, zw, pad=1, layout=NHWC, scaling=True, target=255, M0=
         raise ValueError(f"oracle invariant violated (status {st})")
     return WinoResult(out32, y8, M, Mpp, st)
 
+
+
+# ---------------------------------------------------------------- F(2x2) x uint8 (the paper's evaluated configuration)
+def filter_transform2_u8(w, zw, layout=NHWC, scaling=True, target=255):
+    """F(2x2) offline filter path on uint8 weights with zero point zw (int9 values)."""
+    w = _c(w, np.uint8)
+    Cout = w.shape[0]
+    Cin = w.shape[1] if layout == NCHW else w.shape[3]
+    W = np.zeros((Cout, Cin, 16), np.int64); Wp = np.zeros((Cout, Cin, 16), np.int64)
+    codes = np.zeros((Cout, 16), np.uint8)
+    if lib().oracle_filter_transform2_u8(_p(w), int(zw), Cout, Cin, layout, int(bool(scaling)), target,
+                                         _p(W), _p(Wp), _p(codes)) != 0:
+        raise ValueError("scale factor out of range")
+    return W, Wp, codes
+
+
+def input_transform2_u8(x, zx, pad=1, layout=NHWC) -> np.ndarray:
+    x = _c(x, np.uint8)
+    if layout == NCHW:
+        N, Cin, H, W = x.shape
+    else:
+        N, H, W, Cin = x.shape
+    th, tw = tiles2(H, W, pad)
+    D = np.zeros((N * th * tw, Cin, 16), np.int64)
+    lib().oracle_input_transform2_u8(_p(x), int(zx), N, H, W, Cin, pad, layout, _p(D))
+    return D
+
+
+def wino2_conv_u8(x, w, zx, zw, pad=1, layout=NHWC, scaling=True, target=255, M0=1, S=0,
+                  want_y8=True, want_M=False) -> WinoResult:
+    """The rational F(2x2) pipeline on uint8 tensors with zero points (int9 values)."""
+    x = _c(x, np.uint8); w = _c(w, np.uint8)
+    N, H, W, Cin, Cout = _dims(x, w, layout)
+    Ho, Wo = out_hw(H, W, pad)
+    th, tw = tiles2(H, W, pad)
+    T = N * th * tw
+    shape = (N, Cout, Ho, Wo) if layout == NCHW else (N, Ho, Wo, Cout)
+    out32 = np.zeros(shape, np.int32)
+    y8 = np.zeros(shape, np.int8) if want_y8 else None
+    M = np.zeros((T, Cout, 16), np.int64) if want_M else None
+    Mpp = np.zeros((T, Cout, 16), np.int64) if want_M else None
+    st = lib().oracle_wino2_conv_u8(_p(x), _p(w), int(zx), int(zw), N, H, W, Cin, Cout, pad, layout,
+                                    int(bool(scaling)), target, int(M0), int(S), _p(out32),
+                                    _p(y8) if y8 is not None else None, _p(M) if M is not None else None,
+                                    _p(Mpp) if Mpp is not None else None)
+    if st != 0:
+        raise ValueError(f"oracle invariant violated (status {st})")
+    return WinoResult(out32, y8, M, Mpp, st)

@@ -92,3 +92,34 @@ def test_scaled_u8_invariants_and_error():
         res = O.wino_conv_u8(x, wt, zx, zw, 1, O.NHWC, scaling=True)
         ref = O.direct_conv_u8(x, wt, zx, zw, 1, O.NHWC)
         assert np.abs(res.out32 - ref).mean() <= 0.01 * np.abs(ref).mean()
+
+
+# ---------------------------------------------------------------- F(2x2) x uint8: the paper's evaluated configuration
+@pytest.mark.parametrize("layout", [O.NHWC, O.NCHW])
+def test_unscaled_f2_u8_equals_direct(layout):
+    """Unscaled F(2x2) on uint8 tensors with zero points equals the direct correlation of the int9 values."""
+    rng = np.random.default_rng(71)
+    for (n, h, w, ci, co, pad, zx, zw) in [(1, 7, 9, 5, 3, 1, 128, 128), (2, 6, 5, 3, 4, 0, 0, 255),
+                                           (1, 3, 3, 2, 2, 1, 255, 0), (1, 12, 11, 17, 9, 1, 7, 200)]:
+        x = rng.integers(0, 256, (n, h, w, ci), dtype=np.int64).astype(np.uint8)
+        wt = rng.integers(0, 256, (co, 3, 3, ci), dtype=np.int64).astype(np.uint8)
+        if layout == O.NCHW:
+            x = np.ascontiguousarray(x.transpose(0, 3, 1, 2)); wt = np.ascontiguousarray(wt.transpose(0, 3, 1, 2))
+        r = O.wino2_conv_u8(x, wt, zx, zw, pad, layout, scaling=False)
+        np.testing.assert_array_equal(r.out32.astype(np.int64), O.direct_conv_u8(x, wt, zx, zw, pad, layout))
+
+
+def test_scaled_f2_u8_reaches_the_papers_section41_corner():
+    """P:290-330 on int9 weights: the centre position reaches 9 * 255 = 2295 (12 bits), scaled by the 14/128
+    factor the paper prints; every W' fits 9 bits; the error against direct convolution stays small."""
+    x = np.full((1, 6, 6, 8), 255, np.uint8); w = np.full((4, 3, 3, 8), 255, np.uint8)
+    W, Wp, codes = O.filter_transform2_u8(w, 0, O.NHWC, scaling=True)
+    assert int(np.abs(W[..., 5]).max()) == 9 * 255 and int(np.abs(W[..., 0]).max()) == 4 * 255   # centre, corner
+    assert O.decode_code(int(codes[0, 5])) == (14, 7)         # position (1,1): 2295 -> 14/128 (P:330)
+    assert np.abs(Wp).max() <= 255
+    rng = np.random.default_rng(72)
+    x = rng.integers(0, 256, (2, 10, 9, 16), dtype=np.int64).astype(np.uint8)
+    w = rng.integers(0, 256, (6, 3, 3, 16), dtype=np.int64).astype(np.uint8)
+    ref = O.direct_conv_u8(x, w, 120, 130, 1, O.NHWC)
+    res = O.wino2_conv_u8(x, w, 120, 130, 1, O.NHWC, scaling=True)
+    assert np.abs(res.out32 - ref).mean() <= 0.01 * np.abs(ref).mean()
