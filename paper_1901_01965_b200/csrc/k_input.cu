@@ -301,6 +301,7 @@ cudaError_t launch_input_transform_f(const Geom& g, const int8_t* x, int n0, int
 // ---- rational F(2x2,3x3): 4x4 patch at (2ty - pad, 2tx - pad), D = B^T d B with the
 // F(2,3) matrix B^T = [[1,0,-1,0],[0,1,1,0],[0,-1,1,0],[0,1,0,-1]] (A25), 16 real planes
 // (position i*4 + j), balanced pieces, staged V layout (plane stride = g.planes = 16).
+template <bool U8>   // uint8 + zero point (f2, A28): out-of-map pixels read the zero point (d = 0)
 __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, const int8_t* __restrict__ x, int n0,
                                                                     int imgs, int8_t* __restrict__ vimg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, cons
   pdl_trigger();
   pdl_wait();
   uint32_t w[16];   // 2 channels per pixel
+  const uint32_t zpair = U8 ? (uint32_t)(g.zx | (g.zx << 8)) : 0u;
   {
     int img = 0, iy0 = -1000000, ix0 = -1000000;
     if (t < imgs * g.tpi) {
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, cons
         const bool vy = iy0 + a >= 0 && iy0 + a < g.h;
         const uint16_t* rp = reinterpret_cast<const uint16_t*>(p0 + a * rstride);
 #pragma unroll
-        for (int b = 0; b < 4; b++) w[a * 4 + b] = (vy && vx[b]) ? (uint32_t)__ldg(rp + (b * g.cin >> 1)) : 0u;
+        for (int b = 0; b < 4; b++) w[a * 4 + b] = (vy && vx[b]) ? (uint32_t)__ldg(rp + (b * g.cin >> 1)) : zpair;
       }
     } else {
       const long long cstep = g.layout == 1 ? 1 : (long long)g.h * g.w;
@@ -340,12 +342,12 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, cons
 #pragma unroll
         for (int b = 0; b < 4; b++) {
           const int iy = iy0 + a, ix = ix0 + b;
-          uint32_t v = 0;
+          uint32_t v = zpair;
           if (vx[b] && iy >= 0 && iy < g.h) {
             const long long i0 = g.layout == 1 ? (((long long)img * g.h + iy) * g.w + ix) * g.cin + c
                                                : (((long long)img * g.cin + c) * g.h + iy) * g.w + ix;
             v = (uint8_t)__ldg(x + i0);
-            if (c + 1 < g.cin) v |= (uint32_t)(uint8_t)__ldg(x + i0 + cstep) << 8;
+            v |= (c + 1 < g.cin) ? (uint32_t)(uint8_t)__ldg(x + i0 + cstep) << 8 : (zpair & 0xff00u);
           }
           w[a * 4 + b] = v;
         }
@@ -360,8 +362,8 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, cons
     int r[4][4];   // d' = B^T d, column by column
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      const int d0 = sbyte(w[0 * 4 + j], ch), d1 = sbyte(w[1 * 4 + j], ch), d2 = sbyte(w[2 * 4 + j], ch),
-                d3 = sbyte(w[3 * 4 + j], ch);
+      const int d0 = dval<U8>(g, w[0 * 4 + j], ch), d1 = dval<U8>(g, w[1 * 4 + j], ch),
+                d2 = dval<U8>(g, w[2 * 4 + j], ch), d3 = dval<U8>(g, w[3 * 4 + j], ch);
       r[0][j] = d0 - d2; r[1][j] = d1 + d2; r[2][j] = d2 - d1; r[3][j] = d1 - d3;
     }
 #pragma unroll
@@ -384,7 +386,9 @@ cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int i
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
   dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
-  if (g.alg == 1) return launch_pdl_co(k_input_transform2, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
+  if (g.alg == 1 && g.in_u8)
+    return launch_pdl_co(k_input_transform2<true>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
+  if (g.alg == 1) return launch_pdl_co(k_input_transform2<false>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
   if (g.in_u8) return launch_pdl_co(k_input_transform<true>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
   return launch_pdl_co(k_input_transform<false>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
 }

@@ -118,7 +118,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   if (d.input_type == WINO_IN_UINT8) {
     if (d.x_zero_point < 0 || d.x_zero_point > 255 || d.w_zero_point < 0 || d.w_zero_point > 255)
       return WINO_ERR_INVALID_ARG;
-    if (d.algorithm != WINO_ALG_F4X4 || d.c_in > 224) return WINO_ERR_UNSUPPORTED;
+    if (d.c_in > 224) return WINO_ERR_UNSUPPORTED;   // int32 exactness of Y for int9 values (A28)
   }
   if (d.n < 1 || d.h < 1 || d.w < 1 || d.c_in < 1 || d.c_out < 1) return WINO_ERR_UNSUPPORTED;
   if (d.pad != 0 && d.pad != 1) return WINO_ERR_UNSUPPORTED;

@@ -38,7 +38,7 @@ def test_status_strings_and_pre_cuda_validation():
                        (dict(out_mode=9), L.WINO_ERR_INVALID_ARG), (dict(h=1, pad=0), L.WINO_ERR_UNSUPPORTED),
                        (dict(filter_target_max=127), L.WINO_ERR_UNSUPPORTED), (dict(path=3), L.WINO_ERR_INVALID_ARG),
                        (dict(algorithm=2), L.WINO_ERR_INVALID_ARG),
-                       (dict(algorithm=1, path=1, input_type=1), L.WINO_ERR_UNSUPPORTED),
+                       (dict(algorithm=1, path=1, input_type=1, c_in=225), L.WINO_ERR_UNSUPPORTED),
                        (dict(input_type=2), L.WINO_ERR_INVALID_ARG),
                        (dict(input_type=1, x_zero_point=256, path=1), L.WINO_ERR_INVALID_ARG),
                        (dict(input_type=1, path=0, c_in=225), L.WINO_ERR_UNSUPPORTED),

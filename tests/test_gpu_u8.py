@@ -114,3 +114,39 @@ def test_u8_with_zero_point_128_equals_int8_mode(path):
         conv.transform_filter(torch.from_numpy(sh(w)).cuda())
         outs.append(conv(torch.from_numpy(sh(x)).cuda(), 1, S).cpu().numpy())
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+# ---------------------------------------------------------------- F(2x2) x uint8 (the paper's evaluated configuration)
+@pytest.mark.parametrize("case", [
+    (2, 40, 37, 17, 70, 1, O.NHWC, 128, 128), (1, 23, 30, 64, 16, 0, O.NHWC, 0, 255), (3, 13, 9, 3, 5, 1, O.NCHW, 255, 0),
+    (1, 3, 3, 1, 1, 0, O.NHWC, 7, 200), (4, 18, 18, 96, 128, 1, O.NHWC, 100, 140), (1, 9, 10, 224, 40, 1, O.NHWC, 128, 128)])
+@pytest.mark.parametrize("scaling", [False, True])
+@pytest.mark.parametrize("path", ["staged", "fused"])
+def test_f2_u8_random_shapes(case, scaling, path):
+    import paper_1901_01965_b200 as W
+    n, h, wd, ci, co, pad, layout, zx, zw = case
+    rng = np.random.default_rng(zlib.crc32(repr((case, scaling, "f2u8")).encode()))
+    x, w = _layer(rng, n, h, wd, ci, co, layout)
+    conv = W.WinoConv2d(n, h, wd, ci, co, pad, layout, scaling, W.WINO_OUT_INT32,
+                        path=W.WINO_PATH_STAGED if path == "staged" else W.WINO_PATH_FUSED,
+                        algorithm=W.WINO_ALG_F2X2, input_type=W.WINO_IN_UINT8, x_zero_point=zx, w_zero_point=zw)
+    conv.transform_filter(torch.from_numpy(w).cuda())
+    y = conv(torch.from_numpy(x).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(y, O.wino2_conv_u8(x, w, zx, zw, pad, layout, scaling=scaling).out32)
+    np.testing.assert_array_equal(conv.codes.cpu().numpy(), O.filter_transform2_u8(w, zw, layout, scaling=scaling)[2])
+    if not scaling:
+        np.testing.assert_array_equal(y.astype(np.int64), O.direct_conv_u8(x, w, zx, zw, pad, layout))
+
+
+@pytest.mark.parametrize("path", ["staged", "fused"])
+def test_f2_u8_int9_extremes_and_requant(path):
+    import paper_1901_01965_b200 as W
+    p = W.WINO_PATH_STAGED if path == "staged" else W.WINO_PATH_FUSED
+    for xv, zx, wv, zw in [(0, 255, 255, 0), (255, 0, 255, 0)]:
+        x = np.full((1, 10, 11, 224), xv, np.uint8); w = np.full((8, 3, 3, 224), wv, np.uint8)
+        conv = W.WinoConv2d(1, 10, 11, 224, 8, 1, O.NHWC, True, W.WINO_OUT_INT8, path=p, algorithm=W.WINO_ALG_F2X2,
+                            input_type=W.WINO_IN_UINT8, x_zero_point=zx, w_zero_point=zw)
+        conv.transform_filter(torch.from_numpy(w).cuda())
+        for M0, S in [(1, 12), (3, 16)]:
+            np.testing.assert_array_equal(conv(torch.from_numpy(x).cuda(), M0, S).cpu().numpy(),
+                                          O.wino2_conv_u8(x, w, zx, zw, 1, O.NHWC, True, M0=M0, S=S).y8)
