@@ -579,7 +579,7 @@ def roofline(kern, info, layer, peaks, traffic=None):
     i8_sus = 2.0 * peaks["bf16_tflops_sustained"]   # int8 dense = 2 x bf16 (nominal ratio 4.5/2.25)
     px = info.tile * info.tile                     # output pixels per tile (16 F4x4, 4 F2x2)
     mults = alg_mults(info)                        # general multiplications per (tile, cin, cout)
-    vpc = 2 * info.planes if info.path == 1 else 72   # V bytes per (tile, channel)
+    vpc = 72 if (info.path == 0 and info.algorithm == 0) else 2 * info.planes   # V bytes per (tile, channel)
     x_chunk = chunk_tiles * px * layer.c_in        # ~ bytes of x per chunk
     res = {}
     # K1: reads w (9 Cin Cout B), writes the W' image + codes
