@@ -14,7 +14,7 @@
 // [s16 | s8] and A_lo . [W hi | W lo] into [s8 | s0] (the accumulator slots start at zero and are
 // re-zeroed by the epilogue, so every UMMA accumulates).
 //
-// Persistent CTAs (fewest for the unit rounds), 19 warps (<= 96 registers):
+// Persistent CTAs (fewest for the unit rounds), 19 warps (<= 96 registers: 5 warps on some SM sub-partition):
 //   warps 0..15  epilogue: TMEM lane quadrant w % 4 (32 tiles), couts 8 (w / 4) .. +7
 //   warps 16, 17 producers (one elected lane each, alternate stages): V and W' bulk copies
 //   warp 18      MMA issuer (one elected lane)
@@ -208,7 +208,6 @@ __global__ void __launch_bounds__(kT2Threads, 1)
     const int row = quad * 32 + lane;
     const int etid = threadIdx.x;                       // 0..511
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + cw * kC2;
-    int pc = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int tb = u / nblocks, nb = u - tb * nblocks;
       e2_barrier();   // the previous unit's etab reads are done
@@ -226,10 +225,11 @@ __global__ void __launch_bounds__(kT2Threads, 1)
         for (int j = 0; j < 2; j++)
 #pragma unroll
           for (int c = 0; c < kC2; c++) Y[i][j][c] = 0;
-#pragma unroll 1
-      for (int p = 0; p < 16; p++, pc++) {   // plane p = position (r, cc) = (p / 4, p % 4)
-        const int b = pc % kSlots2;
-        mbar_wait(tfull0 + 8 * b, (pc / kSlots2) & 1);
+#pragma unroll   // compile-time positions: the A coefficients fold into adds, subtractions or nothing
+      for (int p = 0; p < 16; p++) {   // plane p = position (r, cc) = (p / 4, p % 4)
+        // 16 planes per unit over 4 slots: slot p % 4, phase (p / 4) & 1 in every unit
+        const int b = p & (kSlots2 - 1);
+        mbar_wait(tfull0 + 8 * b, (p / kSlots2) & 1);
         tc_fence_after();
         const uint32_t a = lane_base + b * kSlotCols2;
         uint32_t h[8], x[8], l[8];
@@ -244,9 +244,7 @@ __global__ void __launch_bounds__(kT2Threads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty0 + 8 * b);
-        const uint4 m0 = *reinterpret_cast<const uint4*>(etab + p * kN2 + cw * kC2);
-        const uint4 m1 = *reinterpret_cast<const uint4*>(etab + p * kN2 + cw * kC2 + 4);
-        const uint32_t mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+        const uint32_t* mm = etab + p * kN2 + cw * kC2;   // read per cout: fewer live registers
         const int r = p >> 2, cc = p & 3;
 #pragma unroll
         for (int c = 0; c < kC2; c++) {
@@ -256,7 +254,7 @@ __global__ void __launch_bounds__(kT2Threads, 1)
           for (int i = 0; i < 2; i++)
 #pragma unroll
             for (int j = 0; j < 2; j++) {
-              const int coef = a2(r, i) * a2(cc, j);   // r, cc are runtime: coef in {-1, 0, 1}
+              const int coef = a2(r, i) * a2(cc, j);   // in {-1, 0, 1}
               Y[i][j][c] += coef * mv;
             }
         }
