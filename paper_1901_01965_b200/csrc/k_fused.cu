@@ -125,7 +125,9 @@ __device__ __forceinline__ void tmem_zero4(uint32_t taddr) {
 // and a fixed shift.  rha(p / 2^7) = (p + 64 - [p < 0]) >> 7 (floor shift).  The
 // unscaled code is m' = 128, which returns v.
 __device__ __forceinline__ int32_t frscale(int32_t v, uint32_t mq) {
-  const long long p = (long long)v * (long long)mq + (long long)(64 + (v >> 31));
+  // signed 32 x 32 -> 64 multiply-add (one IMAD.WIDE; 64 + (v >> 31) >= 0 adds without a sign fix-up)
+  long long p;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(p) : "r"(v), "r"((int32_t)mq), "l"((long long)(64 + (v >> 31))));
   return (int32_t)(p >> 7);
 }
 
