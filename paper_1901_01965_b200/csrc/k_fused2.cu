@@ -11,8 +11,8 @@
 // Work unit = (128-tile block, 32-cout block): the 16 planes as 8 pairs; the output state is Y (4 words
 // per (tile, cout)), 32 registers per epilogue thread, so the unit can be 32 couts wide (twice the
 // complex fused kernel's) and its UMMAs are N = 64.  Per K step and plane: A_hi . [W hi | W lo] into
-// [s16 | s8] and A_lo . [W hi | W lo] into [s8 | s0] (the accumulator slots start at zero and are
-// re-zeroed by the epilogue, so every UMMA accumulates).
+// [s16 | s8] and A_lo . [W hi | W lo] into [s8 | s0] (the plane's first lo UMMA overwrites [s8 | s0];
+// the s16 block starts at zero and is re-zeroed by the epilogue after each read).
 //
 // Persistent CTAs (fewest for the unit rounds), 19 warps (<= 96 registers: 5 warps on some SM sub-partition):
 //   warps 0..15  epilogue: TMEM lane quadrant w % 4 (32 tiles), couts 8 (w / 4) .. +7
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kT2Threads, 1)
     const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * kC2;
     for (int b = 0; b < kSlots2; b++)
 #pragma unroll
-      for (int blk = 0; blk < 3; blk++) tzero8(lb + b * kSlotCols2 + blk * kN2);
+      for (int blk = 0; blk < 1; blk++) tzero8(lb + b * kSlotCols2 + blk * kN2);   // s16 blocks
     tst_wait();
   }
   tc_fence_before();
@@ -189,8 +189,10 @@ __global__ void __launch_bounds__(kT2Threads, 1)
                 const uint64_t ah = umma_desc(va + kk * kPlaneV, 128, 256);
                 const uint64_t al = umma_desc(va + kk * kPlaneV + kVBlockBytes, 128, 256);
                 const uint64_t bb = umma_desc(wa + kk * kPlaneW, 128, 256);
-                umma_i8(d, ah, bb, id64, 1u);          // [s16 | s8] += hi . [W hi | W lo]
-                umma_i8(d + kN2, al, bb, id64, 1u);    // [s8 | s0]  += lo . [W hi | W lo]
+                // the plane's first K step overwrites [s8 | s0] (columns 32..95); s16 (0..31) was zeroed
+                // by the epilogue, so only one of the three column blocks needs a TMEM store
+                umma_i8(d + kN2, al, bb, id64, (k0 + kk) > 0);   // [s8 | s0]  (+)= lo . [W hi | W lo]
+                umma_i8(d, ah, bb, id64, 1u);                    // [s16 | s8] +=   hi . [W hi | W lo]
               }
             }
             umma_commit(empty0 + 8 * s);   // stage reusable once these MMAs have read it
@@ -239,9 +241,7 @@ __global__ void __launch_bounds__(kT2Threads, 1)
         tld8(a + kN2, x);
         tld8(a + 2 * kN2, l);
         tmem_ld_wait();
-        tzero8(a);
-        tzero8(a + kN2);
-        tzero8(a + 2 * kN2);
+        tzero8(a);   // s16 only: the first K step overwrites s8 and s0
         tst_wait();
         tc_fence_before();
         __syncwarp();
