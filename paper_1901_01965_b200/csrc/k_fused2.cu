@@ -23,11 +23,21 @@
 // TMEM: 4 slots of 96 columns (one plane: [s16 | s8 | s0] x 32 couts), 128 columns spare.
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
 #include "layout.cuh"
 #include "ptx.cuh"
+
+// Debug-only subtraction switches (tools/README.md): 0 in every product build
+#ifndef WINO_F2_NOFEED
+#define WINO_F2_NOFEED 0   // no copies, no UMMAs: the epilogue and the barrier skeleton alone
+#endif
+#ifndef WINO_F2_NOFOLD
+#define WINO_F2_NOFOLD 0   // no reverse scaling / output-transform arithmetic
+#endif
 
 namespace wino {
 
@@ -67,6 +77,12 @@ __device__ __forceinline__ int32_t rscale7(int32_t v, uint32_t mq) {
   asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(p) : "r"(v), "r"((int32_t)mq), "l"((long long)(64 + (v >> 31))));
   return (int32_t)(p >> 7);
 }
+template <typename F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <typename F>
+__device__ __forceinline__ void static_for16(F&& f) { static_for_impl(f, std::make_integer_sequence<int, 16>{}); }
 // A[k][i] of the F(2,3) output transform, A^T = [[1,1,1,0],[0,1,-1,-1]]
 __host__ __device__ constexpr int a2(int k, int i) { return i == 0 ? (k < 3 ? 1 : 0) : (k == 0 ? 0 : (k == 1 ? 1 : -1)); }
 
@@ -140,7 +156,7 @@ __global__ void __launch_bounds__(kT2Threads, 1)
         const int8_t* v0 = V + ((long long)tb * 16 + 2 * pr) * ksteps * kPlaneV;
         const int8_t* w0 = W + ((long long)nb * 16 + 2 * pr) * ksteps * kPlaneW;
         for (int k0 = 0; k0 < ksteps; k0 += KC, it++) {
-          if (it % kP2Warps != pw) continue;
+          if (it % kP2Warps != pw || WINO_F2_NOFEED) continue;
           const int s = it % kStg;
           mbar_wait(empty0 + 8 * s, ((it / kStg) & 1) ^ 1);
           const int kn = min(KC, ksteps - k0);
@@ -175,13 +191,13 @@ __global__ void __launch_bounds__(kT2Threads, 1)
         tc_fence_after();
         for (int k0 = 0; k0 < ksteps; k0 += KC, it++) {
           const int s = it % kStg;
-          mbar_wait(full0 + 8 * s, (it / kStg) & 1);
+          if (!WINO_F2_NOFEED) mbar_wait(full0 + 8 * s, (it / kStg) & 1);
           tc_fence_after();
           const int kn = min(KC, ksteps - k0);
           const uint32_t st = sbase + s * kStgBytes;
           // stage layout: whole-K stages hold plane q at q * ksteps steps, chunked ones at q * KC steps
           const int qs = kn == ksteps ? ksteps : KC;
-          if (elect_one()) {
+          if (!WINO_F2_NOFEED && elect_one()) {
             for (int q = 0; q < 2; ++q) {
               const uint32_t d = tmem + (q ? b1 : b0) * kSlotCols2;
               const uint32_t va = st + (uint32_t)(q * qs) * kPlaneV, wa = st + kStgV + (uint32_t)(q * qs) * kPlaneW;
@@ -200,8 +216,7 @@ __global__ void __launch_bounds__(kT2Threads, 1)
           __syncwarp();
         }
         if (elect_one()) {
-          umma_commit(tfull0 + 8 * b0);
-          umma_commit(tfull0 + 8 * b1);
+          umma_commit(tfull0 + 8 * (b0 >> 1));   // one commit for the pair's two slots (commits cost ~200 cycles)
         }
         __syncwarp();
       }
@@ -229,29 +244,38 @@ __global__ void __launch_bounds__(kT2Threads, 1)
         for (int j = 0; j < 2; j++)
 #pragma unroll
           for (int c = 0; c < kC2; c++) Y[i][j][c] = 0;
-#pragma unroll   // compile-time positions: the A coefficients fold into adds, subtractions or nothing
-      for (int p = 0; p < 16; p++) {   // plane p = position (r, cc) = (p / 4, p % 4)
-        // 16 planes per unit over 4 slots: slot p % 4, phase (p / 4) & 1 in every unit
-        const int b = p & (kSlots2 - 1);
-        mbar_wait(tfull0 + 8 * b, (p / kSlots2) & 1);
+      // Software-pipelined over the 16 planes: the TMEM loads of plane p + 1 are in flight while plane
+      // p is scaled and folded into Y.  16 planes per unit over 4 slots: slot p % 4, phase (p / 4) & 1.
+      uint32_t h[8], x[8], l[8];
+      int32_t v[kC2];   // M of the plane being folded
+      auto fetch = [&](auto pc) {   // wait for plane P's slot and start its three 8-column loads
+        constexpr int P = decltype(pc)::value;
+        // pair barrier (P / 2) % 2 (the pair's slots are 2 (P / 2 % 2) and +1), phase (P / 4) & 1
+        if constexpr ((P & 1) == 0) mbar_wait(tfull0 + 8 * ((P >> 1) & 1), (P / kSlots2) & 1);
         tc_fence_after();
-        const uint32_t a = lane_base + b * kSlotCols2;
-        uint32_t h[8], x[8], l[8];
+        const uint32_t a = lane_base + (P & (kSlots2 - 1)) * kSlotCols2;
         tld8(a, h);
         tld8(a + kN2, x);
         tld8(a + 2 * kN2, l);
+      };
+      auto land = [&](auto pc) {    // loads landed: re-zero s16, release the slot, compose M
+        constexpr int P = decltype(pc)::value;
         tmem_ld_wait();
-        tzero8(a);   // s16 only: the first K step overwrites s8 and s0
+        tzero8(lane_base + (P & (kSlots2 - 1)) * kSlotCols2);   // s16 only: the first K step overwrites s8, s0
         tst_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty0 + 8 * b);
-        const uint32_t* mm = etab + p * kN2 + cw * kC2;   // read per cout: fewer live registers
-        const int r = p >> 2, cc = p & 3;
+        if (lane == 0) mbar_arrive(tempty0 + 8 * (P & (kSlots2 - 1)));
+#pragma unroll
+        for (int c = 0; c < kC2; c++) v[c] = (int32_t)((h[c] << 16) + (x[c] << 8) + l[c]);
+      };
+      auto fold = [&](auto pc) {    // Y[i][j] += A[r][i] A[cc][j] M'' with M'' = rha(M m / 2^q)
+        constexpr int P = decltype(pc)::value, r = P >> 2, cc = P & 3;
+        if (WINO_F2_NOFOLD) return;
+        const uint32_t* mm = etab + P * kN2 + cw * kC2;
 #pragma unroll
         for (int c = 0; c < kC2; c++) {
-          const int32_t mv = rscale7((int32_t)((h[c] << 16) + (x[c] << 8) + l[c]), mm[c]);
-          // Y[i][j] += A[r][i] A[cc][j] M''
+          const int32_t mv = rscale7(v[c], mm[c]);
 #pragma unroll
           for (int i = 0; i < 2; i++)
 #pragma unroll
@@ -260,7 +284,15 @@ __global__ void __launch_bounds__(kT2Threads, 1)
               Y[i][j][c] += coef * mv;
             }
         }
-      }
+      };
+      fetch(std::integral_constant<int, 0>{});
+      land(std::integral_constant<int, 0>{});
+      static_for16([&](auto pc) {
+        constexpr int P = decltype(pc)::value;
+        if constexpr (P + 1 < 16) fetch(std::integral_constant<int, P + 1>{});
+        fold(pc);
+        if constexpr (P + 1 < 16) land(std::integral_constant<int, P + 1>{});
+      });
       // ---- out32 = rha(Y / 4) (A26), requantisation (A14), crop, store
       const int t = tb * kMBlock + row;
       if (t >= imgs * g.tpi) continue;
