@@ -241,6 +241,11 @@ wino_status wino_check_codes(wino_plan_t plan, const uint8_t *scale_codes, int32
  * The buffer must hold num_SMs * 96 uint64.  NULL turns tracing off.      */
 wino_status wino_debug_set_trace(void *device_buffer);
 
+/* Debug / test only: floor(n / d) through the plan-constant fast division the
+ * kernels use for their tile decode (layout.cuh FastDiv), evaluated on the host.
+ * n in [0, 2^31), d >= 1; returns -1 for arguments outside that range.     */
+int wino_debug_fastdiv(int n, int d);
+
 /* Harness op for the VGG stack (A22): 2x2 stride-2 max pool on int8,
  * layout per `layout`, y [N][C][H/2][W/2] or [N][H/2][W/2][C].           */
 wino_status wino_maxpool2_int8(const int8_t *x, int n, int h, int w, int c, int layout,

@@ -22,7 +22,7 @@ WINO_IN_INT8, WINO_IN_UINT8 = 0, 1
 EXPORTS = ("wino_status_string", "wino_last_cuda_error", "wino_plan", "wino_plan_destroy", "wino_plan_query", "wino_filter_bytes",
            "wino_codes_bytes", "wino_workspace_bytes", "wino_output_bytes", "wino_transform_filter",
            "wino_conv2d_int8", "wino_conv2d_int8_host", "wino_conv2d_int8_stage", "wino_check_codes", "wino_maxpool2_int8",
-           "wino_debug_set_trace")
+           "wino_debug_set_trace", "wino_debug_fastdiv")
 
 
 class wino_conv_desc(ctypes.Structure):
@@ -79,6 +79,7 @@ def lib():
         L.wino_check_codes.argtypes = [P, P, P, P]; L.wino_check_codes.restype = I
         L.wino_maxpool2_int8.argtypes = [P, I, I, I, I, I, P, P]; L.wino_maxpool2_int8.restype = I
         L.wino_debug_set_trace.argtypes = [P]; L.wino_debug_set_trace.restype = I
+        L.wino_debug_fastdiv.argtypes = [I, I]; L.wino_debug_fastdiv.restype = I
         _lib = L
     return _lib
 

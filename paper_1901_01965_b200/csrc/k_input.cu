@@ -90,8 +90,8 @@ __device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restri
   {
     int img = 0, iy0 = -1000000, ix0 = -1000000;   // padding tiles read nothing
     if (t < tiles) {
-      const int rem = t % g.tpi, ty = rem / g.tw;
-      img = n0 + t / g.tpi;
+      const int ti = fdiv(t, g.dv_tpi), rem = t - ti * g.tpi, ty = fdiv(rem, g.dv_tw);
+      img = n0 + ti;
       iy0 = 4 * ty - g.pad;
       ix0 = 4 * (rem - ty * g.tw) - g.pad;
     }
@@ -315,8 +315,8 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, cons
   {
     int img = 0, iy0 = -1000000, ix0 = -1000000;
     if (t < imgs * g.tpi) {
-      const int rem = t % g.tpi, ty = rem / g.tw;
-      img = n0 + t / g.tpi;
+      const int ti = fdiv(t, g.dv_tpi), rem = t - ti * g.tpi, ty = fdiv(rem, g.dv_tw);
+      img = n0 + ti;
       iy0 = 2 * ty - g.pad;
       ix0 = 2 * (rem - ty * g.tw) - g.pad;
     }

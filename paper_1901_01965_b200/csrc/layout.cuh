@@ -48,9 +48,27 @@ constexpr int kSlots = 36;    // M'' values per (tile, cout)
 constexpr int kMBlock = 128;   // GEMM M (tiles per CTA) = TMEM lanes
 constexpr int kKStep = 32;     // int8 MMA K
 
+// Division by a plan constant d >= 1 for 0 <= n < 2^31 without the ~25-instruction integer divide:
+// q = (n m) >> (31 + s), s = ceil(log2 d), m = ceil(2^(31+s) / d) < 2^32.  Exact: with m d = 2^(31+s) + e,
+// 0 <= e < d <= 2^s, n m / 2^(31+s) = n / d + n e / (d 2^(31+s)) and the error term is < 1/d.
+struct FastDiv {
+  uint32_t m;
+  int s;
+};
+inline FastDiv make_fastdiv(int d) {
+  int s = 0;
+  while ((1ll << s) < d) s++;
+  const unsigned long long num = 1ull << (31 + s);
+  return FastDiv{(uint32_t)((num + (unsigned long long)d - 1) / (unsigned long long)d), s};
+}
+__host__ __device__ __forceinline__ int fdiv(int n, FastDiv f) {
+  return (int)(((unsigned long long)(uint32_t)n * f.m) >> (31 + f.s));
+}
+
 struct Geom {
   int n, h, w, cin, cout, pad, layout;
   int ho, wo, th, tw, tpi;     // output size, tiles per row/col, tiles per image
+  FastDiv dv_tw, dv_tpi;       // divisions by tw and tpi (tile decode in K2)
   int cin_pad, cout_pad, nblk, ksteps;
   int scaling, target, out_mode;
   int path;                    // WINO_PATH_FUSED (0) or WINO_PATH_STAGED (1)

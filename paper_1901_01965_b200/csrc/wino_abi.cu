@@ -160,6 +160,8 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.th = (g.ho + g.tile - 1) / g.tile;
   g.tw = (g.wo + g.tile - 1) / g.tile;
   g.tpi = g.th * g.tw;
+  g.dv_tw = wino::make_fastdiv(g.tw);
+  g.dv_tpi = wino::make_fastdiv(g.tpi);
   g.cin_pad = (int)round_up(d.c_in, wino::kKStep);
   const int cout16 = (int)round_up(d.c_out, 16);
   g.path = d.path;
@@ -315,6 +317,11 @@ wino_status wino_check_codes(wino_plan_t p, const uint8_t* codes, int32_t* bad_f
   if (!p || !codes || !bad_flag) return WINO_ERR_INVALID_ARG;
   return cuda_status(wino::launch_check_codes(codes, p->d.c_out * p->g.npos, p->g.w1, bad_flag,
                                               static_cast<cudaStream_t>(stream)));
+}
+
+int wino_debug_fastdiv(int n, int d) {
+  if (n < 0 || d < 1) return -1;
+  return wino::fdiv(n, wino::make_fastdiv(d));
 }
 
 wino_status wino_debug_set_trace(void* device_buffer) {

@@ -66,3 +66,27 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(import\s+oracle|from\s+oracle|liboracle|oracle\.c\b|oracle/)", txt), f
+
+
+def test_fast_division_matches_integer_division():
+    """The kernels' tile decode divides by plan constants with a multiply-shift (layout.cuh FastDiv);
+    it must equal floor division for every n in [0, 2^31) -- checked at the edges (n = q d - 1, q d,
+    q d + 1, 2^31 - 1), for powers of two and their neighbours, and on random pairs."""
+    import numpy as np
+    import paper_1901_01965_b200._lib as L
+    f = L.lib().wino_debug_fastdiv
+    rng = np.random.default_rng(7)
+    ds = {1, 2, 3, 5, 7, 14, 28, 49, 56, 196, 784, 3136, 12544, 2 ** 31 - 1}
+    for e in range(1, 31):
+        ds |= {2 ** e - 1, 2 ** e, 2 ** e + 1}
+    ds |= set(int(v) for v in rng.integers(1, 2 ** 31 - 1, 200))
+    top = 2 ** 31 - 1
+    for d in sorted(ds):
+        ns = {0, 1, d - 1, d, d + 1, top, top - 1, top - d, (top // d) * d, (top // d) * d - 1}
+        ns |= set(int(v) for v in rng.integers(0, top, 20))
+        for q in (1, 2, 3, 1000):
+            ns |= {q * d - 1, q * d, q * d + 1}
+        for n in ns:
+            if 0 <= n <= top:
+                assert f(n, d) == n // d, (n, d)
+    assert f(-1, 3) == -1 and f(5, 0) == -1
