@@ -587,9 +587,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
       const int rr = etid & (kMBlock - 1);
       const int tt = tb_i * kMBlock + rr;
       if (tt < imgs * g.tpi) {
-        const int rem = tt % g.tpi, ty = rem / g.tw;
+        const int ti = fdiv(tt, g.dv_tpi), rem = tt - ti * g.tpi, ty = fdiv(rem, g.dv_tw);
         const int oyb = 4 * ty, oxb = 4 * (rem - ty * g.tw);
-        int8_t* base = static_cast<int8_t*>(y) + (long long)(n0 + tt / g.tpi) * g.ho * g.wo * g.cout + nb * kFN;
+        int8_t* base = static_cast<int8_t*>(y) + (long long)(n0 + ti) * g.ho * g.wo * g.cout + nb * kFN;
 #pragma unroll
         for (int q = 0; q < (16 * kMBlock) / (kFEpiWarps * 32); q++) {
           const int ch = etid + q * kFEpiWarps * 32;
@@ -738,8 +738,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const bool tvalid = t < imgs * g.tpi;
         int img = 0, oy0 = 0, ox0 = 0, ni = 0, nj = 0;
         if (tvalid) {
-          const int rem = t % g.tpi, ty = rem / g.tw;
-          img = n0 + t / g.tpi;
+          const int ti = fdiv(t, g.dv_tpi), rem = t - ti * g.tpi, ty = fdiv(rem, g.dv_tw);
+          img = n0 + ti;
           oy0 = 4 * ty;
           ox0 = 4 * (rem - ty * g.tw);
           ni = min(4, g.ho - oy0);

@@ -296,8 +296,8 @@ __global__ void __launch_bounds__(kT2Threads, 1)
       // ---- out32 = rha(Y / 4) (A26), requantisation (A14), crop, store
       const int t = tb * kMBlock + row;
       if (t >= imgs * g.tpi) continue;
-      const int rem = t % g.tpi, ty = rem / g.tw;
-      const int img = n0 + t / g.tpi, oy0 = 2 * ty, ox0 = 2 * (rem - ty * g.tw);
+      const int ti = fdiv(t, g.dv_tpi), rem = t - ti * g.tpi, ty = fdiv(rem, g.dv_tw);
+      const int img = n0 + ti, oy0 = 2 * ty, ox0 = 2 * (rem - ty * g.tw);
       const int ni = min(2, g.ho - oy0), nj = min(2, g.wo - ox0);
       const int co0 = nb * kN2 + cw * kC2;
       auto outv = [&](int32_t yv) -> int32_t {

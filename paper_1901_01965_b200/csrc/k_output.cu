@@ -79,8 +79,8 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
     zr[2] = w1r + w2r - w3r - w4r;              zi[2] = w1i + w2i - w3i - w4i;
     zr[3] = w1r - w2r + w3i - w4i + w5r;        zi[3] = w1i - w2i - w3r + w4r + w5i;
   }
-  const int img = n0 + t / g.tpi, rem = t % g.tpi;
-  const int ty = rem / g.tw, tx = rem - ty * g.tw;
+  const int ti = fdiv(t, g.dv_tpi), img = n0 + ti, rem = t - ti * g.tpi;
+  const int ty = fdiv(rem, g.dv_tw), tx = rem - ty * g.tw;
   const int oy0 = 4 * ty, ox0 = 4 * tx;
   const int ni = min(4, g.ho - oy0), nj = min(4, g.wo - ox0);
   // output element (oy0 + i, ox0 + j) = ybase + i * ystride + j * xstride (element units)
@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(256, 2) k_output_transform4(Geom g, const int3
   int4 v[36];
 #pragma unroll
   for (int s = 0; s < 36; s++) v[s] = __ldg(mp + s * ps4);
-  const int img = n0 + t / g.tpi, rem = t % g.tpi;
-  const int ty = rem / g.tw, tx = rem - ty * g.tw;
+  const int ti = fdiv(t, g.dv_tpi), img = n0 + ti, rem = t - ti * g.tpi;
+  const int ty = fdiv(rem, g.dv_tw), tx = rem - ty * g.tw;
   const int oy0 = 4 * ty, ox0 = 4 * tx;
   const int ni = min(4, g.ho - oy0), nj = min(4, g.wo - ox0);
   const uint32_t rq_half = rq_shift > 0 ? (1u << (rq_shift - 1)) : 0u;
@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(256) k_output_transform2(Geom g, const int32_t
     Z[0][j] = m[0 * 4 + j] + m[1 * 4 + j] + m[2 * 4 + j];
     Z[1][j] = m[1 * 4 + j] - m[2 * 4 + j] - m[3 * 4 + j];
   }
-  const int img = n0 + t / g.tpi, rem = t % g.tpi;
-  const int ty = rem / g.tw, tx = rem - ty * g.tw;
+  const int ti = fdiv(t, g.dv_tpi), img = n0 + ti, rem = t - ti * g.tpi;
+  const int ty = fdiv(rem, g.dv_tw), tx = rem - ty * g.tw;
   const int oy0 = 2 * ty, ox0 = 2 * tx;
   const int ni = min(2, g.ho - oy0), nj = min(2, g.wo - ox0);
   const uint32_t rq_half = rq_shift > 0 ? (1u << (rq_shift - 1)) : 0u;
