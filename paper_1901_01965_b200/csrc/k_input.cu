@@ -225,7 +225,9 @@ __device__ __forceinline__ void st_bal(int8_t* p_hi, int v0, int v1) {
   st16(p_hi + 4096, __byte_perm((uint32_t)v0, (uint32_t)v1, 0x0040));            // [lo0, lo1]
 }
 
-template <bool U8>
+// KS: g.ksteps as a compile-time constant (1, 2, 4, 8, 16; 0 = runtime), so that every piece's store
+// offset from the thread's base pointer is an immediate
+template <bool U8, int KS>
 __global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, const int8_t* __restrict__ x, int n0,
                                                                      int imgs, int8_t* __restrict__ vimg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -239,11 +241,13 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, con
 
   const long long tb = t / kMBlock;
   const int row = t % kMBlock;
-  const long long kst = (long long)g.ksteps * kVBlockBytes;
+  const long long kst = (long long)(KS ? KS : g.ksteps) * kVBlockBytes;
   int8_t* base = vimg + tb * kVPiecesF * kst + tiled_offset(row, c & 31, kMBlock);
   const int ks = c >> 5;
+  int8_t* base2 = base + (long long)(ks * 2) * kVBlockBytes;   // groups of 2 pieces (real)
+  int8_t* base4 = base + (long long)(ks * 4) * kVBlockBytes;   // groups of 4 pieces (complex)
   // first (hi) piece of group gi for this K step
-  auto gp = [&](int gi) { return base + fg_vprefix(gi) * kst + (long long)(ks * fg_pieces(gi)) * kVBlockBytes; };
+  auto gp = [&](int gi) { return (fg_pieces(gi) == 2 ? base2 : base4) + fg_vprefix(gi) * kst; };
   auto real_row = [&](auto ric, const int (&e0)[6], const int (&e1)[6]) {
     constexpr int ri = decltype(ric)::value;
     int v0[7], v1[7];
@@ -293,15 +297,26 @@ cudaError_t launch_input_transform_f(const Geom& g, const int8_t* x, int n0, int
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
   dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
-  if (g.in_u8)   // uint8 + zero point (f2, A28)
-    return launch_pdl_co(k_input_transform_f<true>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
-  return launch_pdl_co(k_input_transform_f<false>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
+#define WINO_K2F(U, K) launch_pdl_co(k_input_transform_f<U, K>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg)
+#define WINO_K2F_KS(U)                                                                                          \
+  switch (g.ksteps) {                                                                                           \
+    case 1: return WINO_K2F(U, 1);                                                                              \
+    case 2: return WINO_K2F(U, 2);                                                                              \
+    case 4: return WINO_K2F(U, 4);                                                                              \
+    case 8: return WINO_K2F(U, 8);                                                                              \
+    case 16: return WINO_K2F(U, 16);                                                                            \
+    default: return WINO_K2F(U, 0);                                                                             \
+  }
+  if (g.in_u8) { WINO_K2F_KS(true) }   // uint8 + zero point (f2, A28)
+  WINO_K2F_KS(false)
+#undef WINO_K2F_KS
+#undef WINO_K2F
 }
 
 // ---- rational F(2x2,3x3): 4x4 patch at (2ty - pad, 2tx - pad), D = B^T d B with the
 // F(2,3) matrix B^T = [[1,0,-1,0],[0,1,1,0],[0,-1,1,0],[0,1,0,-1]] (A25), 16 real planes
 // (position i*4 + j), balanced pieces, staged V layout (plane stride = g.planes = 16).
-template <bool U8>   // uint8 + zero point (f2, A28): out-of-map pixels read the zero point (d = 0)
+template <bool U8, int KS>   // uint8 + zero point (f2, A28): out-of-map pixels read the zero point (d = 0)
 __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, const int8_t* __restrict__ x, int n0,
                                                                     int imgs, int8_t* __restrict__ vimg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -353,7 +368,7 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, cons
         }
     }
   }
-  const long long pstride = (long long)g.ksteps * 2 * kVBlockBytes;
+  const long long pstride = (long long)(KS ? KS : g.ksteps) * 2 * kVBlockBytes;
   int8_t* base = vimg + (t / kMBlock) * g.planes * pstride + (long long)(c >> 5) * 2 * kVBlockBytes +
                  tiled_offset(t % kMBlock, c & 31, kMBlock);
   int Dv[2][16];
@@ -386,9 +401,20 @@ cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int i
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
   dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
-  if (g.alg == 1 && g.in_u8)
-    return launch_pdl_co(k_input_transform2<true>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
-  if (g.alg == 1) return launch_pdl_co(k_input_transform2<false>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
+#define WINO_K22(U, K) launch_pdl_co(k_input_transform2<U, K>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg)
+#define WINO_K22_KS(U)                                                                                          \
+  switch (g.ksteps) {                                                                                           \
+    case 1: return WINO_K22(U, 1);                                                                              \
+    case 2: return WINO_K22(U, 2);                                                                              \
+    case 4: return WINO_K22(U, 4);                                                                              \
+    case 8: return WINO_K22(U, 8);                                                                              \
+    case 16: return WINO_K22(U, 16);                                                                            \
+    default: return WINO_K22(U, 0);                                                                             \
+  }
+  if (g.alg == 1 && g.in_u8) { WINO_K22_KS(true) }
+  if (g.alg == 1) { WINO_K22_KS(false) }
+#undef WINO_K22_KS
+#undef WINO_K22
   if (g.in_u8) return launch_pdl_co(k_input_transform<true>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
   return launch_pdl_co(k_input_transform<false>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
 }
