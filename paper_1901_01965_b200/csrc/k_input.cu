@@ -71,8 +71,9 @@ __device__ __forceinline__ void st16(int8_t* p, uint32_t v) { *reinterpret_cast<
 template <int PL>
 __device__ __forceinline__ void store_plane(int8_t* base, long long pstride, int v0, int v1) {
   int8_t* p = base + PL * pstride;
-  st16(p, __byte_perm((uint32_t)(v0 + 128), (uint32_t)(v1 + 128), 0x0051));   // [hi0, hi1]
-  st16(p + 4096, __byte_perm((uint32_t)v0, (uint32_t)v1, 0x0040));            // [lo0, lo1]
+  const uint32_t w0 = (uint32_t)(v0 + 128), w1 = (uint32_t)(v1 + 128);   // byte 0 of v + 128 = lo ^ 0x80
+  st16(p, __byte_perm(w0, w1, 0x0051));                                  // [hi0, hi1]
+  st16(p + 4096, __byte_perm(w0, w1, 0x0040) ^ 0x8080u);                 // [lo0, lo1]
 }
 
 // Gather the zero-padded 6x6 patch of chunk tile t for channels c, c+1 and form
@@ -221,8 +222,10 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
 // ---- fused-path V image (layout.cuh "fused-path operand layouts"): per group, balanced s8 pieces
 // hi = (v + 128) >> 8 (byte 1 of v + 128), lo = v - 256 hi (byte 0 of v), stored for both channels.
 __device__ __forceinline__ void st_bal(int8_t* p_hi, int v0, int v1) {
-  st16(p_hi, __byte_perm((uint32_t)(v0 + 128), (uint32_t)(v1 + 128), 0x0051));   // [hi0, hi1]
-  st16(p_hi + 4096, __byte_perm((uint32_t)v0, (uint32_t)v1, 0x0040));            // [lo0, lo1]
+  // one biased value per channel: the +128 folds into the add that forms v; byte 0 of v + 128 = lo ^ 0x80
+  const uint32_t w0 = (uint32_t)(v0 + 128), w1 = (uint32_t)(v1 + 128);
+  st16(p_hi, __byte_perm(w0, w1, 0x0051));                      // [hi0, hi1]
+  st16(p_hi + 4096, __byte_perm(w0, w1, 0x0040) ^ 0x8080u);     // [lo0, lo1]
 }
 
 // KS: g.ksteps as a compile-time constant (1, 2, 4, 8, 16; 0 = runtime), so that every piece's store
