@@ -112,10 +112,18 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
   __shared__ __align__(16) int8_t s_stage[kFilterWarps][kRows][32];
   __shared__ int s_max[kFilterWarps][26];
   __shared__ int s_n[26], s_p[26];
+  __shared__ uint8_t s_gi[FUSED ? kRows : 1];   // FUSED: group of each staged row (read after pass 1's barriers)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int co = blockIdx.x;
   const bool live = co < g.cout;
   pdl_trigger();
+  if constexpr (FUSED) {
+    for (int sr = threadIdx.x; sr < kRows; sr += blockDim.x) {   // the last group whose 2 * wprefix <= sr
+      int gi = 0;
+      for (int q = 1; q < kFGroupsN; q++) gi += (2 * fg_wprefix(q) <= sr) ? 1 : 0;
+      s_gi[sr] = (uint8_t)gi;
+    }
+  }
   pdl_wait();   // w_wino / codes are read by the previous step's GEMM
 
   int mx[26];
@@ -246,10 +254,7 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
       const int nb = co / kFN16, cr = co % kFN16;
       for (int idx = lane; idx < kRows * 2; idx += 32) {   // (staged row, 16-channel half)
         const int sr = idx >> 1, hf = idx & 1;
-        // group of staged row sr: the last group whose 2 * wprefix <= sr
-        int gi = 0;
-#pragma unroll
-        for (int q = 1; q < kFGroupsN; q++) gi += (2 * fg_wprefix(q) <= sr) ? 1 : 0;
+        const int gi = s_gi[sr];   // group of staged row sr
         const int j = sr - 2 * fg_wprefix(gi);
         const int4 v = *reinterpret_cast<const int4*>(&s_stage[warp][sr][hf * 16]);
         *reinterpret_cast<int4*>(wimg + wf_offset(g, gi, nb, j * kFN16 + cr, c0 + hf * 16)) = v;
