@@ -78,7 +78,7 @@ __device__ __forceinline__ void store_plane(int8_t* base, long long pstride, int
 
 // Gather the zero-padded 6x6 patch of chunk tile t for channels c, c+1 and form
 // d' = B^T d column by column for both channels.
-template <bool U8>
+template <bool U8, int KS = 0>
 __device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restrict__ x, int n0, int imgs, int t, int c,
                                            Rows (&r)[2]) {
   const int tiles = imgs * g.tpi;
@@ -104,12 +104,24 @@ __device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restri
       // NHWC, even Cin: one 16-bit load per pixel; row pointer hoisted, column offsets b*Cin
       const int8_t* p0 = x + ((long long)img * g.h * g.w + (long long)iy0 * g.w + ix0) * g.cin + c;
       const long long rstride = (long long)g.w * g.cin;
+      // interior warps (every lane's patch inside the map) with c_in = 32 KS: unpredicated loads at
+      // immediate column offsets b * c_in (the border test and address arithmetic were ~6 instructions per load)
+      const bool inside = cok && iy0 >= 0 && iy0 + 6 <= g.h && ix0 >= 0 && ix0 + 6 <= g.w;
+      if (KS > 0 && g.cin == 32 * KS && __all_sync(0xffffffffu, inside)) {
 #pragma unroll
-      for (int a = 0; a < 6; a++) {
-        const bool vy = iy0 + a >= 0 && iy0 + a < g.h;
-        const uint16_t* rp = reinterpret_cast<const uint16_t*>(p0 + a * rstride);
+        for (int a = 0; a < 6; a++) {
+          const uint16_t* rp = reinterpret_cast<const uint16_t*>(p0 + a * rstride);
 #pragma unroll
-        for (int b = 0; b < 6; b++) w[a * 6 + b] = (vy && vx[b]) ? (uint32_t)__ldg(rp + (b * g.cin >> 1)) : zpair;
+          for (int b = 0; b < 6; b++) w[a * 6 + b] = (uint32_t)__ldg(rp + b * 16 * KS);
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < 6; a++) {
+          const bool vy = iy0 + a >= 0 && iy0 + a < g.h;
+          const uint16_t* rp = reinterpret_cast<const uint16_t*>(p0 + a * rstride);
+#pragma unroll
+          for (int b = 0; b < 6; b++) w[a * 6 + b] = (vy && vx[b]) ? (uint32_t)__ldg(rp + (b * g.cin >> 1)) : zpair;
+        }
       }
     } else {
       // generic path (NCHW or odd Cin): byte loads
@@ -240,7 +252,7 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, con
   pdl_trigger();
   pdl_wait();
   Rows r[2];
-  input_rows<U8>(g, x, n0, imgs, t, c, r);
+  input_rows<U8, KS>(g, x, n0, imgs, t, c, r);
 
   const long long tb = t / kMBlock;
   const int row = t % kMBlock;
@@ -346,12 +358,22 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, cons
       // NHWC, even Cin: one 16-bit load per pixel; row pointer hoisted, column offsets b*Cin (as in K2)
       const int8_t* p0 = x + ((long long)img * g.h * g.w + (long long)iy0 * g.w + ix0) * g.cin + c;
       const long long rstride = (long long)g.w * g.cin;
+      const bool inside = cok && iy0 >= 0 && iy0 + 4 <= g.h && ix0 >= 0 && ix0 + 4 <= g.w;
+      if (KS > 0 && g.cin == 32 * KS && __all_sync(0xffffffffu, inside)) {   // interior warp: as in K2F
 #pragma unroll
-      for (int a = 0; a < 4; a++) {
-        const bool vy = iy0 + a >= 0 && iy0 + a < g.h;
-        const uint16_t* rp = reinterpret_cast<const uint16_t*>(p0 + a * rstride);
+        for (int a = 0; a < 4; a++) {
+          const uint16_t* rp = reinterpret_cast<const uint16_t*>(p0 + a * rstride);
 #pragma unroll
-        for (int b = 0; b < 4; b++) w[a * 4 + b] = (vy && vx[b]) ? (uint32_t)__ldg(rp + (b * g.cin >> 1)) : zpair;
+          for (int b = 0; b < 4; b++) w[a * 4 + b] = (uint32_t)__ldg(rp + b * 16 * KS);
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < 4; a++) {
+          const bool vy = iy0 + a >= 0 && iy0 + a < g.h;
+          const uint16_t* rp = reinterpret_cast<const uint16_t*>(p0 + a * rstride);
+#pragma unroll
+          for (int b = 0; b < 4; b++) w[a * 4 + b] = (vy && vx[b]) ? (uint32_t)__ldg(rp + (b * g.cin >> 1)) : zpair;
+        }
       }
     } else {
       const long long cstep = g.layout == 1 ? 1 : (long long)g.h * g.w;
