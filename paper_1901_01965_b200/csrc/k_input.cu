@@ -161,7 +161,7 @@ __device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restri
   }
 }
 
-template <bool U8>
+template <bool U8, int KS>   // KS: g.ksteps at compile time (0 = runtime), as in K2F
 __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const int8_t* __restrict__ x, int n0,
                                                                    int imgs, int8_t* __restrict__ vimg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -171,14 +171,14 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
   pdl_trigger();
   pdl_wait();   // x may come from the previous kernel (layer stacks); V may still be read by the previous GEMM
   Rows r[2];
-  input_rows<U8>(g, x, n0, imgs, t, c, r);
+  input_rows<U8, KS>(g, x, n0, imgs, t, c, r);
 
   // ---- D = d' B along rows; store every plane as soon as it is formed
   const long long tb = t / kMBlock;
   const int row = t % kMBlock;
   const int k = c;   // channel index inside cin_pad
   // plane p, piece q of this (tile, channel) at base + p * pstride + q * 4 KB (v_offset, layout.cuh)
-  const long long pstride = (long long)g.ksteps * 2 * kVBlockBytes;
+  const long long pstride = (long long)(KS ? KS : g.ksteps) * 2 * kVBlockBytes;
   int8_t* base = vimg + tb * kPlanes * pstride + (long long)(k >> 5) * 2 * kVBlockBytes +
                  tiled_offset(row, k & 31, kMBlock);
   {
@@ -440,8 +440,20 @@ cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int i
   if (g.alg == 1) { WINO_K22_KS(false) }
 #undef WINO_K22_KS
 #undef WINO_K22
-  if (g.in_u8) return launch_pdl_co(k_input_transform<true>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
-  return launch_pdl_co(k_input_transform<false>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg);
+#define WINO_K2S(U, K) launch_pdl_co(k_input_transform<U, K>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg)
+#define WINO_K2S_KS(U)                                                                                          \
+  switch (g.ksteps) {                                                                                           \
+    case 1: return WINO_K2S(U, 1);                                                                              \
+    case 2: return WINO_K2S(U, 2);                                                                              \
+    case 4: return WINO_K2S(U, 4);                                                                              \
+    case 8: return WINO_K2S(U, 8);                                                                              \
+    case 16: return WINO_K2S(U, 16);                                                                            \
+    default: return WINO_K2S(U, 0);                                                                             \
+  }
+  if (g.in_u8) { WINO_K2S_KS(true) }
+  WINO_K2S_KS(false)
+#undef WINO_K2S_KS
+#undef WINO_K2S
 }
 
 cudaError_t setup_input_transform() { return cudaSuccess; }
