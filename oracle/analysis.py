@@ -142,16 +142,48 @@ def table1():
 
 
 # ------------------------------------------------------------ static error
-def static_error(population):
+def static_error(population, exact_inverse=False):
     """Down-then-up error of each weight: f = scale_factor(w),
-    down = rha(w n / 2^p), up = rha(down m / 2^q)."""
+    down = rha(w n / 2^p), up = rha(down m / 2^q) with the 8-bit inverse of
+    P:366 (A8), or up = down 2^p / n exactly (`exact_inverse`).  Returns
+    (mean |up - w|, mean |up - w| / |w|, mean (up - w)) over the scaled
+    weights of the population."""
     num, prop, signed = [], [], []
     for w in population:
         n, p = O.scale_factor(int(w))
         if n == 0:
             continue
-        m, q = O.reverse_factor(n, p)
         down = O.rha_shift(int(w) * n, p)
-        up = O.rha_shift(down * m, q)
+        if exact_inverse:
+            up = Fraction(down * 2 ** p, n)
+        else:
+            m, q = O.reverse_factor(n, p)
+            up = O.rha_shift(down * m, q)
         num.append(abs(up - w)); prop.append(abs(up - w) / abs(w)); signed.append(up - w)
     return float(np.mean(num)), float(np.mean(prop)), float(np.mean(signed))
+
+
+def static_error_bound(w):
+    """Derived bound on |up - w| for one weight w > 255 (8-bit inverse):
+    |down - w n/2^p| <= 1/2 (rha), |m - 2^(q+p)/n| <= 1/2 (rha) and the final
+    rha adds <= 1/2, so
+      |up - w| <= |down| |m/2^q - 2^p/n| + (2^p/n)|down - w n/2^p| + 1/2
+               <= 255 / 2^(q+1) + 2^(p-1)/n + 1/2      (|down| <= 255, P:312)."""
+    n, p = O.scale_factor(int(w))
+    if n == 0:
+        return Fraction(0)
+    _, q = O.reverse_factor(n, p)
+    return Fraction(255, 2 ** (q + 1)) + Fraction(2 ** (p - 1), n) + Fraction(1, 2)
+
+
+def f2_reachable_population():
+    """A21's second population: the magnitudes an F(2x2) Winograd-domain
+    filter value can take from int8 weights (G' = 2G): the 4
+    corner positions are 4 g (multiples of 4 up to 4*255 = 1020 for int9),
+    the 8 edge positions 2 (g0 +- g1 + g2) (even values up to 1530), the 4
+    centre positions any value up to 2295 (P:330's worst case); each kept
+    above 255 (scaled), as a multiset."""
+    corners = [v for v in range(256, 1021) if v % 4 == 0]
+    edges = [v for v in range(256, 1531) if v % 2 == 0]
+    centre = list(range(256, 2296))
+    return corners * 4 + edges * 8 + centre * 4
