@@ -11,9 +11,14 @@ Parity status per function:
   wino_conv, scaling off       pinned (== direct_conv exactly; Im Y == 0)
   filter/input/output tiles    pinned (identity 16*correlation, conjugate layout)
   scale_factor / codes         pinned (brute force over all (n, p); Table 1)
+  filter_transform selection   pinned (per-OFM independence, maximal grid
+                               factor, A5 magnitude, A16; tests/test_oracle_selection.py)
   reverse_factor               pinned (exhaustive over q; relative-error bound)
-  wino_conv, scaling on        pinned only by invariants and the power-of-two
-                               special case; general values: parity unpinned
-                               beyond those invariants (A21/A17)
+  wino_conv, scaling on        pinned by invariants, the power-of-two special
+                               case (exact) and, in general, the error bound
+                               derived from its three roundings against direct
+                               convolution (test_oracle_selection.py); the
+                               static-error POPULATION of P:376 is unstated
+                               (A21): that figure alone is reported, unpinned
 """
 from .oracle import *  # noqa: F401,F403

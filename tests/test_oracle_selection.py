@@ -151,3 +151,62 @@ def test_config_banks_selection_is_per_ofm_and_maximal():
             assert f * int(peak[o, pos]) <= 255
             larger = [h for h in GRID if h > f]
             assert not larger or larger[0] * int(peak[o, pos]) > 255
+
+
+def _error_bound_case(seed, n, h, w_, ci, co, sigma, xdist="uniform"):
+    rng = np.random.default_rng(seed)
+    x = rng.integers(-128, 128, (n, h, w_, ci)).astype(np.int8)
+    if xdist == "relu":
+        x = np.maximum(x, 0).astype(np.int8)
+    w = _bank(rng, co, ci, sigma)
+    return x, w
+
+
+@pytest.mark.parametrize("case", [(31, 1, 9, 11, 7, 5, 32.0), (32, 2, 8, 8, 16, 4, 24.0),
+                                  (33, 1, 6, 13, 3, 6, 127.0), (34, 1, 12, 12, 40, 3, 24.0)])
+def test_scaled_pipeline_within_the_derived_error_bound(case):
+    """The whole scaled pipeline (O1-O10) against direct convolution, within
+    the error bound derived from its three roundings -- the check that the C
+    pipeline's indexing, Karatsuba/complex products, reverse scaling and
+    output transform are those of the paper (a transposed operand, a wrong
+    position or a dropped term would leave it far outside).  Per position,
+    with f = n/2^p (P:312), r = m/2^q (P:366):
+      W' = f W + e, |e_re|, |e_im| <= 1/2                       (A7)
+      M'' = rha(r M') = r M' + eps, |eps| <= 1/2 per component   (A9)
+      M'' - M = (r f - 1) M + r sum_c e D + eps, so per component
+      |d| <= |r f - 1| |M_comp| + r sum_c (|D_re| + |D_im|) / 2 + 1/2,
+    M = sum_c W D the exact product of the pinned transforms.  Y = A^T M A
+    adds |Re dM| + |Im dM| per nonzero A^T coefficient pair (|a| <= 1), and
+    out32 = rha(Y / 16) adds 1/2."""
+    seed, n, h, w_, ci, co, sigma = case
+    x, w = _error_bound_case(seed, n, h, w_, ci, co, sigma)
+    W, _, codes = O.filter_transform(w, O.NHWC, scaling=True)
+    D = O.input_transform(x, 1, O.NHWC)                          # [T][ci][36][2]
+    res = O.wino_conv(x, w, 1, O.NHWC, scaling=True)
+    direct = O.direct_conv(x, w, 1, O.NHWC)
+    _, _, AT = O.matrices()
+    Wc = W[..., 0] + 1j * W[..., 1]                              # [co][ci][36]
+    Dc = D[..., 0] + 1j * D[..., 1]                              # [T][ci][36]
+    M = np.einsum("tcp,ocp->top", Dc, Wc)                        # exact product (|.| < 2^53)
+    sumD = np.abs(D).sum(axis=3).sum(axis=1)                     # [T][36]: sum_c |D_re| + |D_im|
+    rf1 = np.zeros((co, 36)); r = np.ones((co, 36))
+    for o in range(co):
+        for p_ in range(36):
+            if codes[o, p_]:
+                nn, pp = O.decode_code(int(codes[o, p_]))
+                m, q = O.reverse_factor(nn, pp)
+                r[o, p_] = m / 2 ** q
+                rf1[o, p_] = abs(m / 2 ** q * nn / 2 ** pp - 1)
+    scaled = codes > 0                                           # [co][36]
+    dre = rf1[None] * np.abs(M.real) + scaled[None] * (r[None] * sumD[:, None, :] / 2 + 0.5)
+    dim = rf1[None] * np.abs(M.imag) + scaled[None] * (r[None] * sumD[:, None, :] / 2 + 0.5)
+    dM = (dre + dim).reshape(-1, co, 6, 6)                       # [T][co][6][6]
+    absA = (np.abs(AT) > 0).astype(float)                        # |a| in {0, 1}
+    dY = np.einsum("ir,tkrc,jc->tkij", absA, dM, absA)           # [T][co][4][4]
+    Ho, Wo = h, w_
+    th, tw = (Ho + 3) // 4, (Wo + 3) // 4
+    bound = dY.reshape(n, th, tw, co, 4, 4).transpose(0, 1, 4, 2, 5, 3).reshape(n, 4 * th, 4 * tw, co)
+    bound = bound[:, :Ho, :Wo] / 16 + 0.5 + 1e-6
+    err = np.abs(res.out32.astype(np.int64) - direct)
+    assert (err <= bound).all(), float((err - bound).max())
+    assert (codes > 0).any() and err.max() > 0                   # the case really is scaled and lossy
