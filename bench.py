@@ -284,7 +284,7 @@ def run_ours(args):
         full = sh["n"] == layer.n and sh["co"] == layer.c_out and args.alg == "f4" and args.input == "i8" and \
             args.target == 255
         roof = roofline(kern, info, synth.LayerCfg(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad),
-                        peaks, load_traffic(args.config, "staged" if info.path == 1 else "fused") if full else None)
+                        peaks, load_traffic(args.config, "staged" if info.path == 2 else "fused") if full else None)
         path = path_roofline(synth.LayerCfg(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad), info,
                              peaks, t_max / args.steps)
         line = {
@@ -297,8 +297,8 @@ def run_ours(args):
                 "c_in": layer.c_in, "c_out": layer.c_out, "pad": layer.pad, "layout": "NHWC",
                 "filter_scaling": layer.scaling, "output": f"int8 requantised (M0=1, S={S})",
                 "step": "filter transform + scaling (K1) + conv (" +
-                        ("K2, K3F fused GEMM+output per chunk)" if info.path == 0 else "K2,K3,K4 per chunk)"),
-                "path": "fused" if info.path == 0 else "staged",
+                        ("K2, K3F fused GEMM+output per chunk)" if info.path == 1 else "K2,K3,K4 per chunk)"),
+                "path": "fused" if info.path == 1 else "staged",
                 "input": "uint8, zero points 128 (SURVEY f2)" if u8 else "int8",
                 "filter_target_max": args.target if layer.scaling else None,
                 "algorithm": "F(2x2,3x3) rational (SURVEY f1)" if info.algorithm == 1 else
@@ -437,7 +437,7 @@ def run_ours_stack(args):
             "config": {"workload": f"C5: {cfg.description}", "batch_per_gpu": n, "layers": len(cfg.layers),
                        "layout": "NHWC", "filter_scaling": True, "requant_shifts": shifts,
                        "step": "13 filter transforms + 13 convs + 4 max pools",
-                       "paths": ["fused" if c.info.path == 0 else "staged" for c in st.convs],
+                       "paths": ["fused" if c.info.path == 1 else "staged" for c in st.convs],
                        "l2": "activations 0.8 GB per layer >> 126 MiB L2; 2 input sets rotated",
                        "parallelism": f"dp{world} (replicated per-rank batches, weak scaling)"},
             "path_roofline": {"t_roof_us": round(t_roof * 1e6, 2), "t_step_us": round(t_max / args.steps * 1e6, 2),
@@ -526,7 +526,7 @@ def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps):
     from paper_1901_01965_b200 import _lib as L
     info = conv.info
     sp = stream.cuda_stream
-    names = {1: "k1_filter", 2: "k2_input", 3: "k3_gemm", 4: "k4_output"} if info.path == 1 else \
+    names = {1: "k1_filter", 2: "k2_input", 3: "k3_gemm", 4: "k4_output"} if info.path == 2 else \
         {1: "k1_filter", 2: "k2_input", 3: "k3_fused"}
     w_wino, codes, wsp = conv.w_wino.data_ptr(), conv.codes.data_ptr(), conv.workspace.data_ptr()
     out = {}
@@ -579,7 +579,7 @@ def roofline(kern, info, layer, peaks, traffic=None):
     i8_sus = 2.0 * peaks["bf16_tflops_sustained"]   # int8 dense = 2 x bf16 (nominal ratio 4.5/2.25)
     px = info.tile * info.tile                     # output pixels per tile (16 F4x4, 4 F2x2)
     mults = alg_mults(info)                        # general multiplications per (tile, cin, cout)
-    vpc = 72 if (info.path == 0 and info.algorithm == 0) else 2 * info.planes   # V bytes per (tile, channel)
+    vpc = 72 if (info.path == 1 and info.algorithm == 0) else 2 * info.planes   # V bytes per (tile, channel)
     x_chunk = chunk_tiles * px * layer.c_in        # ~ bytes of x per chunk
     res = {}
     # K1: reads w (9 Cin Cout B), writes the W' image + codes
@@ -597,13 +597,13 @@ def roofline(kern, info, layer, peaks, traffic=None):
     # HBM bytes (V in, W' in, M'' or y out) against the HBM peak.  The binding roof is the one with the
     # larger minimum time (the kernel's arithmetic intensity against the ridge point); the bench line
     # reports that one and keeps the other as a second view.
-    gemm = "k3_gemm" if info.path == 1 else "k3_fused"
-    if info.path != 1:
+    gemm = "k3_gemm" if info.path == 2 else "k3_fused"
+    if info.path != 2:
         k3_bytes = k3f_bytes
     t_tc, t_hbm = k3_ops / (i8_sus * 1e12), k3_bytes / (hbm * 1e9)
     gemm_spec = ("hbm", k3_bytes, hbm, "GB/s") if t_hbm >= t_tc else ("tensor", k3_ops, i8_sus, "TOPS")
     spec = {"k1_filter": ("hbm", k1_bytes, hbm, "GB/s"), "k2_input": ("hbm", k2_bytes, hbm, "GB/s"), gemm: gemm_spec}
-    if info.path == 1:
+    if info.path == 2:
         spec["k4_output"] = ("hbm", k4_bytes, hbm, "GB/s")
     all_k = {}
     for name, (bound, work, peak, unit) in spec.items():
@@ -795,9 +795,9 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "fused", "staged"],
                     help="auto: the plan picks fused for c_in <= 256 (C2-C4, C5 layers 1-8), staged otherwise")
     ap.add_argument("--input", default="i8", choices=["i8", "u8"],
-                    help="u8: uint8 tensors with zero points (SURVEY f2, staged F(4x4), c_in <= 224)")
+                    help="u8: uint8 tensors with zero points (SURVEY f2; either algorithm and path, c_in <= 224)")
     ap.add_argument("--alg", default="f4", choices=["f4", "f2"],
-                    help="f4: complex F(4x4,3x3) (the north star); f2: rational F(2x2,3x3) (SURVEY f1, staged only)")
+                    help="f4: complex F(4x4,3x3) (the north star); f2: rational F(2x2,3x3) (SURVEY f1, either path)")
     ap.add_argument("--target", type=int, default=255, choices=[255, 127],
                     help="filter scaling target: 255 = the paper's (two-piece W'); 127 = int8-native single-piece "
                          "W' (SURVEY f3, staged F(4x4) int8)")

@@ -24,11 +24,18 @@
  *   - All tensor pointers passed to wino_transform_filter / wino_conv2d_int8
  *     are DEVICE pointers on the plan's device, 16-byte aligned, owned by
  *     the caller (the library never allocates or frees device memory).
+ *   - Scale codes are validated at the boundary (P:330 read as A4: 0, or
+ *     (n << 2) | (p - 4) with n in [8, 15]): a code buffer is checked on the
+ *     device, synchronously, the first time a plan sees it (or by
+ *     wino_validate_codes), and an invalid entry returns WINO_ERR_RANGE
+ *     before any kernel of the conv is enqueued.  Buffers written by the
+ *     plan's own wino_transform_filter are valid by construction.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *     stream).  Work is enqueued asynchronously; launch errors are returned
  *     at once, device faults surface at the caller's next synchronisation.
  *   - Calls on different streams are safe when each uses its own workspace.
- *   - int8 tensors are two's-complement; there are no zero points (A12).
+ *   - int8 tensors are two's-complement with no zero points (A12); uint8
+ *     input (input_type) carries explicit zero points (A28).
  */
 #ifndef WINO_H
 #define WINO_H
@@ -45,7 +52,8 @@ typedef enum {
     WINO_ERR_INVALID_ARG = -1,   /* NULL / misaligned pointer, bad enum, wrong device  */
     WINO_ERR_UNSUPPORTED = -2,   /* shape or flag outside the supported set            */
     WINO_ERR_SHAPE = -3,         /* inconsistent sizes                                  */
-    WINO_ERR_RANGE = -4,         /* requant shift out of [0, 62], multiplier < 1        */
+    WINO_ERR_RANGE = -4,         /* invalid scale code; requant shift out of [0, 62] or
+                                    multiplier < 1                                      */
     WINO_ERR_CUDA = -5,          /* a CUDA runtime call failed (launch or attribute)    */
     WINO_ERR_NOMEM = -6          /* host allocation of the plan failed                  */
 } wino_status;
@@ -70,18 +78,22 @@ typedef struct {
     int pad;              /* 0 or 1; h + 2 pad >= 3 and w + 2 pad >= 3                 */
     int layout;           /* WINO_NCHW or WINO_NHWC                                    */
     int filter_scaling;   /* 0: exact (codes all 0); 1: the paper's scheme */
-    int filter_target_max;/* 255 (the paper's int9 target, A6); only value supported   */
+    int filter_target_max;/* 255: the paper's int9 target (A6, the default);
+                             127: the int8-native target (needs
+                             filter_scaling, the staged path, F4x4 and int8 input)   */
     int out_mode;         /* WINO_OUT_INT8 or WINO_OUT_INT32                           */
     int workspace_mb;     /* batch-chunk budget for V (+ M) in MiB; 0 = default (128, or
                              env WINO_CHUNK_MB).  Larger = fewer, longer launches.     */
-    int path;             /* WINO_PATH_FUSED (0, default): K2 input transform, then ONE
-                             kernel for the GEMMs + Karatsuba + reverse scaling + output
-                             transform + store (M'' stays on chip).
-                             WINO_PATH_STAGED (1): K2, K3 GEMMs -> M'' in the workspace,
-                             K4 output transform (M'' inspectable, see wino_plan_info).
-                             WINO_PATH_AUTO (2): fused for F2x2, and for F4x4 when
-                             c_in <= 256 (target 255 only), else staged;
-                             wino_plan_info.path reports the choice.                   */
+    int path;             /* WINO_PATH_AUTO (0, the default everywhere -- this ABI, the
+                             Python WinoConv2d and ConvStack): fused for F2x2, and for
+                             F4x4 when c_in <= 256 (target 255), else staged;
+                             wino_plan_info.path reports the choice.
+                             WINO_PATH_FUSED (1): K2 input transform, then ONE kernel for
+                             the GEMMs (4-multiplication complex form, 36 planes) +
+                             reverse scaling + output transform + store (M'' on chip).
+                             WINO_PATH_STAGED (2): K2, K3 GEMMs (46 planes: 16 real +
+                             10 Karatsuba x 3) -> M'' in the workspace,
+                             K4 output transform (M'' inspectable, wino_plan_info).   */
     int algorithm;        /* WINO_ALG_F4X4 (0, default): complex F(4x4,3x3) over the
                              Gaussian integers, points {0, +-1, +-i};
                              WINO_ALG_F2X2 (1): rational F(2x2,3x3), G' = 2G,
@@ -90,14 +102,14 @@ typedef struct {
     int input_type;       /* WINO_IN_INT8 (0, default) or WINO_IN_UINT8 (1): x and w are
                              uint8 with the zero points below (the paper's affine model,
                              P:251); the convolution is that of the int9 values x - zx,
-                             w - zw, padding = real 0 (A28).  uint8 needs
-                             F4x4 and c_in <= 224 (int32 exactness); either path.      */
+                             w - zw, padding = real 0 (A28).  c_in <= 224
+                             (int32 exactness); either algorithm, either path.        */
     int x_zero_point;     /* [0, 255], uint8 input only                                  */
     int w_zero_point;     /* [0, 255], uint8 input only                                  */
 } wino_conv_desc;
 
 /* Hot-path kernel structure (wino_conv_desc.path). */
-enum { WINO_PATH_FUSED = 0, WINO_PATH_STAGED = 1, WINO_PATH_AUTO = 2 };
+enum { WINO_PATH_AUTO = 0, WINO_PATH_FUSED = 1, WINO_PATH_STAGED = 2 };
 
 /* Winograd algorithm (wino_conv_desc.algorithm). */
 enum { WINO_ALG_F4X4 = 0, WINO_ALG_F2X2 = 1 };
@@ -116,14 +128,15 @@ typedef struct {
     int cout_pad;               /* c_out rounded up to n_block                        */
     int n_block;                /* GEMM N tile (couts per CTA)                         */
     int m_block;                /* GEMM M tile (tiles per CTA) = 128                   */
-    int planes;                 /* staged: 46 = 16 real + 10 x {re, im, re+im};
-                                   fused: 36 = 16 real + 10 x {re, im}                 */
+    int planes;                 /* staged F4x4: 46 = 16 real + 10 x {re, im, re+im}
+                                   (P:228); fused F4x4: 36 = 16 real + 10 x {re, im};
+                                   F2x2: 16                                            */
     int pieces;                 /* 2 balanced s8 pieces per operand value:
                                    v = 256 hi + lo, lo = low byte of v     */
     int chunk_images;           /* images per workspace chunk                          */
     int n_chunks;
     long long chunk_tiles_pad;  /* tiles per chunk rounded up to m_block               */
-    int path;                   /* WINO_PATH_FUSED or WINO_PATH_STAGED                 */
+    int path;                   /* WINO_PATH_FUSED or WINO_PATH_STAGED (AUTO resolved)  */
     int stages;                 /* kernels per chunk: 2 (fused) or 3 (staged)          */
     int algorithm;              /* WINO_ALG_F4X4 or WINO_ALG_F2X2                      */
     int tile;                   /* output tile edge: 4 (F4x4) or 2 (F2x2)             */
@@ -132,9 +145,10 @@ typedef struct {
     size_t m_offset, m_bytes;   /* M'' = 36 int32 per (tile, cout) after Karatsuba and
                                    reverse scaling; swizzled tiles; staged
                                    path only (m_bytes = 0 on the fused path)           */
-    size_t workspace_bytes;
+    size_t workspace_bytes;     /* V (+ M'') of one chunk + a 256-byte status block
+                                   (the code-validation flag)                          */
     size_t filter_bytes;        /* transformed-filter buffer (w_wino)                  */
-    size_t codes_bytes;         /* c_out * 36 bytes                                    */
+    size_t codes_bytes;         /* c_out * positions bytes (36 F4x4, 16 F2x2)         */
     size_t x_bytes, y_bytes;    /* input / output tensor sizes in bytes                */
 } wino_plan_info;
 
@@ -148,16 +162,19 @@ const char *wino_last_cuda_error(void);
 /* Validate `desc` and build an immutable plan for CUDA device `device`.
  * The plan holds host metadata only.  Returns WINO_ERR_UNSUPPORTED for
  * pad not in {0,1}, n/h/w/c < 1, h + 2 pad < 3 or w + 2 pad < 3,
- * c_in > 896 (> 768 with filter_scaling), c_out > 2048, filter_target_max != 255, and WINO_ERR_INVALID_ARG for bad
- * enums or NULL pointers.  The device must be sm_100 (B200).            */
+ * c_in > 896 (> 768 with filter_scaling; > 224 for uint8 input), c_out > 2048,
+ * filter_target_max not in {255, 127} (127 only with scaling, staged, F4x4,
+ * int8), and WINO_ERR_INVALID_ARG for bad enums or NULL pointers.  The device
+ * must be sm_100 (B200).  A plan's only mutable state is its set of known-valid
+ * code buffers (thread-safe).                                            */
 wino_status wino_plan(const wino_conv_desc *desc, int device, wino_plan_t *out);
 wino_status wino_plan_destroy(wino_plan_t plan);
 wino_status wino_plan_query(wino_plan_t plan, wino_plan_info *info);
 
 /* Sizes of the caller-allocated device buffers (0 on a NULL plan). */
 size_t wino_filter_bytes(wino_plan_t plan);     /* w_wino                      */
-size_t wino_codes_bytes(wino_plan_t plan);      /* scale_codes = c_out * 36    */
-size_t wino_workspace_bytes(wino_plan_t plan);  /* V and M of one batch chunk  */
+size_t wino_codes_bytes(wino_plan_t plan);      /* scale_codes = c_out * positions */
+size_t wino_workspace_bytes(wino_plan_t plan);  /* V and M of one batch chunk + status */
 size_t wino_output_bytes(wino_plan_t plan);     /* y                            */
 
 /* Offline filter transform: for every output channel,
@@ -165,13 +182,18 @@ size_t wino_output_bytes(wino_plan_t plan);     /* y                            
  *   per position (X-Y location) the max over input channels of
  *   max(|Re W|, |Im W|) (A5) selects the code (n, p) of P:317-330 read as A3
  *   (code = (n << 2) | (p - 4), 0 = unscaled, A4; mirrors share their
- *   primary's code); W' = rha(W n / 2^p) (A7);
- *   then the 46 GEMM operand planes (16 real, and re, im, re+im per complex
- *   primary for the Karatsuba product) split into int8 pieces.
+ *   primary's code; 7-bit (n << 3) | (p - 4) for target 127, A29);
+ *   W' = rha(W n / 2^p) (A7); then the GEMM operand planes split into balanced
+ *   int8 pieces: staged path 46 planes (16 real, and re, im, re+im per complex
+ *   primary for the Karatsuba product), fused path 16 real planes +
+ *   the [Wr | Wi] / [-Wi | Wr] blocks of the 4-multiplication complex product
+ *   (identical integers).  F2x2: W = G' g G'^T (G' = 2G),
+ *   16 real planes, 16 codes per c_out.  The codes buffer is recorded as valid
+ *   for this plan.
  *   w           device, int8, layout per desc (OIHW or OHWI)
  *   w_wino      device, wino_filter_bytes(plan) bytes, written (opaque layout,
  *               documented in DESIGN.md "HBM layout")
- *   scale_codes device, [c_out][36] uint8, written (all 0 when
+ *   scale_codes device, [c_out][positions] uint8, written (all 0 when
  *               filter_scaling == 0)                                        */
 wino_status wino_transform_filter(wino_plan_t plan, const int8_t *w, void *w_wino,
                                   uint8_t *scale_codes, void *stream);
@@ -185,11 +207,16 @@ wino_status wino_transform_filter(wino_plan_t plan, const int8_t *w, void *w_win
  * requantisation, store.
  *   x            device, int8 input, layout per desc
  *   w_wino       device, produced by wino_transform_filter for this plan
- *   scale_codes  device, [c_out][36] 6-bit codes -- THE explicit filter-scale
- *                parameter: the codes W' was scaled with (from
- *                wino_transform_filter, or any codes applied consistently);
- *                every entry must be 0 or decode to n in [8,15] (else the
- *                result is unspecified; validate with wino_check_codes)
+ *   scale_codes  device, [c_out][positions] 6-bit codes -- THE explicit
+ *                filter-scale parameter: the codes W' was scaled with (from
+ *                wino_transform_filter, or any codes applied consistently).
+ *                Every entry must be 0 or decode to n in [8,15] (A4; 7-bit
+ *                codes, p in [4,8], for target 127): on the first call with a
+ *                buffer the plan has not seen, the codes are checked on the
+ *                device and the stream is synchronised; an invalid entry
+ *                returns WINO_ERR_RANGE and nothing is enqueued.  A caller
+ *                that rewrites a buffer the plan has already accepted with
+ *                codes of its own re-checks it with wino_validate_codes.
  *   requant_mult, requant_shift  used for WINO_OUT_INT8 only: mult >= 1,
  *                shift in [0, 62], else WINO_ERR_RANGE
  *   y            device, wino_output_bytes(plan) bytes, written
@@ -226,9 +253,16 @@ wino_status wino_conv2d_int8_stage(wino_plan_t plan, int stage, int chunk, const
                                    int32_t requant_mult, int requant_shift, void *y,
                                    void *workspace, void *stream);
 
-/* Device-side validation of a code table: writes 1 to *bad_flag (device
- * int32, caller-zeroed) if any of the c_out*36 codes is neither 0 nor a
- * valid code (n in [8,15]).                                               */
+/* Synchronous validation of a code buffer against this plan (A4):
+ * checks all c_out * positions entries on the device (flag in the workspace's
+ * status block), synchronises `stream`, and returns WINO_OK (and records the
+ * buffer as valid for the plan) or WINO_ERR_RANGE (and forgets it).
+ * codes and workspace are device pointers as for wino_conv2d_int8.         */
+wino_status wino_validate_codes(wino_plan_t plan, const uint8_t *scale_codes, void *workspace, void *stream);
+
+/* Asynchronous device-side check of a code table: writes 1 to *bad_flag
+ * (device int32, caller-zeroed) if any of the c_out * positions codes is
+ * neither 0 nor a valid code (n in [8,15]).                               */
 wino_status wino_check_codes(wino_plan_t plan, const uint8_t *scale_codes, int32_t *bad_flag,
                              void *stream);
 

@@ -10,5 +10,5 @@ from ._lib import (WINO_NCHW, WINO_NHWC, WINO_OUT_INT8, WINO_OUT_INT32, WINO_PAT
                    WINO_ALG_F4X4, WINO_ALG_F2X2, WINO_IN_INT8, WINO_IN_UINT8,
                    WinoError,
                    wino_conv_desc, wino_plan, wino_plan_destroy, wino_plan_query, wino_transform_filter,
-                   wino_conv2d_int8, wino_conv2d_int8_host)
+                   wino_conv2d_int8, wino_conv2d_int8_host, wino_validate_codes)
 from .conv import WinoConv2d, maxpool2  # noqa: F401

@@ -14,14 +14,14 @@ WINO_OK, WINO_ERR_INVALID_ARG, WINO_ERR_UNSUPPORTED, WINO_ERR_SHAPE = 0, -1, -2,
 WINO_ERR_RANGE, WINO_ERR_CUDA, WINO_ERR_NOMEM = -4, -5, -6
 WINO_NCHW, WINO_NHWC = 0, 1
 WINO_OUT_INT8, WINO_OUT_INT32 = 0, 1
-WINO_PATH_FUSED, WINO_PATH_STAGED, WINO_PATH_AUTO = 0, 1, 2
+WINO_PATH_AUTO, WINO_PATH_FUSED, WINO_PATH_STAGED = 0, 1, 2
 WINO_ALG_F4X4, WINO_ALG_F2X2 = 0, 1
 WINO_IN_INT8, WINO_IN_UINT8 = 0, 1
 
 # every symbol include/wino.h declares
 EXPORTS = ("wino_status_string", "wino_last_cuda_error", "wino_plan", "wino_plan_destroy", "wino_plan_query", "wino_filter_bytes",
            "wino_codes_bytes", "wino_workspace_bytes", "wino_output_bytes", "wino_transform_filter",
-           "wino_conv2d_int8", "wino_conv2d_int8_host", "wino_conv2d_int8_stage", "wino_check_codes", "wino_maxpool2_int8",
+           "wino_conv2d_int8", "wino_conv2d_int8_host", "wino_conv2d_int8_stage", "wino_validate_codes", "wino_check_codes", "wino_maxpool2_int8",
            "wino_debug_set_trace", "wino_debug_fastdiv")
 
 
@@ -76,6 +76,7 @@ def lib():
         L.wino_conv2d_int8_host.argtypes = [P, P, P, P, I32, I, P, P, P, P, P]; L.wino_conv2d_int8_host.restype = I
         L.wino_conv2d_int8_stage.argtypes = [P, I, I, P, P, P, I32, I, P, P, P]
         L.wino_conv2d_int8_stage.restype = I
+        L.wino_validate_codes.argtypes = [P, P, P, P]; L.wino_validate_codes.restype = I
         L.wino_check_codes.argtypes = [P, P, P, P]; L.wino_check_codes.restype = I
         L.wino_maxpool2_int8.argtypes = [P, I, I, I, I, I, P, P]; L.wino_maxpool2_int8.restype = I
         L.wino_debug_set_trace.argtypes = [P]; L.wino_debug_set_trace.restype = I
@@ -139,6 +140,10 @@ def wino_conv2d_int8_stage(plan, stage: int, chunk: int, x_ptr: int, w_wino_ptr:
     _check(lib().wino_conv2d_int8_stage(plan, int(stage), int(chunk), x_ptr, w_wino_ptr, codes_ptr,
                                         int(requant_mult), int(requant_shift), y_ptr, ws_ptr, stream),
            "wino_conv2d_int8_stage")
+
+
+def wino_validate_codes(plan, codes_ptr: int, ws_ptr: int, stream: int) -> None:
+    _check(lib().wino_validate_codes(plan, codes_ptr, ws_ptr, stream), "wino_validate_codes")
 
 
 def wino_check_codes(plan, codes_ptr: int, bad_ptr: int, stream: int) -> None:

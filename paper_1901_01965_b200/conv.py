@@ -15,7 +15,7 @@ class WinoConv2d:
     """
 
     def __init__(self, n, h, w, c_in, c_out, pad=1, layout=L.WINO_NHWC, filter_scaling=True,
-                 out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0, path=L.WINO_PATH_STAGED,
+                 out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0, path=L.WINO_PATH_AUTO,
                  algorithm=L.WINO_ALG_F4X4, input_type=L.WINO_IN_INT8, x_zero_point=0, w_zero_point=0,
                  filter_target_max=255):
         if device is None:

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "../../include/wino.h"
@@ -13,11 +14,15 @@
 #include "layout.cuh"
 
 struct wino_plan_s {
-  wino_conv_desc d;
-  int device;
-  wino::Geom g;
-  int n_chunks;
-  size_t v_bytes, m_bytes, ws_bytes, f_bytes, x_bytes, y_bytes;
+  wino_conv_desc d;           // as given (d.path may be WINO_PATH_AUTO)
+  int device = 0;
+  wino::Geom g{};             // g.path: the kernel path, 0 fused / 1 staged (layout.cuh)
+  int n_chunks = 0;
+  size_t v_bytes = 0, m_bytes = 0, status_offset = 0, ws_bytes = 0, f_bytes = 0, x_bytes = 0, y_bytes = 0;
+  // scale-code buffers known to hold valid codes (written by wino_transform_filter of this plan, or
+  // checked by wino_validate_codes); the only mutable state of a plan, guarded by `mu`
+  std::mutex mu;
+  std::vector<const uint8_t*> valid_codes;
 };
 
 namespace {
@@ -76,6 +81,37 @@ size_t chunk_budget_bytes(int desc_mb) {
 
 }  // namespace
 
+// ---------------------------------------------------------------- scale-code validation (wino.h)
+static bool codes_known_valid(wino_plan_s* p, const uint8_t* codes) {
+  std::lock_guard<std::mutex> lk(p->mu);
+  for (const uint8_t* c : p->valid_codes)
+    if (c == codes) return true;
+  return false;
+}
+static void codes_mark(wino_plan_s* p, const uint8_t* codes, bool valid) {
+  std::lock_guard<std::mutex> lk(p->mu);
+  for (size_t i = 0; i < p->valid_codes.size(); i++)
+    if (p->valid_codes[i] == codes) {
+      if (!valid) p->valid_codes.erase(p->valid_codes.begin() + (long)i);
+      return;
+    }
+  if (!valid) return;
+  if (p->valid_codes.size() >= 64) p->valid_codes.erase(p->valid_codes.begin());   // oldest out
+  p->valid_codes.push_back(codes);
+}
+// Synchronous device check of c_out * positions codes: the flag lives in the workspace's status block.
+static wino_status validate_codes(wino_plan_s* p, const uint8_t* codes, void* workspace, cudaStream_t s) {
+  int32_t* flag = reinterpret_cast<int32_t*>(static_cast<int8_t*>(workspace) + p->status_offset);
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int32_t), s);
+  if (e == cudaSuccess) e = wino::launch_check_codes(codes, p->d.c_out * p->g.npos, p->g.w1, flag, s);
+  int32_t bad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, flag, sizeof(bad), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e);
+  codes_mark(p, codes, bad == 0);
+  return bad ? WINO_ERR_RANGE : WINO_OK;
+}
+
 extern "C" {
 
 const char* wino_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda_error); }
@@ -86,7 +122,7 @@ const char* wino_status_string(wino_status s) {
     case WINO_ERR_INVALID_ARG: return "invalid argument (null/misaligned pointer, bad enum or wrong device)";
     case WINO_ERR_UNSUPPORTED: return "unsupported shape or flag";
     case WINO_ERR_SHAPE: return "inconsistent sizes";
-    case WINO_ERR_RANGE: return "value out of range (requant multiplier/shift)";
+    case WINO_ERR_RANGE: return "value out of range (invalid scale code, or requant multiplier/shift)";
     case WINO_ERR_CUDA: return "CUDA runtime error";
     case WINO_ERR_NOMEM: return "out of host memory";
   }
@@ -98,9 +134,9 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   *out = nullptr;
   if (desc->path != WINO_PATH_FUSED && desc->path != WINO_PATH_STAGED && desc->path != WINO_PATH_AUTO)
     return WINO_ERR_INVALID_ARG;
-  // WINO_PATH_AUTO: the fused kernels where they measured faster -- the complex F(4x4) one at c_in <= 256
-  // (C2-C4; tools/path_ab.py), the rational F(2x2) one everywhere (C2-C4: 1.4-1.7x the staged path) --
-  // for target 255; else staged
+  // WINO_PATH_AUTO (the default, 0): the fused kernels where they measured faster -- the complex F(4x4) one at
+  // c_in <= 256 (C2-C4; tools/path_ab.py), the rational F(2x2) one everywhere (C2-C4: 1.4-1.7x the staged
+  // path) -- for target 255; else staged
   wino_conv_desc dr = *desc;
   if (dr.path == WINO_PATH_AUTO)
     dr.path = (dr.filter_target_max == 255 &&
@@ -140,10 +176,9 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   wino_status st = setup_device(device);
   if (st != WINO_OK) return st;
 
-  wino_plan_s* p = new (std::nothrow) wino_plan_s;
+  wino_plan_s* p = new (std::nothrow) wino_plan_s();
   if (!p) return WINO_ERR_NOMEM;
-  std::memset(p, 0, sizeof(*p));
-  p->d = d;
+  p->d = *desc;
   p->device = device;
   wino::Geom& g = p->g;
   g.n = d.n; g.h = d.h; g.w = d.w; g.cin = d.c_in; g.cout = d.c_out; g.pad = d.pad; g.layout = d.layout;
@@ -164,7 +199,7 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.dv_tpi = wino::make_fastdiv(g.tpi);
   g.cin_pad = (int)round_up(d.c_in, wino::kKStep);
   const int cout16 = (int)round_up(d.c_out, 16);
-  g.path = d.path;
+  g.path = d.path == WINO_PATH_FUSED ? 0 : 1;
   // fused path: 16-cout units (UMMA N = 16); staged path: widest N that the cout count fills
   g.nblk = d.path == WINO_PATH_FUSED ? (d.algorithm == WINO_ALG_F2X2 ? 32 : 16)
                                      : (cout16 <= 16 ? 16 : (cout16 <= 32 ? 32 : 64));
@@ -186,7 +221,9 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   p->n_chunks = (int)((d.n + imgs - 1) / imgs);
   p->v_bytes = v_per_tile_ch * g.chunk_tiles_pad * g.cin_pad;
   p->m_bytes = d.path == WINO_PATH_STAGED ? (size_t)g.npos * g.chunk_tiles_pad * g.cout_pad * 4 : 0;
-  p->ws_bytes = p->v_bytes + p->m_bytes;
+  // + one 256-byte status block (the code-validation flag of wino_validate_codes)
+  p->status_offset = (size_t)round_up((long long)(p->v_bytes + p->m_bytes), 256);
+  p->ws_bytes = p->status_offset + 256;
   // W': 92 B per (cin, cout) staged (46 planes x 2 pieces); 112 B fused (56 rows x 2 couts-halves, layout.cuh)
   p->f_bytes = (size_t)(fused_f4 ? 2 * wino::kWRowUnitsF : (g.w1 ? 1 : 2) * g.planes) * g.cout_pad * g.cin_pad;
   p->x_bytes = (size_t)d.n * d.h * d.w * d.c_in;
@@ -209,13 +246,13 @@ wino_status wino_plan_query(wino_plan_t p, wino_plan_info* info) {
   info->tiles = (long long)p->d.n * p->g.tpi;
   info->cin_pad = p->g.cin_pad; info->cout_pad = p->g.cout_pad;
   info->n_block = p->g.nblk; info->m_block = wino::kMBlock;
-  info->planes = p->g.path == WINO_PATH_FUSED && p->g.alg == 0 ? 36 : p->g.planes;   // fused F4: 16 + 10 x (re, im)
+  info->planes = p->g.path == 0 && p->g.alg == 0 ? 36 : p->g.planes;   // fused F4: 16 + 10 x (re, im)
   info->algorithm = p->g.alg; info->tile = p->g.tile; info->positions = p->g.npos;
   info->pieces = wino::kPieces;
   info->chunk_images = p->g.chunk_imgs; info->n_chunks = p->n_chunks;
   info->chunk_tiles_pad = p->g.chunk_tiles_pad;
-  info->path = p->g.path;
-  info->stages = p->g.path == WINO_PATH_FUSED ? 2 : 3;
+  info->path = p->g.path == 0 ? WINO_PATH_FUSED : WINO_PATH_STAGED;
+  info->stages = p->g.path == 0 ? 2 : 3;
   info->v_offset = 0; info->v_bytes = p->v_bytes;
   info->m_offset = p->v_bytes; info->m_bytes = p->m_bytes;
   info->workspace_bytes = p->ws_bytes;
@@ -237,6 +274,7 @@ wino_status wino_transform_filter(wino_plan_t p, const int8_t* w, void* w_wino, 
   if (st != WINO_OK) return st;
   cudaError_t e = wino::launch_filter_transform(p->g, w, static_cast<int8_t*>(w_wino), codes,
                                                 static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) codes_mark(p, codes, true);   // K1 writes valid codes by construction
   return cuda_status(e);
 }
 
@@ -251,9 +289,9 @@ static wino_status run_stage(const wino_plan_s* p, int stage, int chunk, const i
   int32_t* m = reinterpret_cast<int32_t*>(static_cast<int8_t*>(workspace) + p->v_bytes);
   cudaError_t e = cudaErrorInvalidValue;
   if (stage == 2)
-    e = g.path == WINO_PATH_FUSED && g.alg == 0 ? wino::launch_input_transform_f(g, x, n0, imgs, vimg, s)
+    e = g.path == 0 && g.alg == 0 ? wino::launch_input_transform_f(g, x, n0, imgs, vimg, s)
                                   : wino::launch_input_transform(g, x, n0, imgs, vimg, s);
-  if (g.path == WINO_PATH_FUSED) {
+  if (g.path == 0) {
     if (stage == 3)
       e = g.alg == 1 ? wino::launch_fused2(g, tiles_pad, n0, imgs, vimg, static_cast<const int8_t*>(w_wino), codes,
                                            rq_mult, rq_shift, y, s)
@@ -279,7 +317,11 @@ wino_status wino_conv2d_int8(wino_plan_t p, const int8_t* x, const void* w_wino,
   wino_status st = check_conv_args(p, x, w_wino, codes, rq_mult, rq_shift, y, workspace);
   if (st != WINO_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int last = p->g.path == WINO_PATH_FUSED ? 3 : 4;
+  if (!codes_known_valid(p, codes)) {   // first use of this code buffer: synchronous check (wino.h)
+    st = validate_codes(p, codes, workspace, s);
+    if (st != WINO_OK) return st;
+  }
+  const int last = p->g.path == 0 ? 3 : 4;
   for (int c = 0; c < p->n_chunks; c++)
     for (int stage = 2; stage <= last; stage++) {
       st = run_stage(p, stage, c, x, w_wino, codes, rq_mult, rq_shift, y, workspace, s);
@@ -293,8 +335,12 @@ wino_status wino_conv2d_int8_stage(wino_plan_t p, int stage, int chunk, const in
                                    void* stream) {
   wino_status st = check_conv_args(p, x, w_wino, codes, rq_mult, rq_shift, y, workspace);
   if (st != WINO_OK) return st;
-  const int last = p->g.path == WINO_PATH_FUSED ? 3 : 4;
+  const int last = p->g.path == 0 ? 3 : 4;
   if (stage < 2 || stage > last || chunk < 0 || chunk >= p->n_chunks) return WINO_ERR_INVALID_ARG;
+  if (stage >= 3 && !codes_known_valid(p, codes)) {
+    st = validate_codes(p, codes, workspace, static_cast<cudaStream_t>(stream));
+    if (st != WINO_OK) return st;
+  }
   return run_stage(p, stage, chunk, x, w_wino, codes, rq_mult, rq_shift, y, workspace,
                    static_cast<cudaStream_t>(stream));
 }
@@ -315,8 +361,17 @@ wino_status wino_conv2d_int8_host(wino_plan_t p, const int8_t* x_host, const voi
 
 wino_status wino_check_codes(wino_plan_t p, const uint8_t* codes, int32_t* bad_flag, void* stream) {
   if (!p || !codes || !bad_flag) return WINO_ERR_INVALID_ARG;
+  wino_status st = check_device(p);
+  if (st != WINO_OK) return st;
   return cuda_status(wino::launch_check_codes(codes, p->d.c_out * p->g.npos, p->g.w1, bad_flag,
                                               static_cast<cudaStream_t>(stream)));
+}
+
+wino_status wino_validate_codes(wino_plan_t p, const uint8_t* codes, void* workspace, void* stream) {
+  if (!p || !codes || !workspace || !aligned16(workspace)) return WINO_ERR_INVALID_ARG;
+  wino_status st = check_device(p);
+  if (st != WINO_OK) return st;
+  return validate_codes(p, codes, workspace, static_cast<cudaStream_t>(stream));
 }
 
 int wino_debug_fastdiv(int n, int d) {

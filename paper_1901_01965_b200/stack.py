@@ -13,7 +13,7 @@ from .conv import WinoConv2d, maxpool2
 
 class ConvStack:
     def __init__(self, n, layers, pools_after, shifts, layout=L.WINO_NHWC, device=None, workspace_mb=1024,
-                 path=L.WINO_PATH_STAGED):
+                 path=L.WINO_PATH_AUTO):
         """layers: sequence of objects with h, w, c_in, c_out, pad, scaling; shifts: requant
         shift per layer (multiplier 1)."""
         if device is None:

@@ -36,17 +36,17 @@ def test_status_strings_and_pre_cuda_validation():
     for kw, status in [(dict(pad=2), L.WINO_ERR_UNSUPPORTED), (dict(c_in=897, filter_scaling=0), L.WINO_ERR_UNSUPPORTED),
                        (dict(c_in=769), L.WINO_ERR_UNSUPPORTED), (dict(layout=5), L.WINO_ERR_INVALID_ARG),
                        (dict(out_mode=9), L.WINO_ERR_INVALID_ARG), (dict(h=1, pad=0), L.WINO_ERR_UNSUPPORTED),
-                       (dict(filter_target_max=127), L.WINO_ERR_UNSUPPORTED), (dict(path=3), L.WINO_ERR_INVALID_ARG),
+                       (dict(filter_target_max=127, path=1), L.WINO_ERR_UNSUPPORTED), (dict(path=3), L.WINO_ERR_INVALID_ARG),
                        (dict(algorithm=2), L.WINO_ERR_INVALID_ARG),
-                       (dict(algorithm=1, path=1, input_type=1, c_in=225), L.WINO_ERR_UNSUPPORTED),
+                       (dict(algorithm=1, path=2, input_type=1, c_in=225), L.WINO_ERR_UNSUPPORTED),
                        (dict(input_type=2), L.WINO_ERR_INVALID_ARG),
-                       (dict(input_type=1, x_zero_point=256, path=1), L.WINO_ERR_INVALID_ARG),
-                       (dict(input_type=1, path=0, c_in=225), L.WINO_ERR_UNSUPPORTED),
+                       (dict(input_type=1, x_zero_point=256, path=2), L.WINO_ERR_INVALID_ARG),
                        (dict(input_type=1, path=1, c_in=225), L.WINO_ERR_UNSUPPORTED),
-                       (dict(filter_target_max=126, path=1), L.WINO_ERR_UNSUPPORTED),
-                       (dict(filter_target_max=127, path=1, filter_scaling=0), L.WINO_ERR_UNSUPPORTED),
-                       (dict(filter_target_max=127, path=1, algorithm=1), L.WINO_ERR_UNSUPPORTED),
-                       (dict(filter_target_max=127, path=1, input_type=1), L.WINO_ERR_UNSUPPORTED)]:
+                       (dict(input_type=1, path=2, c_in=225), L.WINO_ERR_UNSUPPORTED),
+                       (dict(filter_target_max=126, path=2), L.WINO_ERR_UNSUPPORTED),
+                       (dict(filter_target_max=127, path=2, filter_scaling=0), L.WINO_ERR_UNSUPPORTED),
+                       (dict(filter_target_max=127, path=2, algorithm=1), L.WINO_ERR_UNSUPPORTED),
+                       (dict(filter_target_max=127, path=2, input_type=1), L.WINO_ERR_UNSUPPORTED)]:
         d = dict(base); d.update(kw)
         with pytest.raises(L.WinoError) as e:
             L.wino_plan(L.wino_conv_desc(**d), 0)

@@ -14,17 +14,17 @@ import layout_decode as LD
 pytestmark = pytest.mark.gpu
 
 
-PATHS = [pytest.param(1, id="staged"), pytest.param(0, id="fused")]
+PATHS = [pytest.param(2, id="staged"), pytest.param(1, id="fused")]   # WINO_PATH_STAGED / _FUSED
 
 
-def _conv(n, h, w, ci, co, pad, layout, scaling, out_mode=1, chunk_mb=0, path=1):
+def _conv(n, h, w, ci, co, pad, layout, scaling, out_mode=1, chunk_mb=0, path=2):
     import paper_1901_01965_b200 as W
     return W.WinoConv2d(n, h, w, ci, co, pad, layout, scaling, out_mode, workspace_mb=chunk_mb,
                         path=path, algorithm=W.WINO_ALG_F2X2)
 
 
-def _check(x, w, layout, pad=1, scaling=True, intermediates=True, path=1):
-    intermediates = intermediates and path == 1   # V / W' / M'' decoders: staged layouts
+def _check(x, w, layout, pad=1, scaling=True, intermediates=True, path=2):
+    intermediates = intermediates and path == 2   # V / W' / M'' decoders: staged layouts
     if layout == O.NCHW:
         n, ci, h, wd = x.shape
     else:
@@ -130,4 +130,4 @@ def test_f2_fused_plan_reports_its_shape():
     conv = W.WinoConv2d(1, 8, 8, 4, 4, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=W.WINO_PATH_FUSED,
                         algorithm=W.WINO_ALG_F2X2)
     i = conv.info
-    assert i.path == 0 and i.stages == 2 and i.positions == 16 and i.tile == 2 and i.n_block == 32
+    assert i.path == W.WINO_PATH_FUSED and i.stages == 2 and i.positions == 16 and i.tile == 2 and i.n_block == 32

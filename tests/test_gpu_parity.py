@@ -19,7 +19,7 @@ def _wino():
     return W
 
 
-FUSED, STAGED = 0, 1
+FUSED, STAGED = 1, 2   # WINO_PATH_FUSED / WINO_PATH_STAGED (WINO_PATH_AUTO = 0)
 PATHS = [pytest.param(FUSED, id="fused"), pytest.param(STAGED, id="staged")]
 
 
@@ -213,6 +213,41 @@ def test_host_entry_point_matches_device_path():
     np.testing.assert_array_equal(yh.numpy(), O.wino_conv(x, w, 1, O.NHWC, True, M0=1, S=S).y8)
 
 
+def test_invalid_scale_code_is_range_at_the_boundary():
+    """a scale_codes entry that does not decode to n in [8, 15] (A4) is
+    WINO_ERR_RANGE from wino_conv2d_int8 itself (nothing enqueued); the same buffer made valid
+    passes after wino_validate_codes; codes written by wino_transform_filter are accepted."""
+    W = _wino()
+    L = W._lib
+    for path in (FUSED, STAGED):
+        conv = W.WinoConv2d(1, 8, 8, 4, 4, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=path)
+        x, w = synth.config_inputs("C1", O.NHWC)
+        xd = torch.from_numpy(x).cuda()
+        conv.transform_filter(torch.from_numpy(w).cuda())
+        good = conv(xd).cpu().numpy()                          # the plan's own codes: accepted
+        np.testing.assert_array_equal(good, O.wino_conv(x, w, 1, O.NHWC, True).out32)
+        bad = conv.codes.clone()
+        bad[1, 3] = 5 << 2                                      # n = 5: not a code of P:330
+        y = torch.full(conv.y_shape, 7, dtype=torch.int32, device="cuda")
+        with pytest.raises(W.WinoError) as e:
+            conv(xd, y=y, codes=bad)
+        assert e.value.status == L.WINO_ERR_RANGE
+        assert (y == 7).all().item()                            # nothing was enqueued
+        with pytest.raises(W.WinoError) as e:
+            L.wino_validate_codes(conv.plan, bad.data_ptr(), conv.workspace.data_ptr(),
+                                  torch.cuda.current_stream().cuda_stream)
+        assert e.value.status == L.WINO_ERR_RANGE
+        bad[1, 3] = conv.codes[1, 3]                            # repaired, re-validated, accepted
+        L.wino_validate_codes(conv.plan, bad.data_ptr(), conv.workspace.data_ptr(),
+                              torch.cuda.current_stream().cuda_stream)
+        np.testing.assert_array_equal(conv(xd, codes=bad).cpu().numpy(), good)
+        for v in (1, 31, 64, 200):                              # n < 8, n = 7 max, > 6 bits
+            b2 = conv.codes.clone(); b2[0, 0] = v
+            with pytest.raises(W.WinoError) as e:
+                conv(xd, codes=b2)
+            assert e.value.status == L.WINO_ERR_RANGE, v
+
+
 def test_check_codes_and_maxpool():
     W = _wino()
     conv = W.WinoConv2d(1, 8, 8, 4, 4, 1, W.WINO_NHWC, True, W.WINO_OUT_INT8)
@@ -234,10 +269,10 @@ def test_check_codes_and_maxpool():
 
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", ["C2", "C3", "C4"])
-def test_full_size_configs_sampled(name, path):
+def test_full_size_configs_every_image(name, path):
     """Full BASELINE sizes in the bench launch configuration (NHWC, int8 out,
-    default chunking); whole images sampled (first, middle, last) and compared
-    bit-exactly with the oracle run on those images alone."""
+    default chunking): EVERY image of the batch compared bit-exactly with the
+    oracle run on the whole batch."""
     W = _wino()
     layer = synth.CONFIGS[name].layers[0]
     x, w = synth.config_inputs(name)
@@ -246,9 +281,9 @@ def test_full_size_configs_sampled(name, path):
                         W.WINO_OUT_INT8, path=path)
     conv.transform_filter(torch.from_numpy(w).cuda())
     y = conv(torch.from_numpy(x).cuda(), 1, S).cpu().numpy()
-    for i in sorted({0, layer.n // 2, layer.n - 1}):
-        ref = O.wino_conv(x[i:i + 1], w, 1, O.NHWC, True, M0=1, S=S)
-        np.testing.assert_array_equal(y[i:i + 1], ref.y8)
+    ref = O.wino_conv(x, w, 1, O.NHWC, True, M0=1, S=S)
+    assert y.shape == ref.y8.shape
+    np.testing.assert_array_equal(y, ref.y8)
     # codes computed on the device equal the oracle's
     np.testing.assert_array_equal(conv.codes.cpu().numpy(), O.filter_transform(w, O.NHWC, True)[2])
 
@@ -263,7 +298,7 @@ def _oracle_stack(x, ws, shifts, pools):
     return outs
 
 
-@pytest.mark.parametrize("path", [pytest.param(STAGED, id="staged"), pytest.param(2, id="auto")])
+@pytest.mark.parametrize("path", [pytest.param(STAGED, id="staged"), pytest.param(0, id="auto")])
 def test_vgg16_stack_full_size_sampled(path):
     """BASELINE configs[4] at full size (13 layers, 224x224, batch 256, requantised,
     max-pooled): images 0 and 255 compared layer by layer with the oracle; all layers staged,
@@ -273,7 +308,7 @@ def test_vgg16_stack_full_size_sampled(path):
     shifts = synth.stack_shifts("C5")
     x, ws = synth.stack_inputs("C5")
     st = ConvStack(x.shape[0], cfg.layers, cfg.pools_after, shifts, path=path)
-    if path == 2:
+    if path == 0:
         assert [c.info.path for c in st.convs] == [FUSED] * 8 + [STAGED] * 5
     st.transform_filters([torch.from_numpy(w).cuda() for w in ws])
     st(torch.from_numpy(x).cuda())
