@@ -170,7 +170,7 @@ def test_plan_rejects():
     W = _wino()
     L = W._lib
     bad = [dict(pad=2), dict(c_in=897, filter_scaling=0), dict(c_in=769, filter_scaling=1), dict(h=0),
-           dict(h=1, pad=0), dict(filter_target_max=127)]
+           dict(h=1, pad=0), dict(filter_target_max=127, path=1)]   # 127 needs the staged path
     for kw in bad:
         d = dict(n=1, h=8, w=8, c_in=4, c_out=4, pad=1, layout=1, filter_scaling=1, filter_target_max=255,
                  out_mode=0)

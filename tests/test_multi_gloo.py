@@ -69,3 +69,40 @@ def test_split_is_a_partition():
             pos = 0
             for s, c in parts:
                 assert s == pos; pos += c
+
+
+@pytest.mark.parametrize("config,gpus", [("C2", 2), ("C1", 8), ("C5", 2)])
+def test_bench_gpus_spawns_ranks_with_their_shards(config, gpus):
+    """`bench.py --gpus N` with no WORLD_SIZE re-runs itself under torch.distributed.run with N ranks
+    (gloo here, --plan-only: no CUDA); each rank gets its slice of the configured batch (Cout for
+    C1's batch 1, where ranks 4-7 of 8 get an empty shard), and the checking gather reassembles the
+    full output with every element owned by exactly one rank."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    env["OMP_NUM_THREADS"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(gpus), "--config", config,
+                        "--plan-only"], capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["world"] == gpus and line["torchrun"]
+    layer = synth.CONFIGS[config].layers[0]
+    shards = line["shards"]
+    assert len(shards) == gpus
+    for rank, sh in enumerate(shards):
+        assert sh == SH.shard(layer.n, layer.c_out, gpus, rank)
+    ho, wo = layer.h + 2 * layer.pad - 2, layer.w + 2 * layer.pad - 2
+    assert line["gathered_shape"] == [layer.n, ho, wo, layer.c_out]
+    per_rank = line["elements_per_rank"]
+    assert sum(per_rank) == layer.n * ho * wo * layer.c_out
+    for rank, sh in enumerate(shards):
+        assert per_rank[rank] == sh["n"] * ho * wo * sh["co"]
+    if config == "C1":
+        assert all(s["mode"] == "cout" for s in shards)
+        assert [s["co"] for s in shards] == [1, 1, 1, 1, 0, 0, 0, 0]
+    else:
+        assert all(s["mode"] == "batch" for s in shards)
+    assert line["max_over_ranks"] == 0.25 * gpus
