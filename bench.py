@@ -720,7 +720,7 @@ def run_ours_stack(args):
     sh = _shard(args, n_all, cfg.layers[0].c_out, world, rank)      # batch 256 >= world: by batch
     n = sh["n"]
     path = {"staged": L.WINO_PATH_STAGED, "fused": L.WINO_PATH_FUSED, "auto": L.WINO_PATH_AUTO}[args.path]
-    st = ConvStack(n, cfg.layers, cfg.pools_after, shifts, device=local_rank, path=path)
+    st = ConvStack(n, cfg.layers, cfg.pools_after, shifts, device=local_rank, path=path, workspace_mb=args.chunk_mb)
     n_sets = 2
     xs, wss = [], []
     for i in range(n_sets):
@@ -829,6 +829,7 @@ def run_ours_stack(args):
                        "step": "13 filter transforms + 13 convs + 4 max pools",
                        "paths": ["fused" if c.info.path == L.WINO_PATH_FUSED else "staged" for c in st.convs],
                        "l2": "activations 0.8 GB per layer >> 126 MiB L2; 2 input sets rotated",
+                       "chunk_mb": args.chunk_mb, "chunks": [c.info.n_chunks for c in st.convs],
                        "parallelism": f"dp{world}: " + ("batch-partitioned (strong scaling)" if args.scaling == "strong"
                                                         else "replicated per-rank batches (weak scaling)") +
                                       "; no data-path collective"},
@@ -1020,6 +1021,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=24.0,
                     help="CPU oracle baseline budget (about half of it is the timed sample)")
+    ap.add_argument("--chunk-mb", type=int, default=1024,
+                    help="C5: per-layer batch-chunk budget for the V (+ M'') workspace in MiB (wino_conv_desc.workspace_mb)")
     ap.add_argument("--plan-only", action="store_true", help="CPU/gloo: spawn the ranks and print their shards")
     args = ap.parse_args()
     if args.steps is None:

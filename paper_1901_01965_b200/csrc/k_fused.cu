@@ -125,10 +125,17 @@ __device__ __forceinline__ void tmem_zero4(uint32_t taddr) {
 // and a fixed shift.  rha(p / 2^7) = (p + 64 - [p < 0]) >> 7 (floor shift).  The
 // unscaled code is m' = 128, which returns v.
 __device__ __forceinline__ int32_t frscale(int32_t v, uint32_t mq) {
-  // signed 32 x 32 -> 64 multiply-add (one IMAD.WIDE; 64 + (v >> 31) >= 0 adds without a sign fix-up)
-  long long p;
-  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(p) : "r"(v), "r"((int32_t)mq), "l"((long long)(64 + (v >> 31))));
-  return (int32_t)(p >> 7);
+  // signed 32 x 32 -> 64 multiply-add with the rounding term as the addend: the addend 64 + (v >> 31) is
+  // non-negative, so its 64-bit form is {lo, 0} (one LEA.HI + one IMAD.WIDE + one funnel shift, no
+  // carry chain); the low word of p >> 7 is the result (exact mod 2^32, A23)
+  uint32_t lo, hi;
+  asm("{\n\t.reg .b64 c, p;\n\t"
+      "mov.b64 c, {%2, %4};\n\t"
+      "mad.wide.s32 p, %3, %5, c;\n\t"
+      "mov.b64 {%0, %1}, p;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "r"((uint32_t)(64 + (v >> 31))), "r"(v), "r"(0u), "r"((int32_t)mq));
+  return (int32_t)__funnelshift_r(lo, hi, 7);
 }
 
 // a_k[c] for the real indices c in {0,1,2,5}
@@ -165,7 +172,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
 #ifndef WINO_FUSED_DBG
   dbg = 0;   // the WINO_FUSED_DBG ablation modes exist only in debug builds (-DWINO_FUSED_DBG)
 #endif
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index broadcast from lane 0: warp-uniform to the compiler, so the TMEM addresses derived from it
+  // live in uniform registers (no per-access R2UR moves before LDTM / STTM)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   uint8_t* part = smem + kFStages * kFStageBytes;                            // Z_0 / Z_5 | output staging
   uint32_t* etab = reinterpret_cast<uint32_t*>(part + kFPartBytes);          // [26 groups][16 couts] m'
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(etab) + kFETabBytes);
@@ -203,7 +212,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   if constexpr (MG > 0) {   // every accumulator slot starts at zero (the epilogue re-zeroes each after reading)
     if (warp < kFEpiWarps) {
       const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * kFC;

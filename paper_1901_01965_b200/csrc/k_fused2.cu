@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kT2Threads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int kStg = KC == 2 ? 4 : 2;
   constexpr uint32_t kStgBytes = kRing2 / kStg, kStgV = 2 * KC * kPlaneV;   // V of a pair, then W' of the pair
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;   // warp-uniform: TMEM addresses in uniform registers
   uint32_t* etab = reinterpret_cast<uint32_t*>(smem + kRing2);           // [16 positions][32 couts] m'
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kRing2 + 16 * kN2 * 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStg + 2 * kSlots2);
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kT2Threads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   if (warp < kE2Warps) {   // accumulator slots start at zero (the epilogue re-zeroes each after reading)
     const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * kC2;
     for (int b = 0; b < kSlots2; b++)

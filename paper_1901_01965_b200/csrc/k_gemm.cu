@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #define WINO_TRACE(i, ev) do { } while (0)
 #endif
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;   // warp-uniform: TMEM addresses in uniform registers
   const uint32_t a_bytes = kps * kABytesPerKStep;
   const uint32_t b_bytes = kps * (uint32_t)NBLK * kKStep;
   const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
   if (warp == kProducerWarp) {
     {
