@@ -124,19 +124,7 @@ __device__ __forceinline__ void tmem_zero4(uint32_t taddr) {
 // m' = m 2^(7-q) (q in [4,7], so m' <= 2040): one constant per (position, cout)
 // and a fixed shift.  rha(p / 2^7) = (p + 64 - [p < 0]) >> 7 (floor shift).  The
 // unscaled code is m' = 128, which returns v.
-__device__ __forceinline__ int32_t frscale(int32_t v, uint32_t mq) {
-  // signed 32 x 32 -> 64 multiply-add with the rounding term as the addend: the addend 64 + (v >> 31) is
-  // non-negative, so its 64-bit form is {lo, 0} (one LEA.HI + one IMAD.WIDE + one funnel shift, no
-  // carry chain); the low word of p >> 7 is the result (exact mod 2^32, A23)
-  uint32_t lo, hi;
-  asm("{\n\t.reg .b64 c, p;\n\t"
-      "mov.b64 c, {%2, %4};\n\t"
-      "mad.wide.s32 p, %3, %5, c;\n\t"
-      "mov.b64 {%0, %1}, p;\n\t}"
-      : "=r"(lo), "=r"(hi)
-      : "r"((uint32_t)(64 + (v >> 31))), "r"(v), "r"(0u), "r"((int32_t)mq));
-  return (int32_t)__funnelshift_r(lo, hi, 7);
-}
+__device__ __forceinline__ int32_t frscale(int32_t v, uint32_t mq) { return rha_mul_shr7(v, mq); }
 
 // a_k[c] for the real indices c in {0,1,2,5}
 __host__ __device__ constexpr int areal(int k, int c) {

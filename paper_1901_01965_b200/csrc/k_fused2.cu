@@ -71,12 +71,7 @@ __device__ __forceinline__ void tzero8(uint32_t taddr) {
 __device__ __forceinline__ void tst_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // M'' = rha(v m / 2^q) as rha(v m' / 2^7), m' = m 2^(7-q) (q >= 3: m' <= 4080); m' = 128 is the identity
-__device__ __forceinline__ int32_t rscale7(int32_t v, uint32_t mq) {
-  // signed 32 x 32 -> 64 multiply-add (one IMAD.WIDE; 64 + (v >> 31) >= 0 adds without a sign fix-up)
-  long long p;
-  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(p) : "r"(v), "r"((int32_t)mq), "l"((long long)(64 + (v >> 31))));
-  return (int32_t)(p >> 7);
-}
+__device__ __forceinline__ int32_t rscale7(int32_t v, uint32_t mq) { return rha_mul_shr7(v, mq); }
 template <typename F, int... I>
 __device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
   (f(std::integral_constant<int, I>{}), ...);

@@ -128,15 +128,9 @@ __device__ __forceinline__ void tmem_ld<8>(uint32_t taddr, uint32_t (&r)[8]) {
                : "r"(taddr));
 }
 
-// M'' = rha(M m / 2^q) = sign(M) ((|M| m + 2^(q-1)) >> q) (A9) with
-// e = m | q << 8 | 2^(q-1) << 16; the unscaled code maps to m = 1, q = 0.
-__device__ __forceinline__ int32_t rscale_e(uint32_t v, uint32_t e) {
-  const int32_t vi = (int32_t)v;
-  const uint32_t m = e & 0xffu, q = (e >> 8) & 0xffu, half = e >> 16;
-  const uint64_t prod = (uint64_t)(uint32_t)abs(vi) * m + half;
-  const int32_t r = (int32_t)(uint32_t)(prod >> q);
-  return vi < 0 ? -r : r;
-}
+// M'' = rha(M m / 2^q) (A9) as rha(M m' / 2^7) with e = m' = m 2^(7-q) (q >= 3: m' <= 4080); the unscaled
+// code maps to m' = 128 (the identity)
+__device__ __forceinline__ int32_t rscale_e(uint32_t v, uint32_t e) { return rha_mul_shr7((int32_t)v, e); }
 
 __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync %0, %1;" ::"n"(kEpiBarrier), "n"(kEpiWarps * 32) : "memory");
@@ -177,7 +171,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* staging = smem + nst * stage_bytes;                           // 2 x kTileBytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(staging + 2 * kTileBytes);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 4);
-  uint32_t* lut = tmem_slot + 4;                                         // 128: code -> (m, q, half)
+  uint32_t* lut = tmem_slot + 4;                                         // 128: code -> m' = m 2^(7-q)
   uint8_t* s_codes = reinterpret_cast<uint8_t*>(lut + 128);              // [26 positions][cout_pad]
   const uint32_t sbase = smem_u32(smem);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kMaxStages);
@@ -207,7 +201,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (W1) decode_code7(threadIdx.x, n, p);
     else decode_code(threadIdx.x & 63, n, p);
     if (n >= 8) inverse_factor(n, p, m, q);
-    lut[threadIdx.x] = (uint32_t)m | ((uint32_t)q << 8) | ((q ? (1u << (q - 1)) : 0u) << 16);
+    lut[threadIdx.x] = n >= 8 ? (uint32_t)m << (7 - q) : 128u;   // m' (rscale_e); code 0: identity
   }
   pdl_wait();   // V, W' and the codes come from the kernels just before
   for (int i = threadIdx.x; i < Alg<F2>::kUnits * cout_pad; i += blockDim.x) {   // codes, position-major

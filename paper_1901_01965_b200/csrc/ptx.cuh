@@ -173,4 +173,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 
+// ---------------------------------------------------------------- reverse scaling (A9)
+// rha(v m' / 2^7) for m' = m 2^(7-q) > 0 (one constant per (position, cout), a fixed shift): the signed
+// 32 x 32 -> 64 product plus the rounding term c = 64 + (v >> 31) >= 0 as an extended-precision
+// multiply-add pair (mad.lo.cc + madc.hi: one IMAD.WIDE with a {c, 0} addend, no carry chain), then the
+// low word of p >> 7 (a funnel shift).  Exact mod 2^32 (A23); m' = 128 is the identity (unscaled code).
+__device__ __forceinline__ int32_t rha_mul_shr7(int32_t v, uint32_t mq) {
+  uint32_t lo, hi;
+  asm("{\n\t.reg .u32 c;\n\t"
+      "shr.s32 c, %2, 31;\n\t"
+      "add.u32 c, c, 64;\n\t"
+      "mad.lo.cc.u32 %0, %2, %3, c;\n\t"
+      "madc.hi.s32 %1, %2, %3, 0;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(v), "r"(mq));
+  return (int32_t)__funnelshift_r(lo, hi, 7);
+}
+
 }  // namespace wino
