@@ -265,6 +265,13 @@ def test_check_codes_and_maxpool():
             x = np.ascontiguousarray(x.transpose(0, 3, 1, 2))
         y = W.maxpool2(torch.from_numpy(x).cuda(), layout).cpu().numpy()
         np.testing.assert_array_equal(y, O.maxpool2(x, layout))
+    # the vectorised NHWC path (c % 16 == 0): signed byte max over the int8 extremes, odd map sizes
+    for (h, w, c) in [(10, 13, 32), (224, 224, 64), (3, 2, 16)]:
+        x = rng.integers(-128, 128, (2, h, w, c)).astype(np.int8)
+        x[0, 0, 0, :8] = -128
+        x[0, 0, 1, 8:] = 127
+        y = W.maxpool2(torch.from_numpy(x).cuda(), O.NHWC).cpu().numpy()
+        np.testing.assert_array_equal(y, O.maxpool2(x, O.NHWC))
 
 
 @pytest.mark.parametrize("path", PATHS)
