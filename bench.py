@@ -720,7 +720,8 @@ def run_ours_stack(args):
     sh = _shard(args, n_all, cfg.layers[0].c_out, world, rank)      # batch 256 >= world: by batch
     n = sh["n"]
     path = {"staged": L.WINO_PATH_STAGED, "fused": L.WINO_PATH_FUSED, "auto": L.WINO_PATH_AUTO}[args.path]
-    st = ConvStack(n, cfg.layers, cfg.pools_after, shifts, device=local_rank, path=path, workspace_mb=args.chunk_mb)
+    st = ConvStack(n, cfg.layers, cfg.pools_after, shifts, device=local_rank, path=path, workspace_mb=args.chunk_mb,
+                   lanes=args.lanes)
     n_sets = 2
     xs, wss = [], []
     for i in range(n_sets):
@@ -735,8 +736,9 @@ def run_ours_stack(args):
 
     def step(j, k1=True):
         if k1:
-            st.transform_filters(wss[j], stream)
-        st(xs[j], stream)
+            st.step(xs[j], wss[j], stream)     # the 13 filter transforms forked onto a side stream
+        else:
+            st(xs[j], stream)
 
     graphs, graphs_nok1 = [], []
     with torch.cuda.stream(stream):
@@ -809,8 +811,7 @@ def run_ours_stack(args):
         e0.record(stream)
         for i in range(reps):
             xd.copy_(xh, non_blocking=True)
-            st.transform_filters(wss[0], stream)
-            step_out = st(xd, stream)
+            step_out = st.step(xd, wss[0], stream)
             yh.copy_(step_out, non_blocking=True)
         e1.record(stream)
         stream.synchronize()
@@ -830,6 +831,7 @@ def run_ours_stack(args):
                        "paths": ["fused" if c.info.path == L.WINO_PATH_FUSED else "staged" for c in st.convs],
                        "l2": "activations 0.8 GB per layer >> 126 MiB L2; 2 input sets rotated",
                        "chunk_mb": args.chunk_mb, "chunks": [c.info.n_chunks for c in st.convs],
+                       "lanes": [c.info.lanes for c in st.convs],
                        "parallelism": f"dp{world}: " + ("batch-partitioned (strong scaling)" if args.scaling == "strong"
                                                         else "replicated per-rank batches (weak scaling)") +
                                       "; no data-path collective"},
@@ -1021,8 +1023,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=24.0,
                     help="CPU oracle baseline budget (about half of it is the timed sample)")
-    ap.add_argument("--chunk-mb", type=int, default=1024,
+    ap.add_argument("--chunk-mb", type=int, default=256,
                     help="C5: per-layer batch-chunk budget for the V (+ M'') workspace in MiB (wino_conv_desc.workspace_mb)")
+    ap.add_argument("--lanes", type=int, default=3,
+                    help="C5: concurrent chunk pipelines inside each conv call (wino_conv_desc.lanes; 0 = one)")
     ap.add_argument("--plan-only", action="store_true", help="CPU/gloo: spawn the ranks and print their shards")
     args = ap.parse_args()
     if args.steps is None:

@@ -69,7 +69,14 @@ enum { WINO_NCHW = 0, WINO_NHWC = 1 };
  *                   unscaled; int32, wraps never: |y| < 2^31 for Cin <= 896).
  *   WINO_OUT_INT8:  y = clamp(rha(out32 * requant_mult / 2^requant_shift),
  *                   -128, 127) with a 64-bit product (A14).                     */
-enum { WINO_OUT_INT8 = 0, WINO_OUT_INT32 = 1 };
+enum { WINO_OUT_INT8 = 0, WINO_OUT_INT32 = 1, WINO_OUT_INT8_POOL2 = 2 };
+/*   WINO_OUT_INT8_POOL2: the int8 output above followed by the 2x2 stride-2 max
+ *                   pool of the VGG stack (A22), fused into the output stage:
+ *                   y [N][Ho/2][Wo/2][Cout] (floor); NHWC, complex F(4x4),
+ *                   c_out % 16 == 0 (fused path) or % 4 == 0 (staged path),
+ *                   else WINO_ERR_UNSUPPORTED.  Identical to wino_maxpool2_int8
+ *                   applied to the WINO_OUT_INT8 result (requantisation is
+ *                   monotone, so the pool commutes with it).                  */
 
 typedef struct {
     int n, h, w;          /* batch and input spatial size, each >= 1                  */
@@ -81,7 +88,7 @@ typedef struct {
     int filter_target_max;/* 255: the paper's int9 target (A6, the default);
                              127: the int8-native target (needs
                              filter_scaling, the staged path, F4x4 and int8 input)   */
-    int out_mode;         /* WINO_OUT_INT8 or WINO_OUT_INT32                           */
+    int out_mode;         /* WINO_OUT_INT8, WINO_OUT_INT32 or WINO_OUT_INT8_POOL2       */
     int workspace_mb;     /* batch-chunk budget for V (+ M) in MiB; 0 = default (128, or
                              env WINO_CHUNK_MB).  Larger = fewer, longer launches.     */
     int path;             /* WINO_PATH_AUTO (0, the default everywhere -- this ABI, the
@@ -106,6 +113,13 @@ typedef struct {
                              (int32 exactness); either algorithm, either path.        */
     int x_zero_point;     /* [0, 255], uint8 input only                                  */
     int w_zero_point;     /* [0, 255], uint8 input only                                  */
+    int lanes;            /* 0 or 1: the chunks of a call run one after another on the
+                             caller's stream.  2..8: chunk c runs on lane c % lanes, each
+                             lane with its own V (+ M'') buffer in the workspace and its
+                             own stream (the plan's, forked from and joined back into the
+                             caller's stream with events, so CUDA-graph capture works);
+                             one chunk's input transform then overlaps another's GEMM.
+                             Capped at the chunk count.  Results are identical.         */
 } wino_conv_desc;
 
 /* Hot-path kernel structure (wino_conv_desc.path). */
@@ -135,18 +149,21 @@ typedef struct {
                                    v = 256 hi + lo, lo = low byte of v     */
     int chunk_images;           /* images per workspace chunk                          */
     int n_chunks;
+    int lanes;                  /* chunk pipelines actually used (<= n_chunks)          */
+    size_t lane_bytes;          /* workspace bytes per lane (V + M'' of one chunk)     */
     long long chunk_tiles_pad;  /* tiles per chunk rounded up to m_block               */
     int path;                   /* WINO_PATH_FUSED or WINO_PATH_STAGED (AUTO resolved)  */
     int stages;                 /* kernels per chunk: 2 (fused) or 3 (staged)          */
     int algorithm;              /* WINO_ALG_F4X4 or WINO_ALG_F2X2                      */
     int tile;                   /* output tile edge: 4 (F4x4) or 2 (F2x2)             */
     int positions;              /* Winograd positions = codes per c_out: 36 or 16     */
-    size_t v_offset, v_bytes;   /* V  = B^T d B operand planes inside the workspace    */
+    size_t v_offset, v_bytes;   /* V  = B^T d B operand planes inside the workspace (lane 0;
+                                   lane k at + k * lane_bytes; chunk c on lane c % lanes) */
     size_t m_offset, m_bytes;   /* M'' = 36 int32 per (tile, cout) after Karatsuba and
                                    reverse scaling; swizzled tiles; staged
                                    path only (m_bytes = 0 on the fused path)           */
-    size_t workspace_bytes;     /* V (+ M'') of one chunk + a 256-byte status block
-                                   (the code-validation flag)                          */
+    size_t workspace_bytes;     /* lanes x lane_bytes + a 256-byte status block (the
+                                   code-validation flag)                               */
     size_t filter_bytes;        /* transformed-filter buffer (w_wino)                  */
     size_t codes_bytes;         /* c_out * positions bytes (36 F4x4, 16 F2x2)         */
     size_t x_bytes, y_bytes;    /* input / output tensor sizes in bytes                */

@@ -6,7 +6,7 @@ the C ABI of include/wino.h); this package is a thin binding.  Importing it
 does not load the library; the first call does, and raises if it is missing.
 """
 from . import _lib  # noqa: F401
-from ._lib import (WINO_NCHW, WINO_NHWC, WINO_OUT_INT8, WINO_OUT_INT32, WINO_PATH_FUSED, WINO_PATH_STAGED, WINO_PATH_AUTO,  # noqa: F401
+from ._lib import (WINO_NCHW, WINO_NHWC, WINO_OUT_INT8, WINO_OUT_INT32, WINO_OUT_INT8_POOL2, WINO_PATH_FUSED, WINO_PATH_STAGED, WINO_PATH_AUTO,  # noqa: F401
                    WINO_ALG_F4X4, WINO_ALG_F2X2, WINO_IN_INT8, WINO_IN_UINT8,
                    WinoError,
                    wino_conv_desc, wino_plan, wino_plan_destroy, wino_plan_query, wino_transform_filter,

@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(HERE, "libwino.so")
 WINO_OK, WINO_ERR_INVALID_ARG, WINO_ERR_UNSUPPORTED, WINO_ERR_SHAPE = 0, -1, -2, -3
 WINO_ERR_RANGE, WINO_ERR_CUDA, WINO_ERR_NOMEM = -4, -5, -6
 WINO_NCHW, WINO_NHWC = 0, 1
-WINO_OUT_INT8, WINO_OUT_INT32 = 0, 1
+WINO_OUT_INT8, WINO_OUT_INT32, WINO_OUT_INT8_POOL2 = 0, 1, 2
 WINO_PATH_AUTO, WINO_PATH_FUSED, WINO_PATH_STAGED = 0, 1, 2
 WINO_ALG_F4X4, WINO_ALG_F2X2 = 0, 1
 WINO_IN_INT8, WINO_IN_UINT8 = 0, 1
@@ -30,7 +30,8 @@ class wino_conv_desc(ctypes.Structure):
                 ("c_out", ctypes.c_int), ("pad", ctypes.c_int), ("layout", ctypes.c_int),
                 ("filter_scaling", ctypes.c_int), ("filter_target_max", ctypes.c_int), ("out_mode", ctypes.c_int),
                 ("workspace_mb", ctypes.c_int), ("path", ctypes.c_int), ("algorithm", ctypes.c_int),
-                ("input_type", ctypes.c_int), ("x_zero_point", ctypes.c_int), ("w_zero_point", ctypes.c_int)]
+                ("input_type", ctypes.c_int), ("x_zero_point", ctypes.c_int), ("w_zero_point", ctypes.c_int),
+                ("lanes", ctypes.c_int)]
 
 
 class wino_plan_info(ctypes.Structure):
@@ -38,6 +39,7 @@ class wino_plan_info(ctypes.Structure):
                 ("tiles", ctypes.c_longlong), ("cin_pad", ctypes.c_int), ("cout_pad", ctypes.c_int),
                 ("n_block", ctypes.c_int), ("m_block", ctypes.c_int), ("planes", ctypes.c_int),
                 ("pieces", ctypes.c_int), ("chunk_images", ctypes.c_int), ("n_chunks", ctypes.c_int),
+                ("lanes", ctypes.c_int), ("lane_bytes", ctypes.c_size_t),
                 ("chunk_tiles_pad", ctypes.c_longlong), ("path", ctypes.c_int), ("stages", ctypes.c_int),
                 ("algorithm", ctypes.c_int), ("tile", ctypes.c_int), ("positions", ctypes.c_int),
                 ("v_offset", ctypes.c_size_t), ("v_bytes", ctypes.c_size_t),

@@ -17,13 +17,14 @@ class WinoConv2d:
     def __init__(self, n, h, w, c_in, c_out, pad=1, layout=L.WINO_NHWC, filter_scaling=True,
                  out_mode=L.WINO_OUT_INT8, device=None, workspace=None, workspace_mb=0, path=L.WINO_PATH_AUTO,
                  algorithm=L.WINO_ALG_F4X4, input_type=L.WINO_IN_INT8, x_zero_point=0, w_zero_point=0,
-                 filter_target_max=255):
+                 filter_target_max=255, lanes=0):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device)
         # filter_target_max: 255 = the paper's two-piece W'; 127 = int8-native single-piece W' (f3, A29)
         self.desc = L.wino_conv_desc(n, h, w, c_in, c_out, pad, layout, int(bool(filter_scaling)), filter_target_max,
-                                     out_mode, workspace_mb, path, algorithm, input_type, x_zero_point, w_zero_point)
+                                     out_mode, workspace_mb, path, algorithm, input_type, x_zero_point, w_zero_point,
+                                     lanes)
         self.in_dtype = torch.uint8 if input_type == L.WINO_IN_UINT8 else torch.int8
         self.plan = L.wino_plan(self.desc, device)
         self.info = L.wino_plan_query(self.plan)
@@ -31,8 +32,10 @@ class WinoConv2d:
         ho, wo = self.info.ho, self.info.wo
         self.x_shape = (n, c_in, h, w) if layout == L.WINO_NCHW else (n, h, w, c_in)
         self.y_shape = (n, c_out, ho, wo) if layout == L.WINO_NCHW else (n, ho, wo, c_out)
+        if out_mode == L.WINO_OUT_INT8_POOL2:   # the 2x2/2 max pool fused into the output stage (NHWC)
+            self.y_shape = (n, ho // 2, wo // 2, c_out)
         self.w_shape = (c_out, c_in, 3, 3) if layout == L.WINO_NCHW else (c_out, 3, 3, c_in)
-        self.y_dtype = torch.int8 if out_mode == L.WINO_OUT_INT8 else torch.int32
+        self.y_dtype = torch.int32 if out_mode == L.WINO_OUT_INT32 else torch.int8
         self.w_wino = torch.empty(self.info.filter_bytes, dtype=torch.int8, device=self.device)
         self.codes = torch.empty((c_out, self.info.positions), dtype=torch.uint8, device=self.device)
         if workspace is not None:   # caller-shared scratch (e.g. one buffer for a layer stack)

@@ -325,6 +325,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
       // ------------------------------------------------ MMA issuer
       const uint32_t id16 = idesc_i8(kMBlock, 16, 1, 1), id32 = idesc_i8(kMBlock, 32, 1, 1),
                      id64 = idesc_i8(kMBlock, 64, 1, 1);
+      // lo pieces of V are u8 (v = 256 hi + lo, lo = v & 255; K2F, layout.cuh): unsigned A operand
+      const uint32_t id16u = idesc_i8(kMBlock, 16, 0, 1), id32u = idesc_i8(kMBlock, 32, 0, 1),
+                     id64u = idesc_i8(kMBlock, 64, 0, 1);
       int it = 0, sgc = 0;
       if constexpr (MG == 3) {
         constexpr uint32_t kSB = kFStages * kFStageBytes / 2, kSV = 65536;
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
                       const uint64_t al = umma_desc(va + (2 * kk + 1) * kVBlockBytes, 128, 256);
                       const uint64_t bb = umma_desc(wa + kk * 1024, 128, 256);
                       umma_i8(d, ah, bb, id32, 1u);
-                      umma_i8(d + 16, al, bb, id32, 1u);
+                      umma_i8(d + 16, al, bb, id32u, 1u);
                     }
                   }
                 } else {
@@ -363,9 +366,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     const uint32_t bw = st + kSV + kk * 4096;
                     const uint64_t b0 = umma_desc(bw, 128, 256), b1 = umma_desc(bw + 2048, 128, 256);
                     umma_i8(d0, rh, b0, id64, 1u);
-                    umma_i8(d0 + 32, rl, b0, id64, 1u);
+                    umma_i8(d0 + 32, rl, b0, id64u, 1u);
                     umma_i8(d0, ih, b1, id64, 1u);
-                    umma_i8(d0 + 32, il, b1, id64, 1u);
+                    umma_i8(d0 + 32, il, b1, id64u, 1u);
                   }
                 }
                 umma_commit(empty0 + 8 * s);   // stage reusable once these MMAs have read it
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     const uint64_t al = umma_desc(va + (2 * kk + 1) * kVBlockBytes, 128, 256);
                     const uint64_t bb = umma_desc(wa + kk * 1024, 128, 256);
                     umma_i8(d, ah, bb, id32, 1u);                             // [s16 | s8] += hi . [W hi | W lo]
-                    umma_i8(d + 16, al, bb, id32, 1u);                        // [s8 | s0]  += lo . [W hi | W lo]
+                    umma_i8(d + 16, al, bb, id32u, 1u);                        // [s8 | s0]  += lo . [W hi | W lo]
                   }
                 }
               } else {         // complex group: all K steps in the stage
@@ -416,9 +419,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
                   const uint32_t bw = st + kMgStageV + kk * 4096;
                   const uint64_t b0 = umma_desc(bw, 128, 256), b1 = umma_desc(bw + 2048, 128, 256);
                   umma_i8(d0, rh, b0, id64, 1u);        // [Re16 Im16 Re8 Im8] += Vr hi . B0
-                  umma_i8(d0 + 32, rl, b0, id64, 1u);   // [Re8 Im8 Re0 Im0]   += Vr lo . B0
+                  umma_i8(d0 + 32, rl, b0, id64u, 1u);   // [Re8 Im8 Re0 Im0]   += Vr lo . B0
                   umma_i8(d0, ih, b1, id64, 1u);
-                  umma_i8(d0 + 32, il, b1, id64, 1u);
+                  umma_i8(d0 + 32, il, b1, id64u, 1u);
                 }
               }
               umma_commit(tfull0 + 8 * b);    // slot complete (and stage s free, see the producer)
@@ -457,10 +460,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     const uint64_t bb = umma_desc(bw, 128, 256), bl = umma_desc(bw + 512, 128, 256);
                     umma_i8(d, ah, bb, id32, first ? 0u : 1u);                // [s16 | s8]
                     if (first) {
-                      umma_i8(d + 32, al, bl, id16, 0u);                      // s0
-                      umma_i8(d + 16, al, bb, id16, 1u);                      // s8 += lo.hi
+                      umma_i8(d + 32, al, bl, id16u, 0u);                      // s0
+                      umma_i8(d + 16, al, bb, id16u, 1u);                      // s8 += lo.hi
                     } else {
-                      umma_i8(d + 16, al, bb, id32, 1u);                      // [s8 | s0]
+                      umma_i8(d + 16, al, bb, id32u, 1u);                      // [s8 | s0]
                     }
                   } else {
                     const uint32_t a0 = st + (4 * kk) * kVBlockBytes;
@@ -472,13 +475,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     const uint64_t b1 = umma_desc(bw + 2048, 128, 256);
                     umma_i8(d, rh, b0, id64, first ? 0u : 1u);                // [Re16 Im16 Re8 Im8]
                     if (first) {
-                      umma_i8(d + 64, rl, b0l, id32, 0u);                     // [Re0 Im0]
-                      umma_i8(d + 32, rl, b0, id32, 1u);                      // [Re8 Im8] += lo.hi
+                      umma_i8(d + 64, rl, b0l, id32u, 0u);                     // [Re0 Im0]
+                      umma_i8(d + 32, rl, b0, id32u, 1u);                      // [Re8 Im8] += lo.hi
                     } else {
-                      umma_i8(d + 32, rl, b0, id64, 1u);                      // [Re8 Im8 Re0 Im0]
+                      umma_i8(d + 32, rl, b0, id64u, 1u);                      // [Re8 Im8 Re0 Im0]
                     }
                     umma_i8(d, ih, b1, id64, 1u);
-                    umma_i8(d + 32, il, b1, id64, 1u);
+                    umma_i8(d + 32, il, b1, id64u, 1u);
                   }
                 }
               }
@@ -580,6 +583,20 @@ __global__ void __launch_bounds__(kFThreads, 1)
     bool pending = false;
     int pend_tb = 0, pend_nb = 0;
     auto store_staged = [&](int tb_i, int nb) {
+      if (g.pool2) {   // fused 2x2/2 max pool: staged as [pooled px 4][tile][16 couts], one chunk per thread
+        const int rr = etid & (kMBlock - 1), ppx = etid >> 7;
+        const int tt = tb_i * kMBlock + rr;
+        if (tt < imgs * g.tpi) {
+          const int ti = fdiv(tt, g.dv_tpi), rem = tt - ti * g.tpi, ty = fdiv(rem, g.dv_tw);
+          const int pho = g.ho >> 1, pwo = g.wo >> 1;
+          const int py = 2 * ty + (ppx >> 1), px = 2 * (rem - ty * g.tw) + (ppx & 1);
+          if (py < pho && px < pwo) {
+            int8_t* dst = static_cast<int8_t*>(y) + (((long long)(n0 + ti) * pho + py) * pwo + px) * g.cout + nb * kFN;
+            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(part + etid * 16);
+          }
+        }
+        return;
+      }
       // chunk ch = etid + q * 512: tile rr = etid % 128 for every q (512 = 4 x 128), pixel px = ch / 128
       const int rr = etid & (kMBlock - 1);
       const int tt = tb_i * kMBlock + rr;
@@ -843,10 +860,28 @@ __global__ void __launch_bounds__(kFThreads, 1)
             }
           }
         };
-        emit_row(0, Y0);
-        emit_row(1, Y1);
-        emit_row(2, Y2);
-        emit_row(3, Y3);
+        if (stage8 && g.pool2) {   // int8 words of the 4 x 4 block, then the 2 x 2 pooled block (signed byte max)
+          auto word = [&](const int32_t (&Yi)[4][4], int j) -> uint32_t {
+            return RQFAST ? pack_sat4(outv_unclamped(Yi[j][0]), outv_unclamped(Yi[j][1]), outv_unclamped(Yi[j][2]),
+                                      outv_unclamped(Yi[j][3]))
+                          : __byte_perm(__byte_perm((uint32_t)outv(Yi[j][0]), (uint32_t)outv(Yi[j][1]), 0x0040),
+                                        __byte_perm((uint32_t)outv(Yi[j][2]), (uint32_t)outv(Yi[j][3]), 0x0040), 0x5410);
+          };
+#pragma unroll
+          for (int pj = 0; pj < 2; pj++) {
+            const uint32_t top = __vmaxs4(__vmaxs4(word(Y0, 2 * pj), word(Y0, 2 * pj + 1)),
+                                          __vmaxs4(word(Y1, 2 * pj), word(Y1, 2 * pj + 1)));
+            const uint32_t bot = __vmaxs4(__vmaxs4(word(Y2, 2 * pj), word(Y2, 2 * pj + 1)),
+                                          __vmaxs4(word(Y3, 2 * pj), word(Y3, 2 * pj + 1)));
+            *reinterpret_cast<uint32_t*>(part + ((0 * 2 + pj) * kMBlock + row) * 16 + cw * kFC) = top;
+            *reinterpret_cast<uint32_t*>(part + ((1 * 2 + pj) * kMBlock + row) * 16 + cw * kFC) = bot;
+          }
+        } else {
+          emit_row(0, Y0);
+          emit_row(1, Y1);
+          emit_row(2, Y2);
+          emit_row(3, Y3);
+        }
         if (warp == 0 && lane == 0) FTRACE(uc * 8 + 3, 3);
         fepi_barrier();                                // staging complete; etab of the next unit visible
         if (warp == 0 && lane == 0) FTRACE(uc * 8 + 4, 3);

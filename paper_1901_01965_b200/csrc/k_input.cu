@@ -231,13 +231,12 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
   }
 }
 
-// ---- fused-path V image (layout.cuh "fused-path operand layouts"): per group, balanced s8 pieces
-// hi = (v + 128) >> 8 (byte 1 of v + 128), lo = v - 256 hi (byte 0 of v), stored for both channels.
+// ---- fused-path V image (layout.cuh "fused-path operand layouts"): per group, pieces hi = v >> 8 (s8,
+// byte 1 of v) and lo = v & 255 (u8, byte 0 of v; the fused GEMM reads lo as an unsigned A operand),
+// stored for both channels.  (NCHW and uint8 input; NHWC int8 runs k_input4.cu.)
 __device__ __forceinline__ void st_bal(int8_t* p_hi, int v0, int v1) {
-  // one biased value per channel: the +128 folds into the add that forms v; byte 0 of v + 128 = lo ^ 0x80
-  const uint32_t w0 = (uint32_t)(v0 + 128), w1 = (uint32_t)(v1 + 128);
-  st16(p_hi, __byte_perm(w0, w1, 0x0051));                      // [hi0, hi1]
-  st16(p_hi + 4096, __byte_perm(w0, w1, 0x0040) ^ 0x8080u);     // [lo0, lo1]
+  st16(p_hi, __byte_perm((uint32_t)v0, (uint32_t)v1, 0x0051));          // [hi0, hi1]
+  st16(p_hi + 4096, __byte_perm((uint32_t)v0, (uint32_t)v1, 0x0040));   // [lo0, lo1]
 }
 
 // KS: g.ksteps as a compile-time constant (1, 2, 4, 8, 16; 0 = runtime), so that every piece's store

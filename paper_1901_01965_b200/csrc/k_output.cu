@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) k_output_transform(Geom g, const int32_t*
 // (4 couts share one 16-byte chunk of an M'' tile row, layout.cuh), 16 threads cover a tile row of
 // 64 couts (256 contiguous bytes).  Requires cout % 4 == 0.
 constexpr int kOut4Quads = 16, kOut4Tiles = 16;   // 256 threads: 16 tiles x 64 couts
-template <bool NHWC, bool OUT8, bool RQFAST>
+template <bool NHWC, bool OUT8, bool RQFAST, bool POOL = false>
 __global__ void __launch_bounds__(256, 2) k_output_transform4(Geom g, const int32_t* __restrict__ M, int n0, int imgs,
                                                            int32_t rq_mult, int rq_shift, void* __restrict__ y) {
   const int tl = threadIdx.x / kOut4Quads, ql = threadIdx.x % kOut4Quads;
@@ -186,6 +186,29 @@ __global__ void __launch_bounds__(256, 2) k_output_transform4(Geom g, const int3
       out[c][2][j] = (uint32_t)requant(Z[1][j] + Z[2][j] - 2 * zr[j]);
       out[c][3][j] = (uint32_t)requant(Z[1][j] - Z[2][j] + Z[3][j] + 2 * zi[j]);
     }
+  }
+  if constexpr (POOL) {   // NHWC int8 with the fused 2x2/2 max pool (g.pool2): the tile's 2x2 pooled block
+    const int pho = g.ho >> 1, pwo = g.wo >> 1;
+#pragma unroll
+    for (int pi = 0; pi < 2; pi++) {
+      const int py = 2 * ty + pi;
+      if (py >= pho) break;
+#pragma unroll
+      for (int pj = 0; pj < 2; pj++) {
+        const int px = 2 * tx + pj;
+        if (px >= pwo) break;
+        uint32_t word = 0;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          const int m = max(max((int)out[c][2 * pi][2 * pj], (int)out[c][2 * pi][2 * pj + 1]),
+                            max((int)out[c][2 * pi + 1][2 * pj], (int)out[c][2 * pi + 1][2 * pj + 1]));
+          word |= ((uint32_t)m & 0xffu) << (8 * c);
+        }
+        *reinterpret_cast<uint32_t*>(static_cast<int8_t*>(y) + (((long long)img * pho + py) * pwo + px) * g.cout +
+                                     co0) = word;
+      }
+    }
+    return;
   }
 #pragma unroll
   for (int i = 0; i < 4; i++) {
@@ -290,6 +313,13 @@ cudaError_t launch_output_transform(const Geom& g, const int32_t* m, int n0, int
   if (nhwc && (g.cout & 3) == 0) {   // vectorised variant (NHWC; NCHW keeps one cout per thread)
     dim3 grid4((unsigned)((tiles + kOut4Tiles - 1) / kOut4Tiles), (unsigned)((g.cout + 63) / 64));
 #define WINO_K4V(B, C) e = launch_pdl_co(k_output_transform4<true, B, C>, grid4, dim3(256), 0, st, kCarveL1, g, m, n0, imgs, rq_mult, rq_shift, y)
+    if (g.pool2) {
+      if (fast) e = launch_pdl_co(k_output_transform4<true, true, true, true>, grid4, dim3(256), 0, st, kCarveL1, g, m,
+                                  n0, imgs, rq_mult, rq_shift, y);
+      else e = launch_pdl_co(k_output_transform4<true, true, false, true>, grid4, dim3(256), 0, st, kCarveL1, g, m, n0,
+                             imgs, rq_mult, rq_shift, y);
+      return e;
+    }
     if (!out8) WINO_K4V(false, false);
     else if (fast) WINO_K4V(true, true);
     else WINO_K4V(true, false);

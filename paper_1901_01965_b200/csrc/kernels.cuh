@@ -70,6 +70,8 @@ cudaError_t setup_input_transform();
 cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st);
 //   fused-path V image (group layout, balanced pieces; layout.cuh)
 cudaError_t launch_input_transform_f(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st);
+// NHWC int8 input, 4 channels per thread in 16-bit SWAR lanes (k_input4.cu); same V image as the above
+cudaError_t launch_input_transform_f4(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st);
 
 // K3: 46 Winograd-domain int8 GEMMs on tcgen05 + Karatsuba + reverse scaling -> M'' (k_gemm.cu)
 cudaError_t setup_gemm();

@@ -47,6 +47,7 @@ constexpr int kPieces = 2;
 constexpr int kSlots = 36;    // M'' values per (tile, cout)
 constexpr int kMBlock = 128;   // GEMM M (tiles per CTA) = TMEM lanes
 constexpr int kKStep = 32;     // int8 MMA K
+constexpr int kMaxLanes = 8;   // concurrent chunk pipelines of one conv call (wino_conv_desc.lanes)
 
 // Division by a plan constant d >= 1 for 0 <= n < 2^31 without the ~25-instruction integer divide:
 // q = (n m) >> (31 + s), s = ceil(log2 d), m = ceil(2^(31+s) / d) < 2^32.  Exact: with m d = 2^(31+s) + e,
@@ -70,7 +71,8 @@ struct Geom {
   int ho, wo, th, tw, tpi;     // output size, tiles per row/col, tiles per image
   FastDiv dv_tw, dv_tpi;       // divisions by tw and tpi (tile decode in K2)
   int cin_pad, cout_pad, nblk, ksteps;
-  int scaling, target, out_mode;
+  int scaling, target, out_mode;   // out_mode: WINO_OUT_INT8 or WINO_OUT_INT32 (the pooled mode maps to INT8)
+  int pool2;                   // 2x2/2 max pool of the int8 output fused into the output stage (NHWC)
   int path;                    // WINO_PATH_FUSED (0) or WINO_PATH_STAGED (1)
   int alg;                     // WINO_ALG_F4X4 (0) or WINO_ALG_F2X2 (1)
   int tile;                    // output tile edge (4 or 2)

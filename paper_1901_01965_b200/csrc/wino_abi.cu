@@ -23,6 +23,22 @@ struct wino_plan_s {
   // checked by wino_validate_codes); the only mutable state of a plan, guarded by `mu`
   std::mutex mu;
   std::vector<const uint8_t*> valid_codes;
+  // chunk pipelines (wino_conv_desc.lanes): chunk c runs on lane c % lanes with its own V (+ M'') buffer
+  // at workspace + lane * lane_bytes; lane 0 is the caller's stream, lanes 1.. are the plan's own streams,
+  // forked from and joined back into the caller's stream with events (graph-capture safe)
+  int lanes = 1;
+  size_t lane_bytes = 0;
+  std::mutex lane_mu;
+  bool lane_init = false;
+  cudaStream_t aux[wino::kMaxLanes] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[wino::kMaxLanes] = {};
+  ~wino_plan_s() {
+    for (int i = 0; i < wino::kMaxLanes; i++) {
+      if (aux[i]) cudaStreamDestroy(aux[i]);
+      if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+  }
 };
 
 namespace {
@@ -65,6 +81,12 @@ wino_status check_device(const wino_plan_s* p) {
 }
 
 long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
+
+// WINO_K2F_LEGACY=1: the two-channel K2F for NHWC int8 as well (A/B experiments)
+bool k2f_legacy() {
+  static const bool v = [] { const char* e = std::getenv("WINO_K2F_LEGACY"); return e && std::atoi(e) != 0; }();
+  return v;
+}
 
 // WINO_PATH_AUTO's c_in limit for the fused path; WINO_AUTO_FUSED_CIN overrides (experiments)
 int auto_fused_max_cin() {
@@ -145,7 +167,8 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
                   : WINO_PATH_STAGED;
   const wino_conv_desc& d = dr;
   if (d.layout != WINO_NCHW && d.layout != WINO_NHWC) return WINO_ERR_INVALID_ARG;
-  if (d.out_mode != WINO_OUT_INT8 && d.out_mode != WINO_OUT_INT32) return WINO_ERR_INVALID_ARG;
+  if (d.out_mode != WINO_OUT_INT8 && d.out_mode != WINO_OUT_INT32 && d.out_mode != WINO_OUT_INT8_POOL2)
+    return WINO_ERR_INVALID_ARG;
   if (d.filter_scaling != 0 && d.filter_scaling != 1) return WINO_ERR_INVALID_ARG;
   if (d.workspace_mb < 0) return WINO_ERR_INVALID_ARG;
   if (d.path != WINO_PATH_FUSED && d.path != WINO_PATH_STAGED) return WINO_ERR_INVALID_ARG;
@@ -167,6 +190,13 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
                                      d.input_type != WINO_IN_INT8))
     return WINO_ERR_UNSUPPORTED;
   if (d.c_out > 2048 || (long long)d.n * d.h * d.w > (1ll << 40)) return WINO_ERR_UNSUPPORTED;
+  if (d.lanes < 0 || d.lanes > wino::kMaxLanes) return WINO_ERR_INVALID_ARG;
+  // int8 output with the 2x2/2 max pool fused into the output stage (the VGG stack's pools, A22): NHWC,
+  // complex F(4x4); fused path with c_out % 16 == 0, staged path with c_out % 4 == 0
+  if (d.out_mode == WINO_OUT_INT8_POOL2 &&
+      (d.layout != WINO_NHWC || d.algorithm != WINO_ALG_F4X4 || d.h + 2 * d.pad - 2 < 2 || d.w + 2 * d.pad - 2 < 2 ||
+       (d.c_out % (d.path == WINO_PATH_FUSED ? 16 : 4)) != 0))
+    return WINO_ERR_UNSUPPORTED;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess) return WINO_ERR_CUDA;
   if (device < 0 || device >= ndev) return WINO_ERR_INVALID_ARG;
@@ -207,7 +237,8 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.ksteps = g.cin_pad / wino::kKStep;
   g.scaling = d.filter_scaling;
   g.target = d.filter_target_max;
-  g.out_mode = d.out_mode;
+  g.pool2 = d.out_mode == WINO_OUT_INT8_POOL2;
+  g.out_mode = g.pool2 ? WINO_OUT_INT8 : d.out_mode;   // the kernels requantise to int8 either way
   // batch chunk: V (+ M on the staged path) of one chunk within the budget
   const size_t m_per_tile = d.path == WINO_PATH_STAGED ? (size_t)g.npos * 4 * (size_t)g.cout_pad : 0;
   const bool fused_f4 = d.path == WINO_PATH_FUSED && d.algorithm == WINO_ALG_F4X4;
@@ -222,12 +253,15 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   p->v_bytes = v_per_tile_ch * g.chunk_tiles_pad * g.cin_pad;
   p->m_bytes = d.path == WINO_PATH_STAGED ? (size_t)g.npos * g.chunk_tiles_pad * g.cout_pad * 4 : 0;
   // + one 256-byte status block (the code-validation flag of wino_validate_codes)
-  p->status_offset = (size_t)round_up((long long)(p->v_bytes + p->m_bytes), 256);
+  p->lanes = d.lanes > 1 ? (d.lanes < p->n_chunks ? d.lanes : p->n_chunks) : 1;
+  p->lane_bytes = (size_t)round_up((long long)(p->v_bytes + p->m_bytes), 256);
+  p->status_offset = p->lane_bytes * p->lanes;
   p->ws_bytes = p->status_offset + 256;
   // W': 92 B per (cin, cout) staged (46 planes x 2 pieces); 112 B fused (56 rows x 2 couts-halves, layout.cuh)
   p->f_bytes = (size_t)(fused_f4 ? 2 * wino::kWRowUnitsF : (g.w1 ? 1 : 2) * g.planes) * g.cout_pad * g.cin_pad;
   p->x_bytes = (size_t)d.n * d.h * d.w * d.c_in;
-  p->y_bytes = (size_t)d.n * g.ho * g.wo * d.c_out * (d.out_mode == WINO_OUT_INT32 ? 4 : 1);
+  p->y_bytes = g.pool2 ? (size_t)d.n * (g.ho / 2) * (g.wo / 2) * d.c_out
+                       : (size_t)d.n * g.ho * g.wo * d.c_out * (d.out_mode == WINO_OUT_INT32 ? 4 : 1);
   *out = p;
   return WINO_OK;
 }
@@ -250,6 +284,7 @@ wino_status wino_plan_query(wino_plan_t p, wino_plan_info* info) {
   info->algorithm = p->g.alg; info->tile = p->g.tile; info->positions = p->g.npos;
   info->pieces = wino::kPieces;
   info->chunk_images = p->g.chunk_imgs; info->n_chunks = p->n_chunks;
+  info->lanes = p->lanes; info->lane_bytes = p->lane_bytes;
   info->chunk_tiles_pad = p->g.chunk_tiles_pad;
   info->path = p->g.path == 0 ? WINO_PATH_FUSED : WINO_PATH_STAGED;
   info->stages = p->g.path == 0 ? 2 : 3;
@@ -285,11 +320,13 @@ static wino_status run_stage(const wino_plan_s* p, int stage, int chunk, const i
   const int n0 = chunk * g.chunk_imgs;
   const int imgs = p->d.n - n0 < g.chunk_imgs ? p->d.n - n0 : g.chunk_imgs;
   const long long tiles_pad = round_up((long long)imgs * g.tpi, wino::kMBlock);
-  int8_t* vimg = static_cast<int8_t*>(workspace);
-  int32_t* m = reinterpret_cast<int32_t*>(static_cast<int8_t*>(workspace) + p->v_bytes);
+  int8_t* vimg = static_cast<int8_t*>(workspace) + (size_t)(chunk % p->lanes) * p->lane_bytes;
+  int32_t* m = reinterpret_cast<int32_t*>(vimg + p->v_bytes);
   cudaError_t e = cudaErrorInvalidValue;
   if (stage == 2)
-    e = g.path == 0 && g.alg == 0 ? wino::launch_input_transform_f(g, x, n0, imgs, vimg, s)
+    e = g.path == 0 && g.alg == 0 ? (g.layout == WINO_NHWC && !g.in_u8 && !k2f_legacy()
+                                         ? wino::launch_input_transform_f4(g, x, n0, imgs, vimg, s)
+                                         : wino::launch_input_transform_f(g, x, n0, imgs, vimg, s))
                                   : wino::launch_input_transform(g, x, n0, imgs, vimg, s);
   if (g.path == 0) {
     if (stage == 3)
@@ -308,7 +345,7 @@ static wino_status check_conv_args(const wino_plan_s* p, const int8_t* x, const 
                                    int32_t rq_mult, int rq_shift, void* y, void* workspace) {
   if (!p || !x || !w_wino || !codes || !y || !workspace) return WINO_ERR_INVALID_ARG;
   if (!aligned16(x) || !aligned16(w_wino) || !aligned16(y) || !aligned16(workspace)) return WINO_ERR_INVALID_ARG;
-  if (p->d.out_mode == WINO_OUT_INT8 && (rq_mult < 1 || rq_shift < 0 || rq_shift > 62)) return WINO_ERR_RANGE;
+  if (p->g.out_mode == WINO_OUT_INT8 && (rq_mult < 1 || rq_shift < 0 || rq_shift > 62)) return WINO_ERR_RANGE;
   return check_device(p);
 }
 
@@ -322,12 +359,44 @@ wino_status wino_conv2d_int8(wino_plan_t p, const int8_t* x, const void* w_wino,
     if (st != WINO_OK) return st;
   }
   const int last = p->g.path == 0 ? 3 : 4;
-  for (int c = 0; c < p->n_chunks; c++)
+  if (p->lanes <= 1) {
+    for (int c = 0; c < p->n_chunks; c++)
+      for (int stage = 2; stage <= last; stage++) {
+        st = run_stage(p, stage, c, x, w_wino, codes, rq_mult, rq_shift, y, workspace, s);
+        if (st != WINO_OK) return st;
+      }
+    return WINO_OK;
+  }
+  // chunk pipelines: lane k runs chunks k, k + lanes, ... in order on its stream (its V buffer is reused,
+  // each chunk's K2 waits for the lane's previous GEMM through stream order); lanes run concurrently, so
+  // one chunk's input transform overlaps another's GEMM and the launch tails fill in
+  std::lock_guard<std::mutex> lk(p->lane_mu);
+  cudaError_t e = cudaSuccess;
+  if (!p->lane_init) {
+    e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
+    for (int i = 1; i < p->lanes && e == cudaSuccess; i++) {
+      e = cudaStreamCreateWithFlags(&p->aux[i], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_join[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return cuda_status(e);
+    p->lane_init = true;
+  }
+  e = cudaEventRecord(p->ev_fork, s);
+  for (int i = 1; i < p->lanes && e == cudaSuccess; i++) e = cudaStreamWaitEvent(p->aux[i], p->ev_fork, 0);
+  if (e != cudaSuccess) return cuda_status(e);
+  for (int c = 0; c < p->n_chunks; c++) {
+    const int lane = c % p->lanes;
+    cudaStream_t ls = lane == 0 ? s : p->aux[lane];
     for (int stage = 2; stage <= last; stage++) {
-      st = run_stage(p, stage, c, x, w_wino, codes, rq_mult, rq_shift, y, workspace, s);
+      st = run_stage(p, stage, c, x, w_wino, codes, rq_mult, rq_shift, y, workspace, ls);
       if (st != WINO_OK) return st;
     }
-  return WINO_OK;
+  }
+  for (int i = 1; i < p->lanes && e == cudaSuccess; i++) {
+    e = cudaEventRecord(p->ev_join[i], p->aux[i]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, p->ev_join[i], 0);
+  }
+  return cuda_status(e);
 }
 
 wino_status wino_conv2d_int8_stage(wino_plan_t p, int stage, int chunk, const int8_t* x, const void* w_wino,

@@ -107,7 +107,7 @@ def _prefixes(sizes):
 
 
 def decode_v_fused(buf: np.ndarray, tiles: int, ksteps: int, cin: int):
-    """V image [tile_block][group][kstep][piece][4 KB], balanced s8 pieces -> (real [16][T][cin],
+    """V image [tile_block][group][kstep][piece][4 KB], pieces hi (s8) and lo (u8) -> (real [16][T][cin],
     re [10][T][cin], im [10][T][cin]) as hi * 256 + lo."""
     groups = fused_groups()
     pcs = [4 if g[0] == "cpx" else 2 for g in groups]
@@ -119,7 +119,7 @@ def decode_v_fused(buf: np.ndarray, tiles: int, ksteps: int, cin: int):
     b = buf.astype(np.int64)   # int8 buffer: signed pieces
     for gi, (kind, idx) in enumerate(groups):
         base = ((t // 128) * 72 + pre[gi]) * ksteps + (k >> 5) * pcs[gi]
-        val = lambda p: b[(base + p) * 4096 + within] * 256 + b[(base + p + 1) * 4096 + within]
+        val = lambda p: b[(base + p) * 4096 + within] * 256 + (b[(base + p + 1) * 4096 + within] & 255)
         if kind == "real":
             real[idx] = val(0)
         else:

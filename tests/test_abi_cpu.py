@@ -46,7 +46,8 @@ def test_status_strings_and_pre_cuda_validation():
                        (dict(filter_target_max=126, path=2), L.WINO_ERR_UNSUPPORTED),
                        (dict(filter_target_max=127, path=2, filter_scaling=0), L.WINO_ERR_UNSUPPORTED),
                        (dict(filter_target_max=127, path=2, algorithm=1), L.WINO_ERR_UNSUPPORTED),
-                       (dict(filter_target_max=127, path=2, input_type=1), L.WINO_ERR_UNSUPPORTED)]:
+                       (dict(filter_target_max=127, path=2, input_type=1), L.WINO_ERR_UNSUPPORTED),
+                       (dict(lanes=9), L.WINO_ERR_INVALID_ARG), (dict(lanes=-1), L.WINO_ERR_INVALID_ARG)]:
         d = dict(base); d.update(kw)
         with pytest.raises(L.WinoError) as e:
             L.wino_plan(L.wino_conv_desc(**d), 0)

@@ -248,6 +248,50 @@ def test_invalid_scale_code_is_range_at_the_boundary():
             assert e.value.status == L.WINO_ERR_RANGE, v
 
 
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("lanes", [2, 3])
+def test_chunk_lanes_match_the_oracle(path, lanes):
+    """wino_conv_desc.lanes: chunks on concurrent streams with their own V (+ M'') buffers give the oracle's
+    result, eagerly and inside a captured CUDA graph (the fork/join is captured)."""
+    W = _wino()
+    rng = np.random.default_rng(50 + lanes)
+    x, w = synth.random_layer(rng, 13, 30, 26, 64, 48, O.NHWC)
+    conv = W.WinoConv2d(13, 30, 26, 64, 48, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=path, workspace_mb=1,
+                        lanes=lanes)
+    assert conv.info.n_chunks >= 2 and conv.info.lanes == min(lanes, conv.info.n_chunks)
+    conv.transform_filter(torch.from_numpy(w).cuda())
+    xd = torch.from_numpy(x).cuda()
+    ref = O.wino_conv(x, w, 1, O.NHWC, True).out32
+    np.testing.assert_array_equal(conv(xd).cpu().numpy(), ref)
+    y = torch.zeros(conv.y_shape, dtype=torch.int32, device="cuda")
+    st = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(g, stream=st):
+            conv(xd, y=y, stream=st)
+    g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("shape", [(2, 16, 24, 32, 48), (1, 14, 10, 64, 16), (3, 28, 28, 40, 64), (1, 9, 7, 8, 32)])
+def test_fused_pool_output_mode(path, shape):
+    """WINO_OUT_INT8_POOL2 (the VGG stack's 2x2/2 max pool fused into the output stage) equals the oracle's
+    requantised output followed by its max pool, incl. odd / non-multiple-of-4 maps (floor)."""
+    W = _wino()
+    n, h, w_, ci, co = shape
+    rng = np.random.default_rng(sum(shape))
+    x, w = synth.random_layer(rng, n, h, w_, ci, co, O.NHWC)
+    conv = W.WinoConv2d(n, h, w_, ci, co, 1, W.WINO_NHWC, True, W.WINO_OUT_INT8_POOL2, path=path, lanes=2,
+                        workspace_mb=1)
+    conv.transform_filter(torch.from_numpy(w).cuda())
+    y = conv(torch.from_numpy(x).cuda(), 1, 9).cpu().numpy()
+    ref = O.maxpool2(O.wino_conv(x, w, 1, O.NHWC, True, M0=1, S=9).y8, O.NHWC)
+    assert y.shape == ref.shape
+    np.testing.assert_array_equal(y, ref)
+
+
 def test_check_codes_and_maxpool():
     W = _wino()
     conv = W.WinoConv2d(1, 8, 8, 4, 4, 1, W.WINO_NHWC, True, W.WINO_OUT_INT8)
@@ -317,8 +361,12 @@ def test_vgg16_stack_full_size_sampled(path):
     st = ConvStack(x.shape[0], cfg.layers, cfg.pools_after, shifts, path=path)
     if path == 0:
         assert [c.info.path for c in st.convs] == [FUSED] * 8 + [STAGED] * 5
-    st.transform_filters([torch.from_numpy(w).cuda() for w in ws])
-    st(torch.from_numpy(x).cuda())
+    wd = [torch.from_numpy(w).cuda() for w in ws]
+    if path == 0:     # as bench.py runs it: filter transforms forked onto a side stream (ConvStack.step)
+        st.step(torch.from_numpy(x).cuda(), wd)
+    else:
+        st.transform_filters(wd)
+        st(torch.from_numpy(x).cuda())
     torch.cuda.synchronize()
     for img in (0, x.shape[0] - 1):
         ref = _oracle_stack(x[img:img + 1], ws, shifts, set(cfg.pools_after))

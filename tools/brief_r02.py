@@ -1,7 +1,10 @@
 """One line per bench JSON: value, ms/step, per-kernel us, roofline frac, self-check.
     python tools/brief_r02.py <bench json files>"""
 import json
+import signal
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 
 for f in sys.argv[1:]:
     try:
