@@ -331,28 +331,41 @@ def _trials(run, per_step_s, job_ops, dist, streams, dev, n_trials=5, min_s=0.1)
             "max_tops": round(float(np.max(vals)), 3)}
 
 
-def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps):
-    """Average device duration of each kernel type: for each kernel, a CUDA graph of `reps`
-    back-to-back launches of that kernel alone (input/output slots rotated, chunks cycled), timed with
-    CUDA events on the launching stream; duration = elapsed / reps (median of 3)."""
+def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps, lanes=1):
+    """Average device duration of each kernel type: for each kernel, a CUDA graph of `reps` launches of
+    that kernel alone (input/output slots rotated, chunks cycled), spread round-robin over `lanes` streams
+    forked from `stream` as the timed run overlaps them (1 = back to back on one stream), timed with CUDA
+    events on `stream`; duration = elapsed / reps (median of 3)."""
     import torch
     from paper_1901_01965_b200 import _lib as L
     info = conv.info
-    sp = stream.cuda_stream
     names = {1: "k1_filter", 2: "k2_input", 3: "k3_gemm", 4: "k4_output"} if info.path == L.WINO_PATH_STAGED \
         else {1: "k1_filter", 2: "k2_input", 3: "k3_fused"}
     w_wino, codes, wsp = conv.w_wino.data_ptr(), conv.codes.data_ptr(), conv.workspace.data_ptr()
+    lanes = max(1, min(lanes, info.lanes if info.lanes > 1 else lanes))
+    aux = [stream] + [torch.cuda.Stream(device=stream.device) for _ in range(lanes - 1)]
     out = {}
     for st in sorted(names):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
+            fork = torch.cuda.Event()
+            fork.record(stream)
+            for a in aux[1:]:
+                a.wait_event(fork)
             for r in range(reps):
                 j, c = r % n_sets, r % info.n_chunks
+                # a chunk's V buffer belongs to lane c % info.lanes: keep chunks of one buffer on one stream
+                sp = aux[(c if info.lanes > 1 else r) % lanes].cuda_stream
                 if st == 1:
+                    sp = aux[r % lanes].cuda_stream
                     L.wino_transform_filter(conv.plan, ws[j].data_ptr(), w_wino, codes, sp)
                 else:
                     L.wino_conv2d_int8_stage(conv.plan, st, c, xs[j].data_ptr(), w_wino, codes, 1, S,
                                              ys[j].data_ptr(), wsp, sp)
+            for a in aux[1:]:
+                e_ = torch.cuda.Event()
+                e_.record(a)
+                stream.wait_event(e_)
         times = []
         with torch.cuda.stream(stream):
             g.replay()
@@ -778,7 +791,8 @@ def run_ours_stack(args):
     # per-layer kernels timed alone on the stack's own buffers (outside the timed region)
     kern_l, cur = [], xs[0]
     for i, c in enumerate(st.convs):
-        kern_l.append(profile_kernels(c, [cur], [wss[0][i]], [st.outs[i]], shifts[i], stream, 1, 10))
+        kern_l.append(profile_kernels(c, [cur], [wss[0][i]], [st.outs[i]], shifts[i], stream, 1,
+                                      max(10, 2 * c.info.n_chunks), lanes=c.info.lanes))
         cur = st.pooled.get(i, st.outs[i])
     t_roof = 0.0
     for l, c in zip(cfg.layers, st.convs):

@@ -286,9 +286,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
               const uint32_t vb = (uint32_t)(ksteps * pcs) * kVBlockBytes, wb = (uint32_t)(ksteps * wu) * 1024;
               const uint32_t st = sbase + s * kMgStageBytes;
               if (elect_one()) {
-                mbar_arrive_expect_tx(full0 + 8 * s, vb + wb);
-                bulk_g2s(st, vg, vb, full0 + 8 * s);
-                bulk_g2s(st + kMgStageV, wg, wb, full0 + 8 * s);
+                if (dbg & 4) {   // debug builds only: no copies (the stage is marked full at once)
+                  mbar_arrive(full0 + 8 * s);
+                } else {
+                  mbar_arrive_expect_tx(full0 + 8 * s, vb + wb);
+                  bulk_g2s(st, vg, vb, full0 + 8 * s);
+                  bulk_g2s(st + kMgStageV, wg, wb, full0 + 8 * s);
+                }
                 if (it < 64) FTRACE(it, 0);
               }
               __syncwarp();
@@ -520,6 +524,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
       return lane_base + b * kFSlotCols;
     };
     auto zero_slot = [&](uint32_t a) {   // MG variants: the columns this warp read, back to zero
+      if (dbg & 16) return;              // debug builds only: no re-zeroing (results wrong; timing)
       if constexpr (MG > 0) {
 #pragma unroll
         for (int blk = 0; blk < 6; blk++) tmem_zero4(a + blk * 16);
@@ -544,13 +549,18 @@ __global__ void __launch_bounds__(kFThreads, 1)
     auto take_real2 = [&](int gi, int32_t (&m0)[4], int32_t (&m1)[4]) {
       const uint32_t a = slot_wait();
       uint32_t h0[4], x0[4], l0[4], h1[4], x1[4], l1[4];
-      tmem_ld4(a, h0);
-      tmem_ld4(a + 16, x0);
-      tmem_ld4(a + 32, l0);
-      tmem_ld4(a + 48, h1);
-      tmem_ld4(a + 64, x1);
-      tmem_ld4(a + 80, l1);
-      tmem_ld_wait();
+      if (dbg & 32) {   // debug builds only: no accumulator loads (results wrong; timing)
+#pragma unroll
+        for (int j = 0; j < 4; j++) { h0[j] = x0[j] = l0[j] = h1[j] = x1[j] = l1[j] = (uint32_t)(a + j); }
+      } else {
+        tmem_ld4(a, h0);
+        tmem_ld4(a + 16, x0);
+        tmem_ld4(a + 32, l0);
+        tmem_ld4(a + 48, h1);
+        tmem_ld4(a + 64, x1);
+        tmem_ld4(a + 80, l1);
+        tmem_ld_wait();
+      }
       zero_slot(a);
       slot_release();
       combine(h0, x0, l0, m0);
@@ -561,13 +571,18 @@ __global__ void __launch_bounds__(kFThreads, 1)
     auto take_cpx = [&](int gi, int32_t (&re)[4], int32_t (&im)[4]) {
       const uint32_t a = slot_wait();
       uint32_t rh[4], ih[4], rx[4], ix[4], rl[4], il[4];
-      tmem_ld4(a, rh);
-      tmem_ld4(a + 16, ih);
-      tmem_ld4(a + 32, rx);
-      tmem_ld4(a + 48, ix);
-      tmem_ld4(a + 64, rl);
-      tmem_ld4(a + 80, il);
-      tmem_ld_wait();
+      if (dbg & 32) {   // debug builds only: no accumulator loads (results wrong; timing)
+#pragma unroll
+        for (int j = 0; j < 4; j++) { rh[j] = ih[j] = rx[j] = ix[j] = rl[j] = il[j] = (uint32_t)(a + j); }
+      } else {
+        tmem_ld4(a, rh);
+        tmem_ld4(a + 16, ih);
+        tmem_ld4(a + 32, rx);
+        tmem_ld4(a + 48, ix);
+        tmem_ld4(a + 64, rl);
+        tmem_ld4(a + 80, il);
+        tmem_ld_wait();
+      }
       zero_slot(a);
       slot_release();
       combine(rh, rx, rl, re);
@@ -904,7 +919,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
 static int g_fused_sms = 0;
 static uint64_t* g_fused_trace = nullptr;
 void set_fused_trace(void* buf) { g_fused_trace = static_cast<uint64_t*>(buf); }
-// WINO_FUSED_DBG env (debug builds with -DWINO_FUSED_DBG only): 2 no MMAs, 8 epilogue handshake only
+// WINO_FUSED_DBG env (debug builds with -DWINO_FUSED_DBG only): 2 no MMAs, 4 no copies (MG > 0), 8 epilogue
+// handshake only
 static int g_fused_dbg = 0;
 // fewest CTAs for the same number of unit rounds (C2: 196 units -> 98 CTAs x 2 instead of 148 + 48): the
 // freed SMs run the other streams' kernels for the whole launch (C2 190.7 -> 203.1, C3 310.7 -> 332.1 TOPS
