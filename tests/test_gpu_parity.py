@@ -292,6 +292,61 @@ def test_fused_pool_output_mode(path, shape):
     np.testing.assert_array_equal(y, ref)
 
 
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("variant", ["i32", "i8_lanes", "pool", "f2", "u8"])
+def test_kernels_write_only_inside_their_buffers(path, variant):
+    """compute-sanitizer is closed on this pool, so out-of-bounds WRITES are caught with canaries: every
+    device buffer the library writes (W', codes, workspace, y) sits inside a larger allocation whose 4 KB
+    guard bands on both sides hold a pattern that must survive K1..K4 unchanged; the result is also the
+    oracle's.  Covers a partial last tile block (3 x 30 x 34 maps), two chunks and lanes."""
+    W = _wino()
+    L = W._lib
+    rng = np.random.default_rng(71)
+    n, h, w_, ci, co = 3, 30, 34, 40, 32
+    x, w = synth.random_layer(rng, n, h, w_, ci, co, O.NHWC)
+    kw = dict(path=path)
+    out_mode = W.WINO_OUT_INT32
+    if variant == "i8_lanes":
+        out_mode, kw["lanes"], kw["workspace_mb"] = W.WINO_OUT_INT8, 2, 1
+    elif variant == "pool":
+        out_mode = W.WINO_OUT_INT8_POOL2
+    elif variant == "f2":
+        kw["algorithm"] = W.WINO_ALG_F2X2
+    elif variant == "u8":
+        kw.update(input_type=W.WINO_IN_UINT8, x_zero_point=128, w_zero_point=128)
+    conv = W.WinoConv2d(n, h, w_, ci, co, 1, W.WINO_NHWC, True, out_mode, **kw)
+    G = 4096
+    def guarded(nbytes):
+        buf = torch.full((nbytes + 2 * G,), 0x5A, dtype=torch.uint8, device="cuda")
+        return buf, buf[G:G + nbytes]
+    i = conv.info
+    wbuf, wwin = guarded(i.filter_bytes)
+    cbuf, cod = guarded(i.codes_bytes)
+    sbuf, wsp = guarded(i.workspace_bytes)
+    ybytes = i.y_bytes
+    ybuf, yv = guarded(ybytes)
+    to_in = (lambda a: (a.astype(np.int16) + 128).astype(np.uint8)) if variant == "u8" else (lambda a: a)
+    xd = torch.from_numpy(np.ascontiguousarray(to_in(x))).cuda()
+    wd = torch.from_numpy(np.ascontiguousarray(to_in(w))).cuda()
+    sp = torch.cuda.current_stream().cuda_stream
+    L.wino_transform_filter(conv.plan, wd.data_ptr(), wwin.data_ptr(), cod.data_ptr(), sp)
+    L.wino_conv2d_int8(conv.plan, xd.data_ptr(), wwin.data_ptr(), cod.data_ptr(), 1, 9, yv.data_ptr(),
+                       wsp.data_ptr(), sp)
+    torch.cuda.synchronize()
+    for buf in (wbuf, cbuf, sbuf, ybuf):
+        assert bool((buf[:G] == 0x5A).all()) and bool((buf[-G:] == 0x5A).all())
+    if variant == "f2":
+        ref = O.wino2_conv(x, w, 1, O.NHWC, True).out32
+    elif variant == "pool":
+        ref = O.maxpool2(O.wino_conv(x, w, 1, O.NHWC, True, M0=1, S=9).y8, O.NHWC)
+    elif variant == "i8_lanes":
+        ref = O.wino_conv(x, w, 1, O.NHWC, True, M0=1, S=9).y8
+    else:
+        ref = O.wino_conv(x, w, 1, O.NHWC, True).out32
+    got = yv.view(torch.int32 if ref.dtype == np.int32 else torch.int8).cpu().numpy().reshape(ref.shape)
+    np.testing.assert_array_equal(got, ref)
+
+
 def test_check_codes_and_maxpool():
     W = _wino()
     conv = W.WinoConv2d(1, 8, 8, 4, 4, 1, W.WINO_NHWC, True, W.WINO_OUT_INT8)
