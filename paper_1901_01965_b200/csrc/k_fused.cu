@@ -83,6 +83,10 @@ __host__ __device__ constexpr int fg_kchunk(int gi) { return fg_complex(gi) ? 2 
 // slot-group sg -> first group and group count
 __device__ __forceinline__ int sg_first(int sg) { return sg < 12 ? (sg / 3) * 5 + (sg % 3) * 2 : 20 + sg - 12; }
 __device__ __forceinline__ int sg_count(int sg) { return (sg < 12 && sg % 3 < 2) ? 2 : 1; }
+// MG = 4 (one K step): V and W' bytes of slot-group sg (a real pair: 2 x 2 pieces, 2 W' units; a complex
+// group: 4 pieces, 4 W' units)
+__device__ __forceinline__ uint32_t sg_vbytes1(int sg) { return 4u * kVBlockBytes; }
+__device__ __forceinline__ uint32_t sg_wbytes1(int sg) { return sg_count(sg) == 2 ? 2048u : 4096u; }
 // position index (r*6 + c) of group gi
 __device__ __forceinline__ int fg_pos(int gi) {
   return fg_complex(gi) ? cpx_pos(fg_primary(gi)) : real_pos(fg_real_plane(gi));
@@ -220,7 +224,37 @@ __global__ void __launch_bounds__(kFThreads, 1)
       // ------------------------------------------------ producers: warp p issues the stages it with it % P == p
       const int pw = warp - kFProducerWarp;
       int it = 0;
-      if constexpr (MG == 3) {
+      if constexpr (MG == 4) {
+        // one K step (c_in <= 32): a 40 KB stage holds TWO consecutive slot-groups (their groups are
+        // contiguous in V and W'), one V and one W' copy per stage, 9 stages per unit instead of 18; the
+        // stage is released by its own commit (empty barrier) after the second slot-group's UMMAs
+        constexpr uint32_t kSV = 32768;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+          const int tb = u / nblocks, nb = u - tb * nblocks;
+          for (int pr = 0; pr < kFSlotGroups / 2; pr++, it++) {
+            if (it % kFProducers != pw) continue;
+            const int s = it % kFStages;
+            mbar_wait(empty0 + 8 * s, ((it / kFStages) & 1) ^ 1);
+            const int g0 = sg_first(2 * pr);
+            const uint32_t vb = sg_vbytes1(2 * pr) + sg_vbytes1(2 * pr + 1);
+            const uint32_t wb = sg_wbytes1(2 * pr) + sg_wbytes1(2 * pr + 1);
+            const int8_t* vg = V + ((long long)tb * kVPiecesF + fg_vprefix(g0)) * kVBlockBytes;
+            const int8_t* wg = W + ((long long)nb * kWRowUnitsF + fg_wprefix(g0)) * 1024;
+            const uint32_t st = sbase + s * kFStageBytes;
+            if (elect_one()) {
+              if (dbg & 4) {   // debug builds only: no copies
+                mbar_arrive(full0 + 8 * s);
+              } else {
+                mbar_arrive_expect_tx(full0 + 8 * s, vb + wb);
+                bulk_g2s(st, vg, vb, full0 + 8 * s);
+                bulk_g2s(st + kSV, wg, wb, full0 + 8 * s);
+              }
+              if (it < 64) FTRACE(it, 0);
+            }
+            __syncwarp();
+          }
+        }
+      } else if constexpr (MG == 3) {
         // two 80 KB stages, each 4 K steps of one slot-group (a pair: both groups' chunks, 2 + 2 copies),
         // released by stage commits as in the general loops
         constexpr uint32_t kSB = kFStages * kFStageBytes / 2, kSV = 65536;
@@ -333,6 +367,54 @@ __global__ void __launch_bounds__(kFThreads, 1)
       const uint32_t id16u = idesc_i8(kMBlock, 16, 0, 1), id32u = idesc_i8(kMBlock, 32, 0, 1),
                      id64u = idesc_i8(kMBlock, 64, 0, 1);
       int it = 0, sgc = 0;
+      if constexpr (MG == 4) {
+        constexpr uint32_t kSV = 32768;
+        const uint64_t D0 = umma_desc(sbase, 128, 256);   // + (offset >> 4): see the MG 1..3 loop below
+        const uint32_t d0lo = (uint32_t)D0, d0hi = (uint32_t)(D0 >> 32);
+        auto dsc = [&](uint32_t off) -> uint64_t { return ((uint64_t)d0hi << 32) | (uint64_t)(d0lo + (off >> 4)); };
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+          for (int pr = 0; pr < kFSlotGroups / 2; pr++, it++) {
+            const int s = it % kFStages;
+            mbar_wait(full0 + 8 * s, (it / kFStages) & 1);
+            tc_fence_after();
+            if (it < 64 && lane == 0) FTRACE(it, 1);
+            uint32_t voff = s * kFStageBytes, woff = s * kFStageBytes + kSV;
+#pragma unroll
+            for (int h = 0; h < 2; h++, sgc++) {
+              const int sg = 2 * pr + h;
+              const int b = sgc % kFSlots;
+              mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
+              tc_fence_after();
+              if (sgc < 32 && lane == 0) FTRACE(64 + sgc, 0);
+              const uint32_t d0 = tmem + b * kFSlotCols;
+              if (elect_one()) {
+                if (dbg & 2) {   // debug builds only: no UMMAs
+                } else if (sg_count(sg) == 2) {   // real pair: group q's pieces at q * 8 KB, W' at q * 1 KB
+#pragma unroll
+                  for (int q = 0; q < 2; ++q) {
+                    const uint64_t bb = dsc(woff + q * 1024);
+                    umma_i8(d0 + q * 48, dsc(voff + (2 * q) * kVBlockBytes), bb, id32, 1u);
+                    umma_i8(d0 + q * 48 + 16, dsc(voff + (2 * q + 1) * kVBlockBytes), bb, id32u, 1u);
+                  }
+                } else {
+                  const uint64_t b0 = dsc(woff), b1 = dsc(woff + 2048);
+                  umma_i8(d0, dsc(voff), b0, id64, 1u);
+                  umma_i8(d0 + 32, dsc(voff + kVBlockBytes), b0, id64u, 1u);
+                  umma_i8(d0, dsc(voff + 2 * kVBlockBytes), b1, id64, 1u);
+                  umma_i8(d0 + 32, dsc(voff + 3 * kVBlockBytes), b1, id64u, 1u);
+                }
+                umma_commit(tfull0 + 8 * b);   // slot complete
+              }
+              __syncwarp();
+              voff += sg_vbytes1(sg);
+              woff += sg_wbytes1(sg);
+            }
+            if (elect_one()) umma_commit(empty0 + 8 * s);   // both slot-groups' UMMAs read: stage free
+            __syncwarp();
+            if (it < 64 && lane == 0) FTRACE(it, 2);
+          }
+        }
+      } else
       if constexpr (MG == 3) {
         constexpr uint32_t kSB = kFStages * kFStageBytes / 2, kSV = 65536;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -386,18 +468,24 @@ __global__ void __launch_bounds__(kFThreads, 1)
       } else if constexpr (MG > 0) {
         constexpr int kMgStages = MG == 2 ? 2 : 4;
         constexpr uint32_t kMgStageBytes = kFStages * kFStageBytes / kMgStages, kMgStageV = MG == 2 ? 65536 : kFStageV;
+        // every operand of this loop is K-major, no swizzle, LBO 128 / SBO 256: its descriptor is the ring
+        // base's plus (offset >> 4) in the 14-bit address field (no carry: shared memory < 256 KB), so each
+        // descriptor costs one uniform add instead of a shift / mask / or chain per UMMA
+        const uint64_t D0 = umma_desc(sbase, 128, 256);
+        const uint32_t d0lo = (uint32_t)D0, d0hi = (uint32_t)(D0 >> 32);
+        auto dsc = [&](uint32_t off) -> uint64_t { return ((uint64_t)d0hi << 32) | (uint64_t)(d0lo + (off >> 4)); };
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
           for (int sg = 0; sg < kFSlotGroups; sg++, sgc++, it++) {   // one stage per slot-group
             const int b = sgc % kFSlots;
             mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
             tc_fence_after();
             if (sgc < 32 && lane == 0) FTRACE(64 + sgc, 0);
-            const int g0 = sg_first(sg), ng = sg_count(sg);
+            const int ng = sg_count(sg);
             const int s = it % kMgStages;
             mbar_wait(full0 + 8 * s, (it / kMgStages) & 1);
             tc_fence_after();
             if (it < 64 && lane == 0) FTRACE(it, 1);
-            const uint32_t st = sbase + s * kMgStageBytes;
+            const uint32_t st = s * kMgStageBytes;   // stage offset from the ring base
             const uint32_t d0 = tmem + b * kFSlotCols;
             if (elect_one()) {
               if (dbg & 2) {   // debug builds only: no UMMAs
@@ -407,25 +495,20 @@ __global__ void __launch_bounds__(kFThreads, 1)
                   const uint32_t va = st + (uint32_t)(q * 2 * ksteps) * kVBlockBytes;
                   const uint32_t wa = st + kMgStageV + (uint32_t)(q * ksteps) * 1024;
                   for (int kk = 0; kk < ksteps; ++kk) {   // slots start at zero: every UMMA accumulates
-                    const uint64_t ah = umma_desc(va + (2 * kk) * kVBlockBytes, 128, 256);
-                    const uint64_t al = umma_desc(va + (2 * kk + 1) * kVBlockBytes, 128, 256);
-                    const uint64_t bb = umma_desc(wa + kk * 1024, 128, 256);
-                    umma_i8(d, ah, bb, id32, 1u);                             // [s16 | s8] += hi . [W hi | W lo]
-                    umma_i8(d + 16, al, bb, id32u, 1u);                        // [s8 | s0]  += lo . [W hi | W lo]
+                    const uint64_t bb = dsc(wa + kk * 1024);
+                    umma_i8(d, dsc(va + (2 * kk) * kVBlockBytes), bb, id32, 1u);        // [s16 | s8] += hi . [W hi | W lo]
+                    umma_i8(d + 16, dsc(va + (2 * kk + 1) * kVBlockBytes), bb, id32u, 1u);   // [s8 | s0] += lo . [W hi | W lo]
                   }
                 }
               } else {         // complex group: all K steps in the stage
                 for (int kk = 0; kk < ksteps; ++kk) {
                   const uint32_t a0 = st + (4 * kk) * kVBlockBytes;
-                  const uint64_t rh = umma_desc(a0, 128, 256), rl = umma_desc(a0 + kVBlockBytes, 128, 256);
-                  const uint64_t ih = umma_desc(a0 + 2 * kVBlockBytes, 128, 256),
-                                 il = umma_desc(a0 + 3 * kVBlockBytes, 128, 256);
                   const uint32_t bw = st + kMgStageV + kk * 4096;
-                  const uint64_t b0 = umma_desc(bw, 128, 256), b1 = umma_desc(bw + 2048, 128, 256);
-                  umma_i8(d0, rh, b0, id64, 1u);        // [Re16 Im16 Re8 Im8] += Vr hi . B0
-                  umma_i8(d0 + 32, rl, b0, id64u, 1u);   // [Re8 Im8 Re0 Im0]   += Vr lo . B0
-                  umma_i8(d0, ih, b1, id64, 1u);
-                  umma_i8(d0 + 32, il, b1, id64u, 1u);
+                  const uint64_t b0 = dsc(bw), b1 = dsc(bw + 2048);
+                  umma_i8(d0, dsc(a0), b0, id64, 1u);                           // [Re16 Im16 Re8 Im8] += Vr hi . B0
+                  umma_i8(d0 + 32, dsc(a0 + kVBlockBytes), b0, id64u, 1u);      // [Re8 Im8 Re0 Im0]   += Vr lo . B0
+                  umma_i8(d0, dsc(a0 + 2 * kVBlockBytes), b1, id64, 1u);
+                  umma_i8(d0 + 32, dsc(a0 + 3 * kVBlockBytes), b1, id64u, 1u);
                 }
               }
               umma_commit(tfull0 + 8 * b);    // slot complete (and stage s free, see the producer)
@@ -926,7 +1009,7 @@ static int g_fused_dbg = 0;
 // freed SMs run the other streams' kernels for the whole launch (C2 190.7 -> 203.1, C3 310.7 -> 332.1 TOPS
 // with three batches in flight); WINO_FUSED_BALANCE=0 restores the full grid (experiments)
 static int g_fused_balance = 1;
-static int g_fused_merge = 3;   // WINO_FUSED_MERGE: 0 general loops only, 1 merged stages at c_in <= 64,
+static int g_fused_merge = 4;   // WINO_FUSED_MERGE: 4 also two slot-groups per stage at c_in <= 32; 0 general loops only, 1 merged stages at c_in <= 64,
                                 // 2 also at c_in <= 128, 3 also 4-K-step slot-group stages above
 
 cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int imgs, const int8_t* vimg,
@@ -944,7 +1027,10 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 20;
   cudaError_t e;
 #define WINO_KF(A, B, C)                                                                                       \
-  e = g.ksteps <= 2 && g_fused_merge >= 1                                                                        \
+  e = g.ksteps == 1 && g_fused_merge >= 4                                                                        \
+          ? launch_pdl(k_fused<A, B, C, 4>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
+                       tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
+      : g.ksteps <= 2 && g_fused_merge >= 1                                                                        \
           ? launch_pdl(k_fused<A, B, C, 1>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
                        tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
       : g.ksteps <= 4 && g_fused_merge >= 2                                                                      \
@@ -980,7 +1066,8 @@ cudaError_t setup_fused() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
   WINO_KF_ATTR(true, false, false);
   WINO_KF_ATTR(true, true, true);
   WINO_KF_ATTR(true, true, false);
