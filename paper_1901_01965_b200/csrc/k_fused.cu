@@ -497,6 +497,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
                   for (int kk = 0; kk < ksteps; ++kk) {   // slots start at zero: every UMMA accumulates
                     const uint64_t bb = dsc(wa + kk * 1024);
                     umma_i8(d, dsc(va + (2 * kk) * kVBlockBytes), bb, id32, 1u);        // [s16 | s8] += hi . [W hi | W lo]
+                    if (dbg & 64) break;   // debug builds only: one UMMA per group (timing)
                     umma_i8(d + 16, dsc(va + (2 * kk + 1) * kVBlockBytes), bb, id32u, 1u);   // [s8 | s0] += lo . [W hi | W lo]
                   }
                 }
@@ -506,6 +507,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
                   const uint32_t bw = st + kMgStageV + kk * 4096;
                   const uint64_t b0 = dsc(bw), b1 = dsc(bw + 2048);
                   umma_i8(d0, dsc(a0), b0, id64, 1u);                           // [Re16 Im16 Re8 Im8] += Vr hi . B0
+                  if (dbg & 64) break;   // debug builds only: one UMMA per group (timing)
                   umma_i8(d0 + 32, dsc(a0 + kVBlockBytes), b0, id64u, 1u);      // [Re8 Im8 Re0 Im0]   += Vr lo . B0
                   umma_i8(d0, dsc(a0 + 2 * kVBlockBytes), b1, id64, 1u);
                   umma_i8(d0 + 32, dsc(a0 + 3 * kVBlockBytes), b1, id64u, 1u);
@@ -678,6 +680,16 @@ __global__ void __launch_bounds__(kFThreads, 1)
     // Deferred into the NEXT unit's row 0 (after its first two slot-groups, before Z_0 overwrites the
     // staging), so the accumulators of that unit are drained meanwhile instead of stalling its MMAs.
     const bool stage8 = NHWC && OUT8 && (g.cout & 15) == 0;
+    // staging tile: the 4-byte word of couts 4cw..4cw+3 of a (pixel, tile) chunk sits at word cw ^ ((tile >> 3) & 3)
+    // of its 16-byte chunk, so the 32 rows of a warp store into 32 different banks (the unswizzled layout was a
+    // 4-way conflict per store); store_staged puts the words back in cout order
+    const uint32_t stg_word = (uint32_t)((cw ^ ((row >> 3) & 3)) * kFC);
+    auto unswizzle = [](uint4 v, int rr) -> uint4 {
+      const int k = (rr >> 3) & 3;
+      if (k & 1) v = make_uint4(v.y, v.x, v.w, v.z);
+      if (k & 2) v = make_uint4(v.z, v.w, v.x, v.y);
+      return v;
+    };
     bool pending = false;
     int pend_tb = 0, pend_nb = 0;
     auto store_staged = [&](int tb_i, int nb) {
@@ -690,7 +702,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           const int py = 2 * ty + (ppx >> 1), px = 2 * (rem - ty * g.tw) + (ppx & 1);
           if (py < pho && px < pwo) {
             int8_t* dst = static_cast<int8_t*>(y) + (((long long)(n0 + ti) * pho + py) * pwo + px) * g.cout + nb * kFN;
-            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(part + etid * 16);
+            *reinterpret_cast<uint4*>(dst) = unswizzle(*reinterpret_cast<const uint4*>(part + etid * 16), rr);
           }
         }
         return;
@@ -708,7 +720,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           const int px = ch >> 7;
           const int oy = oyb + (px >> 2), ox = oxb + (px & 3);
           if (oy >= g.ho || ox >= g.wo) continue;
-          const uint4 val = *reinterpret_cast<const uint4*>(part + ch * 16);
+          const uint4 val = unswizzle(*reinterpret_cast<const uint4*>(part + ch * 16), rr);
           *reinterpret_cast<uint4*>(base + ((long long)oy * g.wo + ox) * g.cout) = val;
         }
       }
@@ -899,7 +911,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
                                         : __byte_perm(__byte_perm((uint32_t)outv(Yi[j][0]), (uint32_t)outv(Yi[j][1]), 0x0040),
                                                       __byte_perm((uint32_t)outv(Yi[j][2]), (uint32_t)outv(Yi[j][3]), 0x0040),
                                                       0x5410);
-              *reinterpret_cast<uint32_t*>(part + ((i * 4 + j) * kMBlock + row) * 16 + cw * kFC) = w;
+              *reinterpret_cast<uint32_t*>(part + ((i * 4 + j) * kMBlock + row) * 16 + stg_word) = w;
             }
             return;
           }
@@ -971,8 +983,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
                                           __vmaxs4(word(Y1, 2 * pj), word(Y1, 2 * pj + 1)));
             const uint32_t bot = __vmaxs4(__vmaxs4(word(Y2, 2 * pj), word(Y2, 2 * pj + 1)),
                                           __vmaxs4(word(Y3, 2 * pj), word(Y3, 2 * pj + 1)));
-            *reinterpret_cast<uint32_t*>(part + ((0 * 2 + pj) * kMBlock + row) * 16 + cw * kFC) = top;
-            *reinterpret_cast<uint32_t*>(part + ((1 * 2 + pj) * kMBlock + row) * 16 + cw * kFC) = bot;
+            *reinterpret_cast<uint32_t*>(part + ((0 * 2 + pj) * kMBlock + row) * 16 + stg_word) = top;
+            *reinterpret_cast<uint32_t*>(part + ((1 * 2 + pj) * kMBlock + row) * 16 + stg_word) = bot;
           }
         } else {
           emit_row(0, Y0);
