@@ -38,18 +38,24 @@ __device__ __forceinline__ void pieces4(uint32_t A, uint32_t B, uint32_t& lo, ui
 }
 
 __device__ __forceinline__ void st32(int8_t* p, uint32_t v) { *reinterpret_cast<uint32_t*>(p) = v; }
+__device__ __forceinline__ void st32d(int8_t* p, uint32_t v, int dbg) {
+  if (!(dbg & 1) || v == 0x7f7f7f7fu) st32(p, v);   // debug: stores skipped (kept live by the impossible test)
+}
 
 // store the value (A, B) of a group's value slot: pieces at p (hi) and p + 4 KB (lo)
-__device__ __forceinline__ void store_val(int8_t* p_hi, uint32_t A, uint32_t B) {
+__device__ __forceinline__ void store_val(int8_t* p_hi, uint32_t A, uint32_t B, int dbg) {
   uint32_t lo, hi;
   pieces4(A, B, lo, hi);
-  st32(p_hi, hi);
-  st32(p_hi + kVBlockBytes, lo);
+  st32d(p_hi, hi, dbg);
+  st32d(p_hi + kVBlockBytes, lo, dbg);
 }
 
 template <int KS, int MINB>   // KS: g.ksteps as a compile-time constant (1, 2, 4, 8, 16; 0 = runtime)
 __global__ void __launch_bounds__(kI4Warps * 32, MINB)
-    k_input_transform_f4(Geom g, const int8_t* __restrict__ x, int n0, int imgs, int8_t* __restrict__ vimg) {
+    k_input_transform_f4(Geom g, const int8_t* __restrict__ x, int n0, int imgs, int8_t* __restrict__ vimg, int dbg) {
+#ifndef WINO_K2_DBG
+  dbg = 0;   // ablation bits (debug builds only): 1 no V stores, 2 no x loads
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * kI4TilesPerCta + warp * kI4TilesPerWarp + (lane >> 2);
   const int c = blockIdx.y * kI4ChPerCta + 4 * (lane & 3);
@@ -88,7 +94,10 @@ __global__ void __launch_bounds__(kI4Warps * 32, MINB)
     const long long rstride = (long long)g.w * g.cin;
     const int8_t* p0 = x + ((long long)img * g.h * g.w + (long long)iy0 * g.w + ix0) * g.cin + c;
     const bool inside = t < tiles && c + 4 <= g.cin && iy0 >= 0 && iy0 + 6 <= g.h && ix0 >= 0 && ix0 + 6 <= g.w;
-    if ((g.cin & 3) == 0 && __all_sync(0xffffffffu, inside)) {
+    if (dbg & 2) {   // debug: no loads (a lane-dependent pattern instead)
+#pragma unroll
+      for (int i = 0; i < 36; i++) w[i] = (uint32_t)(t * 0x01010101u + i);
+    } else if ((g.cin & 3) == 0 && __all_sync(0xffffffffu, inside)) {
       // interior warp: unpredicated 4-byte loads; column offsets b * c_in are immediates when c_in = 32 KS
       const int cst = (KS > 0 && g.cin == 32 * KS) ? 32 * KS : g.cin;
 #pragma unroll
@@ -167,10 +176,10 @@ __global__ void __launch_bounds__(kI4Warps * 32, MINB)
       v[1][1] -= 0x08000800u;
     }
 #pragma unroll
-    for (int s = 0; s < 4; s++) store_val(gp(fg_of_real(ri * 4 + s)), v[s][0], v[s][1]);
+    for (int s = 0; s < 4; s++) store_val(gp(fg_of_real(ri * 4 + s)), v[s][0], v[s][1], dbg);
     int8_t* pc = gp(fg_of_primary(ri));
-    store_val(pc, v[4][0], v[4][1]);                      // Re: pieces 0 (hi), 1 (lo)
-    store_val(pc + 2 * kVBlockBytes, v[5][0], v[5][1]);   // Im: pieces 2, 3
+    store_val(pc, v[4][0], v[4][1], dbg);                      // Re: pieces 0 (hi), 1 (lo)
+    store_val(pc + 2 * kVBlockBytes, v[5][0], v[5][1], dbg);   // Im: pieces 2, 3
   };
   real_row(std::integral_constant<int, 0>{}, e0);
   real_row(std::integral_constant<int, 1>{}, e1);
@@ -195,16 +204,16 @@ __global__ void __launch_bounds__(kI4Warps * 32, MINB)
 #pragma unroll
   for (int j = 0; j < 4; j++) {
     int8_t* pc = gp(fg_of_primary(4 + j));
-    store_val(pc, re[j][0], re[j][1]);
-    store_val(pc + 2 * kVBlockBytes, im[j][0], im[j][1]);
+    store_val(pc, re[j][0], re[j][1], dbg);
+    store_val(pc + 2 * kVBlockBytes, im[j][0], im[j][1], dbg);
   }
   {
     int8_t* pc = gp(fg_of_primary(8));
-    store_val(pc, q[0][0], q[0][1]);
-    store_val(pc + 2 * kVBlockBytes, q[1][0], q[1][1]);
+    store_val(pc, q[0][0], q[0][1], dbg);
+    store_val(pc + 2 * kVBlockBytes, q[1][0], q[1][1], dbg);
     pc = gp(fg_of_primary(9));
-    store_val(pc, q[2][0], q[2][1]);
-    store_val(pc + 2 * kVBlockBytes, q[3][0], q[3][1]);
+    store_val(pc, q[2][0], q[2][1], dbg);
+    store_val(pc + 2 * kVBlockBytes, q[3][0], q[3][1], dbg);
   }
 }
 
@@ -214,9 +223,10 @@ cudaError_t launch_input_transform_f4(const Geom& g, const int8_t* x, int n0, in
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
   dim3 grid((unsigned)(tiles_pad / kI4TilesPerCta), g.cin_pad / kI4ChPerCta);
   // CTAs per SM the register budget targets (WINO_K2F4_MINB; 3 measured best at C2 and the VGG-16 stack)
+  static const int dbg = [] { const char* e = std::getenv("WINO_K2_DBG"); return e ? std::atoi(e) : 0; }();
   static const int minb = [] { const char* e = std::getenv("WINO_K2F4_MINB"); return e ? std::atoi(e) : 3; }();
 #define WINO_K2F4(K, M) \
-  launch_pdl_co(k_input_transform_f4<K, M>, grid, dim3(kI4Warps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg)
+  launch_pdl_co(k_input_transform_f4<K, M>, grid, dim3(kI4Warps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg, dbg)
 #define WINO_K2F4_M(M)              \
   switch (g.ksteps) {               \
     case 1: return WINO_K2F4(1, M);   \
