@@ -151,6 +151,8 @@ typedef struct {
     int n_chunks;
     int lanes;                  /* chunk pipelines actually used (<= n_chunks)          */
     size_t lane_bytes;          /* workspace bytes per lane (V + M'' of one chunk)     */
+    int packing;                /* 1; 4 = the fused path's quarter-K packing at c_in <= 8
+                                   (two slot-groups per 32-byte K row)    */
     long long chunk_tiles_pad;  /* tiles per chunk rounded up to m_block               */
     int path;                   /* WINO_PATH_FUSED or WINO_PATH_STAGED (AUTO resolved)  */
     int stages;                 /* kernels per chunk: 2 (fused) or 3 (staged)          */

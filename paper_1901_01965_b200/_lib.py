@@ -39,7 +39,7 @@ class wino_plan_info(ctypes.Structure):
                 ("tiles", ctypes.c_longlong), ("cin_pad", ctypes.c_int), ("cout_pad", ctypes.c_int),
                 ("n_block", ctypes.c_int), ("m_block", ctypes.c_int), ("planes", ctypes.c_int),
                 ("pieces", ctypes.c_int), ("chunk_images", ctypes.c_int), ("n_chunks", ctypes.c_int),
-                ("lanes", ctypes.c_int), ("lane_bytes", ctypes.c_size_t),
+                ("lanes", ctypes.c_int), ("lane_bytes", ctypes.c_size_t), ("packing", ctypes.c_int),
                 ("chunk_tiles_pad", ctypes.c_longlong), ("path", ctypes.c_int), ("stages", ctypes.c_int),
                 ("algorithm", ctypes.c_int), ("tile", ctypes.c_int), ("positions", ctypes.c_int),
                 ("v_offset", ctypes.c_size_t), ("v_bytes", ctypes.c_size_t),

@@ -229,6 +229,46 @@ __global__ void __launch_bounds__(kFilterWarps * 32) k_filter_transform(Geom g, 
         const int4 v = *reinterpret_cast<const int4*>(&s_stage[warp][pp][hf * 16]);
         *reinterpret_cast<int4*>(wimg + w_offset(g, pp >> 1, pp & 1, co, c0 + hf * 16)) = v;
       }
+    } else if (g.qk) {
+      // quarter-K packing (c_in <= 8, layout.cuh): this cout's 10 rows of each pack's B (4 rows of slot 2P,
+      // 2 zero rows, 4 rows of slot 2P+1), 32 K bytes each, channel ci at byte part * 8 + ci of its slot half
+      int8_t (*st8)[32] = s_stage[warp];
+      for (int i = lane; i < kQkPacks * 10 * 8; i += 32) reinterpret_cast<int*>(st8)[i] = 0;
+      __syncwarp();
+      if (ci < 8) {
+#pragma unroll
+        for (int pk = 0; pk < kQkPacks; pk++)
+#pragma unroll
+          for (int sp = 0; sp < 2; sp++) {
+            const int sg = 2 * pk + sp, g0 = qk_sg_first(sg);
+            int8_t (*r)[32] = st8 + pk * 10 + (sp ? 6 : 0);   // the slot's 4 rows
+            const int b0 = sp * 16 + ci, b1 = b0 + 8;          // value parts 0 and 1
+            if (!fg_complex(g0)) {
+              const int v0 = vals[fg_real_plane(g0)], v1 = vals[fg_real_plane(g0 + 1)];
+              r[0][b0] = (int8_t)bal_hi(v0);
+              r[1][b1] = (int8_t)bal_hi(v1);
+              r[2][b0] = (int8_t)bal_lo(v0);
+              r[3][b1] = (int8_t)bal_lo(v1);
+            } else {
+              const int k = fg_primary(g0);
+              const int wr = vals[16 + 3 * k], wi = vals[16 + 3 * k + 1], nwi = -wi;
+              r[0][b0] = (int8_t)bal_hi(wr);  r[0][b1] = (int8_t)bal_hi(nwi);   // Re16: Vr Wr - Vi Wi
+              r[1][b0] = (int8_t)bal_hi(wi);  r[1][b1] = (int8_t)bal_hi(wr);    // Im16: Vr Wi + Vi Wr
+              r[2][b0] = (int8_t)bal_lo(wr);  r[2][b1] = (int8_t)bal_lo(nwi);
+              r[3][b0] = (int8_t)bal_lo(wi);  r[3][b1] = (int8_t)bal_lo(wr);
+            }
+          }
+      }
+      __syncwarp();
+      if (c0 == 0) {
+        const int nb = co / kFN16, cr = co % kFN16;
+        for (int idx = lane; idx < kQkPacks * 10 * 2; idx += 32) {   // (pack, staged row, 16-byte K half)
+          const int pk = idx / 20, j = (idx >> 1) % 10, kh = idx & 1;
+          const int row = (j < 4 ? 16 * j : (j < 6 ? 64 + 16 * (j - 4) : 96 + 16 * (j - 6))) + cr;
+          const int4 v = *reinterpret_cast<const int4*>(&st8[pk * 10 + j][kh * 16]);
+          *reinterpret_cast<int4*>(wimg + wq_offset(nb, pk, row, kh * 16)) = v;
+        }
+      }
     } else {
       // staged row 2 * wprefix(gi) + j holds piece-row j of group gi for this cout
 #pragma unroll

@@ -224,7 +224,30 @@ __global__ void __launch_bounds__(kFThreads, 1)
       // ------------------------------------------------ producers: warp p issues the stages it with it % P == p
       const int pw = warp - kFProducerWarp;
       int it = 0;
-      if constexpr (MG == 4) {
+      if constexpr (MG == 5) {
+        // quarter-K packing (c_in <= 8, layout.cuh): one stage per pack (8 KB of V + 5 KB of W': two slot-groups),
+        // released by its own commit
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+          const int tb = u / nblocks, nb = u - tb * nblocks;
+          for (int pk = 0; pk < kQkPacks; pk++, it++) {
+            if (it % kFProducers != pw) continue;
+            const int s = it % kFStages;
+            mbar_wait(empty0 + 8 * s, ((it / kFStages) & 1) ^ 1);
+            const uint32_t st = sbase + s * kFStageBytes;
+            if (elect_one()) {
+              if (dbg & 4) {   // debug builds only: no copies
+                mbar_arrive(full0 + 8 * s);
+              } else {
+                mbar_arrive_expect_tx(full0 + 8 * s, kQkPackV + kQkPackW);
+                bulk_g2s(st, V + ((long long)tb * kQkPacks + pk) * kQkPackV, kQkPackV, full0 + 8 * s);
+                bulk_g2s(st + kQkPackV, W + ((long long)nb * kQkPacks + pk) * kQkPackW, kQkPackW, full0 + 8 * s);
+              }
+              if (it < 64) FTRACE(it, 0);
+            }
+            __syncwarp();
+          }
+        }
+      } else if constexpr (MG == 4) {
         // one K step (c_in <= 32): a 40 KB stage holds TWO consecutive slot-groups (their groups are
         // contiguous in V and W'), one V and one W' copy per stage, 9 stages per unit instead of 18; the
         // stage is released by its own commit (empty barrier) after the second slot-group's UMMAs
@@ -367,6 +390,39 @@ __global__ void __launch_bounds__(kFThreads, 1)
       const uint32_t id16u = idesc_i8(kMBlock, 16, 0, 1), id32u = idesc_i8(kMBlock, 32, 0, 1),
                      id64u = idesc_i8(kMBlock, 64, 0, 1);
       int it = 0, sgc = 0;
+      if constexpr (MG == 5) {
+        // one N = 160 UMMA pair per pack fills two adjacent TMEM slots (layout.cuh quarter-K packing)
+        const uint32_t id160 = idesc_i8(kMBlock, kQkRows, 1, 1), id160u = idesc_i8(kMBlock, kQkRows, 0, 1);
+        const uint64_t D0 = umma_desc(sbase, 128, 256);
+        const uint32_t d0lo = (uint32_t)D0, d0hi = (uint32_t)(D0 >> 32);
+        auto dsc = [&](uint32_t off) -> uint64_t { return ((uint64_t)d0hi << 32) | (uint64_t)(d0lo + (off >> 4)); };
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+          for (int pk = 0; pk < kQkPacks; pk++, it++, sgc += 2) {
+            const int s = it % kFStages;
+            const int b = sgc % kFSlots;            // even: slots b, b + 1 are adjacent
+            mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
+            mbar_wait(tempty0 + 8 * (b + 1), (((sgc + 1) / kFSlots) & 1) ^ 1);
+            mbar_wait(full0 + 8 * s, (it / kFStages) & 1);
+            tc_fence_after();
+            if (it < 64 && lane == 0) FTRACE(it, 1);
+            if (sgc < 32 && lane == 0) FTRACE(64 + sgc, 0);
+            const uint32_t st = s * kFStageBytes;
+            const uint32_t d0 = tmem + b * kFSlotCols;
+            if (elect_one()) {
+              if (!(dbg & 2)) {
+                const uint64_t bw = dsc(st + kQkPackV);
+                umma_i8(d0, dsc(st), bw, id160, 1u);                       // hi: [slot b: ... | 0 | slot b+1]
+                umma_i8(d0 + 32, dsc(st + kVBlockBytes), bw, id160u, 1u);  // lo (u8) at the piece offset 32
+              }
+              umma_commit(tfull0 + 8 * b);
+              umma_commit(tfull0 + 8 * (b + 1));
+              umma_commit(empty0 + 8 * s);
+              if (it < 64) FTRACE(it, 2);
+            }
+            __syncwarp();
+          }
+        }
+      } else
       if constexpr (MG == 4) {
         constexpr uint32_t kSV = 32768;
         const uint64_t D0 = umma_desc(sbase, 128, 256);   // + (offset >> 4): see the MG 1..3 loop below
@@ -638,12 +694,14 @@ __global__ void __launch_bounds__(kFThreads, 1)
 #pragma unroll
         for (int j = 0; j < 4; j++) { h0[j] = x0[j] = l0[j] = h1[j] = x1[j] = l1[j] = (uint32_t)(a + j); }
       } else {
+        // MG 5 (quarter-K packing): the pair's piece blocks interleave [g0 s16 | g1 s16 | g0 s8 | g1 s8 | ...]
+        constexpr uint32_t kO1 = MG == 5 ? 16 : 48, kOs = MG == 5 ? 32 : 16;
         tmem_ld4(a, h0);
-        tmem_ld4(a + 16, x0);
-        tmem_ld4(a + 32, l0);
-        tmem_ld4(a + 48, h1);
-        tmem_ld4(a + 64, x1);
-        tmem_ld4(a + 80, l1);
+        tmem_ld4(a + kOs, x0);
+        tmem_ld4(a + 2 * kOs, l0);
+        tmem_ld4(a + kO1, h1);
+        tmem_ld4(a + kO1 + kOs, x1);
+        tmem_ld4(a + kO1 + 2 * kOs, l1);
         tmem_ld_wait();
       }
       zero_slot(a);
@@ -1039,7 +1097,10 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 20;
   cudaError_t e;
 #define WINO_KF(A, B, C)                                                                                       \
-  e = g.ksteps == 1 && g_fused_merge >= 4                                                                        \
+  e = g.qk                                                                                                      \
+          ? launch_pdl(k_fused<A, B, C, 5>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
+                       tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
+      : g.ksteps == 1 && g_fused_merge >= 4                                                                        \
           ? launch_pdl(k_fused<A, B, C, 4>, dim3(grid), dim3(kFThreads), smem, st, vimg, wimg, codes, g, n0, imgs,    \
                        tblocks, rq_mult, rq_shift, y, g_fused_dbg, g_fused_trace)                                \
       : g.ksteps <= 2 && g_fused_merge >= 1                                                                        \
@@ -1079,7 +1140,8 @@ cudaError_t setup_fused() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
   WINO_KF_ATTR(true, false, false);
   WINO_KF_ATTR(true, true, true);
   WINO_KF_ATTR(true, true, false);

@@ -50,15 +50,18 @@ __device__ __forceinline__ void store_val(int8_t* p_hi, uint32_t A, uint32_t B, 
   st32d(p_hi + kVBlockBytes, lo, dbg);
 }
 
-template <int KS, int MINB>   // KS: g.ksteps as a compile-time constant (1, 2, 4, 8, 16; 0 = runtime)
+// QK: the quarter-K packed V image (c_in <= 8, layout.cuh): thread = (tile, 4 of the 8 channel slots), warp =
+// 16 tiles, CTA = one 128-tile block; the (group, value part) of a value selects its pack and K byte
+template <int KS, int MINB, bool QK = false>   // KS: g.ksteps as a compile-time constant (1, 2, 4, 8, 16; 0 = runtime)
 __global__ void __launch_bounds__(kI4Warps * 32, MINB)
     k_input_transform_f4(Geom g, const int8_t* __restrict__ x, int n0, int imgs, int8_t* __restrict__ vimg, int dbg) {
 #ifndef WINO_K2_DBG
   dbg = 0;   // ablation bits (debug builds only): 1 no V stores, 2 no x loads
 #endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * kI4TilesPerCta + warp * kI4TilesPerWarp + (lane >> 2);
-  const int c = blockIdx.y * kI4ChPerCta + 4 * (lane & 3);
+  const int t = QK ? blockIdx.x * kMBlock + warp * 16 + (lane >> 1)
+                   : blockIdx.x * kI4TilesPerCta + warp * kI4TilesPerWarp + (lane >> 2);
+  const int c = QK ? 4 * (lane & 1) : blockIdx.y * kI4ChPerCta + 4 * (lane & 3);
   pdl_trigger();
   pdl_wait();   // x may come from the previous kernel; V may still be read by the previous GEMM
 
@@ -68,9 +71,20 @@ __global__ void __launch_bounds__(kI4Warps * 32, MINB)
   int8_t* base2 = base + (long long)((c >> 5) * 2) * kVBlockBytes;   // real groups: 2 pieces per K step
   int8_t* base4 = base + (long long)((c >> 5) * 4) * kVBlockBytes;   // complex groups: 4 pieces
   auto gp = [&](int gi) { return (fg_pieces(gi) == 2 ? base2 : base4) + fg_vprefix(gi) * kst; };
+  // QK: (t / 128) pack blocks, row r, channel slot c; value part vp of group gi at byte qk_kbyte(gi, vp, c)
+  int8_t* qbase = vimg + (long long)(t / kMBlock) * kQkPacks * kQkPackV + tiled_offset(t % kMBlock, c, kMBlock);
+  // hi-piece address of value part vp (0; 1 = a complex group's Im) of group gi (lo piece 4 KB after it)
+  auto vp_addr = [&](int gi, int vp) -> int8_t* {
+    if constexpr (QK) {
+      const int kb = qk_kbyte(gi, vp, 0);
+      return qbase + (qk_sg_of(gi) / 2) * kQkPackV + (kb >> 4) * 128 + (kb & 15);
+    } else {
+      return gp(gi) + vp * 2 * kVBlockBytes;
+    }
+  };
 
   const int tiles = imgs * g.tpi;
-  if (blockIdx.y * kI4ChPerCta >= g.cin) {   // a slice of padding channels only: V = 0 (both pieces)
+  if (!QK && blockIdx.y * kI4ChPerCta >= g.cin) {   // a slice of padding channels only: V = 0 (both pieces)
 #pragma unroll
     for (int gi = 0; gi < kFGroupsN; gi++) {
       int8_t* p = gp(gi);
@@ -176,10 +190,12 @@ __global__ void __launch_bounds__(kI4Warps * 32, MINB)
       v[1][1] -= 0x08000800u;
     }
 #pragma unroll
-    for (int s = 0; s < 4; s++) store_val(gp(fg_of_real(ri * 4 + s)), v[s][0], v[s][1], dbg);
-    int8_t* pc = gp(fg_of_primary(ri));
-    store_val(pc, v[4][0], v[4][1], dbg);                      // Re: pieces 0 (hi), 1 (lo)
-    store_val(pc + 2 * kVBlockBytes, v[5][0], v[5][1], dbg);   // Im: pieces 2, 3
+    for (int s = 0; s < 4; s++) {
+      const int gi = fg_of_real(ri * 4 + s);
+      store_val(vp_addr(gi, QK ? gi - qk_sg_first(qk_sg_of(gi)) : 0), v[s][0], v[s][1], dbg);
+    }
+    store_val(vp_addr(fg_of_primary(ri), 0), v[4][0], v[4][1], dbg);   // Re: pieces 0 (hi), 1 (lo)
+    store_val(vp_addr(fg_of_primary(ri), 1), v[5][0], v[5][1], dbg);   // Im: pieces 2, 3 (QK: value part 1)
   };
   real_row(std::integral_constant<int, 0>{}, e0);
   real_row(std::integral_constant<int, 1>{}, e1);
@@ -203,18 +219,13 @@ __global__ void __launch_bounds__(kI4Warps * 32, MINB)
   }
 #pragma unroll
   for (int j = 0; j < 4; j++) {
-    int8_t* pc = gp(fg_of_primary(4 + j));
-    store_val(pc, re[j][0], re[j][1], dbg);
-    store_val(pc + 2 * kVBlockBytes, im[j][0], im[j][1], dbg);
+    store_val(vp_addr(fg_of_primary(4 + j), 0), re[j][0], re[j][1], dbg);
+    store_val(vp_addr(fg_of_primary(4 + j), 1), im[j][0], im[j][1], dbg);
   }
-  {
-    int8_t* pc = gp(fg_of_primary(8));
-    store_val(pc, q[0][0], q[0][1], dbg);
-    store_val(pc + 2 * kVBlockBytes, q[1][0], q[1][1], dbg);
-    pc = gp(fg_of_primary(9));
-    store_val(pc, q[2][0], q[2][1], dbg);
-    store_val(pc + 2 * kVBlockBytes, q[3][0], q[3][1], dbg);
-  }
+  store_val(vp_addr(fg_of_primary(8), 0), q[0][0], q[0][1], dbg);
+  store_val(vp_addr(fg_of_primary(8), 1), q[1][0], q[1][1], dbg);
+  store_val(vp_addr(fg_of_primary(9), 0), q[2][0], q[2][1], dbg);
+  store_val(vp_addr(fg_of_primary(9), 1), q[3][0], q[3][1], dbg);
 }
 
 cudaError_t launch_input_transform_f4(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg,
@@ -235,6 +246,10 @@ cudaError_t launch_input_transform_f4(const Geom& g, const int8_t* x, int n0, in
     case 8: return WINO_K2F4(8, M);   \
     case 16: return WINO_K2F4(16, M); \
     default: return WINO_K2F4(0, M);  \
+  }
+  if (g.qk) {   // quarter-K packed V (c_in <= 8): one CTA per 128-tile block
+    return launch_pdl_co(k_input_transform_f4<1, 3, true>, dim3((unsigned)(tiles_pad / kMBlock)),
+                         dim3(kI4Warps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg, dbg);
   }
   if (minb >= 4) { WINO_K2F4_M(4) }
   if (minb == 3) { WINO_K2F4_M(3) }

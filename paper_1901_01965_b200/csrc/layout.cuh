@@ -80,6 +80,7 @@ struct Geom {
   int planes;                  // staged GEMM planes per (tile, channel) (46 or 16)
   int in_u8, zx, zw;           // uint8 x/w with zero points (f2, A28); 0, 0, 0 for int8
   int w1;                      // int8-native target (f3, A29): W' is ONE s8 piece per plane, 7-bit codes
+  int qk;                      // fused path, quarter-K packing (c_in <= 8, NHWC int8): V / W' per pack (above)
   int chunk_imgs;
   long long chunk_tiles_pad;   // multiple of kMBlock
 };
@@ -163,6 +164,39 @@ __host__ __device__ __forceinline__ long long wf_offset(const Geom& g, int gi, i
   const int rows = 32 * fg_wunits(gi);
   return ((long long)(nb * kWRowUnitsF + fg_wprefix(gi)) * g.ksteps + (long long)(k >> 5) * fg_wunits(gi)) * 1024 +
          tiled_offset(row, k & 31, rows);
+}
+
+// ---------------------------------------------------------------- fused path, quarter-K packing (c_in <= 8)
+// With one K step and at most 8 input channels, a 32-byte K row carries TWO slot-groups (a "pack"): slot-group
+// 2P in bytes 0..15 and 2P+1 in bytes 16..31, each as two 8-channel value parts -- a real pair's groups g0, g1,
+// or a complex group's Re and Im.  V (per 128-tile block): [pack 0..8][piece hi, lo][128 rows x 32 B] = 72 KB
+// (4x less than the unpacked 288 KB at c_in_pad 32).  W' (per 16-cout block): [pack][160 rows x 32 B], the
+// block-diagonal B of one N = 160 UMMA pair that fills two adjacent TMEM slots at once: rows 0..63 slot 2P,
+// 64..95 zero, 96..159 slot 2P+1; a slot's 64 rows are (cout = row % 16)
+//   real pair (interleaved slot [g0 s16 | g1 s16 | g0 s8 | g1 s8 | g0 s0 | g1 s0]):
+//     rows 0-15 W hi(g0) in part 0, 16-31 W hi(g1) in part 1, 32-47 W lo(g0) part 0, 48-63 W lo(g1) part 1
+//   complex (slot [Re16 | Im16 | Re8 | Im8 | Re0 | Im0], A = [Vr | Vi] along K):
+//     rows 0-15 [Wr hi | (-Wi) hi], 16-31 [Wi hi | Wr hi], 32-47 [Wr lo | (-Wi) lo], 48-63 [Wi lo | Wr lo]
+// A = the pack's hi (or lo) block, at TMEM slot 2P's column 0 (hi) and 32 (lo): one UMMA pair per two
+// slot-groups (K = 32, N = 160) instead of 2 or 4 per slot-group.
+constexpr int kQkPacks = 9;
+constexpr int kQkRows = 160;
+constexpr uint32_t kQkPackW = kQkRows * 32;        // 5120 B of W' per (pack, 16-cout block)
+constexpr uint32_t kQkPackV = 2 * kVBlockBytes;    // 8 KB of V per (pack, tile block)
+// slot-group of fused group gi (processing order of k_fused.cu: rows 0, 5, 1, 2 as pair, pair, complex;
+// then row 3's six complex groups), its first group and its group count
+__host__ __device__ constexpr int qk_sg_of(int gi) {
+  return gi < 20 ? (gi / 5) * 3 + ((gi % 5) < 4 ? (gi % 5) / 2 : 2) : 12 + gi - 20;
+}
+__host__ __device__ constexpr int qk_sg_first(int sg) { return sg < 12 ? (sg / 3) * 5 + (sg % 3) * 2 : 20 + sg - 12; }
+// byte of value part vp (0/1) of group gi's slot-group inside the pack's 32-byte K row, channel ch (< 8)
+__host__ __device__ constexpr int qk_kbyte(int gi, int vp, int ch) { return (qk_sg_of(gi) % 2) * 16 + vp * 8 + ch; }
+__host__ __device__ __forceinline__ long long vq_offset(long long t, int pack, int piece, int kbyte) {
+  return ((t / kMBlock) * kQkPacks + pack) * (long long)kQkPackV + piece * kVBlockBytes +
+         tiled_offset((int)(t % kMBlock), kbyte, kMBlock);
+}
+__host__ __device__ __forceinline__ long long wq_offset(int nb, int pack, int row, int kbyte) {
+  return (long long)(nb * kQkPacks + pack) * kQkPackW + tiled_offset(row, kbyte, kQkRows);
 }
 
 // Byte offset of the single s8 W' piece (int8-native target, f3) of plane `plane`, cout co, channel k:

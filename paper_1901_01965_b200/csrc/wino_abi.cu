@@ -83,6 +83,11 @@ wino_status check_device(const wino_plan_s* p) {
 long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 
 // WINO_K2F_LEGACY=1: the two-channel K2F for NHWC int8 as well (A/B experiments)
+// WINO_QK_OFF=1: no quarter-K packing at c_in <= 8 (A/B experiments)
+bool qk_off() {
+  static const bool v = [] { const char* e = std::getenv("WINO_QK_OFF"); return e && std::atoi(e) != 0; }();
+  return v;
+}
 bool k2f_legacy() {
   static const bool v = [] { const char* e = std::getenv("WINO_K2F_LEGACY"); return e && std::atoi(e) != 0; }();
   return v;
@@ -228,6 +233,9 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   g.dv_tw = wino::make_fastdiv(g.tw);
   g.dv_tpi = wino::make_fastdiv(g.tpi);
   g.cin_pad = (int)round_up(d.c_in, wino::kKStep);
+  // quarter-K packing of the fused complex path at c_in <= 8 (layout.cuh): NHWC int8 (the SWAR K2)
+  g.qk = d.path == WINO_PATH_FUSED && d.algorithm == WINO_ALG_F4X4 && d.layout == WINO_NHWC &&
+         d.input_type == WINO_IN_INT8 && d.c_in <= 8 && !k2f_legacy() && !qk_off();
   const int cout16 = (int)round_up(d.c_out, 16);
   g.path = d.path == WINO_PATH_FUSED ? 0 : 1;
   // fused path: 16-cout units (UMMA N = 16); staged path: widest N that the cout count fills
@@ -243,14 +251,16 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   const size_t m_per_tile = d.path == WINO_PATH_STAGED ? (size_t)g.npos * 4 * (size_t)g.cout_pad : 0;
   const bool fused_f4 = d.path == WINO_PATH_FUSED && d.algorithm == WINO_ALG_F4X4;
   const size_t v_per_tile_ch = fused_f4 ? wino::kVPiecesF : 2 * (size_t)g.planes;
-  const size_t per_img = (size_t)g.tpi * (v_per_tile_ch * (size_t)g.cin_pad + m_per_tile);
+  const size_t per_img = g.qk ? (size_t)g.tpi * (wino::kQkPacks * wino::kQkPackV / wino::kMBlock)
+                              : (size_t)g.tpi * (v_per_tile_ch * (size_t)g.cin_pad + m_per_tile);
   long long imgs = (long long)(chunk_budget_bytes(d.workspace_mb) / (per_img ? per_img : 1));
   if (imgs < 1) imgs = 1;
   if (imgs > d.n) imgs = d.n;
   g.chunk_imgs = (int)imgs;
   g.chunk_tiles_pad = round_up((long long)imgs * g.tpi, wino::kMBlock);
   p->n_chunks = (int)((d.n + imgs - 1) / imgs);
-  p->v_bytes = v_per_tile_ch * g.chunk_tiles_pad * g.cin_pad;
+  p->v_bytes = g.qk ? (size_t)(g.chunk_tiles_pad / wino::kMBlock) * wino::kQkPacks * wino::kQkPackV
+                   : v_per_tile_ch * g.chunk_tiles_pad * g.cin_pad;
   p->m_bytes = d.path == WINO_PATH_STAGED ? (size_t)g.npos * g.chunk_tiles_pad * g.cout_pad * 4 : 0;
   // + one 256-byte status block (the code-validation flag of wino_validate_codes)
   p->lanes = d.lanes > 1 ? (d.lanes < p->n_chunks ? d.lanes : p->n_chunks) : 1;
@@ -258,7 +268,8 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   p->status_offset = p->lane_bytes * p->lanes;
   p->ws_bytes = p->status_offset + 256;
   // W': 92 B per (cin, cout) staged (46 planes x 2 pieces); 112 B fused (56 rows x 2 couts-halves, layout.cuh)
-  p->f_bytes = (size_t)(fused_f4 ? 2 * wino::kWRowUnitsF : (g.w1 ? 1 : 2) * g.planes) * g.cout_pad * g.cin_pad;
+  p->f_bytes = g.qk ? (size_t)(g.cout_pad / 16) * wino::kQkPacks * wino::kQkPackW
+                   : (size_t)(fused_f4 ? 2 * wino::kWRowUnitsF : (g.w1 ? 1 : 2) * g.planes) * g.cout_pad * g.cin_pad;
   p->x_bytes = (size_t)d.n * d.h * d.w * d.c_in;
   p->y_bytes = g.pool2 ? (size_t)d.n * (g.ho / 2) * (g.wo / 2) * d.c_out
                        : (size_t)d.n * g.ho * g.wo * d.c_out * (d.out_mode == WINO_OUT_INT32 ? 4 : 1);
@@ -285,6 +296,7 @@ wino_status wino_plan_query(wino_plan_t p, wino_plan_info* info) {
   info->pieces = wino::kPieces;
   info->chunk_images = p->g.chunk_imgs; info->n_chunks = p->n_chunks;
   info->lanes = p->lanes; info->lane_bytes = p->lane_bytes;
+  info->packing = p->g.qk ? 4 : 1;
   info->chunk_tiles_pad = p->g.chunk_tiles_pad;
   info->path = p->g.path == 0 ? WINO_PATH_FUSED : WINO_PATH_STAGED;
   info->stages = p->g.path == 0 ? 2 : 3;

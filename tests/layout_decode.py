@@ -158,3 +158,69 @@ def complex_to_values(Z: np.ndarray):
     re = np.stack([Z[..., p, 0] for p in CPX_POS], 0)
     im = np.stack([Z[..., p, 1] for p in CPX_POS], 0)
     return real, re, im
+
+
+# ---------------------------------------------------------------- quarter-K packing (c_in <= 8, layout.cuh)
+def qk_sg_of(gi):
+    return (gi // 5) * 3 + ((gi % 5) // 2 if gi % 5 < 4 else 2) if gi < 20 else 12 + gi - 20
+
+
+def qk_sg_first(sg):
+    return (sg // 3) * 5 + (sg % 3) * 2 if sg < 12 else 20 + sg - 12
+
+
+def decode_w_qk(buf: np.ndarray, cout_pad: int, cin: int):
+    """Packed W' [16-cout block][pack 0..8][160 rows x 32 B] -> (real [16][cout][cin], re, im, ok) as
+    hi * 256 + lo; ok: the -Wi / Wr duplicates, the zero rows and the other slot's K half are as specified."""
+    groups = fused_groups()
+    b = buf.astype(np.int64)
+    co = np.arange(cout_pad)[:, None]; ch = np.arange(cin)[None, :]
+    nb, cr = co // 16, co % 16
+    real = np.zeros((16, cout_pad, cin), np.int64); re = np.zeros((10, cout_pad, cin), np.int64)
+    im = re.copy(); ok = True
+
+    def at(pack, row, kbyte):
+        return b[(nb * 9 + pack) * 5120 + tiled_offset(row, kbyte, 160)]
+
+    for gi, (kind, idx) in enumerate(groups):
+        sg = qk_sg_of(gi); pack, sp = sg // 2, sg % 2
+        base = 96 * sp
+        if kind == "real":
+            vp = gi - qk_sg_first(sg)
+            kb = sp * 16 + vp * 8 + ch
+            real[idx] = at(pack, base + 16 * vp + cr, kb) * 256 + at(pack, base + 32 + 16 * vp + cr, kb)
+            ok &= not at(pack, base + 16 * (1 - vp) + cr, kb).any()     # the other group's rows: 0 here
+        else:
+            k0, k1 = sp * 16 + ch, sp * 16 + 8 + ch
+            re[idx] = at(pack, base + cr, k0) * 256 + at(pack, base + 32 + cr, k0)
+            im[idx] = at(pack, base + 16 + cr, k0) * 256 + at(pack, base + 48 + cr, k0)
+            ok &= bool(np.array_equal(at(pack, base + cr, k1) * 256 + at(pack, base + 32 + cr, k1), -im[idx]))
+            ok &= bool(np.array_equal(at(pack, base + 16 + cr, k1) * 256 + at(pack, base + 48 + cr, k1), re[idx]))
+        other = (1 - sp) * 16 + ch            # the other slot's K half of this slot's rows
+        for r in range(4):
+            ok &= not at(pack, base + 16 * r + cr, other).any() and not at(pack, base + 16 * r + cr, other + 8).any()
+    for pack in range(9):
+        for r in (64, 80):
+            for kb in range(32):
+                ok &= not at(pack, r + cr, np.full_like(ch, kb)).any()
+    return real, re, im, ok
+
+
+def decode_v_qk(buf: np.ndarray, tiles: int, cin: int):
+    """Packed V [tile block][pack][piece hi (s8), lo (u8)][4 KB] -> (real [16][T][cin], re, im)."""
+    groups = fused_groups()
+    b = buf.astype(np.int64)
+    t = np.arange(tiles)[:, None]; ch = np.arange(cin)[None, :]
+    real = np.zeros((16, tiles, cin), np.int64); re = np.zeros((10, tiles, cin), np.int64); im = re.copy()
+
+    def val(pack, kbyte):
+        off = ((t // 128) * 9 + pack) * 8192 + tiled_offset(t % 128, kbyte, 128)
+        return b[off] * 256 + (b[off + 4096] & 255)
+
+    for gi, (kind, idx) in enumerate(groups):
+        sg = qk_sg_of(gi); pack, sp = sg // 2, sg % 2
+        if kind == "real":
+            real[idx] = val(pack, sp * 16 + (gi - qk_sg_first(sg)) * 8 + ch)
+        else:
+            re[idx], im[idx] = val(pack, sp * 16 + ch), val(pack, sp * 16 + 8 + ch)
+    return real, re, im

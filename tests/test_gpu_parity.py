@@ -56,7 +56,16 @@ def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates
         _, Wp, codes = O.filter_transform(w, layout, scaling=scaling)
         np.testing.assert_array_equal(conv.codes.cpu().numpy(), codes)
         wbuf = conv.w_wino.cpu().numpy()
-        if path == FUSED:
+        if path == FUSED and info.packing == 4:   # quarter-K packed W' (c_in <= 8)
+            wr, wre, wim, dup_ok = LD.decode_w_qk(wbuf, info.cout_pad, ci)
+            er, ere, eim = LD.complex_to_values(Wp)
+            np.testing.assert_array_equal(wr[:, :co], er)
+            np.testing.assert_array_equal(wre[:, :co], ere)
+            np.testing.assert_array_equal(wim[:, :co], eim)
+            assert dup_ok, "packed B: -Wi / Wr duplicates, zero rows and the other slot's K half"
+            for a_ in (wr, wre, wim):
+                assert not a_[:, co:, :].any()
+        elif path == FUSED:
             wr, wre, wim, dup_ok = LD.decode_w_fused(wbuf, info.cout_pad, info.cin_pad // 32, info.cin_pad)
             er, ere, eim = LD.complex_to_values(Wp)
             np.testing.assert_array_equal(wr[:, :co, :ci], er)
@@ -75,7 +84,8 @@ def _check_layer(x, w, layout, pad=1, scaling=True, chunk_mb=None, intermediates
             vbuf = conv.v_image().cpu().numpy()
             D = O.input_transform(x, pad, layout)
             if path == FUSED:
-                vr, vre, vim = LD.decode_v_fused(vbuf, T, info.cin_pad // 32, info.cin_pad)
+                vr, vre, vim = (LD.decode_v_qk(vbuf, T, ci) if info.packing == 4 else
+                                LD.decode_v_fused(vbuf, T, info.cin_pad // 32, info.cin_pad))
                 er, ere, eim = LD.complex_to_values(D)
                 np.testing.assert_array_equal(vr[:, :, :ci], er)
                 np.testing.assert_array_equal(vre[:, :, :ci], ere)
