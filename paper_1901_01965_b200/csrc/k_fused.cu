@@ -92,6 +92,23 @@ __device__ __forceinline__ int fg_pos(int gi) {
   return fg_complex(gi) ? cpx_pos(fg_primary(gi)) : real_pos(fg_real_plane(gi));
 }
 
+// barrier waits of the MMA issuer and of the epilogue's accumulator handshake: suspending try_wait, or a
+// non-suspending test_wait poll (no wake-up latency after the phase flips) under WINO_SPIN_MMA / WINO_SPIN_EPI
+__device__ __forceinline__ void mma_wait(uint32_t bar, uint32_t parity) {
+#ifdef WINO_SPIN_MMA
+  mbar_spin(bar, parity);
+#else
+  mbar_wait(bar, parity);
+#endif
+}
+__device__ __forceinline__ void epi_wait(uint32_t bar, uint32_t parity) {
+#ifdef WINO_SPIN_EPI
+  mbar_spin(bar, parity);
+#else
+  mbar_wait(bar, parity);
+#endif
+}
+
 __device__ __forceinline__ void fepi_barrier() {
   asm volatile("bar.sync %0, %1;" ::"n"(kFEpiBar), "n"(kFEpiWarps * 32) : "memory");
 }
@@ -400,9 +417,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
           for (int pk = 0; pk < kQkPacks; pk++, it++, sgc += 2) {
             const int s = it % kFStages;
             const int b = sgc % kFSlots;            // even: slots b, b + 1 are adjacent
-            mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
-            mbar_wait(tempty0 + 8 * (b + 1), (((sgc + 1) / kFSlots) & 1) ^ 1);
-            mbar_wait(full0 + 8 * s, (it / kFStages) & 1);
+            mma_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
+            mma_wait(tempty0 + 8 * (b + 1), (((sgc + 1) / kFSlots) & 1) ^ 1);
+            mma_wait(full0 + 8 * s, (it / kFStages) & 1);
             tc_fence_after();
             if (it < 64 && lane == 0) FTRACE(it, 1);
             if (sgc < 32 && lane == 0) FTRACE(64 + sgc, 0);
@@ -411,7 +428,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
             if (elect_one()) {
               if (!(dbg & 2)) {
                 const uint64_t bw = dsc(st + kQkPackV);
-                umma_i8(d0, dsc(st), bw, id160, 1u);                       // hi: [slot b: ... | 0 | slot b+1]
+                // hi, accumulate off: writes columns [0, 160) of the slot pair (slot b whole, its s0 block from the
+                // zero rows; slot b+1 s16 / s8), so only slot b+1's s0 block [160, 192) must start at zero
+                umma_i8(d0, dsc(st), bw, id160, 0u);                       // hi: [slot b: ... | 0 | slot b+1]
                 umma_i8(d0 + 32, dsc(st + kVBlockBytes), bw, id160u, 1u);  // lo (u8) at the piece offset 32
               }
               umma_commit(tfull0 + 8 * b);
@@ -431,7 +450,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
           for (int pr = 0; pr < kFSlotGroups / 2; pr++, it++) {
             const int s = it % kFStages;
-            mbar_wait(full0 + 8 * s, (it / kFStages) & 1);
+            mma_wait(full0 + 8 * s, (it / kFStages) & 1);
             tc_fence_after();
             if (it < 64 && lane == 0) FTRACE(it, 1);
             uint32_t voff = s * kFStageBytes, woff = s * kFStageBytes + kSV;
@@ -439,7 +458,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             for (int h = 0; h < 2; h++, sgc++) {
               const int sg = 2 * pr + h;
               const int b = sgc % kFSlots;
-              mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
+              mma_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
               tc_fence_after();
               if (sgc < 32 && lane == 0) FTRACE(64 + sgc, 0);
               const uint32_t d0 = tmem + b * kFSlotCols;
@@ -476,13 +495,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
           for (int sg = 0; sg < kFSlotGroups; sg++, sgc++) {
             const int b = sgc % kFSlots;
-            mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
+            mma_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
             tc_fence_after();
             const int g0 = sg_first(sg), ng = sg_count(sg);
             const uint32_t d0 = tmem + b * kFSlotCols;
             for (int k0 = 0; k0 < ksteps; k0 += 4, it++) {
               const int s = it & 1;
-              mbar_wait(full0 + 8 * s, (it >> 1) & 1);
+              mma_wait(full0 + 8 * s, (it >> 1) & 1);
               tc_fence_after();
               const int kn = min(4, ksteps - k0);
               const uint32_t st = sbase + s * kSB;
@@ -533,12 +552,12 @@ __global__ void __launch_bounds__(kFThreads, 1)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
           for (int sg = 0; sg < kFSlotGroups; sg++, sgc++, it++) {   // one stage per slot-group
             const int b = sgc % kFSlots;
-            mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
+            mma_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);
             tc_fence_after();
             if (sgc < 32 && lane == 0) FTRACE(64 + sgc, 0);
             const int ng = sg_count(sg);
             const int s = it % kMgStages;
-            mbar_wait(full0 + 8 * s, (it / kMgStages) & 1);
+            mma_wait(full0 + 8 * s, (it / kMgStages) & 1);
             tc_fence_after();
             if (it < 64 && lane == 0) FTRACE(it, 1);
             const uint32_t st = s * kMgStageBytes;   // stage offset from the ring base
@@ -579,7 +598,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         for (int sg = 0; sg < kFSlotGroups; sg++, sgc++) {
           const int b = sgc % kFSlots;
-          mbar_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);   // epilogue drained this slot
+          mma_wait(tempty0 + 8 * b, ((sgc / kFSlots) & 1) ^ 1);   // epilogue drained this slot
           tc_fence_after();
           if (sgc < 32 && lane == 0) FTRACE(64 + sgc, 0);
           const int g0 = sg_first(sg), ng = sg_count(sg);
@@ -590,7 +609,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             const uint32_t d = tmem + b * kFSlotCols + q * 48;
             for (int k0 = 0; k0 < ksteps; k0 += kc, it++) {
               const int s = it % kFStages;
-              mbar_wait(full0 + 8 * s, (it / kFStages) & 1);
+              mma_wait(full0 + 8 * s, (it / kFStages) & 1);
               tc_fence_after();
               if (it < 64 && lane == 0) FTRACE(it, 1);
               const int kn = min(kc, ksteps - k0);
@@ -659,14 +678,20 @@ __global__ void __launch_bounds__(kFThreads, 1)
     };
     auto slot_wait = [&]() -> uint32_t {
       const int b = sgc % kFSlots;
-      mbar_wait(tfull0 + 8 * b, (sgc / kFSlots) & 1);
+      epi_wait(tfull0 + 8 * b, (sgc / kFSlots) & 1);
       tc_fence_after();
       if (warp == 0 && lane == 0 && sgc < 32) FTRACE(64 + sgc, 1);
       return lane_base + b * kFSlotCols;
     };
     auto zero_slot = [&](uint32_t a) {   // MG variants: the columns this warp read, back to zero
       if (dbg & 16) return;              // debug builds only: no re-zeroing (results wrong; timing)
-      if constexpr (MG > 0) {
+      if constexpr (MG == 5) {   // the pack's first UMMA overwrites all but the odd slot's s0 block
+        if (sgc & 1) {
+          tmem_zero4(a + 64);
+          tmem_zero4(a + 80);
+          tmem_st_wait();
+        }
+      } else if constexpr (MG > 0) {
 #pragma unroll
         for (int blk = 0; blk < 6; blk++) tmem_zero4(a + blk * 16);
         tmem_st_wait();
@@ -679,8 +704,12 @@ __global__ void __launch_bounds__(kFThreads, 1)
       if (warp == 0 && lane == 0 && sgc < 32) FTRACE(64 + sgc, 2);
       sgc++;
     };
-    auto rscale = [&](int32_t (&v)[4], int gi) {
-      const uint4 m = *reinterpret_cast<const uint4*>(etab + gi * kFN + cw * kFC);
+    auto etab_ld = [&](int gi) -> uint4 { return *reinterpret_cast<const uint4*>(etab + gi * kFN + cw * kFC); };
+    auto rscale = [&](int32_t (&v)[4], const uint4 m) {
+      if (dbg & 128) {   // debug builds only: no reverse scaling (results wrong; timing)
+        v[0] += m.x; v[1] += m.y; v[2] += m.z; v[3] += m.w;
+        return;
+      }
       v[0] = frscale(v[0], m.x);
       v[1] = frscale(v[1], m.y);
       v[2] = frscale(v[2], m.z);
@@ -688,6 +717,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
     };
     // two real groups of one slot: M of both, reverse scaled
     auto take_real2 = [&](int gi, int32_t (&m0)[4], int32_t (&m1)[4]) {
+      // the m' loads go ahead of the slot wait (the barrier asm is a compiler fence): their latency hides there
+      const uint4 ma = etab_ld(gi), mb = etab_ld(gi + 1);
       const uint32_t a = slot_wait();
       uint32_t h0[4], x0[4], l0[4], h1[4], x1[4], l1[4];
       if (dbg & 32) {   // debug builds only: no accumulator loads (results wrong; timing)
@@ -708,10 +739,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
       slot_release();
       combine(h0, x0, l0, m0);
       combine(h1, x1, l1, m1);
-      rscale(m0, gi);
-      rscale(m1, gi + 1);
+      rscale(m0, ma);
+      rscale(m1, mb);
     };
     auto take_cpx = [&](int gi, int32_t (&re)[4], int32_t (&im)[4]) {
+      const uint4 m = etab_ld(gi);
       const uint32_t a = slot_wait();
       uint32_t rh[4], ih[4], rx[4], ix[4], rl[4], il[4];
       if (dbg & 32) {   // debug builds only: no accumulator loads (results wrong; timing)
@@ -730,8 +762,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
       slot_release();
       combine(rh, rx, rl, re);
       combine(ih, ix, il, im);
-      rscale(re, gi);
-      rscale(im, gi);
+      rscale(re, m);
+      rscale(im, m);
     };
     // Z of real row R[ri] (processing slot k): real (r, cc) adds a_j[cc] M''; the pair adds 2 Re(i^j z)
     // int8 NHWC output of a unit, staged in `part` as [px][tile][16 couts]: 16-byte chunks to global.
@@ -772,14 +804,17 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const int ti = fdiv(tt, g.dv_tpi), rem = tt - ti * g.tpi, ty = fdiv(rem, g.dv_tw);
         const int oyb = 4 * ty, oxb = 4 * (rem - ty * g.tw);
         int8_t* base = static_cast<int8_t*>(y) + (long long)(n0 + ti) * g.ho * g.wo * g.cout + nb * kFN;
+        constexpr int kQ = (16 * kMBlock) / (kFEpiWarps * 32);
+        uint4 val[kQ];
 #pragma unroll
-        for (int q = 0; q < (16 * kMBlock) / (kFEpiWarps * 32); q++) {
-          const int ch = etid + q * kFEpiWarps * 32;
-          const int px = ch >> 7;
+        for (int q = 0; q < kQ; q++)   // all staging loads first: one LDS latency instead of kQ
+          val[q] = *reinterpret_cast<const uint4*>(part + (etid + q * kFEpiWarps * 32) * 16);
+#pragma unroll
+        for (int q = 0; q < kQ; q++) {
+          const int px = (etid + q * kFEpiWarps * 32) >> 7;
           const int oy = oyb + (px >> 2), ox = oxb + (px & 3);
           if (oy >= g.ho || ox >= g.wo) continue;
-          const uint4 val = unswizzle(*reinterpret_cast<const uint4*>(part + ch * 16), rr);
-          *reinterpret_cast<uint4*>(base + ((long long)oy * g.wo + ox) * g.cout) = val;
+          *reinterpret_cast<uint4*>(base + ((long long)oy * g.wo + ox) * g.cout) = unswizzle(val[q], rr);
         }
       }
     };
