@@ -303,7 +303,7 @@ def test_fused_pool_output_mode(path, shape):
 
 
 @pytest.mark.parametrize("path", PATHS)
-@pytest.mark.parametrize("variant", ["i32", "i8_lanes", "pool", "f2", "u8"])
+@pytest.mark.parametrize("variant", ["i32", "i8_lanes", "pool", "f2", "u8", "qk"])
 def test_kernels_write_only_inside_their_buffers(path, variant):
     """compute-sanitizer is closed on this pool, so out-of-bounds WRITES are caught with canaries: every
     device buffer the library writes (W', codes, workspace, y) sits inside a larger allocation whose 4 KB
@@ -313,6 +313,8 @@ def test_kernels_write_only_inside_their_buffers(path, variant):
     L = W._lib
     rng = np.random.default_rng(71)
     n, h, w_, ci, co = 3, 30, 34, 40, 32
+    if variant == "qk":   # c_in <= 8: quarter-K packed V and W' on the fused path
+        ci = 5
     x, w = synth.random_layer(rng, n, h, w_, ci, co, O.NHWC)
     kw = dict(path=path)
     out_mode = W.WINO_OUT_INT32
