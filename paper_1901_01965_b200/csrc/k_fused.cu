@@ -1114,6 +1114,8 @@ static int g_fused_dbg = 0;
 // freed SMs run the other streams' kernels for the whole launch (C2 190.7 -> 203.1, C3 310.7 -> 332.1 TOPS
 // with three batches in flight); WINO_FUSED_BALANCE=0 restores the full grid (experiments)
 static int g_fused_balance = 1;
+// WINO_FUSED_MAXCTA: cap on the fused kernel's grid, leaving SMs to the other lanes' kernels (experiments)
+static int g_fused_maxcta = 0;
 static int g_fused_merge = 4;   // WINO_FUSED_MERGE: 4 also two slot-groups per stage at c_in <= 32; 0 general loops only, 1 merged stages at c_in <= 64,
                                 // 2 also at c_in <= 128, 3 also 4-K-step slot-group stages above
 
@@ -1123,7 +1125,8 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
   if (g.nblk != kFN) return cudaErrorInvalidValue;
   const int tblocks = (int)(tiles_pad_launch / kMBlock);
   const int n_units = tblocks * (g.cout_pad / kFN);
-  int grid = n_units < g_fused_sms ? n_units : g_fused_sms;
+  const int cap = g_fused_maxcta > 0 && g_fused_maxcta < g_fused_sms ? g_fused_maxcta : g_fused_sms;
+  int grid = n_units < cap ? n_units : cap;
   if (g_fused_balance) {   // fewest CTAs with the same number of unit rounds: the rest of the SMs stay free
     const int rounds = (n_units + grid - 1) / grid;
     grid = (n_units + rounds - 1) / rounds;
@@ -1169,6 +1172,7 @@ cudaError_t setup_fused() {
   if (const char* d = std::getenv("WINO_FUSED_DBG")) g_fused_dbg = std::atoi(d);
   if (const char* d = std::getenv("WINO_FUSED_BALANCE")) g_fused_balance = std::atoi(d);
   if (const char* d = std::getenv("WINO_FUSED_MERGE")) g_fused_merge = std::atoi(d);
+  if (const char* d = std::getenv("WINO_FUSED_MAXCTA")) g_fused_maxcta = std::atoi(d);
   const int smem = (int)fused_smem_bytes();
 #define WINO_KF_ATTR(A, B, C)                                                                                     \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<A, B, C, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \

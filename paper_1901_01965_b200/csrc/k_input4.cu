@@ -50,21 +50,11 @@ __device__ __forceinline__ void store_val(int8_t* p_hi, uint32_t A, uint32_t B, 
   st32d(p_hi + kVBlockBytes, lo, dbg);
 }
 
-// QK: the quarter-K packed V image (c_in <= 8, layout.cuh): thread = (tile, 4 of the 8 channel slots), warp =
-// 16 tiles, CTA = one 128-tile block; the (group, value part) of a value selects its pack and K byte
-template <int KS, int MINB, bool QK = false>   // KS: g.ksteps as a compile-time constant (1, 2, 4, 8, 16; 0 = runtime)
-__global__ void __launch_bounds__(kI4Warps * 32, MINB)
-    k_input_transform_f4(Geom g, const int8_t* __restrict__ x, int n0, int imgs, int8_t* __restrict__ vimg, int dbg) {
-#ifndef WINO_K2_DBG
-  dbg = 0;   // ablation bits (debug builds only): 1 no V stores, 2 no x loads
-#endif
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = QK ? blockIdx.x * kMBlock + warp * 16 + (lane >> 1)
-                   : blockIdx.x * kI4TilesPerCta + warp * kI4TilesPerWarp + (lane >> 2);
-  const int c = QK ? 4 * (lane & 1) : blockIdx.y * kI4ChPerCta + 4 * (lane & 3);
-  pdl_trigger();
-  pdl_wait();   // x may come from the previous kernel; V may still be read by the previous GEMM
-
+// D = B^T d B of one (tile t, 4 channels c) patch w (SWAR-ready words: 4 int8 channels per pixel, 0 outside the
+// map) and the stores of its 36 values' pieces into the fused V image (or the quarter-K packed image, QK)
+template <int KS, bool QK>
+__device__ __forceinline__ void k2f_transform_store(const Geom& g, const uint32_t (&w)[36], int8_t* __restrict__ vimg,
+                                                    int t, int c, int dbg) {
   const int ksteps = KS ? KS : g.ksteps;
   const long long kst = (long long)ksteps * kVBlockBytes;
   int8_t* base = vimg + (long long)(t / kMBlock) * kVPiecesF * kst + tiled_offset(t % kMBlock, c & 31, kMBlock);
@@ -82,72 +72,6 @@ __global__ void __launch_bounds__(kI4Warps * 32, MINB)
       return gp(gi) + vp * 2 * kVBlockBytes;
     }
   };
-
-  const int tiles = imgs * g.tpi;
-  if (!QK && blockIdx.y * kI4ChPerCta >= g.cin) {   // a slice of padding channels only: V = 0 (both pieces)
-#pragma unroll
-    for (int gi = 0; gi < kFGroupsN; gi++) {
-      int8_t* p = gp(gi);
-#pragma unroll
-      for (int q = 0; q < 4; q++)
-        if (q < fg_pieces(gi)) st32(p + q * kVBlockBytes, 0u);
-    }
-    return;
-  }
-
-  // ---- gather the zero-padded 6x6 patch (4 channels per pixel word; 0 outside the map / past c_in)
-  uint32_t w[36];
-  {
-    int img = 0, iy0 = -1000000, ix0 = -1000000;
-    if (t < tiles) {
-      const int ti = fdiv(t, g.dv_tpi), rem = t - ti * g.tpi, ty = fdiv(rem, g.dv_tw);
-      img = n0 + ti;
-      iy0 = 4 * ty - g.pad;
-      ix0 = 4 * (rem - ty * g.tw) - g.pad;
-    }
-    const long long rstride = (long long)g.w * g.cin;
-    const int8_t* p0 = x + ((long long)img * g.h * g.w + (long long)iy0 * g.w + ix0) * g.cin + c;
-    const bool inside = t < tiles && c + 4 <= g.cin && iy0 >= 0 && iy0 + 6 <= g.h && ix0 >= 0 && ix0 + 6 <= g.w;
-    if (dbg & 2) {   // debug: no loads (a lane-dependent pattern instead)
-#pragma unroll
-      for (int i = 0; i < 36; i++) w[i] = (uint32_t)(t * 0x01010101u + i);
-    } else if ((g.cin & 3) == 0 && __all_sync(0xffffffffu, inside)) {
-      // interior warp: unpredicated 4-byte loads; column offsets b * c_in are immediates when c_in = 32 KS
-      const int cst = (KS > 0 && g.cin == 32 * KS) ? 32 * KS : g.cin;
-#pragma unroll
-      for (int a = 0; a < 6; a++) {
-        const int8_t* rp = p0 + a * rstride;
-#pragma unroll
-        for (int b = 0; b < 6; b++) w[a * 6 + b] = __ldg(reinterpret_cast<const uint32_t*>(rp + b * cst));
-      }
-    } else {
-      bool vx[6];
-#pragma unroll
-      for (int b = 0; b < 6; b++) vx[b] = t < tiles && ix0 + b >= 0 && ix0 + b < g.w;
-      const bool vec = (g.cin & 3) == 0 && c + 4 <= g.cin;
-#pragma unroll
-      for (int a = 0; a < 6; a++) {
-        const bool vy = iy0 + a >= 0 && iy0 + a < g.h;
-        const int8_t* rp = p0 + a * rstride;
-#pragma unroll
-        for (int b = 0; b < 6; b++) {
-          uint32_t v = 0u;
-          if (vy && vx[b]) {
-            const int8_t* pp = rp + (long long)b * g.cin;
-            if (vec) {
-              v = __ldg(reinterpret_cast<const uint32_t*>(pp));
-            } else {   // c_in % 4 != 0 or a partial quad: byte loads of the channels below c_in
-#pragma unroll
-              for (int j = 0; j < 4; j++)
-                if (c + j < g.cin) v |= (uint32_t)(uint8_t)__ldg(pp + j) << (8 * j);
-            }
-          }
-          w[a * 6 + b] = v;
-        }
-      }
-    }
-  }
-
   // ---- d' = B^T d per column on SWAR words: rows e0, e1, e2, e5 real, row 3 = ra + i rb
   uint32_t e0[6][2], e1[6][2], e2[6][2], e5[6][2], ra[6][2], rb[6][2];
 #pragma unroll
@@ -226,6 +150,99 @@ __global__ void __launch_bounds__(kI4Warps * 32, MINB)
   store_val(vp_addr(fg_of_primary(8), 1), q[1][0], q[1][1], dbg);
   store_val(vp_addr(fg_of_primary(9), 0), q[2][0], q[2][1], dbg);
   store_val(vp_addr(fg_of_primary(9), 1), q[3][0], q[3][1], dbg);
+}
+
+// a 16-channel slice past c_in: V = 0 (both pieces of every group) for (tile t, channels c..c+3)
+template <int KS>
+__device__ __forceinline__ void k2f_zero_slice(const Geom& g, int8_t* __restrict__ vimg, int t, int c) {
+  const int ksteps = KS ? KS : g.ksteps;
+  const long long kst = (long long)ksteps * kVBlockBytes;
+  int8_t* base = vimg + (long long)(t / kMBlock) * kVPiecesF * kst + tiled_offset(t % kMBlock, c & 31, kMBlock);
+  int8_t* base2 = base + (long long)((c >> 5) * 2) * kVBlockBytes;
+  int8_t* base4 = base + (long long)((c >> 5) * 4) * kVBlockBytes;
+#pragma unroll
+  for (int gi = 0; gi < kFGroupsN; gi++) {
+    int8_t* p = (fg_pieces(gi) == 2 ? base2 : base4) + fg_vprefix(gi) * kst;
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      if (q < fg_pieces(gi)) st32(p + q * kVBlockBytes, 0u);
+  }
+}
+
+// QK: the quarter-K packed V image (c_in <= 8, layout.cuh): thread = (tile, 4 of the 8 channel slots), warp =
+// 16 tiles, CTA = one 128-tile block; the (group, value part) of a value selects its pack and K byte
+template <int KS, int MINB, bool QK = false>   // KS: g.ksteps as a compile-time constant (1, 2, 4, 8, 16; 0 = runtime)
+__global__ void __launch_bounds__(kI4Warps * 32, MINB)
+    k_input_transform_f4(Geom g, const int8_t* __restrict__ x, int n0, int imgs, int8_t* __restrict__ vimg, int dbg) {
+#ifndef WINO_K2_DBG
+  dbg = 0;   // ablation bits (debug builds only): 1 no V stores, 2 no x loads
+#endif
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = QK ? blockIdx.x * kMBlock + warp * 16 + (lane >> 1)
+                   : blockIdx.x * kI4TilesPerCta + warp * kI4TilesPerWarp + (lane >> 2);
+  const int c = QK ? 4 * (lane & 1) : blockIdx.y * kI4ChPerCta + 4 * (lane & 3);
+  pdl_trigger();
+  pdl_wait();   // x may come from the previous kernel; V may still be read by the previous GEMM
+
+  const int tiles = imgs * g.tpi;
+  if (!QK && blockIdx.y * kI4ChPerCta >= g.cin) {   // a slice of padding channels only: V = 0 (both pieces)
+    k2f_zero_slice<KS>(g, vimg, t, c);
+    return;
+  }
+
+  // ---- gather the zero-padded 6x6 patch (4 channels per pixel word; 0 outside the map / past c_in)
+  uint32_t w[36];
+  {
+    int img = 0, iy0 = -1000000, ix0 = -1000000;
+    if (t < tiles) {
+      const int ti = fdiv(t, g.dv_tpi), rem = t - ti * g.tpi, ty = fdiv(rem, g.dv_tw);
+      img = n0 + ti;
+      iy0 = 4 * ty - g.pad;
+      ix0 = 4 * (rem - ty * g.tw) - g.pad;
+    }
+    const long long rstride = (long long)g.w * g.cin;
+    const int8_t* p0 = x + ((long long)img * g.h * g.w + (long long)iy0 * g.w + ix0) * g.cin + c;
+    const bool inside = t < tiles && c + 4 <= g.cin && iy0 >= 0 && iy0 + 6 <= g.h && ix0 >= 0 && ix0 + 6 <= g.w;
+    if (dbg & 2) {   // debug: no loads (a lane-dependent pattern instead)
+#pragma unroll
+      for (int i = 0; i < 36; i++) w[i] = (uint32_t)(t * 0x01010101u + i);
+    } else if ((g.cin & 3) == 0 && __all_sync(0xffffffffu, inside)) {
+      // interior warp: unpredicated 4-byte loads; column offsets b * c_in are immediates when c_in = 32 KS
+      const int cst = (KS > 0 && g.cin == 32 * KS) ? 32 * KS : g.cin;
+#pragma unroll
+      for (int a = 0; a < 6; a++) {
+        const int8_t* rp = p0 + a * rstride;
+#pragma unroll
+        for (int b = 0; b < 6; b++) w[a * 6 + b] = __ldg(reinterpret_cast<const uint32_t*>(rp + b * cst));
+      }
+    } else {
+      bool vx[6];
+#pragma unroll
+      for (int b = 0; b < 6; b++) vx[b] = t < tiles && ix0 + b >= 0 && ix0 + b < g.w;
+      const bool vec = (g.cin & 3) == 0 && c + 4 <= g.cin;
+#pragma unroll
+      for (int a = 0; a < 6; a++) {
+        const bool vy = iy0 + a >= 0 && iy0 + a < g.h;
+        const int8_t* rp = p0 + a * rstride;
+#pragma unroll
+        for (int b = 0; b < 6; b++) {
+          uint32_t v = 0u;
+          if (vy && vx[b]) {
+            const int8_t* pp = rp + (long long)b * g.cin;
+            if (vec) {
+              v = __ldg(reinterpret_cast<const uint32_t*>(pp));
+            } else {   // c_in % 4 != 0 or a partial quad: byte loads of the channels below c_in
+#pragma unroll
+              for (int j = 0; j < 4; j++)
+                if (c + j < g.cin) v |= (uint32_t)(uint8_t)__ldg(pp + j) << (8 * j);
+            }
+          }
+          w[a * 6 + b] = v;
+        }
+      }
+    }
+  }
+  k2f_transform_store<KS, QK>(g, w, vimg, t, c, dbg);
 }
 
 cudaError_t launch_input_transform_f4(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg,
