@@ -1024,7 +1024,7 @@ def main():
     ap.add_argument("--streams", type=int, default=3,
                     help="C1-C4: independent batches in flight on separate streams (own filter/workspace buffers)")
     ap.add_argument("--path", default="auto", choices=["auto", "fused", "staged"],
-                    help="auto (the plan picks fused for c_in <= 256, staged otherwise)")
+                    help="auto (the plan picks fused for c_in <= 128, staged otherwise)")
     ap.add_argument("--input", default="i8", choices=["i8", "u8"],
                     help="u8: uint8 tensors with zero points (SURVEY f2; either algorithm and path, c_in <= 224)")
     ap.add_argument("--alg", default="f4", choices=["f4", "f2"],

@@ -93,7 +93,7 @@ typedef struct {
                              env WINO_CHUNK_MB).  Larger = fewer, longer launches.     */
     int path;             /* WINO_PATH_AUTO (0, the default everywhere -- this ABI, the
                              Python WinoConv2d and ConvStack): fused for F2x2, and for
-                             F4x4 when c_in <= 256 (target 255), else staged;
+                             F4x4 when c_in <= 128 (target 255), else staged;
                              wino_plan_info.path reports the choice.
                              WINO_PATH_FUSED (1): K2 input transform, then ONE kernel for
                              the GEMMs (4-multiplication complex form, 36 planes) +

@@ -96,7 +96,7 @@ bool k2f_legacy() {
 // WINO_PATH_AUTO's c_in limit for the fused path; WINO_AUTO_FUSED_CIN overrides (experiments)
 int auto_fused_max_cin() {
   const char* env = std::getenv("WINO_AUTO_FUSED_CIN");
-  return env ? std::atoi(env) : 256;
+  return env ? std::atoi(env) : 128;
 }
 
 size_t chunk_budget_bytes(int desc_mb) {
@@ -162,8 +162,9 @@ wino_status wino_plan(const wino_conv_desc* desc, int device, wino_plan_t* out) 
   if (desc->path != WINO_PATH_FUSED && desc->path != WINO_PATH_STAGED && desc->path != WINO_PATH_AUTO)
     return WINO_ERR_INVALID_ARG;
   // WINO_PATH_AUTO (the default, 0): the fused kernels where they measured faster -- the complex F(4x4) one at
-  // c_in <= 256 (C2-C4; tools/path_ab.py), the rational F(2x2) one everywhere (C2-C4: 1.4-1.7x the staged
-  // path) -- for target 255; else staged
+  // c_in <= 128 (C2, C3, VGG-16 layers 1-5; at c_in = 256 the staged path won in r02: C4 435 vs 420 TOPS,
+  // VGG-16 layers 6-8 1348 / 1327 / 636 vs 1538 / 1484 / 657 us), the rational F(2x2) one everywhere (C2-C4:
+  // 1.4-1.7x the staged path) -- for target 255; else staged
   wino_conv_desc dr = *desc;
   if (dr.path == WINO_PATH_AUTO)
     dr.path = (dr.filter_target_max == 255 &&
