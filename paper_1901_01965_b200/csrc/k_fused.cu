@@ -814,6 +814,15 @@ __global__ void __launch_bounds__(kFThreads, 1)
           const int px = (etid + q * kFEpiWarps * 32) >> 7;
           const int oy = oyb + (px >> 2), ox = oxb + (px & 3);
           if (oy >= g.ho || ox >= g.wo) continue;
+          if (dbg & 4096) {   // debug: the same stores to linear (fully coalesced) addresses
+            *reinterpret_cast<uint4*>(static_cast<int8_t*>(y) +
+                                      ((((long long)tb_i * (g.cout_pad / kFN) + nb) * kQ + q) * 512 + etid) * 16) = val[q];
+            continue;
+          }
+          if (dbg & 8192) {   // debug: streaming (evict-first) stores
+            __stcs(reinterpret_cast<uint4*>(base + ((long long)oy * g.wo + ox) * g.cout), unswizzle(val[q], rr));
+            continue;
+          }
           *reinterpret_cast<uint4*>(base + ((long long)oy * g.wo + ox) * g.cout) = unswizzle(val[q], rr);
         }
       }
@@ -828,7 +837,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         for (int c = 0; c < 4; c++) Z[j][c] = areal(j, 0) * m0[c] + areal(j, 1) * m1[c];
       take_real2(gb + 2, m0, m1);   // cc = 2, 5
       if (k == 0 && pending) {      // the previous unit's output, then nobody reads the staging any more
-        store_staged(pend_tb, pend_nb);
+        if (!(dbg & (256 | 2048))) store_staged(pend_tb, pend_nb);
         fepi_barrier();
         pending = false;
       }
@@ -873,10 +882,12 @@ __global__ void __launch_bounds__(kFThreads, 1)
           int32_t Z[4][4];
           real_row(0, Z);                              // row 0 -> Z_0
 #pragma unroll
-          for (int j = 0; j < 4; j++) *part_ptr(0, j) = make_int4(Z[j][0], Z[j][1], Z[j][2], Z[j][3]);
+          for (int j = 0; j < 4; j++)
+            if (!(dbg & (256 | 512))) *part_ptr(0, j) = make_int4(Z[j][0], Z[j][1], Z[j][2], Z[j][3]);
           real_row(1, Z);                              // row 5 -> Z_5
 #pragma unroll
-          for (int j = 0; j < 4; j++) *part_ptr(1, j) = make_int4(Z[j][0], Z[j][1], Z[j][2], Z[j][3]);
+          for (int j = 0; j < 4; j++)
+            if (!(dbg & (256 | 512))) *part_ptr(1, j) = make_int4(Z[j][0], Z[j][1], Z[j][2], Z[j][3]);
         }
         {
           int32_t Z1[4][4], Z2[4][4];
@@ -933,7 +944,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-          const int4 z0 = *part_ptr(0, j), z5 = *part_ptr(1, j);
+          const int4 z0 = (dbg & (256 | 512)) ? make_int4(j, 0, 0, 0) : *part_ptr(0, j);
+          const int4 z5 = (dbg & (256 | 512)) ? make_int4(0, j, 0, 0) : *part_ptr(1, j);
           const int32_t a0[4] = {z0.x, z0.y, z0.z, z0.w}, a5[4] = {z5.x, z5.y, z5.z, z5.w};
 #pragma unroll
           for (int c = 0; c < 4; c++) {
@@ -1004,7 +1016,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
                                         : __byte_perm(__byte_perm((uint32_t)outv(Yi[j][0]), (uint32_t)outv(Yi[j][1]), 0x0040),
                                                       __byte_perm((uint32_t)outv(Yi[j][2]), (uint32_t)outv(Yi[j][3]), 0x0040),
                                                       0x5410);
-              *reinterpret_cast<uint32_t*>(part + ((i * 4 + j) * kMBlock + row) * 16 + stg_word) = w;
+              if (!(dbg & (256 | 1024)) || w == 0x12345678u)   // debug bits 256/1024: no staging (kept live)
+                *reinterpret_cast<uint32_t*>(part + ((i * 4 + j) * kMBlock + row) * 16 + stg_word) = w;
             }
             return;
           }
@@ -1095,7 +1108,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         }
         if (warp == 0 && lane == 0) FTRACE(uc * 8 + 5, 3);
       }
-      if (pending) store_staged(pend_tb, pend_nb);
+      if (pending && !(dbg & (256 | 2048))) store_staged(pend_tb, pend_nb);
     }
   }
   tc_fence_before();
@@ -1108,7 +1121,9 @@ static int g_fused_sms = 0;
 static uint64_t* g_fused_trace = nullptr;
 void set_fused_trace(void* buf) { g_fused_trace = static_cast<uint64_t*>(buf); }
 // WINO_FUSED_DBG env (debug builds with -DWINO_FUSED_DBG only): 2 no MMAs, 4 no copies (MG > 0), 8 epilogue
-// handshake only
+// handshake only, 16 no TMEM re-zeroing, 32 no accumulator loads, 64 one UMMA per group, 128 no reverse-scale
+// multiply, 256 no epilogue shared-memory traffic (= 512 no Z_0/Z_5 parking + 1024 no output staging + 2048 no
+// staged output stores), 4096 output stores to linear addresses, 8192 streaming (.cs) output stores
 static int g_fused_dbg = 0;
 // fewest CTAs for the same number of unit rounds (C2: 196 units -> 98 CTAs x 2 instead of 148 + 48): the
 // freed SMs run the other streams' kernels for the whole launch (C2 190.7 -> 203.1, C3 310.7 -> 332.1 TOPS
