@@ -159,9 +159,27 @@ def _spawn_ranks(args):
     return subprocess.call(cmd)
 
 
+def _phase(name):
+    """WINO_BENCH_TRACE=1: per-rank progress on stderr (debugging multi-rank runs)."""
+    if os.environ.get("WINO_BENCH_TRACE"):
+        print(f"[rank {os.environ.get('RANK', 0)}] {time.strftime('%H:%M:%S')} {name}", file=sys.stderr, flush=True)
+
+
+def _device_index(local_rank):
+    """This rank's GPU: LOCAL_RANK, or round-robin over the visible GPUs in the gloo validation mode."""
+    import torch
+    if os.environ.get("WINO_DIST_BACKEND", "nccl") == "gloo":
+        return local_rank % max(1, torch.cuda.device_count())
+    return local_rank
+
+
 def _init_dist(world, local_rank, backend="nccl"):
+    """The process group of a multi-rank run (None at world size 1).  WINO_DIST_BACKEND=gloo replaces NCCL
+    (a validation mode: with fewer GPUs than ranks, ranks share devices round-robin; the path has no
+    data-path collective, so their kernels never wait on one another -- timings are then not per-GPU)."""
     import torch
     import torch.distributed as dist
+    backend = os.environ.get("WINO_DIST_BACKEND", backend)
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
@@ -391,6 +409,7 @@ def run_ours(args):
 
     rank, local_rank, world = _env_rank()
     dist = _init_dist(world, local_rank)
+    local_rank = _device_index(local_rank)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     cfg = synth.CONFIGS[args.config]
@@ -410,12 +429,17 @@ def run_ours(args):
     xs, ws, ys, lanes, graphs, graphs_nok1 = [], [], [], [], {}, {}
     conv = None
     n_sets = 1
+    l2_label = "empty shard on rank 0"
     if not empty:
         conv = W.WinoConv2d(sh["n"], layer.h, layer.w, layer.c_in, sh["co"], layer.pad, W.WINO_NHWC, layer.scaling,
                             W.WINO_OUT_INT8, **mk)
         info = conv.info
         per_set = info.x_bytes + sh["co"] * 9 * layer.c_in + info.y_bytes
-        n_sets = max(2, math.ceil(1.2 * L2_BYTES / per_set))
+        # rotate enough input sets to exceed L2; capped at 64 (C1, the parity-size case, and its Cout shards
+        # would need thousands -- each one a captured graph per lane): those runs are labelled L2-resident
+        n_sets = min(64, max(2, math.ceil(1.2 * L2_BYTES / per_set)))
+        l2_label = (f"inputs/weights/outputs rotated over {n_sets} sets (> 126 MiB L2)" if n_sets * per_set > L2_BYTES
+                    else f"{n_sets} input sets of {per_set} B: L2-resident (parity-size config, not a bench line)")
         for i in range(n_sets):
             # global tensors of set i (the seeded config for i = 0), this rank's slice
             x, w = synth.config_inputs(args.config, rank=i if args.scaling == "strong" else rank * 1000 + i)
@@ -471,17 +495,20 @@ def run_ours(args):
             return None
 
     launches_per_step = 0 if empty else 1 + conv.info.stages * conv.info.n_chunks
+    _phase("timed")
     # ---------------- the timed region: exactly K steps
     with ClockSampler(local_rank) as clk:
         t_max = _timed(streams, lambda: run_steps(args.steps), dist, dev)
     value = job_ops * args.steps / t_max / 1e12
     per_step = t_max / args.steps
+    _phase("trials")
     # ---------------- outside the timed region: trials, K1 split, single-stream latency
     trials = _trials(run_steps, per_step, job_ops, dist, streams, dev)
     t_nok1 = _timed(streams, lambda: run_steps(args.steps, graphs_nok1), dist, dev)
     n_single = max(20, args.steps // 10)
     t_single = _timed(streams[:1], lambda: run_steps(n_single, graphs, 1), dist, dev)
     single_ms = t_single * 1e3 / n_single
+    _phase("profile")
     kern = profile_kernels(conv, xs, ws, ys, S, streams[0], n_sets, 60) if not empty else {}
     # ---------------- self-check of the timed graphs' output: set 0 (lane 0), this rank's first image
     self_check = None
@@ -490,6 +517,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         if rank == 0:
             self_check = _self_check_layer(args, layer, sh, ys[0], S, u8, zp)
+    _phase("gather")
     # ---------------- partitioned runs: gather the outputs of set 0 (checking only) and compare them with
     # rank 0's single-GPU run of the whole problem
     sharded_check = None
@@ -507,8 +535,9 @@ def run_ours(args):
             y_one = cf(torch.from_numpy(np.ascontiguousarray(to_in(xf))).to(dev), 1, S)
             sharded_check = {"mode": sh["mode"], "gathered_bytes": int(y_all.numel()),
                              "empty_ranks": int(n_empty.item()),
-                             "collective": "all_gather_into_tensor (NCCL), checking only",
+                             "collective": f"all_gather_into_tensor ({dist.get_backend()}), checking only",
                              "equal_to_single_gpu": bool(torch.equal(y_all, y_one))}
+    _phase("e2e")
     scal_err = scaling_error(W, conv, layer, xs[0], ws[0], S, path, dev) if rank == 0 and not empty else None
     e2e = run_e2e(conv, xs, ws, S, streams[0], n_sets, max(3, min(args.steps, 100)), dist, dev, job_ops, empty,
                   n_streams=args.e2e_streams)
@@ -547,7 +576,7 @@ def run_ours(args):
                 "filter_target_max": args.target if layer.scaling else None,
                 "algorithm": "F(2x2,3x3) rational (SURVEY f1)" if info.algorithm == 1 else
                              "F(4x4,3x3) complex (Gaussian integers)",
-                "l2": f"inputs/weights/outputs rotated over {n_sets} sets (> 126 MiB L2)",
+                "l2": l2_label,
                 "parallelism": f"dp{world}: " + (f"{sh['mode']}-partitioned (strong scaling)" if args.scaling == "strong"
                                                  else "replicated per-rank batches (weak scaling)") +
                                "; no data-path collective",
@@ -725,6 +754,7 @@ def run_ours_stack(args):
 
     rank, local_rank, world = _env_rank()
     dist = _init_dist(world, local_rank)
+    local_rank = _device_index(local_rank)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     cfg = synth.CONFIGS["C5"]
