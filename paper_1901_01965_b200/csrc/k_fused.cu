@@ -8,8 +8,10 @@
 //
 // Operands (layout.cuh, "fused-path operand layouts"): per GROUP (a real
 // position, or a complex primary with its conjugate mirror implied),
-// balanced s8 pieces v = 256 hi + lo, group-contiguous so a stage is ONE bulk
-// copy of V (<= 32 KB) and one of W'.  The complex product uses the
+// pieces v = 256 hi + lo (V: hi = v >> 8 s8, lo = v & 255 u8, read as an unsigned
+// A operand; W': balanced s8 hi and lo), group-contiguous so a stage is ONE bulk
+// copy of V (<= 32 KB) and one of W'.  At c_in <= 8 two slot-groups share a K step
+// (quarter-K packing, layout.cuh, MG = 5).  The complex product uses the
 // 4-multiplication form as K/N-concatenated real GEMMs (identical integers to
 // the Karatsuba form of P:83-86, which the staged path implements):
 //   Re = Vr Wr - Vi Wi,  Im = Vr Wi + Vi Wr.
@@ -21,9 +23,10 @@
 //                               A = Vi hi . B1, A = Vi lo . B1 (offset 32)
 //   B0 = [Wr hi | Wi hi | Wr lo | Wi lo], B1 = [-Wi hi | Wr hi | -Wi lo | Wr lo]
 //   -> D[Re16 | Im16 | Re8 | Im8 | Re0 | Im0]; M = 2^16 s16 + 2^8 s8 + s0 (mod 2^32
-//   exact; the true values fit, A23).  On the first K step the overlapping
+//   exact; the true values fit, A23).  MG = 0: on the first K step the overlapping
 //   column blocks are initialised by splitting one UMMA (accumulate flag is per
-//   UMMA, not per column).
+//   UMMA, not per column); MG > 0: every slot starts at zero (the epilogue re-zeroes
+//   what it read) and every UMMA accumulates.
 //
 // Work unit = (128-tile block, 16-cout block): all 26 groups, row by row of the
 // 6x6 Winograd grid in the order rows 0, 5, 1, 2 (real (r,0) (r,1) (r,2) (r,5),
@@ -43,7 +46,9 @@
 //   warp 18      MMA issuer (one elected lane): tcgen05.mma into 4 TMEM accumulator slots of 96
 //                columns (one complex group or two real groups each)
 // Ring (160 KB): MG = 0 four 40 KB stages (a group's K chunk each), MG = 1 four 40 KB stages and
-// MG = 2 two 80 KB stages (one slot-group each), MG = 3 two 80 KB stages (4 K steps of a slot-group).
+// MG = 2 two 80 KB stages (one slot-group each), MG = 3 two 80 KB stages (4 K steps of a slot-group),
+// MG = 4 (one K step) four 40 KB stages of two slot-groups each, MG = 5 (quarter-K packing) four stages
+// of one 13 KB pack each (two slot-groups, one N = 160 UMMA pair).
 // TMEM: [0, 384) accumulator slots, [384, 448) P, [448, 512) Q.
 #include <cstdint>
 #include <cstdlib>

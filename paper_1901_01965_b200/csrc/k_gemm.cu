@@ -2,11 +2,14 @@
 // tcgen05 tensor cores.
 //
 // For each of the 46 operand planes p:  M_p[tiles x Cout] = V_p . W'_p
-// (kind::i8, int32 accumulation in TMEM).  Every operand is split into an s8
-// high and a u8 low piece (layout.cuh), so one plane is four UMMAs per
-// 32-channel K step into three TMEM accumulators
-//     acc_hh += Vhi.Whi   acc_x += Vhi.Wlo + Vlo.Whi   acc_ll += Vlo.Wlo
-// and M_p = 2^16 acc_hh + 2^8 acc_x + acc_ll (exact mod 2^32; the true values
+// (kind::i8, int32 accumulation in TMEM).  Every operand value v is split into
+// two balanced s8 pieces v = 256 hi + lo (layout.cuh), and W' is stored as
+// B = [W hi | W lo] (2 n_block rows), so one plane is two N-concatenated UMMAs
+// per 32-channel K step into three adjacent TMEM column blocks [hh | x | ll]:
+//     A = V hi . [W hi | W lo] -> [hh | x],   A = V lo . [W hi | W lo] -> [x | ll]
+// (the second at column offset n_block; on the first K step the overlap is
+// initialised by splitting it, the accumulate flag being per UMMA), and
+// M_p = 2^16 acc_hh + 2^8 acc_x + acc_ll (exact mod 2^32; the true values
 // fit int32 for the plan's Cin limits, A23).
 //
 // Work unit = (Winograd position, 128-tile block, n_block-cout block).  A real

@@ -8,11 +8,12 @@
 // contiguous 64-byte run.  Per channel only the 16 real values and the 10
 // conjugate primaries are formed: d' = B^T d column by column,
 // then the same combinations along each row of d'.  The two channels'
-// values v0, v1 of a plane are packed with one PRMT into
-// [lo0, lo1, hi0, hi1] (lo = v & 255, hi = v >> 8 as int8 -- the low two
-// bytes of the two's complement int32) and stored as two 16-bit halves.
-// All 92 plane-pieces of a (tile block, K step) are 4 KB apart, so every
-// store is an immediate offset from one base pointer.
+// values v0, v1 of a plane become balanced s8 pieces v = 256 hi + lo
+// (lo = byte 0 of v read as s8, hi = byte 1 of v + 128: two PRMTs on v + 128)
+// stored as two 16-bit pairs [hi0, hi1] and [lo0, lo1], 4 KB apart (staged
+// layout; the fused layout's two-channel variant below keeps lo = v & 255 as
+// u8 and hi = v >> 8).  All 92 plane-pieces of a (tile block, K step) are
+// 4 KB apart, so every store is an immediate offset from one base pointer.
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const
 // ---- fused-path V image (layout.cuh "fused-path operand layouts"): per group, pieces hi = v >> 8 (s8,
 // byte 1 of v) and lo = v & 255 (u8, byte 0 of v; the fused GEMM reads lo as an unsigned A operand),
 // stored for both channels.  (NCHW and uint8 input; NHWC int8 runs k_input4.cu.)
-__device__ __forceinline__ void st_bal(int8_t* p_hi, int v0, int v1) {
+__device__ __forceinline__ void st_fused(int8_t* p_hi, int v0, int v1) {
   st16(p_hi, __byte_perm((uint32_t)v0, (uint32_t)v1, 0x0051));          // [hi0, hi1]
   st16(p_hi + 4096, __byte_perm((uint32_t)v0, (uint32_t)v1, 0x0040));   // [lo0, lo1]
 }
@@ -268,10 +269,10 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, con
     real_row_planes<ri>(e0, v0);
     real_row_planes<ri>(e1, v1);
 #pragma unroll
-    for (int s = 0; s < 4; s++) st_bal(gp(fg_of_real(ri * 4 + s)), v0[s], v1[s]);
+    for (int s = 0; s < 4; s++) st_fused(gp(fg_of_real(ri * 4 + s)), v0[s], v1[s]);
     int8_t* pc = gp(fg_of_primary(ri));
-    st_bal(pc, v0[4], v1[4]);                      // Re (R[ri], 3)
-    st_bal(pc + 2 * kVBlockBytes, v0[5], v1[5]);   // Im
+    st_fused(pc, v0[4], v1[4]);                      // Re (R[ri], 3)
+    st_fused(pc + 2 * kVBlockBytes, v0[5], v1[5]);   // Im
   };
   real_row(std::integral_constant<int, 0>{}, r[0].e0, r[1].e0);
   real_row(std::integral_constant<int, 1>{}, r[0].e1, r[1].e1);
@@ -294,16 +295,16 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, con
 #pragma unroll
   for (int j = 0; j < 4; j++) {
     int8_t* pc = gp(fg_of_primary(4 + j));
-    st_bal(pc, re[0][j], re[1][j]);
-    st_bal(pc + 2 * kVBlockBytes, im[0][j], im[1][j]);
+    st_fused(pc, re[0][j], re[1][j]);
+    st_fused(pc + 2 * kVBlockBytes, im[0][j], im[1][j]);
   }
   {
     int8_t* pc = gp(fg_of_primary(8));
-    st_bal(pc, q[0][0], q[1][0]);
-    st_bal(pc + 2 * kVBlockBytes, q[0][1], q[1][1]);
+    st_fused(pc, q[0][0], q[1][0]);
+    st_fused(pc + 2 * kVBlockBytes, q[0][1], q[1][1]);
     pc = gp(fg_of_primary(9));
-    st_bal(pc, q[0][2], q[1][2]);
-    st_bal(pc + 2 * kVBlockBytes, q[0][3], q[1][3]);
+    st_fused(pc, q[0][2], q[1][2]);
+    st_fused(pc + 2 * kVBlockBytes, q[0][3], q[1][3]);
   }
 }
 
