@@ -100,19 +100,27 @@ __device__ __forceinline__ uint64_t gtimer() {
 __host__ __device__ inline uint32_t gemm_stage_bytes(int nblk, int kps) {
   return 2u * kps * kABytesPerKStep + 2u * kps * (uint32_t)nblk * kKStep;
 }
-// stages + 2 staging tiles (128 x nblk int32) + barriers/LUT (1 KB) + codes [26][cout_pad]
-inline size_t gemm_smem_bytes(int nblk, int cout_pad, int stages, int kps) {
-  return (size_t)stages * gemm_stage_bytes(nblk, kps) + 2 * (size_t)kMBlock * nblk * 4 + 1024 +
-         (size_t)(kPrimaries + kRealPlanes) * cout_pad;
+// stages + nstg staging tiles (128 x nblk int32) + barriers/LUT (1 KB)
+inline size_t gemm_smem_bytes(int nblk, int stages, int kps, int nstg) {
+  return (size_t)stages * gemm_stage_bytes(nblk, kps) + (size_t)nstg * kMBlock * nblk * 4 + 1024;
 }
 constexpr int kMaxCoutPad = 2048;
 constexpr size_t kSmemLimit = 227 * 1024;
 // ring depth: loads in flight per SM are what hides the L2/HBM latency under load
 static int g_stages_cap = kMaxStages;   // WINO_K3_STAGES (experiments): cap on the ring depth
-inline int gemm_stages(int nblk, int cout_pad, int kps) {
+inline int gemm_stages(int nblk, int kps, int nstg) {
   int st = g_stages_cap;
-  while (st > kMinStages && gemm_smem_bytes(nblk, cout_pad, st, kps) > kSmemLimit) --st;
+  while (st > kMinStages && gemm_smem_bytes(nblk, st, kps, nstg) > kSmemLimit) --st;
   return st;
+}
+// output staging tiles: two (the epilogue writes tile t+1 while tile t's strip pass runs), or one when that
+// buys another ring stage and the plane has >= 16 K steps (c_in >= 512 at n_block = 64: 3 -> 4 stages of
+// 48 KB, VGG-16 layers 9-13 K3 -4 %; at c_in = 256 the extra barrier per tile costs more: layers 6-7 +8 %,
+// DESIGN.md 6b); the single buffer costs one more barrier per tile
+static int g_staging_override = 0;   // WINO_K3_STAGING = 1 or 2 (experiments)
+inline int gemm_staging_tiles(int nblk, int kps, int ksteps) {
+  if (g_staging_override == 1 || g_staging_override == 2) return g_staging_override;
+  return ksteps >= 16 && gemm_stages(nblk, kps, 1) > gemm_stages(nblk, kps, 2) ? 1 : 2;
 }
 // K steps per stage: 4 when the plane has that many (fewer stages and commits per plane: C4 K3
 // 43.8 -> 38.9 us), else the plane's whole K range (2 at C2).  WINO_K3_KPS overrides (experiments).
@@ -143,7 +151,7 @@ template <int NBLK, bool F2, bool W1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ Mraw,
            const uint8_t* __restrict__ codes, int cout, int scaling, int ksteps, long long tiles_pad, int tblocks,
-           int cout_pad, int cin_pad, int nst, int kps, uint64_t* __restrict__ trace, int dbg) {
+           int cout_pad, int cin_pad, int nst, int kps, int nstg, uint64_t* __restrict__ trace, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem[];
 #ifndef WINO_K3_DBG
   dbg = 0;   // the WINO_K3_DBG ablation modes exist only in debug builds (-DWINO_K3_DBG)
@@ -171,11 +179,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t a_bytes = kps * kABytesPerKStep;
   const uint32_t b_bytes = kps * (uint32_t)NBLK * kKStep;
   const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
-  uint8_t* staging = smem + nst * stage_bytes;                           // 2 x kTileBytes
-  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + 2 * kTileBytes);
+  uint8_t* staging = smem + nst * stage_bytes;                           // nstg x kTileBytes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + nstg * kTileBytes);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 4);
   uint32_t* lut = tmem_slot + 4;                                         // 128: code -> m' = m 2^(7-q)
-  uint8_t* s_codes = reinterpret_cast<uint8_t*>(lut + 128);              // [26 positions][cout_pad]
   const uint32_t sbase = smem_u32(smem);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kMaxStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * kMaxStages), tempty0 = smem_u32(bars + 2 * kMaxStages + 2);
@@ -207,11 +214,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     lut[threadIdx.x] = n >= 8 ? (uint32_t)m << (7 - q) : 128u;   // m' (rscale_e); code 0: identity
   }
   pdl_wait();   // V, W' and the codes come from the kernels just before
-  for (int i = threadIdx.x; i < Alg<F2>::kUnits * cout_pad; i += blockDim.x) {   // codes, position-major
-    const int pidx = i / cout_pad, co = i - pidx * cout_pad;
-    const int pos = F2 ? pidx : (pidx < kPrimaries ? cpx_pos(pidx) : real_pos(pidx - kPrimaries));
-    s_codes[i] = (scaling && co < cout) ? codes[(long long)co * Alg<F2>::kPos + pos] : 0;
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -354,8 +356,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // -> coalesced 16-byte global stores (a warp writes two whole rows of the tile).
     // Buffer (to & 1) was last read in the strip pass of tile to-2, which every
     // thread finished before arriving at the barrier of tile to-1.
-    auto store_tile = [&](const uint32_t (&v)[kHalf], int32_t* dst, const uint8_t* crow) {
-      int4* tile = reinterpret_cast<int4*>(staging + (to & 1) * kTileBytes);
+    auto store_tile = [&](const uint32_t (&v)[kHalf], int32_t* dst, uint32_t c4) {
+      int4* tile = reinterpret_cast<int4*>(staging + (nstg == 2 ? (to & 1) : 0) * kTileBytes);
 #pragma unroll
       for (int c = 0; c < kHalf; c += 4) {
         const int ch = (col0 + c) >> 2;
@@ -363,7 +365,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       epi_barrier();
       // M'' = rha(M m / 2^q) on this thread's 4 columns (sc*4 .. sc*4+3)
-      const uint32_t c4 = reinterpret_cast<const uint32_t*>(crow)[sc];
       constexpr uint32_t kCm = W1 ? 0x7fu : 0x3fu;
       const uint32_t e0 = lut[c4 & kCm], e1 = lut[(c4 >> 8) & kCm], e2 = lut[(c4 >> 16) & kCm],
                      e3 = lut[(c4 >> 24) & kCm];
@@ -380,14 +381,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         gdst[slot] = make_int4(rscale_e((uint32_t)raw.x, e0), rscale_e((uint32_t)raw.y, e1),
                                rscale_e((uint32_t)raw.z, e2), rscale_e((uint32_t)raw.w, e3));
       }
+      if (nstg == 1) epi_barrier();   // one staging tile: every strip read before the next tile's writes
       if (warp == 0 && lane == 0) WINO_TRACE(pc - 1, 5);
       to++;
+    };
+    // the codes of this thread's 4 strip columns (couts nb*NBLK + 4 sc .. + 3) at position index pidx
+    auto strip_codes = [&](int pidx, int nb) -> uint32_t {
+      if (!scaling) return 0u;
+      const int pos = F2 ? pidx : (pidx < kPrimaries ? cpx_pos(pidx) : real_pos(pidx - kPrimaries));
+      uint32_t c4 = 0;
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int co = nb * NBLK + sc * 4 + i;
+        if (co < cout) c4 |= (uint32_t)__ldg(codes + (long long)co * Alg<F2>::kPos + pos) << (8 * i);
+      }
+      return c4;
     };
     for (int ku = 0, u = cta_unit(0); u < n_units; u = cta_unit(++ku)) {
       int pidx, tb, nb;
       decode_unit(u, tblocks, nblocks, pidx, tb, nb);
       const long long tile_off = ((long long)tb * nblocks + nb) * (kMBlock * NBLK);
-      const uint8_t* crow = s_codes + pidx * cout_pad + nb * NBLK;
+      const uint32_t crow = strip_codes(pidx, nb);
       if (dbg & 2) {                               // debug timing only: drain the accumulators, no tiles
         uint32_t v[kHalf];
         for (int pl = 0; pl < unit_planes<F2>(pidx); pl++) take_plane(v);
@@ -438,19 +452,20 @@ cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t*
     grid = (n_units + rounds - 1) / rounds;
   }
   const int kps = gemm_ksteps_per_stage(g.ksteps);
-  const int nst = gemm_stages(g.nblk, g.cout_pad, kps);
-  const size_t smem = gemm_smem_bytes(g.nblk, g.cout_pad, nst, kps);
+  const int nstg = gemm_staging_tiles(g.nblk, kps, g.ksteps);
+  const int nst = gemm_stages(g.nblk, kps, nstg);
+  const size_t smem = gemm_smem_bytes(g.nblk, nst, kps, nstg);
   cudaError_t e;
 #define WINO_LAUNCH_GEMM(N)                                                                                 \
   e = g.alg == 1 ? launch_pdl(k_gemm<N, true, false>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw,  \
                               codes, g.cout, g.scaling, g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad,         \
-                              g.cin_pad, nst, kps, g_trace, g_gemm_dbg)                                                                 \
+                              g.cin_pad, nst, kps, nstg, g_trace, g_gemm_dbg)                                                                 \
       : g.w1 ? launch_pdl(k_gemm<N, false, true>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw,     \
                           codes, g.cout, g.scaling, g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad,  \
-                          nst, kps, g_trace, g_gemm_dbg)                                                                                \
+                          nst, kps, nstg, g_trace, g_gemm_dbg)                                                                                \
              : launch_pdl(k_gemm<N, false, false>, dim3(grid), dim3(kGemmThreads), smem, st, vimg, wimg, mraw,    \
                           codes, g.cout, g.scaling, g.ksteps, g.chunk_tiles_pad, tblocks, g.cout_pad, g.cin_pad,  \
-                          nst, kps, g_trace, g_gemm_dbg)
+                          nst, kps, nstg, g_trace, g_gemm_dbg)
   switch (g.nblk) {
     case 16: WINO_LAUNCH_GEMM(16); break;
     case 32: WINO_LAUNCH_GEMM(32); break;
@@ -468,6 +483,7 @@ cudaError_t setup_gemm() {
   if (const char* d = std::getenv("WINO_K3_DBG")) g_gemm_dbg = std::atoi(d);
   if (const char* d = std::getenv("WINO_K3_BALANCE")) g_gemm_balance = std::atoi(d);
   if (const char* d = std::getenv("WINO_K3_KPS")) g_kps_override = std::atoi(d);
+  if (const char* d = std::getenv("WINO_K3_STAGING")) g_staging_override = std::atoi(d);
   if (const char* d = std::getenv("WINO_K3_STAGES")) g_stages_cap = std::max(kMinStages, std::min(kMaxStages, std::atoi(d)));
   auto attr = [&](const void* f, int nblk) {
     if (e == cudaSuccess)
