@@ -128,6 +128,9 @@ def test_c1_all_stages(layout, scaling, path):
     (2, 14, 10, 80, 48, 1, O.NCHW),
     (2, 11, 13, 200, 24, 1, O.NHWC),
     (1, 9, 9, 300, 20, 1, O.NHWC),
+    # quarter-K packing (NHWC int8, c_in <= 8): several 128-tile blocks with a ragged last one, a cout tail
+    (3, 30, 34, 3, 64, 1, O.NHWC),
+    (2, 17, 22, 8, 20, 0, O.NHWC),
 ])
 @pytest.mark.parametrize("scaling", [False, True])
 @pytest.mark.parametrize("path", PATHS)
@@ -260,13 +263,15 @@ def test_invalid_scale_code_is_range_at_the_boundary():
 
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("lanes", [2, 3])
-def test_chunk_lanes_match_the_oracle(path, lanes):
+@pytest.mark.parametrize("shape", [(13, 30, 26, 64, 48), (13, 60, 52, 3, 48)])   # the second: quarter-K packing
+def test_chunk_lanes_match_the_oracle(path, lanes, shape):
     """wino_conv_desc.lanes: chunks on concurrent streams with their own V (+ M'') buffers give the oracle's
     result, eagerly and inside a captured CUDA graph (the fork/join is captured)."""
     W = _wino()
     rng = np.random.default_rng(50 + lanes)
-    x, w = synth.random_layer(rng, 13, 30, 26, 64, 48, O.NHWC)
-    conv = W.WinoConv2d(13, 30, 26, 64, 48, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=path, workspace_mb=1,
+    n, h, wd, ci, co = shape
+    x, w = synth.random_layer(rng, n, h, wd, ci, co, O.NHWC)
+    conv = W.WinoConv2d(n, h, wd, ci, co, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=path, workspace_mb=1,
                         lanes=lanes)
     assert conv.info.n_chunks >= 2 and conv.info.lanes == min(lanes, conv.info.n_chunks)
     conv.transform_filter(torch.from_numpy(w).cuda())
