@@ -173,19 +173,23 @@ __device__ __forceinline__ void k2f_zero_slice(const Geom& g, int8_t* __restrict
 // 16 tiles, CTA = one 128-tile block; the (group, value part) of a value selects its pack and K byte
 template <int KS, int MINB, bool QK = false>   // KS: g.ksteps as a compile-time constant (1, 2, 4, 8, 16; 0 = runtime)
 __global__ void __launch_bounds__(kI4Warps * 32, MINB)
-    k_input_transform_f4(Geom g, const int8_t* __restrict__ x, int n0, int imgs, int8_t* __restrict__ vimg, int dbg) {
+    k_input_transform_f4(Geom g, const int8_t* __restrict__ x, int n0, int imgs, int8_t* __restrict__ vimg, int dbg,
+                         int spc) {
 #ifndef WINO_K2_DBG
   dbg = 0;   // ablation bits (debug builds only): 1 no V stores, 2 no x loads
 #endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // spc 16-channel slices per CTA (warp w: tile group w / spc, slice w % spc), so the warps that read the
+  // same pixels' bytes share the CTA's L1 (WINO_K2F4_SPC)
+  const int slice = QK ? 0 : blockIdx.y * spc + warp % spc;
   const int t = QK ? blockIdx.x * kMBlock + warp * 16 + (lane >> 1)
-                   : blockIdx.x * kI4TilesPerCta + warp * kI4TilesPerWarp + (lane >> 2);
-  const int c = QK ? 4 * (lane & 1) : blockIdx.y * kI4ChPerCta + 4 * (lane & 3);
+                   : blockIdx.x * (kI4TilesPerCta / spc) + (warp / spc) * kI4TilesPerWarp + (lane >> 2);
+  const int c = QK ? 4 * (lane & 1) : slice * kI4ChPerCta + 4 * (lane & 3);
   pdl_trigger();
   pdl_wait();   // x may come from the previous kernel; V may still be read by the previous GEMM
 
   const int tiles = imgs * g.tpi;
-  if (!QK && blockIdx.y * kI4ChPerCta >= g.cin) {   // a slice of padding channels only: V = 0 (both pieces)
+  if (!QK && slice * kI4ChPerCta >= g.cin) {   // a slice of padding channels only: V = 0 (both pieces)
     k2f_zero_slice<KS>(g, vimg, t, c);
     return;
   }
@@ -249,12 +253,18 @@ cudaError_t launch_input_transform_f4(const Geom& g, const int8_t* x, int n0, in
                                       cudaStream_t st) {
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
-  dim3 grid((unsigned)(tiles_pad / kI4TilesPerCta), g.cin_pad / kI4ChPerCta);
+  // 16-channel slices per CTA: 4 (2 when c_in_pad is not a multiple of 64) -- the four warps that read a
+  // pixel's 64 channel bytes (two 32-byte sectors) sit in one CTA and share its L1 instead of four CTAs each
+  // pulling the sectors from L2: a batch-512 C2-shaped layer 144 -> 103 us, VGG-16 layers 2-5 K2 -33 %,
+  // C5 526 -> 555 TOPS; WINO_K2F4_SPC = 1 / 2 / 4 overrides (experiments)
+  static const int spc_env = [] { const char* e = std::getenv("WINO_K2F4_SPC"); return e ? std::atoi(e) : 4; }();
+  const int spc = (spc_env == 4 && g.cin_pad % 64 == 0) ? 4 : (spc_env >= 2 ? 2 : 1);
+  dim3 grid((unsigned)(tiles_pad / (kI4TilesPerCta / spc)), g.cin_pad / (kI4ChPerCta * spc));
   // CTAs per SM the register budget targets (WINO_K2F4_MINB; 3 measured best at C2 and the VGG-16 stack)
   static const int dbg = [] { const char* e = std::getenv("WINO_K2_DBG"); return e ? std::atoi(e) : 0; }();
   static const int minb = [] { const char* e = std::getenv("WINO_K2F4_MINB"); return e ? std::atoi(e) : 3; }();
 #define WINO_K2F4(K, M) \
-  launch_pdl_co(k_input_transform_f4<K, M>, grid, dim3(kI4Warps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg, dbg)
+  launch_pdl_co(k_input_transform_f4<K, M>, grid, dim3(kI4Warps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg, dbg, spc)
 #define WINO_K2F4_M(M)              \
   switch (g.ksteps) {               \
     case 1: return WINO_K2F4(1, M);   \
@@ -266,7 +276,7 @@ cudaError_t launch_input_transform_f4(const Geom& g, const int8_t* x, int n0, in
   }
   if (g.qk) {   // quarter-K packed V (c_in <= 8): one CTA per 128-tile block
     return launch_pdl_co(k_input_transform_f4<1, 3, true>, dim3((unsigned)(tiles_pad / kMBlock)),
-                         dim3(kI4Warps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg, dbg);
+                         dim3(kI4Warps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg, dbg, 1);
   }
   if (minb >= 4) { WINO_K2F4_M(4) }
   if (minb == 3) { WINO_K2F4_M(3) }
