@@ -162,13 +162,21 @@ __device__ __forceinline__ void input_rows(const Geom& g, const int8_t* __restri
   }
 }
 
+// 16-channel slices per CTA (4 when c_in_pad is a multiple of 64, else 2; WINO_K2_SPC overrides)
+inline int k2_slices_per_cta(int cin_pad) {
+  static const int env = [] { const char* e = std::getenv("WINO_K2_SPC"); return e ? std::atoi(e) : 4; }();
+  return (env == 4 && cin_pad % 64 == 0) ? 4 : (env >= 2 ? 2 : 1);
+}
+
 template <bool U8, int KS>   // KS: g.ksteps at compile time (0 = runtime), as in K2F
 __global__ void __launch_bounds__(kInWarps * 32) k_input_transform(Geom g, const int8_t* __restrict__ x, int n0,
-                                                                   int imgs, int8_t* __restrict__ vimg) {
+                                                                   int imgs, int8_t* __restrict__ vimg, int spc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tl = lane >> 3, cp = lane & 7;                      // tile within warp, channel pair
-  const int t = blockIdx.x * kInTilesPerCta + warp * kInTilesPerWarp + tl;   // chunk tile
-  const int c = blockIdx.y * kInChPerCta + 2 * cp;              // first channel of the pair
+  // spc 16-channel slices per CTA (warp w: tile group w / spc, slice w % spc): the warps reading a pixel's
+  // channel bytes share the CTA's L1 (k_input4.cu)
+  const int t = blockIdx.x * (kInTilesPerCta / spc) + (warp / spc) * kInTilesPerWarp + tl;   // chunk tile
+  const int c = (blockIdx.y * spc + warp % spc) * kInChPerCta + 2 * cp;   // first channel of the pair
   pdl_trigger();
   pdl_wait();   // x may come from the previous kernel (layer stacks); V may still be read by the previous GEMM
   Rows r[2];
@@ -244,11 +252,13 @@ __device__ __forceinline__ void st_fused(int8_t* p_hi, int v0, int v1) {
 // offset from the thread's base pointer is an immediate
 template <bool U8, int KS>
 __global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, const int8_t* __restrict__ x, int n0,
-                                                                     int imgs, int8_t* __restrict__ vimg) {
+                                                                     int imgs, int8_t* __restrict__ vimg, int spc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tl = lane >> 3, cp = lane & 7;
-  const int t = blockIdx.x * kInTilesPerCta + warp * kInTilesPerWarp + tl;
-  const int c = blockIdx.y * kInChPerCta + 2 * cp;
+  // spc 16-channel slices per CTA (warp w: tile group w / spc, slice w % spc): the warps reading a pixel's
+  // channel bytes share the CTA's L1 (k_input4.cu)
+  const int t = blockIdx.x * (kInTilesPerCta / spc) + (warp / spc) * kInTilesPerWarp + tl;   // chunk tile
+  const int c = (blockIdx.y * spc + warp % spc) * kInChPerCta + 2 * cp;   // first channel of the pair
   pdl_trigger();
   pdl_wait();
   Rows r[2];
@@ -311,8 +321,9 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform_f(Geom g, con
 cudaError_t launch_input_transform_f(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st) {
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
-  dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
-#define WINO_K2F(U, K) launch_pdl_co(k_input_transform_f<U, K>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg)
+  const int spc = k2_slices_per_cta(g.cin_pad);
+  dim3 grid((unsigned)(tiles_pad / (kInTilesPerCta / spc)), g.cin_pad / (kInChPerCta * spc));
+#define WINO_K2F(U, K) launch_pdl_co(k_input_transform_f<U, K>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg, spc)
 #define WINO_K2F_KS(U)                                                                                          \
   switch (g.ksteps) {                                                                                           \
     case 1: return WINO_K2F(U, 1);                                                                              \
@@ -333,11 +344,13 @@ cudaError_t launch_input_transform_f(const Geom& g, const int8_t* x, int n0, int
 // (position i*4 + j), balanced pieces, staged V layout (plane stride = g.planes = 16).
 template <bool U8, int KS>   // uint8 + zero point (f2, A28): out-of-map pixels read the zero point (d = 0)
 __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, const int8_t* __restrict__ x, int n0,
-                                                                    int imgs, int8_t* __restrict__ vimg) {
+                                                                    int imgs, int8_t* __restrict__ vimg, int spc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tl = lane >> 3, cp = lane & 7;
-  const int t = blockIdx.x * kInTilesPerCta + warp * kInTilesPerWarp + tl;
-  const int c = blockIdx.y * kInChPerCta + 2 * cp;
+  // spc 16-channel slices per CTA (warp w: tile group w / spc, slice w % spc): the warps reading a pixel's
+  // channel bytes share the CTA's L1 (k_input4.cu)
+  const int t = blockIdx.x * (kInTilesPerCta / spc) + (warp / spc) * kInTilesPerWarp + tl;   // chunk tile
+  const int c = (blockIdx.y * spc + warp % spc) * kInChPerCta + 2 * cp;   // first channel of the pair
   pdl_trigger();
   pdl_wait();
   uint32_t w[16];   // 2 channels per pixel
@@ -425,8 +438,9 @@ __global__ void __launch_bounds__(kInWarps * 32) k_input_transform2(Geom g, cons
 cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int imgs, int8_t* vimg, cudaStream_t st) {
   const long long tiles = (long long)imgs * g.tpi;
   const long long tiles_pad = (tiles + kMBlock - 1) / kMBlock * kMBlock;
-  dim3 grid((unsigned)(tiles_pad / kInTilesPerCta), g.cin_pad / kInChPerCta);
-#define WINO_K22(U, K) launch_pdl_co(k_input_transform2<U, K>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg)
+  const int spc = k2_slices_per_cta(g.cin_pad);
+  dim3 grid((unsigned)(tiles_pad / (kInTilesPerCta / spc)), g.cin_pad / (kInChPerCta * spc));
+#define WINO_K22(U, K) launch_pdl_co(k_input_transform2<U, K>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg, spc)
 #define WINO_K22_KS(U)                                                                                          \
   switch (g.ksteps) {                                                                                           \
     case 1: return WINO_K22(U, 1);                                                                              \
@@ -440,7 +454,7 @@ cudaError_t launch_input_transform(const Geom& g, const int8_t* x, int n0, int i
   if (g.alg == 1) { WINO_K22_KS(false) }
 #undef WINO_K22_KS
 #undef WINO_K22
-#define WINO_K2S(U, K) launch_pdl_co(k_input_transform<U, K>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg)
+#define WINO_K2S(U, K) launch_pdl_co(k_input_transform<U, K>, grid, dim3(kInWarps * 32), 0, st, kCarveL1, g, x, n0, imgs, vimg, spc)
 #define WINO_K2S_KS(U)                                                                                          \
   switch (g.ksteps) {                                                                                           \
     case 1: return WINO_K2S(U, 1);                                                                              \
