@@ -120,13 +120,14 @@ inline int gemm_stages(int nblk, int kps, int nstg) {
 static int g_staging_override = 0;   // WINO_K3_STAGING = 1 or 2 (experiments)
 inline int gemm_staging_tiles(int nblk, int kps, int ksteps) {
   if (g_staging_override == 1 || g_staging_override == 2) return g_staging_override;
+  if (gemm_smem_bytes(nblk, kMinStages, kps, 2) > kSmemLimit) return 1;   // 96 KB stages (8 K steps)
   return ksteps >= 16 && gemm_stages(nblk, kps, 1) > gemm_stages(nblk, kps, 2) ? 1 : 2;
 }
 // K steps per stage: 4 when the plane has that many (fewer stages and commits per plane: C4 K3
 // 43.8 -> 38.9 us), else the plane's whole K range (2 at C2).  WINO_K3_KPS overrides (experiments).
 static int g_kps_override = 0;
 inline int gemm_ksteps_per_stage(int ksteps) {
-  if (g_kps_override == 2 || g_kps_override == 4) return g_kps_override;
+  if (g_kps_override == 2 || g_kps_override == 4 || g_kps_override == 8) return g_kps_override;
   return ksteps >= 4 ? 4 : 2;
 }
 
