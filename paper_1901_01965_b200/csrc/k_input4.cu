@@ -169,6 +169,29 @@ __device__ __forceinline__ void k2f_zero_slice(const Geom& g, int8_t* __restrict
   }
 }
 
+// c_in < 4: the 6 pixels of each of the 6 patch rows from aligned words (see the QK gather below)
+template <int CIN>
+__device__ __forceinline__ void gather_rows_small(const int8_t* p0, long long rstride, uint32_t (&w)[36]) {
+  constexpr uint32_t kMask = (1u << (8 * CIN)) - 1u;
+#pragma unroll
+  for (int a = 0; a < 6; a++) {
+    const int8_t* rp = p0 + a * rstride;
+    const uint32_t off = (uint32_t)(reinterpret_cast<uintptr_t>(rp) & 3u);
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(rp - off);
+    uint32_t W[6], R[5];
+#pragma unroll
+    for (int k = 0; k < 6; k++) W[k] = __ldg(wp + k);
+#pragma unroll
+    for (int k = 0; k < 5; k++) R[k] = __funnelshift_r(W[k], W[k + 1], off * 8u);   // row bytes from byte 0
+#pragma unroll
+    for (int b = 0; b < 6; b++) {
+      const int B = b * CIN;   // compile-time after unrolling
+      const uint32_t v = (B & 3) == 0 ? R[B >> 2] : __funnelshift_r(R[B >> 2], R[(B >> 2) + 1], (B & 3) * 8);
+      w[a * 6 + b] = v & kMask;
+    }
+  }
+}
+
 // QK: the quarter-K packed V image (c_in <= 8, layout.cuh): thread = (tile, 4 of the 8 channel slots), warp =
 // 16 tiles, CTA = one 128-tile block; the (group, value part) of a value selects its pack and K byte
 template <int KS, int MINB, bool QK = false>   // KS: g.ksteps as a compile-time constant (1, 2, 4, 8, 16; 0 = runtime)
@@ -210,6 +233,19 @@ __global__ void __launch_bounds__(kI4Warps * 32, MINB)
     if (dbg & 2) {   // debug: no loads (a lane-dependent pattern instead)
 #pragma unroll
       for (int i = 0; i < 36; i++) w[i] = (uint32_t)(t * 0x01010101u + i);
+    } else if (QK && g.cin < 4 && __all_sync(0xffffffffu, t >= tiles || c > 0 ||
+                                                 (iy0 >= 0 && iy0 + 6 < g.h && ix0 >= 0 && ix0 + 6 <= g.w))) {
+      // c_in < 4 (VGG-16 layer 1: 3 bytes per pixel): a patch row is 6 c_in contiguous bytes; read it as the
+      // 6 aligned 4-byte words covering it, realign them with funnel shifts and cut the pixels out at static
+      // byte offsets (6 loads per row instead of 6 c_in byte loads); the row below exists (iy0 + 6 < h), so the
+      // last word stays inside the tensor
+#pragma unroll
+      for (int i = 0; i < 36; i++) w[i] = 0u;
+      if (t < tiles && c == 0) {
+        if (g.cin == 3) gather_rows_small<3>(p0, rstride, w);
+        else if (g.cin == 2) gather_rows_small<2>(p0, rstride, w);
+        else gather_rows_small<1>(p0, rstride, w);
+      }
     } else if ((g.cin & 3) == 0 && __all_sync(0xffffffffu, inside)) {
       // interior warp: unpredicated 4-byte loads; column offsets b * c_in are immediates when c_in = 32 KS
       const int cst = (KS > 0 && g.cin == 32 * KS) ? 32 * KS : g.cin;
