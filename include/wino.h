@@ -145,8 +145,9 @@ typedef struct {
     int planes;                 /* staged F4x4: 46 = 16 real + 10 x {re, im, re+im}
                                    (P:228); fused F4x4: 36 = 16 real + 10 x {re, im};
                                    F2x2: 16                                            */
-    int pieces;                 /* 2 balanced s8 pieces per operand value:
-                                   v = 256 hi + lo, lo = low byte of v     */
+    int pieces;                 /* 2 int8 pieces per operand value, v = 256 hi + lo:
+                                   balanced s8 (lo = low byte of v read as s8), except
+                                   the fused path's V (lo = v & 255 as u8) */
     int chunk_images;           /* images per workspace chunk                          */
     int n_chunks;
     int lanes;                  /* chunk pipelines actually used (<= n_chunks)          */
