@@ -1,3 +1,5 @@
+# HISTORICAL: the experiment switch this script exercises was removed after the measurement (not kept;
+# DESIGN.md 6b records the result); kept to document how the numbers in profiles/ were taken.
 # pipelined K2F (cp.async into a per-thread slot refilled after the column transform, WINO_K2F5=1) vs the
 # current K2F: GPU parity with it on, stage-2 times at C2/C4 and C2-shaped batches 32/128/512, C5 lines
 set -o pipefail

@@ -1,3 +1,5 @@
+# HISTORICAL: the experiment switch this script exercises was removed after the measurement (not kept;
+# DESIGN.md 6b records the result); kept to document how the numbers in profiles/ were taken.
 # storer-warp K3F: GPU tests, C2-C5 lines, C5 per-layer times
 set -o pipefail
 bash tools/quick_r02.sh
