@@ -78,6 +78,7 @@ constexpr int kFSlotGroups = 18;              // per unit: 4 rows x (2 real pair
 constexpr uint32_t kFPartBytes = 65536;       // Z_0, Z_5 partials; aliased by the int8 output staging tile
 constexpr uint32_t kFETabBytes = kFGroupsN * kFN * 4;
 constexpr int kFEpiBar = 1;
+constexpr uint32_t kQkStage = kQkPackV + kQkPackW;   // MG = 5 ring stage (13 KB, packed back to back)
 
 inline size_t fused_smem_bytes() {
   return (size_t)kFStages * kFStageBytes + kFPartBytes + kFETabBytes + 512;
@@ -200,6 +201,12 @@ __global__ void __launch_bounds__(kFThreads, 1)
   const int nblocks = g.cout_pad / kFN;
   const int n_units = tblocks * nblocks;
   const int ksteps = g.ksteps;
+  // quarter-K pairing (MG = 5, int8 NHWC staged output, an even number of cout blocks): the two cout blocks
+  // that share a 32-byte sector of each output pixel run back to back on one CTA, their outputs are staged
+  // side by side and leave as whole sectors (a lane pair per sector) instead of two half-sector stores
+  const bool qpair = MG == 5 && NHWC && OUT8 && (g.cout & 15) == 0 && !g.pool2 && (nblocks & 1) == 0;
+  const int u_first = qpair ? 2 * (int)blockIdx.x : (int)blockIdx.x;
+  auto u_next = [&](int u) -> int { return qpair ? ((u & 1) ? u + 2 * (int)gridDim.x - 1 : u + 1) : u + (int)gridDim.x; };
 
   if (warp == 0) {
     tmem_alloc(smem_u32(tmem_slot), 512);
@@ -249,13 +256,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
       if constexpr (MG == 5) {
         // quarter-K packing (c_in <= 8, layout.cuh): one stage per pack (8 KB of V + 5 KB of W': two slot-groups),
         // released by its own commit
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        for (int u = u_first; u < n_units; u = u_next(u)) {
           const int tb = u / nblocks, nb = u - tb * nblocks;
           for (int pk = 0; pk < kQkPacks; pk++, it++) {
             if (it % kFProducers != pw) continue;
             const int s = it % kFStages;
             mbar_wait(empty0 + 8 * s, ((it / kFStages) & 1) ^ 1);
-            const uint32_t st = sbase + s * kFStageBytes;
+            const uint32_t st = sbase + s * kQkStage;
             if (elect_one()) {
               if (dbg & 4) {   // debug builds only: no copies
                 mbar_arrive(full0 + 8 * s);
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const uint64_t D0 = umma_desc(sbase, 128, 256);
         const uint32_t d0lo = (uint32_t)D0, d0hi = (uint32_t)(D0 >> 32);
         auto dsc = [&](uint32_t off) -> uint64_t { return ((uint64_t)d0hi << 32) | (uint64_t)(d0lo + (off >> 4)); };
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        for (int u = u_first; u < n_units; u = u_next(u)) {
           for (int pk = 0; pk < kQkPacks; pk++, it++, sgc += 2) {
             const int s = it % kFStages;
             const int b = sgc % kFSlots;            // even: slots b, b + 1 are adjacent
@@ -428,7 +435,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             tc_fence_after();
             if (it < 64 && lane == 0) FTRACE(it, 1);
             if (sgc < 32 && lane == 0) FTRACE(64 + sgc, 0);
-            const uint32_t st = s * kFStageBytes;
+            const uint32_t st = s * kQkStage;
             const uint32_t d0 = tmem + b * kFSlotCols;
             if (elect_one()) {
               if (!(dbg & 2)) {
@@ -832,6 +839,32 @@ __global__ void __launch_bounds__(kFThreads, 1)
         }
       }
     };
+    // quarter-K pairing: the sector-pair staging [px 16][tile 128][32 B] behind the 4 x 13 KB ring; the unit of
+    // the even cout block fills bytes 0-15 of each 32-byte chunk, the odd one bytes 16-31 (16-byte halves
+    // swapped by tile bit 2 and words by tile bits 3-4, so both the staging writes and the reads are
+    // conflict-free); after the odd unit a lane pair writes each tile pixel's whole sector
+    uint8_t* pstg = smem + kFStages * kQkStage;
+    auto store_pair = [&](int tb_i, int nb0) {
+      const int half = etid & 1, rr = (etid >> 1) & (kMBlock - 1);
+      const int tt = tb_i * kMBlock + rr;
+      if (tt >= imgs * g.tpi) return;
+      const int ti = fdiv(tt, g.dv_tpi), rem = tt - ti * g.tpi, ty = fdiv(rem, g.dv_tw);
+      const int oyb = 4 * ty, oxb = 4 * (rem - ty * g.tw);
+      int8_t* base = static_cast<int8_t*>(y) + (long long)(n0 + ti) * g.ho * g.wo * g.cout + (nb0 + half) * kFN;
+      uint4 val[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const int px = (etid >> 8) + 2 * k;
+        val[k] = *reinterpret_cast<const uint4*>(pstg + (px * kMBlock + rr) * 32 + ((half ^ ((rr >> 2) & 1)) * 16));
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const int px = (etid >> 8) + 2 * k;
+        const int oy = oyb + (px >> 2), ox = oxb + (px & 3);
+        if (oy >= g.ho || ox >= g.wo) continue;
+        *reinterpret_cast<uint4*>(base + ((long long)oy * g.wo + ox) * g.cout) = unswizzle(val[k], rr);
+      }
+    };
     auto real_row = [&](int k, int32_t (&Z)[4][4]) {
       const int gb = 5 * k;
       int32_t m0[4], m1[4];
@@ -842,7 +875,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
         for (int c = 0; c < 4; c++) Z[j][c] = areal(j, 0) * m0[c] + areal(j, 1) * m1[c];
       take_real2(gb + 2, m0, m1);   // cc = 2, 5
       if (k == 0 && pending) {      // the previous unit's output, then nobody reads the staging any more
-        if (!(dbg & (256 | 2048))) store_staged(pend_tb, pend_nb);
+        if (!(dbg & (256 | 2048))) {
+          if (qpair) store_pair(pend_tb, pend_nb);
+          else store_staged(pend_tb, pend_nb);
+        }
         fepi_barrier();
         pending = false;
       }
@@ -872,17 +908,17 @@ __global__ void __launch_bounds__(kFThreads, 1)
     };
 
     if (dbg & 8) {   // debug: accumulator handshake only
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x)
+      for (int u = u_first; u < n_units; u = u_next(u))
         for (int sg = 0; sg < kFSlotGroups; sg++) {
           slot_wait();
           slot_release();
         }
     } else {
-      fill_etab(load_code(blockIdx.x));
+      fill_etab(load_code(u_first));
       int uc = 0;   // units done (trace index)
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, uc++) {
+      for (int u = u_first; u < n_units; u = u_next(u), uc++) {
         fepi_barrier();                                // etab visible; staging of the previous unit drained
-        const int next_code = load_code(u + gridDim.x);
+        const int next_code = load_code(u_next(u));
         {
           int32_t Z[4][4];
           real_row(0, Z);                              // row 0 -> Z_0
@@ -1021,8 +1057,14 @@ __global__ void __launch_bounds__(kFThreads, 1)
                                         : __byte_perm(__byte_perm((uint32_t)outv(Yi[j][0]), (uint32_t)outv(Yi[j][1]), 0x0040),
                                                       __byte_perm((uint32_t)outv(Yi[j][2]), (uint32_t)outv(Yi[j][3]), 0x0040),
                                                       0x5410);
-              if (!(dbg & (256 | 1024)) || w == 0x12345678u)   // debug bits 256/1024: no staging (kept live)
+              if (dbg & (256 | 1024)) {   // debug bits 256/1024: no staging (kept live)
+                if (w == 0x12345678u) *reinterpret_cast<uint32_t*>(part) = w;
+              } else if (qpair) {
+                *reinterpret_cast<uint32_t*>(pstg + ((i * 4 + j) * kMBlock + row) * 32 +
+                                             (((nb & 1) ^ ((row >> 2) & 1)) * 16) + stg_word) = w;
+              } else {
                 *reinterpret_cast<uint32_t*>(part + ((i * 4 + j) * kMBlock + row) * 16 + stg_word) = w;
+              }
             }
             return;
           }
@@ -1106,14 +1148,17 @@ __global__ void __launch_bounds__(kFThreads, 1)
         if (warp == 0 && lane == 0) FTRACE(uc * 8 + 3, 3);
         fepi_barrier();                                // staging complete; etab of the next unit visible
         if (warp == 0 && lane == 0) FTRACE(uc * 8 + 4, 3);
-        if (stage8) {   // stored during the next unit's row 0 (or after the last unit)
+        if (stage8 && (!qpair || (nb & 1))) {   // stored during the next unit's row 0 (or after the last unit)
           pending = true;
           pend_tb = tb_i;
-          pend_nb = nb;
+          pend_nb = qpair ? nb - 1 : nb;
         }
         if (warp == 0 && lane == 0) FTRACE(uc * 8 + 5, 3);
       }
-      if (pending && !(dbg & (256 | 2048))) store_staged(pend_tb, pend_nb);
+      if (pending && !(dbg & (256 | 2048))) {
+        if (qpair) store_pair(pend_tb, pend_nb);
+        else store_staged(pend_tb, pend_nb);
+      }
     }
   }
   tc_fence_before();
@@ -1146,10 +1191,14 @@ cudaError_t launch_fused(const Geom& g, long long tiles_pad_launch, int n0, int 
   const int tblocks = (int)(tiles_pad_launch / kMBlock);
   const int n_units = tblocks * (g.cout_pad / kFN);
   const int cap = g_fused_maxcta > 0 && g_fused_maxcta < g_fused_sms ? g_fused_maxcta : g_fused_sms;
-  int grid = n_units < cap ? n_units : cap;
+  // quarter-K pairing (see k_fused): a CTA takes pairs of units
+  const bool qpair = g.qk && g.layout == 1 && g.out_mode == 0 && (g.cout & 15) == 0 && !g.pool2 &&
+                     (g.cout_pad / kFN) % 2 == 0;
+  const int work = qpair ? n_units / 2 : n_units;
+  int grid = work < cap ? work : cap;
   if (g_fused_balance) {   // fewest CTAs with the same number of unit rounds: the rest of the SMs stay free
-    const int rounds = (n_units + grid - 1) / grid;
-    grid = (n_units + rounds - 1) / rounds;
+    const int rounds = (work + grid - 1) / grid;
+    grid = (work + rounds - 1) / rounds;
   }
   const size_t smem = fused_smem_bytes();
   const bool nhwc = g.layout == 1, out8 = g.out_mode == 0, fast = rq_mult == 1 && rq_shift <= 20;

@@ -158,6 +158,26 @@ def test_multi_chunk_matches_single_chunk(path):
     np.testing.assert_array_equal(y, O.wino_conv(x, w, 1, O.NHWC, scaling=True).out32)
 
 
+@pytest.mark.parametrize("shape", [(3, 30, 34, 3, 64), (2, 17, 22, 5, 96), (1, 9, 13, 1, 32), (2, 21, 19, 8, 48)])
+def test_quarter_k_paired_int8_output(shape):
+    """Quarter-K packing (c_in <= 8) with int8 NHWC output: an even number of 16-cout blocks runs as cout-block
+    pairs on one CTA whose outputs leave as whole 32-byte sectors (c_out 64, 96, 32); c_out 48 (three blocks)
+    keeps single units.  Several tile blocks, ragged maps, requantisation with and without rounding."""
+    W = _wino()
+    n, h, wd, ci, co = shape
+    rng = np.random.default_rng(90 + co)
+    x, w = synth.random_layer(rng, n, h, wd, ci, co, O.NHWC)
+    for M0, S in [(1, 0), (1, 9), (3, 11)]:
+        _, y8 = _run(x, w, O.NHWC, scaling=True, out_mode=0, M0=M0, S=S, path=W.WINO_PATH_FUSED)
+        np.testing.assert_array_equal(y8, O.wino_conv(x, w, 1, O.NHWC, scaling=True, M0=M0, S=S).y8)
+    # several chunks on two lanes
+    conv = W.WinoConv2d(n, h, wd, ci, co, 1, W.WINO_NHWC, True, W.WINO_OUT_INT8, path=W.WINO_PATH_FUSED,
+                        workspace_mb=1, lanes=2)
+    conv.transform_filter(torch.from_numpy(w).cuda())
+    np.testing.assert_array_equal(conv(torch.from_numpy(x).cuda(), 1, 9).cpu().numpy(),
+                                  O.wino_conv(x, w, 1, O.NHWC, scaling=True, M0=1, S=9).y8)
+
+
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("cout", [20, 32])
 @pytest.mark.parametrize("layout", [O.NHWC, O.NCHW])
