@@ -403,6 +403,14 @@ def profile_kernels(conv, xs, ws, ys, S, stream, n_sets, reps, lanes=1):
 def run_ours(args):
     import torch
 
+    layer0 = synth.CONFIGS[args.config].layers[0]
+    if args.input == "u8" and layer0.c_in > 224:   # the plan would refuse it (WINO_ERR_UNSUPPORTED)
+        if int(os.environ.get("RANK", 0)) == 0:
+            print(json.dumps({"metric": METRIC, "config": {"workload": args.config, "input": "u8"},
+                              "unsupported": f"uint8 input needs c_in <= 224 (int32 exactness of the int9 values, "
+                                             f"DESIGN.md A28); {args.config} has c_in = {layer0.c_in}"}), flush=True)
+        return
+
     import paper_1901_01965_b200 as W
     from paper_1901_01965_b200 import _lib as L
     from paper_1901_01965_b200 import shard as SH
