@@ -435,17 +435,361 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------------------------------------
+// K3 on CTA pairs (tcgen05.mma.cta_group::2, complex F(4x4), W' in two pieces): the staged GEMM is bound by
+// shared-memory bandwidth (per K step a plane's two N = 2 n_block UMMAs read 16 KB of operands while the bulk
+// copies write 12 KB).  A cluster of two CTAs on one TPC runs M = 256 UMMAs: each CTA holds the
+// V of its own 128-tile block and ONE half of B = [W hi | W lo] (rank 0 the W hi rows, rank 1 the W lo rows),
+// so each SM reads and writes half the W' bytes.  The leader (rank 0) issues every UMMA and its commits
+// multicast to both CTAs' barriers; the peer forwards its stage completions (pfull) and accumulator drains
+// (ptempty) to the leader with remote mbarrier arrives.  The first K step's hi UMMA overwrites [hh | x]; the
+// ll block starts at zero (re-zeroed by the epilogue after reading).  Unit = (position, tile-block pair,
+// cout block); an odd last tile block pairs with nothing (the peer loads W' only and stores nothing).
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank0(uint32_t addr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(0));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(   // non-suspending poll: a suspended try_wait is not woken promptly by a remote arrive
+        "{ .reg .pred p; mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void umma2_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_commit_both(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   bar),
+               "h"((uint16_t)3)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait2() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr), "r"(0)
+               : "memory");
+}
+
+// stage of the pair kernel per CTA: V hi + lo of kps K steps, a 1-row-block pad, and the stage's whole
+// [W hi | W lo] block (one bulk copy): rank 0 copies it to the B base, so each K step's W hi rows sit at the
+// B address of that K step; rank 1 copies it one row block (n_block x 32 B) lower, so its W lo rows sit there
+__host__ __device__ inline uint32_t gemm2_stage_bytes(int nblk, int kps) {
+  return 2u * kps * kABytesPerKStep + (uint32_t)nblk * kKStep + 2u * kps * (uint32_t)nblk * kKStep;
+}
+inline size_t gemm2_smem_bytes(int nblk, int stages, int kps) {
+  return (size_t)stages * gemm2_stage_bytes(nblk, kps) + 2 * (size_t)kMBlock * nblk * 4 + 1024;
+}
+inline int gemm2_stages(int nblk, int kps) {
+  int st = g_stages_cap;
+  while (st > kMinStages && gemm2_smem_bytes(nblk, st, kps) > kSmemLimit) --st;
+  return st;
+}
+
+template <int NBLK>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm2(const int8_t* __restrict__ V, const int8_t* __restrict__ W, int32_t* __restrict__ Mraw,
+            const uint8_t* __restrict__ codes, int cout, int scaling, int ksteps, long long tiles_pad, int tblocks,
+            int cout_pad, int nst, int kps) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int kHalf = NBLK / 2;
+  constexpr int kCpr = NBLK / 4;
+  constexpr int kSwz = (kCpr < 8 ? kCpr : 8) - 1;
+  constexpr uint32_t kAccCols = 3 * NBLK;              // hh, x, ll
+  constexpr uint32_t kTmemCols = 512;
+  constexpr uint32_t kTileBytes = kMBlock * NBLK * 4;
+  static_assert(2 * kAccCols <= kTmemCols, "double-buffered accumulators must fit TMEM");
+
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const uint32_t a_bytes = kps * kABytesPerKStep;                  // one V piece of a stage
+  const uint32_t stage_bytes = gemm2_stage_bytes(NBLK, kps);
+  uint8_t* staging = smem + nst * stage_bytes;                    // 2 x kTileBytes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + 2 * kTileBytes);
+  // [full | empty | pfull] x kMaxStages, [tfull | tempty | ptempty] x 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 6);
+  uint32_t* lut = tmem_slot + 4;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kMaxStages), pfull0 = smem_u32(bars + 2 * kMaxStages);
+  const uint32_t tfull0 = smem_u32(bars + 3 * kMaxStages), tempty0 = tfull0 + 16, ptempty0 = tfull0 + 32;
+  const int nblocks = cout_pad / NBLK;
+  const int tbp_count = (tblocks + 1) / 2;
+  const int n_units = tbp_count * nblocks * kPositions;
+  const int n_it = (ksteps + kps - 1) / kps;
+  const int ncl = (int)gridDim.x / 2, cl = (int)blockIdx.x / 2;
+  auto cunit = [&](int k) { return k * ncl + ((k & 1) ? ncl - 1 - cl : cl); };
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (threadIdx.x == 32 * kProducerWarp) {
+    for (int s = 0; s < nst; s++) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+      mbar_init(pfull0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(tfull0 + 8 * b, 1);
+      mbar_init(tempty0 + 8 * b, kEpiWarps);
+      mbar_init(ptempty0 + 8 * b, kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  pdl_trigger();
+  if (threadIdx.x < 64) {
+    int n, p, m = 1, q = 0;
+    decode_code(threadIdx.x, n, p);
+    if (n >= 8) inverse_factor(n, p, m, q);
+    lut[threadIdx.x] = n >= 8 ? (uint32_t)m << (7 - q) : 128u;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  if (warp < kEpiWarps) {   // the ll blocks of both accumulator sets start at zero
+    const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * kHalf + 2 * NBLK;
+#pragma unroll
+    for (int b = 0; b < 2; b++)
+#pragma unroll
+      for (int c = 0; c < kHalf; c += 8) tmem_zero8(lb + b * kAccCols + c);
+    tmem_st_wait2();
+  }
+  pdl_wait();   // V, W' and the codes come from the kernels just before
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();   // both CTAs' barriers initialised and TMEM zeroed before any remote arrive or MMA
+  tc_fence_after();
+
+  if (warp == kProducerWarp) {
+    // ------------------------------------------------ producer (both CTAs): own V, own half of W'
+    int s = 0, ph = 0;
+    for (int ku = 0, u = cunit(0); u < n_units; u = cunit(++ku)) {
+      int pidx, tbp, nb;
+      decode_unit(u, tbp_count, nblocks, pidx, tbp, nb);
+      const int tb = 2 * tbp + (int)rank;
+      const bool valid = tb < tblocks;
+      for (int pl = 0; pl < unit_planes<false>(pidx); pl++) {
+        const int plane = unit_plane0<false>(pidx) + pl;
+        const int8_t* vpl = V + ((long long)tb * kPlanes + plane) * ksteps * (2 * kVBlockBytes);
+        const int8_t* wpl = W + ((long long)plane * nblocks + nb) * ksteps * (2 * NBLK * kKStep);
+        for (int ks = 0; ks < n_it; ks++) {
+          mbar_wait(empty0 + 8 * s, ph ^ 1);
+          const int k0 = ks * kps;
+          const int kn = min(kps, ksteps - k0);
+          const uint32_t ab = valid ? kn * 2 * kABytesPerKStep : 0u, bb = kn * 2u * (uint32_t)NBLK * kKStep;
+          const uint32_t st = sbase + s * stage_bytes;
+          if (elect_one()) {
+            mbar_arrive_expect_tx(full0 + 8 * s, ab + bb);
+            if (valid) bulk_g2s(st, vpl + (long long)k0 * 2 * kVBlockBytes, ab, full0 + 8 * s);
+            bulk_g2s(st + 2 * a_bytes + (1u - rank) * NBLK * kKStep, wpl + (long long)k0 * 2 * NBLK * kKStep, bb,
+                     full0 + 8 * s);
+          }
+          __syncwarp();
+          if (++s == nst) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp && rank == 1) {
+    // ------------------------------------------------ peer forwarder: this CTA's stage completions to the leader
+    int s = 0, ph = 0;
+    const uint32_t rpfull0 = mapa_rank0(pfull0);
+    for (int ku = 0, u = cunit(0); u < n_units; u = cunit(++ku)) {
+      int pidx, tbp, nb;
+      decode_unit(u, tbp_count, nblocks, pidx, tbp, nb);
+      for (int pl = 0; pl < unit_planes<false>(pidx); pl++) {
+        for (int ks = 0; ks < n_it; ks++) {
+          mbar_wait(full0 + 8 * s, ph);
+          if (elect_one()) mbar_arrive_remote(rpfull0 + 8 * s);
+          __syncwarp();
+          if (++s == nst) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------ MMA issuer (leader only): M = 256 over the pair
+    const uint32_t id = idesc_i8(2 * kMBlock, 2 * NBLK, 1, 1);
+    int s = 0, ph = 0, pc = 0;
+    for (int ku = 0, u = cunit(0); u < n_units; u = cunit(++ku)) {
+      int pidx, tbp, nb;
+      decode_unit(u, tbp_count, nblocks, pidx, tbp, nb);
+      for (int pl = 0; pl < unit_planes<false>(pidx); pl++, pc++) {
+        const int b = pc & 1;
+        mbar_wait(tempty0 + 8 * b, ((pc >> 1) & 1) ^ 1);            // own epilogue drained this set
+        mbar_wait_cluster(ptempty0 + 8 * b, ((pc >> 1) & 1) ^ 1);   // and the peer's
+        tc_fence_after();
+        const uint32_t acc_hh = tmem + b * kAccCols, acc_x = acc_hh + NBLK;
+        for (int ks = 0; ks < n_it; ks++) {
+          mbar_wait(full0 + 8 * s, ph);
+          mbar_wait_cluster(pfull0 + 8 * s, ph);
+          tc_fence_after();
+          const int k0 = ks * kps;
+          const int kn = min(kps, ksteps - k0);
+          const uint32_t st = sbase + s * stage_bytes;
+          for (int kk = 0; kk < kn; ++kk) {
+            const uint64_t a_hi = umma_desc(st + (2 * kk) * kABytesPerKStep, 128, 256);
+            const uint64_t a_lo = umma_desc(st + (2 * kk + 1) * kABytesPerKStep, 128, 256);
+            const uint64_t bd = umma_desc(st + 2 * a_bytes + NBLK * kKStep + kk * 2 * NBLK * kKStep, 128, 256);
+            if (elect_one()) {
+              umma2_i8(acc_hh, a_hi, bd, id, (k0 + kk) > 0 ? 1u : 0u);   // [hh | x] (=, then +=) hi . [W hi | W lo]
+              umma2_i8(acc_x, a_lo, bd, id, 1u);                         // [x | ll] += lo . [W hi | W lo]
+            }
+            __syncwarp();
+          }
+          if (elect_one()) umma2_commit_both(empty0 + 8 * s);   // both CTAs' stage s reusable
+          __syncwarp();
+          if (++s == nst) { s = 0; ph ^= 1; }
+        }
+        if (elect_one()) umma2_commit_both(tfull0 + 8 * b);     // both CTAs' accumulator set b complete
+        __syncwarp();
+      }
+    }
+  } else if (warp < kEpiWarps) {
+    // ------------------------------------------------ epilogue (both CTAs): this CTA's 128 tiles
+    const int quad = warp & 3;
+    const int col0 = (warp >> 2) * kHalf;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + col0;
+    const long long ps = tiles_pad * (long long)cout_pad;
+    const uint32_t drain0 = rank == 0 ? tempty0 : mapa_rank0(ptempty0);
+    int pc = 0, to = 0;
+    auto take_plane = [&](uint32_t (&v)[kHalf]) {
+      const int b = pc & 1;
+      mbar_wait_cluster(tfull0 + 8 * b, (pc >> 1) & 1);
+      tc_fence_after();
+      const uint32_t acc = lane_base + b * kAccCols;
+#pragma unroll
+      for (int c = 0; c < kHalf; c += 8) {
+        uint32_t h[8], x[8], l[8];
+        tmem_ld<8>(acc + c, h);
+        tmem_ld<8>(acc + NBLK + c, x);
+        tmem_ld<8>(acc + 2 * NBLK + c, l);
+        tmem_ld_wait();
+        tmem_zero8(acc + 2 * NBLK + c);   // ll back to zero for the set's next plane
+#pragma unroll
+        for (int j = 0; j < 8; j++) v[c + j] = (h[j] << 16) + (x[j] << 8) + l[j];
+      }
+      tmem_st_wait2();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0) mbar_arrive(drain0 + 8 * b);
+        else mbar_arrive_remote(drain0 + 8 * b);
+      }
+      pc++;
+    };
+    constexpr int kEpiThreads = kEpiWarps * 32;
+    constexpr int kStripStep = kEpiThreads / kCpr;
+    constexpr int kStripRows = kMBlock / kStripStep;
+    const int sc = threadIdx.x % kCpr, sr0 = threadIdx.x / kCpr;
+    auto store_tile = [&](const uint32_t (&v)[kHalf], int32_t* dst, uint32_t c4) {
+      int4* tile = reinterpret_cast<int4*>(staging + (to & 1) * kTileBytes);
+#pragma unroll
+      for (int c = 0; c < kHalf; c += 4) {
+        const int ch = (col0 + c) >> 2;
+        tile[row * kCpr + (ch ^ (row & kSwz))] = make_int4((int)v[c], (int)v[c + 1], (int)v[c + 2], (int)v[c + 3]);
+      }
+      epi_barrier();
+      const uint32_t e0 = lut[c4 & 0x3fu], e1 = lut[(c4 >> 8) & 0x3fu], e2 = lut[(c4 >> 16) & 0x3fu],
+                     e3 = lut[(c4 >> 24) & 0x3fu];
+      int4* gdst = reinterpret_cast<int4*>(dst);
+#pragma unroll
+      for (int k = 0; k < kStripRows; k++) {
+        const int r = sr0 + k * kStripStep;
+        const int slot = r * kCpr + (sc ^ (r & kSwz));
+        const int4 raw = tile[slot];
+        gdst[slot] = make_int4(rscale_e((uint32_t)raw.x, e0), rscale_e((uint32_t)raw.y, e1),
+                               rscale_e((uint32_t)raw.z, e2), rscale_e((uint32_t)raw.w, e3));
+      }
+      to++;
+    };
+    auto strip_codes = [&](int pidx, int nb) -> uint32_t {
+      if (!scaling) return 0u;
+      const int pos = pidx < kPrimaries ? cpx_pos(pidx) : real_pos(pidx - kPrimaries);
+      uint32_t c4 = 0;
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int co = nb * NBLK + sc * 4 + i;
+        if (co < cout) c4 |= (uint32_t)__ldg(codes + (long long)co * 36 + pos) << (8 * i);
+      }
+      return c4;
+    };
+    for (int ku = 0, u = cunit(0); u < n_units; u = cunit(++ku)) {
+      int pidx, tbp, nb;
+      decode_unit(u, tbp_count, nblocks, pidx, tbp, nb);
+      const int tb = 2 * tbp + (int)rank;
+      const bool valid = tb < tblocks;   // uniform over the CTA
+      const long long tile_off = ((long long)tb * nblocks + nb) * (kMBlock * NBLK);
+      const uint32_t crow = strip_codes(pidx, nb);
+      if (pidx >= kPrimaries) {
+        uint32_t v[kHalf];
+        take_plane(v);
+        if (valid) store_tile(v, Mraw + (long long)(pidx - kPrimaries) * ps + tile_off, crow);
+      } else {
+        uint32_t re[kHalf], sm[kHalf], v[kHalf];
+        take_plane(re);
+#pragma unroll
+        for (int j = 0; j < kHalf; j++) sm[j] = re[j];
+        take_plane(v);
+#pragma unroll
+        for (int j = 0; j < kHalf; j++) { re[j] -= v[j]; sm[j] += v[j]; }
+        take_plane(v);
+#pragma unroll
+        for (int j = 0; j < kHalf; j++) v[j] -= sm[j];
+        if (valid) {
+          store_tile(re, Mraw + (long long)(kRealPlanes + pidx) * ps + tile_off, crow);
+          store_tile(v, Mraw + (long long)(kRealPlanes + kPrimaries + pidx) * ps + tile_off, crow);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();   // the peer's MMAs and remote arrives are over before either CTA frees its TMEM
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
 static int g_num_sms = 0;
 static uint64_t* g_trace = nullptr;
 // WINO_K3_DBG env (debug builds with -DWINO_K3_DBG only): 1 no M stores, 2 no tiles, 4 no MMAs, 8 no loads
 static int g_gemm_dbg = 0;
 static int g_gemm_balance = 0;   // WINO_K3_BALANCE (experiments)
+static int g_gemm_pair = 0;      // WINO_K3_PAIR: CTA-pair GEMM (k_gemm2)
 void set_gemm_trace(void* buf) { g_trace = static_cast<uint64_t*>(buf); }
 
 cudaError_t launch_gemm(const Geom& g, long long tiles_pad_launch, const int8_t* vimg, const int8_t* wimg,
                         const uint8_t* codes, int32_t* mraw, cudaStream_t st) {
   // tile blocks of this launch; M strides use the full chunk geometry (K4 reads with it)
   const int tblocks = (int)(tiles_pad_launch / kMBlock);
+  if (g_gemm_pair && g.alg == 0 && !g.w1 && g.nblk == 64) {   // CTA pairs (k_gemm2)
+    const int kps2 = gemm_ksteps_per_stage(g.ksteps);
+    const int nst2 = gemm2_stages(g.nblk, kps2);
+    const int units2 = ((tblocks + 1) / 2) * (g.cout_pad / g.nblk) * kPositions;
+    const int clusters = units2 < g_num_sms / 2 ? units2 : g_num_sms / 2;
+    return launch_pdl_cluster(k_gemm2<64>, dim3(2 * clusters), dim3(kGemmThreads), gemm2_smem_bytes(g.nblk, nst2, kps2),
+                              st, 2, vimg, wimg, mraw, codes, g.cout, g.scaling, g.ksteps, g.chunk_tiles_pad, tblocks,
+                              g.cout_pad, nst2, kps2);
+  }
   const int n_units = tblocks * (g.cout_pad / g.nblk) * (g.alg == 1 ? 16 : kPositions);
   int grid = n_units < g_num_sms ? n_units : g_num_sms;
   if (g_gemm_balance) {   // fewest CTAs with the same number of unit rounds (see launch_fused)
@@ -483,6 +827,7 @@ cudaError_t setup_gemm() {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (const char* d = std::getenv("WINO_K3_DBG")) g_gemm_dbg = std::atoi(d);
   if (const char* d = std::getenv("WINO_K3_BALANCE")) g_gemm_balance = std::atoi(d);
+  if (const char* d = std::getenv("WINO_K3_PAIR")) g_gemm_pair = std::atoi(d);
   if (const char* d = std::getenv("WINO_K3_KPS")) g_kps_override = std::atoi(d);
   if (const char* d = std::getenv("WINO_K3_STAGING")) g_staging_override = std::atoi(d);
   if (const char* d = std::getenv("WINO_K3_STAGES")) g_stages_cap = std::max(kMinStages, std::min(kMaxStages, std::atoi(d)));
@@ -499,6 +844,7 @@ cudaError_t setup_gemm() {
   attr((const void*)k_gemm<64, false, false>, 64);
   attr((const void*)k_gemm<64, true, false>, 64);
   attr((const void*)k_gemm<64, false, true>, 64);
+  attr((const void*)k_gemm2<64>, 64);
   return e;
 }
 

@@ -490,3 +490,33 @@ def test_auto_path_choice_and_parity():
     conv.transform_filter(torch.from_numpy(w).cuda())
     np.testing.assert_array_equal(conv(torch.from_numpy(x).cuda()).cpu().numpy(),
                                   O.wino_conv(x, w, 1, O.NHWC, True).out32)
+
+
+@pytest.mark.gpu
+def test_staged_gemm_cta_pair_variant_matches_the_oracle():
+    """WINO_K3_PAIR=1 (read once per process, so in a subprocess): the staged GEMM on CTA pairs
+    (tcgen05.mma.cta_group::2, M = 256, B split between the pair) -- an odd tile-block count (the last block
+    unpaired), c_out 64 (n_block 64), scaling on, int32 out -- equals the oracle."""
+    import subprocess, sys, textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent("""
+        import sys, numpy as np, torch
+        sys.path.insert(0, %r); sys.path.insert(0, %r)
+        import synth, paper_1901_01965_b200 as W
+        from oracle import oracle as O
+        rng = np.random.default_rng(7)
+        x, w = synth.random_layer(rng, 6, 28, 28, 96, 64, O.NHWC)   # 6 x 49 = 294 tiles: three blocks (one unpaired)
+        c = W.WinoConv2d(6, 28, 28, 96, 64, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=W.WINO_PATH_STAGED)
+        c.transform_filter(torch.from_numpy(w).cuda())
+        y = c(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert np.array_equal(y, O.wino_conv(x, w, 1, O.NHWC, True).out32)
+        x, w = synth.random_layer(rng, 7, 30, 30, 64, 128, O.NHWC)  # 7 x 64 = 448 tiles: four blocks, two cout blocks
+        c = W.WinoConv2d(7, 30, 30, 64, 128, 1, W.WINO_NHWC, True, W.WINO_OUT_INT32, path=W.WINO_PATH_STAGED)
+        c.transform_filter(torch.from_numpy(w).cuda())
+        y = c(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert np.array_equal(y, O.wino_conv(x, w, 1, O.NHWC, True).out32)
+        print("ok")
+    """ % (root, os.path.join(root, "tests")))
+    env = dict(os.environ, WINO_K3_PAIR="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
