@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
       if (k & 2) v = make_uint4(v.z, v.w, v.x, v.y);
       return v;
     };
-    bool pending = false;
+    bool pending = false, staged_read = false;
     int pend_tb = 0, pend_nb = 0;
     auto store_staged = [&](int tb_i, int nb) {
       if (g.pool2) {   // fused 2x2/2 max pool: staged as [pooled px 4][tile][16 couts], one chunk per thread
@@ -879,7 +879,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
           if (qpair) store_pair(pend_tb, pend_nb);
           else store_staged(pend_tb, pend_nb);
         }
-        fepi_barrier();
+        // the staging (aliased by Z_0, except in pair mode) is free once every thread has read it: the barrier
+        // sits just before the Z_0 parking, so the skew of the stores is absorbed by the row's complex group
+        staged_read = !qpair;
         pending = false;
       }
 #pragma unroll
@@ -922,6 +924,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
         {
           int32_t Z[4][4];
           real_row(0, Z);                              // row 0 -> Z_0
+          if (staged_read) {
+            fepi_barrier();
+            staged_read = false;
+          }
 #pragma unroll
           for (int j = 0; j < 4; j++)
             if (!(dbg & (256 | 512))) *part_ptr(0, j) = make_int4(Z[j][0], Z[j][1], Z[j][2], Z[j][3]);
