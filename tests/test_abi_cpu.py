@@ -91,3 +91,17 @@ def test_fast_division_matches_integer_division():
             if 0 <= n <= top:
                 assert f(n, d) == n // d, (n, d)
     assert f(-1, 3) == -1 and f(5, 0) == -1
+
+
+def test_bench_reports_uint8_above_its_cin_limit_as_unsupported():
+    """bench.py --input u8 on a config whose c_in exceeds the uint8 limit (A28: 224) prints one JSON line that
+    says so (no CUDA needed: the check precedes any launch) instead of failing inside wino_plan."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "C4", "--input", "u8", "--no-cpu"],
+                       capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert "unsupported" in line and "224" in line["unsupported"]
